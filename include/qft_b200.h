@@ -1,0 +1,194 @@
+/*
+ * qft_b200.h -- C-ABI of the B200-native QFT model-state update path.
+ *
+ * This is the drop-in boundary for the reference's quantizer/optimizer API
+ * (/root/reference/proj/include/qft/{quantize,optimizer,gradflow}.hpp).  Every
+ * entry point below names the reference interface it replaces (file:line).
+ * Signatures use plain pointers, sizes and a CUDA stream -- no torch or STL types.
+ *
+ * Memory: every array argument is DEVICE memory unless the name ends in _host.
+ * Layout: row-major [rows x cols], row = output channel (tensor.hpp:13-16).
+ *   codes       u8  [rows*cols]  one byte per element for any bit width <= 8
+ *                                (quantize.hpp:41, :356)
+ *   scale       f32 [rows]       per-channel scale (> 0)
+ *   zero_point  i32 [rows]       unclipped (quantize.hpp:22-25)
+ *   t_min,t_max f32 [rows]       cached dense thresholds (quantize.hpp:66)
+ *   row_ptr     i32 [rows+1]     strict CSR, col_idx ascending within a row
+ *   col_idx     i32 [nnz], values f32 [nnz]   (quantize.hpp:48-57)
+ *
+ * Errors: functions return QFTC_OK (0) or a negative status; qftc_last_error()
+ * returns a thread-local message.  QFTC_EINVAL <-> std::invalid_argument and
+ * QFTC_ERANGE <-> std::out_of_range of the reference, with the same validation
+ * order, so the C++ shim (include/qft_b200/qft.hpp) rethrows the same types.
+ *
+ * Asynchrony: all work is enqueued on `stream`; functions that must return a
+ * host-visible value (nnz, status) say "synchronises".  There is no CPU
+ * fallback: without a CUDA device every compute call returns QFTC_ECUDA.
+ */
+#ifndef QFT_B200_H_
+#define QFT_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* qftc_stream_t; /* == cudaStream_t */
+
+enum {
+  QFTC_OK = 0,
+  QFTC_EINVAL = -1,    /* std::invalid_argument in the reference */
+  QFTC_ERANGE = -2,    /* std::out_of_range in the reference      */
+  QFTC_ECUDA = -3,     /* CUDA runtime error / no device           */
+  QFTC_EOVERFLOW = -4, /* CSR output capacity exceeded (re-run with more) */
+  QFTC_ENOTSUP = -5    /* shape outside what the kernels support   */
+};
+
+enum { QFTC_PERCENTILE = 0, QFTC_RANGE_FRACTION = 1 }; /* ThresholdKind, quantize.hpp:20 */
+enum { QFTC_GRAD_U8 = 0, QFTC_GRAD_F32 = 1, QFTC_GRAD_BF16 = 2 };
+
+const char* qftc_last_error(void);
+int qftc_version(void);
+/* largest row length (cols) the row kernels accept */
+int qftc_max_cols(void);
+
+/* ---------------------------------------------------------------- L0 / L1 */
+
+/* channel_minmax  (tensor.hpp:133-148) */
+int qftc_channel_minmax(const float* x, int rows, int cols, float* mins, float* maxs,
+                        qftc_stream_t stream);
+
+/* affine_params_from_bounds  (quantize.hpp:105-131).  Validation of min <= max
+ * needs the data: this call synchronises and returns QFTC_EINVAL on violation. */
+int qftc_affine_params_from_bounds(const float* mins, const float* maxs, int64_t n,
+                                   int bit_width, float* scale, int32_t* zero_point,
+                                   qftc_stream_t stream);
+
+/* quantize with given params; channels is 1 or rows  (quantize.hpp:149-175) */
+int qftc_quantize(const float* x, int rows, int cols, const float* scale,
+                  const int32_t* zero_point, int channels, int bit_width, uint8_t* codes,
+                  qftc_stream_t stream);
+
+/* quantize_state, affine mode: fresh per-row params + quantize (quantize.hpp:189-193).
+ * Fused row kernel: one HBM read of x.  Synchronises only if `check` != 0 (to
+ * report a NaN-in-column-0 row as QFTC_EINVAL like the reference). */
+int qftc_quantize_state(const float* x, int rows, int cols, int bit_width, uint8_t* codes,
+                        float* scale, int32_t* zero_point, int check, qftc_stream_t stream);
+
+/* dequantize  (quantize.hpp:195-212) -> f32, and the bf16 expansion (RNE of the f32) */
+int qftc_dequantize(const uint8_t* codes, int rows, int cols, const float* scale,
+                    const int32_t* zero_point, int channels, float* out, qftc_stream_t stream);
+int qftc_dequantize_bf16(const uint8_t* codes, int rows, int cols, const float* scale,
+                         const int32_t* zero_point, int channels, uint16_t* out,
+                         qftc_stream_t stream);
+
+/* compute_outlier_thresholds  (quantize.hpp:216-247): exact per-row order
+ * statistics by radix select (percentile) or row range (range_fraction). */
+int qftc_outlier_thresholds(const float* w, int rows, int cols, double fraction, int kind,
+                            float* t_min, float* t_max, qftc_stream_t stream);
+
+/* decompose_dense_sparse  (quantize.hpp:253-290).  Writes dense codes, the
+ * threshold-derived params, row_ptr (rows+1) and up to `capacity` CSR entries.
+ * The true nnz is row_ptr[rows]; if it exceeds capacity the call returns
+ * QFTC_EOVERFLOW (synchronises) and can be re-run with larger buffers. */
+int qftc_decompose_dense_sparse(const float* w, int rows, int cols, const float* t_min,
+                                const float* t_max, int bit_width, uint8_t* codes, float* scale,
+                                int32_t* zero_point, int32_t* row_ptr, int32_t* col_idx,
+                                float* values, int64_t capacity, int64_t* nnz_host,
+                                qftc_stream_t stream);
+
+/* reconstruct  (quantize.hpp:331-338) -> f32, and -> bf16 for the next forward
+ * (network.hpp:208-211 consumer).  row_ptr may hold absolute offsets into a shared
+ * CSR arena (col_idx/values are indexed by row_ptr directly). */
+int qftc_reconstruct(const uint8_t* codes, int rows, int cols, const float* scale,
+                     const int32_t* zero_point, const int32_t* row_ptr, const int32_t* col_idx,
+                     const float* values, float* out, qftc_stream_t stream);
+int qftc_reconstruct_bf16(const uint8_t* codes, int rows, int cols, const float* scale,
+                          const int32_t* zero_point, const int32_t* row_ptr,
+                          const int32_t* col_idx, const float* values, uint16_t* out,
+                          qftc_stream_t stream);
+
+/* ---------------------------------------------------------------- L4: Lion */
+
+/* LionHyper  (optimizer.hpp:15-21) */
+typedef struct {
+  float lr, beta1, beta2, weight_decay;
+} qftc_lion_hyper;
+
+/* One layer of lion_step_quantized (optimizer.hpp:85-120) for a grouped launch.
+ * Ping-pong state: a step with flip=f reads set [f] and writes set [1-f]; the
+ * caller swaps its view after the step.  The weight's dense params and
+ * thresholds are fixed between refreshes (requantize_weight, quantize.hpp:318-329)
+ * and are read-only here.  row_ptr[k] holds ABSOLUTE offsets into the plan's CSR
+ * arena k.  The gradient is the GradientStack entry (u8 codes + per-row params,
+ * gradflow.hpp:77) or, for QFTC_GRAD_F32/BF16, the raw fp gradient that the
+ * backward sink would quantize: the fused kernel applies quantize_state ->
+ * dequantize to it exactly. */
+typedef struct {
+  int32_t rows, cols;
+  uint8_t* w_codes[2];
+  int32_t* row_ptr[2];
+  const float* w_scale;
+  const int32_t* w_zero_point;
+  const float* t_min;
+  const float* t_max;
+  uint8_t* m_codes[2];
+  float* m_scale[2];
+  int32_t* m_zero_point[2];
+  const uint8_t* g_codes;
+  const float* g_scale;
+  const int32_t* g_zero_point;
+  const void* g_raw;
+} qftc_lion_tensor;
+
+typedef struct qftc_plan qftc_plan; /* opaque */
+
+/* Build a grouped step plan over n tensors (uploads descriptors, allocates the
+ * look-back workspace; synchronises).  All tensors share bit_width and gradient
+ * kind.  CSR arenas: col_idx[k]/values[k] with capacity[k] entries, k = 0, 1. */
+int qftc_plan_create(qftc_plan** plan, const qftc_lion_tensor* tensors_host, int n,
+                     int bit_width, int grad_kind, int32_t* col_idx[2], float* values[2],
+                     const int64_t capacity[2], qftc_stream_t stream);
+/* Re-point the CSR arenas (after growing them). */
+int qftc_plan_set_arena(qftc_plan* plan, int32_t* col_idx[2], float* values[2],
+                        const int64_t capacity[2]);
+/* Enqueue one fused quantized Lion step over every row of every tensor
+ * (dequant g,m,w -> Lion -> requant m (fresh params) -> requant w (cached
+ * thresholds) + ordered CSR re-extraction), reading set [flip]. */
+int qftc_plan_step(qftc_plan* plan, int flip, qftc_lion_hyper hyper, qftc_stream_t stream);
+/* Synchronises; returns the new total nnz of the arena written by the last step
+ * and QFTC_EOVERFLOW / QFTC_EINVAL if that step overflowed or hit a degenerate row. */
+int qftc_plan_result(qftc_plan* plan, int64_t* nnz_total, qftc_stream_t stream);
+/* number of kernel launches one qftc_plan_step enqueues (for accounting) */
+int qftc_plan_launches(const qftc_plan* plan);
+int qftc_plan_destroy(qftc_plan* plan);
+
+/* Single-tensor convenience: lion_step_quantized for one layer, out-of-place,
+ * synchronous (reference semantics).  Returns the new nnz in *nnz_host. */
+int qftc_lion_step(int rows, int cols, int bit_width, const uint8_t* g_codes,
+                   const float* g_scale, const int32_t* g_zero_point, const uint8_t* m_codes,
+                   const float* m_scale, const int32_t* m_zero_point, const uint8_t* w_codes,
+                   const float* w_scale, const int32_t* w_zero_point, const float* t_min,
+                   const float* t_max, const int32_t* row_ptr, const int32_t* col_idx,
+                   const float* values, uint8_t* m_codes_out, float* m_scale_out,
+                   int32_t* m_zero_point_out, uint8_t* w_codes_out, int32_t* row_ptr_out,
+                   int32_t* col_idx_out, float* values_out, int64_t capacity,
+                   qftc_lion_hyper hyper, int64_t* nnz_host, qftc_stream_t stream);
+
+/* Pass-through mode (QuantMode::passthrough, quantize.hpp:17): lion_apply on raw
+ * fp32 state, bitwise equal to lion_step_reference (optimizer.hpp:135-142). */
+int qftc_lion_apply(float* w, float* m, const float* g, int64_t n, qftc_lion_hyper hyper,
+                    qftc_stream_t stream);
+
+/* ---------------------------------------------------------------- inputs */
+
+/* Deterministic synthetic tensor, bit-identical to oracle/synth.c qo_synth. */
+int qftc_synth(float* out, int64_t n, uint64_t seed, double sigma, double spike_p,
+               qftc_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QFT_B200_H_ */

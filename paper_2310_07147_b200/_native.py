@@ -1,0 +1,114 @@
+"""ctypes binding of the C-ABI (``include/qft_b200.h``) exported by the in-tree
+``_lib/libqft_b200.so``.
+
+There is no fallback: if the library is missing the import fails loudly, and on
+a host without a CUDA device every compute entry point returns ``QFTC_ECUDA``,
+which :func:`check` raises as ``RuntimeError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libqft_b200.so")
+
+QFTC_OK, QFTC_EINVAL, QFTC_ERANGE, QFTC_ECUDA, QFTC_EOVERFLOW, QFTC_ENOTSUP = 0, -1, -2, -3, -4, -5
+GRAD_U8, GRAD_F32, GRAD_BF16 = 0, 1, 2
+PERCENTILE, RANGE_FRACTION = 0, 1
+
+
+class CsrOverflow(RuntimeError):
+    """The new nnz exceeded the CSR arena capacity (QFTC_EOVERFLOW)."""
+
+
+class LionHyperC(C.Structure):
+    """``qftc_lion_hyper`` == ``LionHyper<float>`` (optimizer.hpp:15-21)."""
+    _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float),
+                ("weight_decay", C.c_float)]
+
+
+class LionTensorC(C.Structure):
+    """``qftc_lion_tensor``: one layer of a grouped quantized Lion step."""
+    _fields_ = [
+        ("rows", C.c_int32), ("cols", C.c_int32),
+        ("w_codes", C.c_void_p * 2), ("row_ptr", C.c_void_p * 2),
+        ("w_scale", C.c_void_p), ("w_zero_point", C.c_void_p),
+        ("t_min", C.c_void_p), ("t_max", C.c_void_p),
+        ("m_codes", C.c_void_p * 2), ("m_scale", C.c_void_p * 2),
+        ("m_zero_point", C.c_void_p * 2),
+        ("g_codes", C.c_void_p), ("g_scale", C.c_void_p), ("g_zero_point", C.c_void_p),
+        ("g_raw", C.c_void_p),
+    ]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build the sm_100a library first "
+            "(python -m paper_2310_07147_b200.build or __graft_entry__.build())")
+    return C.CDLL(LIB_PATH)
+
+
+lib = _load()
+
+_vp, _i, _i64, _d, _u64 = C.c_void_p, C.c_int, C.c_int64, C.c_double, C.c_uint64
+
+_SIGS = {
+    "qftc_last_error": (C.c_char_p, []),
+    "qftc_version": (_i, []),
+    "qftc_max_cols": (_i, []),
+    "qftc_channel_minmax": (_i, [_vp, _i, _i, _vp, _vp, _vp]),
+    "qftc_affine_params_from_bounds": (_i, [_vp, _vp, _i64, _i, _vp, _vp, _vp]),
+    "qftc_quantize": (_i, [_vp, _i, _i, _vp, _vp, _i, _i, _vp, _vp]),
+    "qftc_quantize_state": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, _i, _vp]),
+    "qftc_dequantize": (_i, [_vp, _i, _i, _vp, _vp, _i, _vp, _vp]),
+    "qftc_dequantize_bf16": (_i, [_vp, _i, _i, _vp, _vp, _i, _vp, _vp]),
+    "qftc_outlier_thresholds": (_i, [_vp, _i, _i, _d, _i, _vp, _vp, _vp]),
+    "qftc_decompose_dense_sparse": (_i, [_vp, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp,
+                                         _vp, _i64, C.POINTER(_i64), _vp]),
+    "qftc_reconstruct": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "qftc_reconstruct_bf16": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "qftc_plan_create": (_i, [C.POINTER(_vp), C.POINTER(LionTensorC), _i, _i, _i,
+                              C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_i64), _vp]),
+    "qftc_plan_set_arena": (_i, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_i64)]),
+    "qftc_plan_step": (_i, [_vp, _i, LionHyperC, _vp]),
+    "qftc_plan_result": (_i, [_vp, C.POINTER(_i64), _vp]),
+    "qftc_plan_launches": (_i, [_vp]),
+    "qftc_plan_destroy": (_i, [_vp]),
+    "qftc_lion_step": (_i, [_i, _i, _i] + [_vp] * 21 + [_i64, LionHyperC, C.POINTER(_i64), _vp]),
+    "qftc_lion_apply": (_i, [_vp, _vp, _vp, _i64, LionHyperC, _vp]),
+    "qftc_synth": (_i, [_vp, _i64, _u64, _d, _d, _vp]),
+}
+
+EXPORTS = tuple(_SIGS)
+
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+
+def last_error() -> str:
+    return lib.qftc_last_error().decode()
+
+
+def check(rc: int) -> int:
+    """Map a status code onto the reference's exception types
+    (std::invalid_argument -> ValueError, std::out_of_range -> IndexError)."""
+    if rc == QFTC_OK:
+        return rc
+    msg = last_error()
+    if rc == QFTC_EINVAL:
+        raise ValueError(msg)
+    if rc == QFTC_ERANGE:
+        raise IndexError(msg)
+    if rc == QFTC_EOVERFLOW:
+        raise CsrOverflow(msg)
+    if rc == QFTC_ENOTSUP:
+        raise NotImplementedError(msg)
+    raise RuntimeError(msg)
+
+
+def hyper(lr=1e-4, beta1=0.9, beta2=0.99, weight_decay=0.0) -> LionHyperC:
+    return LionHyperC(lr, beta1, beta2, weight_decay)

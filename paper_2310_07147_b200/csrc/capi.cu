@@ -1,0 +1,571 @@
+// capi.cu -- extern "C" boundary (include/qft_b200.h) over the sm_100a kernels.
+//
+// Validation order and messages follow the reference so the C++ shim can map
+// QFTC_EINVAL/QFTC_ERANGE back onto std::invalid_argument/std::out_of_range.
+// There is no host fallback: without a CUDA device every compute entry point
+// fails with QFTC_ECUDA.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "qft_b200.h"
+#include "qft_internal.h"
+
+namespace qftk {
+cudaError_t launch_channel_minmax(const float*, int, int, float*, float*, cudaStream_t);
+cudaError_t launch_affine_params(const float*, const float*, int64_t, int, float*, int32_t*,
+                                 uint32_t*, cudaStream_t);
+cudaError_t launch_quantize_state(const float*, int, int, int, uint8_t*, float*, int32_t*,
+                                  uint32_t*, cudaStream_t);
+cudaError_t launch_quantize(const float*, int, int, const float*, const int32_t*, int, int,
+                            uint8_t*, cudaStream_t);
+cudaError_t launch_dequantize(const uint8_t*, int, int, const float*, const int32_t*, int, void*,
+                              bool, cudaStream_t);
+cudaError_t launch_thresholds(const float*, int, int, double, int, float*, float*, cudaStream_t);
+cudaError_t launch_lion_apply(float*, float*, const float*, int64_t, float, float, float, float,
+                              cudaStream_t);
+cudaError_t launch_synth(float*, int64_t, uint64_t, double, double, cudaStream_t);
+}  // namespace qftk
+
+using namespace qftk;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(QFTC_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define QFTC_CUDA(expr, where)                 \
+  do {                                         \
+    cudaError_t _e = (expr);                   \
+    if (_e != cudaSuccess) return cuda_fail(_e, where); \
+  } while (0)
+
+int require_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return fail(QFTC_ECUDA, "no CUDA device: the QFT B200 path has no CPU fallback");
+  return QFTC_OK;
+}
+
+int require_bit_width(int b) {
+  if (b < 2 || b > 8)
+    return fail(QFTC_EINVAL, "bit width must be in [2, 8], got " + std::to_string(b));
+  return QFTC_OK;
+}
+
+int require_shape(int rows, int cols, const char* what) {
+  if (rows <= 0 || cols <= 0) return fail(QFTC_EINVAL, std::string(what) + ": empty tensor");
+  return QFTC_OK;
+}
+
+inline bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+// Device scratch for one call: header + status words.
+struct Scratch {
+  void* base = nullptr;
+  Header* hdr = nullptr;
+  unsigned long long* status = nullptr;
+  DevTensor* tensors = nullptr;
+};
+
+int scratch_alloc(Scratch& s, int64_t rows, int n_tensors, cudaStream_t st) {
+  const size_t hb = sizeof(Header);
+  const size_t tb = sizeof(DevTensor) * (size_t)n_tensors;
+  const size_t sb = sizeof(unsigned long long) * (size_t)(rows > 0 ? rows : 1);
+  const size_t total = hb + ((tb + 255) & ~size_t(255)) + sb + 256;
+  QFTC_CUDA(cudaMallocAsync(&s.base, total, st), "cudaMallocAsync");
+  QFTC_CUDA(cudaMemsetAsync(s.base, 0, total, st), "cudaMemsetAsync");
+  s.hdr = reinterpret_cast<Header*>(s.base);
+  s.tensors = reinterpret_cast<DevTensor*>(reinterpret_cast<char*>(s.base) + 256);
+  s.status = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(s.base) + 256 +
+                                                   ((tb + 255) & ~size_t(255)));
+  const uint32_t one = 1;  // epoch starts at 1: zeroed status words read as "not ready"
+  QFTC_CUDA(cudaMemcpyAsync(&s.hdr->epoch, &one, 4, cudaMemcpyHostToDevice, st), "init epoch");
+  return QFTC_OK;
+}
+
+// choose the number of pipeline stages: most CTAs per SM first, then most stages
+int pick_stages(int mode, int gk, int cols_p) {
+  int best_s = 2;
+  long best_score = -1;
+  for (int S = 2; S <= 4; ++S) {
+    const size_t smem = row_engine_smem(mode, gk, cols_p, S);
+    if (smem > 227 * 1024) break;
+    const long per_sm = (long)((228 * 1024) / (smem + 1024));
+    const long blocks = per_sm < 3 ? per_sm : 3;  // register limit (launch_bounds(160,3))
+    const long score = blocks * 16 + S;
+    if (blocks >= 1 && score > best_score) {
+      best_score = score;
+      best_s = S;
+    }
+  }
+  return best_s;
+}
+
+int read_header(const Header* d_hdr, Header* h, cudaStream_t st) {
+  QFTC_CUDA(cudaMemcpyAsync(h, d_hdr, sizeof(Header), cudaMemcpyDeviceToHost, st), "read header");
+  QFTC_CUDA(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+  return QFTC_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* qftc_last_error(void) { return g_err.c_str(); }
+int qftc_version(void) { return 1; }
+int qftc_max_cols(void) { return row_engine_max_cols(); }
+
+int qftc_channel_minmax(const float* x, int rows, int cols, float* mins, float* maxs,
+                        qftc_stream_t stream) {
+  if (int rc = require_shape(rows, cols, "channel_minmax")) return rc;
+  if (int rc = require_device()) return rc;
+  QFTC_CUDA(launch_channel_minmax(x, rows, cols, mins, maxs, (cudaStream_t)stream),
+            "channel_minmax");
+  return QFTC_OK;
+}
+
+int qftc_affine_params_from_bounds(const float* mins, const float* maxs, int64_t n,
+                                   int bit_width, float* scale, int32_t* zp,
+                                   qftc_stream_t stream) {
+  if (int rc = require_bit_width(bit_width)) return rc;
+  if (n <= 0) return fail(QFTC_EINVAL, "affine_params_from_bounds: bad channel count");
+  if (int rc = require_device()) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* err = nullptr;
+  QFTC_CUDA(cudaMallocAsync((void**)&err, 4, st), "cudaMallocAsync");
+  QFTC_CUDA(cudaMemsetAsync(err, 0, 4, st), "memset");
+  QFTC_CUDA(launch_affine_params(mins, maxs, n, bit_width, scale, zp, err, st), "affine_params");
+  uint32_t h = 0;
+  QFTC_CUDA(cudaMemcpyAsync(&h, err, 4, cudaMemcpyDeviceToHost, st), "copy");
+  QFTC_CUDA(cudaFreeAsync(err, st), "free");
+  QFTC_CUDA(cudaStreamSynchronize(st), "sync");
+  if (h) return fail(QFTC_EINVAL, "affine_params_from_bounds: min > max in a channel");
+  return QFTC_OK;
+}
+
+int qftc_quantize(const float* x, int rows, int cols, const float* scale, const int32_t* zp,
+                  int channels, int bit_width, uint8_t* codes, qftc_stream_t stream) {
+  if (channels != 1 && channels != rows)
+    return fail(QFTC_EINVAL, "quantize: channel count " + std::to_string(channels) +
+                                 " does not match rows " + std::to_string(rows));
+  if (int rc = require_shape(rows, cols, "quantize")) return rc;
+  if (int rc = require_bit_width(bit_width)) return rc;
+  if (int rc = require_device()) return rc;
+  QFTC_CUDA(launch_quantize(x, rows, cols, scale, zp, channels, bit_width, codes,
+                            (cudaStream_t)stream),
+            "quantize");
+  return QFTC_OK;
+}
+
+int qftc_quantize_state(const float* x, int rows, int cols, int bit_width, uint8_t* codes,
+                        float* scale, int32_t* zp, int check, qftc_stream_t stream) {
+  if (int rc = require_shape(rows, cols, "compute_affine_params")) return rc;
+  if (int rc = require_bit_width(bit_width)) return rc;
+  if (int rc = require_device()) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* err = nullptr;
+  QFTC_CUDA(cudaMallocAsync((void**)&err, 4, st), "cudaMallocAsync");
+  QFTC_CUDA(cudaMemsetAsync(err, 0, 4, st), "memset");
+  QFTC_CUDA(launch_quantize_state(x, rows, cols, bit_width, codes, scale, zp, err, st),
+            "quantize_state");
+  uint32_t h = 0;
+  if (check) QFTC_CUDA(cudaMemcpyAsync(&h, err, 4, cudaMemcpyDeviceToHost, st), "copy");
+  QFTC_CUDA(cudaFreeAsync(err, st), "free");
+  if (check) {
+    QFTC_CUDA(cudaStreamSynchronize(st), "sync");
+    if (h) return fail(QFTC_EINVAL, "affine_params_from_bounds: min > max in a channel");
+  }
+  return QFTC_OK;
+}
+
+int qftc_dequantize(const uint8_t* codes, int rows, int cols, const float* scale,
+                    const int32_t* zp, int channels, float* out, qftc_stream_t stream) {
+  if (int rc = require_shape(rows, cols, "dequantize")) return rc;
+  if (channels != 1 && channels != rows)
+    return fail(QFTC_EINVAL, "dequantize: channel count does not match rows");
+  if (int rc = require_device()) return rc;
+  QFTC_CUDA(launch_dequantize(codes, rows, cols, scale, zp, channels, out, false,
+                              (cudaStream_t)stream),
+            "dequantize");
+  return QFTC_OK;
+}
+
+int qftc_dequantize_bf16(const uint8_t* codes, int rows, int cols, const float* scale,
+                         const int32_t* zp, int channels, uint16_t* out,
+                         qftc_stream_t stream) {
+  if (int rc = require_shape(rows, cols, "dequantize")) return rc;
+  if (channels != 1 && channels != rows)
+    return fail(QFTC_EINVAL, "dequantize: channel count does not match rows");
+  if (int rc = require_device()) return rc;
+  QFTC_CUDA(launch_dequantize(codes, rows, cols, scale, zp, channels, out, true,
+                              (cudaStream_t)stream),
+            "dequantize_bf16");
+  return QFTC_OK;
+}
+
+int qftc_outlier_thresholds(const float* w, int rows, int cols, double fraction, int kind,
+                            float* t_min, float* t_max, qftc_stream_t stream) {
+  if (int rc = require_shape(rows, cols, "compute_outlier_thresholds")) return rc;
+  if (!(fraction >= 0.0) || fraction >= 0.5)
+    return fail(QFTC_EINVAL, "outlier fraction must be in [0, 0.5)");
+  if (kind != QFTC_PERCENTILE && kind != QFTC_RANGE_FRACTION)
+    return fail(QFTC_EINVAL, "threshold kind must be percentile or range-fraction");
+  if (int rc = require_device()) return rc;
+  QFTC_CUDA(launch_thresholds(w, rows, cols, fraction, kind, t_min, t_max, (cudaStream_t)stream),
+            "outlier_thresholds");
+  return QFTC_OK;
+}
+
+int qftc_decompose_dense_sparse(const float* w, int rows, int cols, const float* t_min,
+                                const float* t_max, int bit_width, uint8_t* codes, float* scale,
+                                int32_t* zp, int32_t* row_ptr, int32_t* col_idx, float* values,
+                                int64_t capacity, int64_t* nnz_host, qftc_stream_t stream) {
+  if (int rc = require_shape(rows, cols, "decompose_dense_sparse")) return rc;
+  if (int rc = require_bit_width(bit_width)) return rc;
+  if (cols > row_engine_max_cols())
+    return fail(QFTC_ENOTSUP, "decompose: cols above " + std::to_string(row_engine_max_cols()));
+  if (int rc = require_device()) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  // params from thresholds (quantize.hpp:264) -- validates t_min <= t_max
+  int rc = qftc_affine_params_from_bounds(t_min, t_max, rows, bit_width, scale, zp, stream);
+  if (rc) return rc;
+  Scratch sc;
+  if ((rc = scratch_alloc(sc, rows, 1, st))) return rc;
+  DevTensor t{};
+  t.rows = rows;
+  t.cols = cols;
+  t.row_base = 0;
+  t.w_f32 = w;
+  t.w_scale = scale;
+  t.w_zp = zp;
+  t.t_min = t_min;
+  t.t_max = t_max;
+  t.w_codes[1] = codes;
+  t.row_ptr[1] = row_ptr;
+  QFTC_CUDA(cudaMemcpyAsync(sc.tensors, &t, sizeof t, cudaMemcpyHostToDevice, st), "upload");
+  LaunchArgs a{};
+  a.tensors = sc.tensors;
+  a.n_tensors = 1;
+  a.total_rows = rows;
+  a.flip = 0;
+  a.bit_width = bit_width;
+  a.col_out = col_idx;
+  a.val_out = values;
+  a.cap_out = capacity;
+  a.hdr = sc.hdr;
+  a.status = sc.status;
+  a.cols_p = (cols + 15) & ~15;
+  a.use_bulk = (cols % 16 == 0) && al16(w) && al16(codes);
+  a.stages = pick_stages(MODE_DECOMPOSE, G_U8, a.cols_p);
+  QFTC_CUDA(launch_row_engine(MODE_DECOMPOSE, G_U8, a, st, nullptr), "decompose kernel");
+  Header h{};
+  rc = read_header(sc.hdr, &h, st);
+  cudaFreeAsync(sc.base, st);
+  if (rc) return rc;
+  if (nnz_host) *nnz_host = h.total_nnz;
+  if (h.err & ERR_PREFIX) return fail(QFTC_ENOTSUP, "decompose: nnz above 2^30");
+  if (h.overflow)
+    return fail(QFTC_EOVERFLOW, "decompose: nnz " + std::to_string(h.total_nnz) +
+                                    " exceeds capacity " + std::to_string(capacity));
+  return QFTC_OK;
+}
+
+static int reconstruct_impl(const uint8_t* codes, int rows, int cols, const float* scale,
+                            const int32_t* zp, const int32_t* row_ptr, const int32_t* col_idx,
+                            const float* values, void* out, bool bf16, qftc_stream_t stream) {
+  if (int rc = require_shape(rows, cols, "dequantize")) return rc;
+  if (cols > row_engine_max_cols())
+    return fail(QFTC_ENOTSUP, "reconstruct: cols above " + std::to_string(row_engine_max_cols()));
+  if (int rc = require_device()) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  Scratch sc;
+  if (int rc = scratch_alloc(sc, 0, 1, st)) return rc;
+  DevTensor t{};
+  t.rows = rows;
+  t.cols = cols;
+  t.w_codes[0] = const_cast<uint8_t*>(codes);
+  t.row_ptr[0] = const_cast<int32_t*>(row_ptr);
+  t.w_scale = scale;
+  t.w_zp = zp;
+  t.out = out;
+  QFTC_CUDA(cudaMemcpyAsync(sc.tensors, &t, sizeof t, cudaMemcpyHostToDevice, st), "upload");
+  LaunchArgs a{};
+  a.tensors = sc.tensors;
+  a.n_tensors = 1;
+  a.total_rows = rows;
+  a.flip = 0;
+  a.bit_width = 8;
+  a.col_in = col_idx;
+  a.val_in = values;
+  a.hdr = sc.hdr;
+  a.status = sc.status;
+  a.cols_p = (cols + 15) & ~15;
+  a.use_bulk = (cols % 16 == 0) && al16(codes) && al16(out);
+  const int mode = bf16 ? MODE_RECON_BF16 : MODE_RECON_F32;
+  a.stages = pick_stages(mode, G_U8, a.cols_p);
+  QFTC_CUDA(launch_row_engine(mode, G_U8, a, st, nullptr), "reconstruct kernel");
+  QFTC_CUDA(cudaFreeAsync(sc.base, st), "free");
+  return QFTC_OK;
+}
+
+int qftc_reconstruct(const uint8_t* codes, int rows, int cols, const float* scale,
+                     const int32_t* zp, const int32_t* row_ptr, const int32_t* col_idx,
+                     const float* values, float* out, qftc_stream_t stream) {
+  return reconstruct_impl(codes, rows, cols, scale, zp, row_ptr, col_idx, values, out, false,
+                          stream);
+}
+
+int qftc_reconstruct_bf16(const uint8_t* codes, int rows, int cols, const float* scale,
+                          const int32_t* zp, const int32_t* row_ptr, const int32_t* col_idx,
+                          const float* values, uint16_t* out, qftc_stream_t stream) {
+  return reconstruct_impl(codes, rows, cols, scale, zp, row_ptr, col_idx, values, out, true,
+                          stream);
+}
+
+// ------------------------------------------------------------------ plans
+}  // extern "C"
+
+struct qftc_plan {
+  Scratch sc;
+  int n = 0;
+  int total_rows = 0;
+  int bit_width = 8;
+  int grad_kind = 0;
+  int cols_p = 16;
+  int stages = 2;
+  int use_bulk = 1;
+  int32_t* col[2] = {nullptr, nullptr};
+  float* val[2] = {nullptr, nullptr};
+  int64_t cap[2] = {0, 0};
+  int last_flip = 0;
+};
+
+extern "C" {
+
+int qftc_plan_create(qftc_plan** out, const qftc_lion_tensor* ts, int n, int bit_width,
+                     int grad_kind, int32_t* col_idx[2], float* values[2],
+                     const int64_t capacity[2], qftc_stream_t stream) {
+  if (!out || !ts || n <= 0) return fail(QFTC_EINVAL, "plan_create: no tensors");
+  if (int rc = require_bit_width(bit_width)) return rc;
+  if (grad_kind < QFTC_GRAD_U8 || grad_kind > QFTC_GRAD_BF16)
+    return fail(QFTC_EINVAL, "plan_create: bad gradient kind");
+  if (int rc = require_device()) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<DevTensor> dts((size_t)n);
+  int64_t rows = 0;
+  int maxc = 1;
+  bool bulk = true;
+  for (int i = 0; i < n; ++i) {
+    const qftc_lion_tensor& t = ts[i];
+    if (t.rows <= 0 || t.cols <= 0)
+      return fail(QFTC_EINVAL, "lion step: empty tensor " + std::to_string(i));
+    if (t.cols > row_engine_max_cols())
+      return fail(QFTC_ENOTSUP, "lion step: cols above " + std::to_string(row_engine_max_cols()));
+    DevTensor& d = dts[(size_t)i];
+    d = DevTensor{};
+    d.rows = t.rows;
+    d.cols = t.cols;
+    d.row_base = (int32_t)rows;
+    for (int k = 0; k < 2; ++k) {
+      d.w_codes[k] = t.w_codes[k];
+      d.row_ptr[k] = t.row_ptr[k];
+      d.m_codes[k] = t.m_codes[k];
+      d.m_scale[k] = t.m_scale[k];
+      d.m_zp[k] = t.m_zero_point[k];
+      bulk = bulk && al16(t.w_codes[k]) && al16(t.m_codes[k]);
+    }
+    d.w_scale = t.w_scale;
+    d.w_zp = t.w_zero_point;
+    d.t_min = t.t_min;
+    d.t_max = t.t_max;
+    d.g_codes = t.g_codes;
+    d.g_scale = t.g_scale;
+    d.g_zp = t.g_zero_point;
+    d.g_raw = t.g_raw;
+    if (grad_kind == QFTC_GRAD_U8) {
+      if (!t.g_codes || !t.g_scale || !t.g_zero_point)
+        return fail(QFTC_EINVAL, "lion step: gradient codes/params missing");
+      bulk = bulk && al16(t.g_codes);
+    } else {
+      if (!t.g_raw) return fail(QFTC_EINVAL, "lion step: raw gradient missing");
+      bulk = bulk && al16(t.g_raw);
+    }
+    bulk = bulk && (t.cols % 16 == 0);
+    rows += t.rows;
+    if (t.cols > maxc) maxc = t.cols;
+  }
+  if (rows > 0x7fffffff) return fail(QFTC_ENOTSUP, "plan: more than 2^31 rows");
+  auto* p = new qftc_plan;
+  int rc = scratch_alloc(p->sc, rows, n, st);
+  if (rc) {
+    delete p;
+    return rc;
+  }
+  cudaError_t e = cudaMemcpyAsync(p->sc.tensors, dts.data(), sizeof(DevTensor) * (size_t)n,
+                                  cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    cudaFree(p->sc.base);
+    delete p;
+    return cuda_fail(e, "plan upload");
+  }
+  p->n = n;
+  p->total_rows = (int)rows;
+  p->bit_width = bit_width;
+  p->grad_kind = grad_kind;
+  p->cols_p = (maxc + 15) & ~15;
+  p->use_bulk = bulk ? 1 : 0;
+  p->stages = pick_stages(MODE_STEP, grad_kind, p->cols_p);
+  for (int k = 0; k < 2; ++k) {
+    p->col[k] = col_idx ? col_idx[k] : nullptr;
+    p->val[k] = values ? values[k] : nullptr;
+    p->cap[k] = capacity ? capacity[k] : 0;
+  }
+  *out = p;
+  return QFTC_OK;
+}
+
+int qftc_plan_set_arena(qftc_plan* p, int32_t* col_idx[2], float* values[2],
+                        const int64_t capacity[2]) {
+  if (!p) return fail(QFTC_EINVAL, "plan: null");
+  for (int k = 0; k < 2; ++k) {
+    p->col[k] = col_idx[k];
+    p->val[k] = values[k];
+    p->cap[k] = capacity[k];
+  }
+  return QFTC_OK;
+}
+
+int qftc_plan_step(qftc_plan* p, int flip, qftc_lion_hyper h, qftc_stream_t stream) {
+  if (!p) return fail(QFTC_EINVAL, "plan: null");
+  if (flip != 0 && flip != 1) return fail(QFTC_EINVAL, "plan_step: flip must be 0 or 1");
+  LaunchArgs a{};
+  a.tensors = p->sc.tensors;
+  a.n_tensors = p->n;
+  a.total_rows = p->total_rows;
+  a.flip = flip;
+  a.bit_width = p->bit_width;
+  a.lr = h.lr;
+  a.b1 = h.beta1;
+  a.b2 = h.beta2;
+  a.wd = h.weight_decay;
+  a.col_in = p->col[flip];
+  a.val_in = p->val[flip];
+  a.col_out = p->col[1 - flip];
+  a.val_out = p->val[1 - flip];
+  a.cap_out = p->cap[1 - flip];
+  a.hdr = p->sc.hdr;
+  a.status = p->sc.status;
+  a.cols_p = p->cols_p;
+  a.stages = p->stages;
+  a.use_bulk = p->use_bulk;
+  p->last_flip = flip;
+  QFTC_CUDA(launch_row_engine(MODE_STEP, p->grad_kind, a, (cudaStream_t)stream, nullptr),
+            "lion step kernel");
+  return QFTC_OK;
+}
+
+int qftc_plan_result(qftc_plan* p, int64_t* nnz_total, qftc_stream_t stream) {
+  if (!p) return fail(QFTC_EINVAL, "plan: null");
+  cudaStream_t st = (cudaStream_t)stream;
+  Header h{};
+  if (int rc = read_header(p->sc.hdr, &h, st)) return rc;
+  if (nnz_total) *nnz_total = h.total_nnz;
+  // clear the sticky flags for the next check
+  QFTC_CUDA(cudaMemsetAsync(&p->sc.hdr->overflow, 0, 8, st), "clear flags");
+  QFTC_CUDA(cudaStreamSynchronize(st), "sync");
+  if (h.err & ERR_MPARAMS)
+    return fail(QFTC_EINVAL, "affine_params_from_bounds: min > max in momentum channel");
+  if (h.err & ERR_GPARAMS)
+    return fail(QFTC_EINVAL, "affine_params_from_bounds: min > max in gradient channel");
+  if (h.err & ERR_PREFIX) return fail(QFTC_ENOTSUP, "lion step: nnz above 2^30");
+  if (h.overflow)
+    return fail(QFTC_EOVERFLOW, "lion step: new nnz " + std::to_string(h.total_nnz) +
+                                    " exceeds the CSR arena capacity");
+  return QFTC_OK;
+}
+
+int qftc_plan_launches(const qftc_plan* p) { return p ? 1 : 0; }
+
+int qftc_plan_destroy(qftc_plan* p) {
+  if (!p) return QFTC_OK;
+  cudaFree(p->sc.base);
+  delete p;
+  return QFTC_OK;
+}
+
+int qftc_lion_step(int rows, int cols, int bit_width, const uint8_t* g_codes,
+                   const float* g_scale, const int32_t* g_zp, const uint8_t* m_codes,
+                   const float* m_scale, const int32_t* m_zp, const uint8_t* w_codes,
+                   const float* w_scale, const int32_t* w_zp, const float* t_min,
+                   const float* t_max, const int32_t* row_ptr, const int32_t* col_idx,
+                   const float* values, uint8_t* m_codes_out, float* m_scale_out,
+                   int32_t* m_zp_out, uint8_t* w_codes_out, int32_t* row_ptr_out,
+                   int32_t* col_idx_out, float* values_out, int64_t capacity,
+                   qftc_lion_hyper hyper, int64_t* nnz_host, qftc_stream_t stream) {
+  qftc_lion_tensor t{};
+  t.rows = rows;
+  t.cols = cols;
+  t.w_codes[0] = const_cast<uint8_t*>(w_codes);
+  t.w_codes[1] = w_codes_out;
+  t.row_ptr[0] = const_cast<int32_t*>(row_ptr);
+  t.row_ptr[1] = row_ptr_out;
+  t.w_scale = w_scale;
+  t.w_zero_point = w_zp;
+  t.t_min = t_min;
+  t.t_max = t_max;
+  t.m_codes[0] = const_cast<uint8_t*>(m_codes);
+  t.m_codes[1] = m_codes_out;
+  t.m_scale[0] = const_cast<float*>(m_scale);
+  t.m_scale[1] = m_scale_out;
+  t.m_zero_point[0] = const_cast<int32_t*>(m_zp);
+  t.m_zero_point[1] = m_zp_out;
+  t.g_codes = g_codes;
+  t.g_scale = g_scale;
+  t.g_zero_point = g_zp;
+  int32_t* cols_arr[2] = {const_cast<int32_t*>(col_idx), col_idx_out};
+  float* vals_arr[2] = {const_cast<float*>(values), values_out};
+  const int64_t caps[2] = {0, capacity};
+  qftc_plan* p = nullptr;
+  int rc = qftc_plan_create(&p, &t, 1, bit_width, QFTC_GRAD_U8, cols_arr, vals_arr, caps, stream);
+  if (rc) return rc;
+  rc = qftc_plan_step(p, 0, hyper, stream);
+  if (!rc) rc = qftc_plan_result(p, nnz_host, stream);
+  qftc_plan_destroy(p);
+  return rc;
+}
+
+int qftc_lion_apply(float* w, float* m, const float* g, int64_t n, qftc_lion_hyper h,
+                    qftc_stream_t stream) {
+  if (n < 0) return fail(QFTC_EINVAL, "lion_apply: negative size");
+  if (n == 0) return QFTC_OK;
+  if (int rc = require_device()) return rc;
+  QFTC_CUDA(launch_lion_apply(w, m, g, n, h.lr, h.beta1, h.beta2, h.weight_decay,
+                              (cudaStream_t)stream),
+            "lion_apply");
+  return QFTC_OK;
+}
+
+int qftc_synth(float* out, int64_t n, uint64_t seed, double sigma, double spike_p,
+               qftc_stream_t stream) {
+  if (n <= 0) return QFTC_OK;
+  if (int rc = require_device()) return rc;
+  QFTC_CUDA(launch_synth(out, n, seed, sigma, spike_p, (cudaStream_t)stream), "synth");
+  return QFTC_OK;
+}
+
+}  // extern "C"

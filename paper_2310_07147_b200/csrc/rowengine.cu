@@ -1,0 +1,841 @@
+// rowengine.cu -- the fused per-row kernels of the QFT update path (sm_100a).
+//
+// One persistent, warp-specialised kernel template serves four modes:
+//   MODE_STEP        fused quantized Lion step  == lion_step_quantized body,
+//                    optimizer.hpp:103-118 (dequant g,m,w -> lion_apply ->
+//                    quantize_state(m) -> requantize_weight(w))
+//   MODE_DECOMPOSE   decompose_dense_sparse     (quantize.hpp:253-290)
+//   MODE_RECON_F32   reconstruct                (quantize.hpp:331-338)
+//   MODE_RECON_BF16  reconstruct -> bf16 for the next forward (network.hpp:208-211)
+//
+// CTA = 1 producer warp + 4 consumer warps.  The unit of work is one ROW
+// (= one output channel: every per-channel quantity -- scales, zero points,
+// thresholds, the m' min/max and the CSR segment -- is row-local).  Rows are
+// handed out by an atomic ticket in global row order across all tensors of the
+// launch (a grouped launch covers a whole model).
+//
+// Producer warp, running up to S stages ahead of the consumers:
+//   ticket -> tensor lookup -> per-row context (params, thresholds, pointers)
+//   -> old CSR segment into a smem bitmap + (col,val) list
+//   -> TMA 1-D bulk copies (cp.async.bulk, SASS UBLKCP) of the row's w/m/g codes
+//      into the stage, completion counted on the stage's mbarrier.
+// Consumer warps (128 threads, 16 elements = one 16-byte vector per thread-step):
+//   pass 1: dequant g,m,w (+old outlier patch) -> Lion (packed FP32x2, no FMA)
+//           -> w' classify / quantize -> dense W codes straight to HBM (STG.128),
+//           m' kept in smem, m' row min/max, new-outlier masks;
+//   named barrier; m' params (fp64, as the reference); pass 2 quantizes m';
+//   warp 0 publishes the row's outlier count and runs a warp-wide decoupled
+//   look-back over the per-row status words to get the row's CSR offset;
+//   named barrier; ordered CSR write (ascending columns within the row).
+// HBM traffic per parameter (u8 gradient): read w,m,g codes (3 B) + old CSR,
+// write w,m codes (2 B) + new CSR -- nothing is read twice.
+#include <cstdio>
+
+#include "qft_device.cuh"
+#include "qft_internal.h"
+
+namespace qftk {
+using namespace qftd;
+
+constexpr int NCW = 4;             // consumer warps
+constexpr int NCT = NCW * 32;      // consumer threads
+constexpr int NT = NCT + 32;       // + producer warp
+constexpr int OLDCAP = 256;        // old CSR entries cached in smem per stage
+constexpr int NCH_MAX = 32;        // chunks of NCT*16 columns
+constexpr int MAX_COLS = NCH_MAX * NCT * 16;  // 65536
+constexpr int MAX_STAGES = 6;
+
+constexpr uint32_t FLAG_A = 1u, FLAG_P = 2u;
+constexpr uint32_t VAL_MASK = (1u << 30) - 1u;
+
+struct StageCtx {
+  int32_t row;        // launch-global row (ticket); -1 = no more work
+  int32_t lrow;       // row inside its tensor
+  int32_t cols;
+  int32_t old_begin;  // absolute arena index of the row's first old outlier
+  int32_t old_n;
+  int32_t is_last;    // lrow == rows-1
+  int32_t zw, zm;
+  float sw, tmin, tmax, sm;
+  float sg;
+  int32_t zg;
+  int32_t zpay;       // clamp(zw, 0, qmax): dense payload under an outlier
+  int32_t _p0;
+  uint8_t* w_out;     // row pointers in HBM
+  uint8_t* m_out;
+  void* aux_out;      // reconstruct output row
+  float* m_scale_out; // tensor arrays
+  int32_t* m_zp_out;
+  int32_t* row_ptr_out;
+  int64_t _p1[2];
+};
+static_assert(sizeof(StageCtx) == 128, "ctx size");
+
+__host__ __device__ inline int round16(int x) { return (x + 15) & ~15; }
+
+// stage data bytes for the mode (all sections 16-byte aligned)
+__host__ __device__ inline int stage_data_bytes(int mode, int gk, int cp) {
+  switch (mode) {
+    case MODE_STEP: return 2 * cp + (gk == G_U8 ? cp : gk == G_F32 ? 4 * cp : 2 * cp);
+    case MODE_DECOMPOSE: return 4 * cp;
+    default: return cp;
+  }
+}
+__host__ __device__ inline int old_bits_bytes(int cp) { return round16((cp + 31) / 32 * 4); }
+__host__ __device__ inline int stage_bytes(int mode, int gk, int cp) {
+  const int old = (mode == MODE_DECOMPOSE) ? 0 : OLDCAP * 8 + old_bits_bytes(cp);
+  return 128 + old + stage_data_bytes(mode, gk, cp);
+}
+struct Tabs {
+  float red_lo[2][NCW];
+  float red_hi[2][NCW];
+  int32_t red_nan[2][NCW];
+  float gred_lo[2][NCW];
+  float gred_hi[2][NCW];
+  int32_t gred_nan[2][NCW];
+  int32_t cnt[2][NCH_MAX][NCW];
+  int32_t pre[2][NCH_MAX][NCW];
+  int32_t prefix[2];
+  int32_t _pad[2];
+};
+__host__ __device__ inline int consumer_bytes(int mode, int cp) {
+  int b = (int)sizeof(Tabs);
+  if (mode == MODE_STEP) b += 4 * ((cp + NCT * 16 - 1) / (NCT * 16)) * (NCT * 16);  // m'
+  if (mode == MODE_STEP || mode == MODE_DECOMPOSE) b += round16(cp / 16 * 2);  // masks
+  return b;
+}
+size_t row_engine_smem(int mode, int gk, int cols_p, int stages) {
+  return 128 /*barriers*/ + (size_t)stages * stage_bytes(mode, gk, cols_p) +
+         consumer_bytes(mode, cols_p);
+}
+int row_engine_max_cols() { return MAX_COLS; }
+
+// ----------------------------------------------------------------------------
+// small helpers
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long pack_status(uint32_t epoch, uint32_t flag,
+                                                          uint32_t v) {
+  return ((unsigned long long)epoch << 32) | ((unsigned long long)flag << 30) | v;
+}
+
+// value of an old outlier at column `col` of the stage's row
+__device__ __noinline__ float old_value(const int32_t* old_cols, const float* old_vals, int n_old,
+                                        int old_begin, int col, const int32_t* col_in,
+                                        const float* val_in) {
+  const int nc = n_old < OLDCAP ? n_old : OLDCAP;
+  int lo = 0, hi = nc;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (old_cols[mid] < col) lo = mid + 1; else hi = mid;
+  }
+  if (lo < nc && old_cols[lo] == col) return old_vals[lo];
+  // beyond the cached prefix: search the arena in HBM
+  lo = nc;
+  hi = n_old;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (col_in[old_begin + mid] < col) lo = mid + 1; else hi = mid;
+  }
+  return val_in[old_begin + lo];
+}
+
+__device__ __forceinline__ uint32_t bits16(const uint32_t* bits, int v) {
+  return (bits[v >> 1] >> ((v & 1) * 16)) & 0xFFFFu;
+}
+
+// spread a 4-bit nibble to a byte mask (bit i -> byte i = 0xFF)
+__device__ __forceinline__ uint32_t nib_to_bytemask(uint32_t nib) {
+  return ((nib * 0x00204081u) & 0x01010101u) * 0xFFu;
+}
+
+template <int GK>
+__device__ __forceinline__ float load_graw(const uint8_t* gdata, int idx) {
+  if (GK == G_F32) return reinterpret_cast<const float*>(gdata)[idx];
+  const uint16_t b = reinterpret_cast<const uint16_t*>(gdata)[idx];
+  return __uint_as_float((uint32_t)b << 16);
+}
+
+// ----------------------------------------------------------------------------
+// the kernel
+// ----------------------------------------------------------------------------
+template <int MODE, int GK, bool ALIGNED>
+__global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + MAX_STAGES;
+  const int cp = a.cols_p;
+  const int S = a.stages;
+  const int sbytes = stage_bytes(MODE, GK, cp);
+  uint8_t* stage0 = smem + 128;
+  uint8_t* cons = stage0 + (size_t)S * sbytes;
+  Tabs* tabs = reinterpret_cast<Tabs*>(cons);
+  float* mprime = reinterpret_cast<float*>(cons + sizeof(Tabs));
+  const int mp_bytes = 4 * ((cp + NCT * 16 - 1) / (NCT * 16)) * (NCT * 16);
+  uint16_t* masks = reinterpret_cast<uint16_t*>(cons + sizeof(Tabs) +
+                                                (MODE == MODE_STEP ? mp_bytes : 0));
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int qmax = (1 << a.bit_width) - 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  auto stage_ptr = [&](int s) { return stage0 + (size_t)s * sbytes; };
+  auto ctx_of = [&](uint8_t* st) { return reinterpret_cast<StageCtx*>(st); };
+  auto oldc_of = [&](uint8_t* st) { return reinterpret_cast<int32_t*>(st + 128); };
+  auto oldv_of = [&](uint8_t* st) { return reinterpret_cast<float*>(st + 128 + OLDCAP * 4); };
+  auto oldb_of = [&](uint8_t* st) {
+    return reinterpret_cast<uint32_t*>(st + 128 + OLDCAP * 8);
+  };
+  auto data_of = [&](uint8_t* st) {
+    return st + 128 + (MODE == MODE_DECOMPOSE ? 0 : OLDCAP * 8 + old_bits_bytes(cp));
+  };
+
+  if (warp == NCW) {
+    // ======================= PRODUCER WARP ===============================
+    const int in = a.flip, out = 1 - a.flip;
+    for (int it = 0;; ++it) {
+      const int s = it % S;
+      const uint32_t round = (uint32_t)(it / S);
+      mbar_wait(&empty[s], (round & 1u) ^ 1u);
+      uint8_t* st = stage_ptr(s);
+      StageCtx* cx = ctx_of(st);
+      int row = 0;
+      if (lane == 0) row = (int)atomicAdd(&a.hdr->ticket, 1u);
+      row = __shfl_sync(0xffffffffu, row, 0);
+      if (row >= a.total_rows) {
+        if (lane == 0) {
+          cx->row = -1;
+          mbar_arrive(&full[s]);
+        }
+        break;
+      }
+      int lo = 0, hi = a.n_tensors - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (a.tensors[mid].row_base <= row) lo = mid; else hi = mid - 1;
+      }
+      const DevTensor& T = a.tensors[lo];
+      const int lrow = row - T.row_base;
+      const int cols = T.cols;
+      const size_t roff = (size_t)lrow * (size_t)cols;
+      int ob = 0, on = 0;
+      if (MODE != MODE_DECOMPOSE) {
+        ob = T.row_ptr[in][lrow];
+        on = T.row_ptr[in][lrow + 1] - ob;
+      }
+      if (lane == 0) {
+        cx->row = row;
+        cx->lrow = lrow;
+        cx->cols = cols;
+        cx->old_begin = ob;
+        cx->old_n = on;
+        cx->is_last = (lrow == T.rows - 1);
+        cx->sw = T.w_scale[lrow];
+        cx->zw = T.w_zp[lrow];
+        const int32_t zw = cx->zw;
+        cx->zpay = zw < 0 ? 0 : (zw > qmax ? qmax : zw);
+        if (MODE == MODE_STEP || MODE == MODE_DECOMPOSE) {
+          cx->tmin = T.t_min[lrow];
+          cx->tmax = T.t_max[lrow];
+        }
+        if (MODE == MODE_STEP) {
+          cx->sm = T.m_scale[in][lrow];
+          cx->zm = T.m_zp[in][lrow];
+          if (GK == G_U8) {
+            cx->sg = T.g_scale[lrow];
+            cx->zg = T.g_zp[lrow];
+          }
+          cx->m_out = T.m_codes[out] + roff;
+          cx->m_scale_out = T.m_scale[out];
+          cx->m_zp_out = T.m_zp[out];
+        }
+        if (MODE == MODE_STEP || MODE == MODE_DECOMPOSE) {
+          cx->w_out = T.w_codes[MODE == MODE_STEP ? out : 1] + roff;
+          cx->row_ptr_out = T.row_ptr[MODE == MODE_STEP ? out : 1];
+        }
+        if (MODE == MODE_RECON_F32)
+          cx->aux_out = reinterpret_cast<float*>(T.out) + roff;
+        if (MODE == MODE_RECON_BF16)
+          cx->aux_out = reinterpret_cast<__nv_bfloat16*>(T.out) + roff;
+      }
+      uint8_t* data = data_of(st);
+      // ---- bulk (TMA) copies of the row payload
+      uint32_t tx = 0;
+      const uint8_t* src_w = nullptr;
+      const uint8_t* src_m = nullptr;
+      const uint8_t* src_g = nullptr;
+      int gbytes = 0;
+      if (MODE == MODE_STEP) {
+        src_w = T.w_codes[in] + roff;
+        src_m = T.m_codes[in] + roff;
+        if (GK == G_U8) { src_g = T.g_codes + roff; gbytes = cols; }
+        else if (GK == G_F32) { src_g = (const uint8_t*)T.g_raw + roff * 4; gbytes = 4 * cols; }
+        else { src_g = (const uint8_t*)T.g_raw + roff * 2; gbytes = 2 * cols; }
+        tx = 2u * cols + gbytes;
+      } else if (MODE == MODE_DECOMPOSE) {
+        src_w = reinterpret_cast<const uint8_t*>(T.w_f32 + roff);
+        tx = 4u * cols;
+      } else {
+        src_w = T.w_codes[in] + roff;
+        tx = cols;
+      }
+      if (ALIGNED) {
+        if (lane == 0) {
+          mbar_expect_tx(&full[s], tx);
+          if (MODE == MODE_STEP) {
+            bulk_g2s(data, src_w, cols, &full[s]);
+            bulk_g2s(data + cp, src_m, cols, &full[s]);
+            bulk_g2s(data + 2 * cp, src_g, gbytes, &full[s]);
+          } else {
+            bulk_g2s(data, src_w, tx, &full[s]);
+          }
+        }
+      }
+      // ---- old CSR segment -> bitmap + cached (col,val) list
+      if (MODE != MODE_DECOMPOSE) {
+        int32_t* oc = oldc_of(st);
+        float* ov = oldv_of(st);
+        uint32_t* bits = oldb_of(st);
+        const int nw = (cp + 31) / 32;
+        for (int i = lane; i < nw; i += 32) bits[i] = 0u;
+        __syncwarp();
+        for (int i = lane; i < on; i += 32) {
+          const int col = a.col_in[ob + i];
+          if (i < OLDCAP) {
+            oc[i] = col;
+            ov[i] = a.val_in[ob + i];
+          }
+          atomicOr(&bits[col >> 5], 1u << (col & 31));
+        }
+      }
+      if (!ALIGNED) {
+        // generic path (rows not 16-byte aligned): the producer lanes copy
+        if (MODE == MODE_STEP) {
+          for (int i = lane; i < cols; i += 32) {
+            data[i] = src_w[i];
+            data[cp + i] = src_m[i];
+          }
+          for (int i = lane; i < gbytes; i += 32) data[2 * cp + i] = src_g[i];
+        } else {
+          for (int i = lane; i < (int)tx; i += 32) data[i] = src_w[i];
+        }
+      }
+      // single arrival (release) after every lane's ctx/bitmap/list stores; the
+      // phase completes once the bulk-copy bytes have landed as well.
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[s]);
+    }
+  } else {
+    // ======================= CONSUMER WARPS ==============================
+    const int ct = threadIdx.x;  // 0..127
+    const int cw = warp;
+    Hyper h;
+    h.lr = a.lr; h.b1 = a.b1; h.b2 = a.b2; h.wd = a.wd;
+    h.c1 = __fsub_rn(1.0f, a.b1);
+    h.c2 = __fsub_rn(1.0f, a.b2);
+    const uint32_t epoch = *(volatile uint32_t*)&a.hdr->epoch;
+
+    for (int it = 0;; ++it) {
+      const int s = it % S;
+      const uint32_t round = (uint32_t)(it / S);
+      const int par = it & 1;
+      mbar_wait(&full[s], round & 1u);
+      uint8_t* st = stage_ptr(s);
+      const StageCtx* cx = ctx_of(st);
+      const int row = cx->row;
+      if (row < 0) break;
+      const int cols = cx->cols;
+      const int nvec = (cols + 15) >> 4;
+      const int nch = (nvec + NCT - 1) / NCT;
+      const uint8_t* data = data_of(st);
+      const uint32_t* obits = oldb_of(st);
+      const int32_t* ocols = oldc_of(st);
+      const float* ovals = oldv_of(st);
+      const int old_n = cx->old_n, old_begin = cx->old_begin;
+
+      const DequantRow dw = make_dequant_row(cx->sw, cx->zw);
+
+      if (MODE == MODE_RECON_F32 || MODE == MODE_RECON_BF16) {
+        for (int k = 0; k < nch; ++k) {
+          const int v = k * NCT + ct;
+          if (v >= nvec) break;
+          const uint4 wq = *reinterpret_cast<const uint4*>(data + v * 16);
+          float w[16];
+          dequant4(wq.x, dw, w);
+          dequant4(wq.y, dw, w + 4);
+          dequant4(wq.z, dw, w + 8);
+          dequant4(wq.w, dw, w + 12);
+          const uint32_t o16 = bits16(obits, v);
+          if (o16) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              if (o16 & (1u << e))
+                w[e] = old_value(ocols, ovals, old_n, old_begin, v * 16 + e, a.col_in, a.val_in);
+          }
+          const int nvalid = min(16, cols - v * 16);
+          if (MODE == MODE_RECON_F32) {
+            float* o = reinterpret_cast<float*>(cx->aux_out) + v * 16;
+            if (ALIGNED) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                reinterpret_cast<float4*>(o)[q] =
+                    make_float4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+            } else {
+              for (int e = 0; e < nvalid; ++e) o[e] = w[e];
+            }
+          } else {
+            __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(cx->aux_out) + v * 16;
+            uint32_t pk[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const __nv_bfloat162 b2 = __floats2bfloat162_rn(w[2 * q], w[2 * q + 1]);
+              pk[q] = *reinterpret_cast<const uint32_t*>(&b2);
+            }
+            if (ALIGNED) {
+              reinterpret_cast<uint4*>(o)[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+              reinterpret_cast<uint4*>(o)[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            } else {
+              for (int e = 0; e < nvalid; ++e)
+                reinterpret_cast<uint16_t*>(o)[e] = (uint16_t)(pk[e >> 1] >> ((e & 1) * 16));
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        continue;
+      }
+
+      // ---------------- STEP / DECOMPOSE ----------------
+      QuantRow qw;
+      {
+        // dense params derive from the cached thresholds (requantize_weight ->
+        // decompose_dense_sparse -> affine_params_from_bounds); the host keeps
+        // (w_scale, w_zp) == affine_params_from_bounds(t_min, t_max).
+        qw = make_quant_row(cx->sw, cx->zw, a.bit_width);
+      }
+      const float tmin = cx->tmin, tmax = cx->tmax;
+      const uint32_t zpay4 = (uint32_t)cx->zpay * 0x01010101u;
+      DequantRow dm, dg;
+      QuantRow qg;
+      if (MODE == MODE_STEP) {
+        dm = make_dequant_row(cx->sm, cx->zm);
+        if (GK == G_U8) dg = make_dequant_row(cx->sg, cx->zg);
+      }
+
+      // ---- raw-gradient modes: fused quantize_state(g) -> dequantize(g)
+      if (MODE == MODE_STEP && GK != G_U8) {
+        float lo = __int_as_float(0x7f800000), hi = __int_as_float(0xff800000);
+        int nan0 = 0;
+        const uint8_t* gd = data + 2 * cp;
+        for (int k = 0; k < nch; ++k) {
+          const int v = k * NCT + ct;
+          if (v < nvec) {
+            const int nvalid = min(16, cols - v * 16);
+            for (int e = 0; e < nvalid; ++e) {
+              const float x = load_graw<GK>(gd, v * 16 + e);
+              lo = fminf(lo, x);
+              hi = fmaxf(hi, x);
+            }
+            if (v == 0 && isnan(load_graw<GK>(gd, 0))) nan0 = 1;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+          hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+          nan0 |= __shfl_xor_sync(0xffffffffu, nan0, o);
+        }
+        if (lane == 0) {
+          tabs->gred_lo[par][cw] = lo;
+          tabs->gred_hi[par][cw] = hi;
+          tabs->gred_nan[par][cw] = nan0;
+        }
+        named_bar_sync(3, NCT);
+        lo = tabs->gred_lo[par][0]; hi = tabs->gred_hi[par][0]; nan0 = tabs->gred_nan[par][0];
+#pragma unroll
+        for (int w2 = 1; w2 < NCW; ++w2) {
+          lo = fminf(lo, tabs->gred_lo[par][w2]);
+          hi = fmaxf(hi, tabs->gred_hi[par][w2]);
+          nan0 |= tabs->gred_nan[par][w2];
+        }
+        if (nan0) lo = hi = __int_as_float(0x7fc00000);
+        float sgv; int32_t zgv;
+        if (!affine_from_bounds(lo, hi, a.bit_width, sgv, zgv)) {
+          if (ct == 0) atomicOr(&a.hdr->err, ERR_GPARAMS);
+          sgv = 1.0f; zgv = 0;
+        }
+        qg = make_quant_row(sgv, zgv, a.bit_width);
+        dg = make_dequant_row(sgv, zgv);
+      }
+
+      float mlo = __int_as_float(0x7f800000), mhi = __int_as_float(0xff800000);
+      int mnan0 = 0;
+
+      // ================= pass 1 =================
+      for (int k = 0; k < nch; ++k) {
+        const int v = k * NCT + ct;
+        uint32_t mask = 0;
+        if (v < nvec) {
+          const int nvalid = min(16, cols - v * 16);
+          const uint32_t valid = nvalid >= 16 ? 0xFFFFu : ((1u << nvalid) - 1u);
+          float w[16];
+          if (MODE == MODE_DECOMPOSE) {
+            const float4* src = reinterpret_cast<const float4*>(data + v * 64);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 f = src[q];
+              w[4 * q] = f.x; w[4 * q + 1] = f.y; w[4 * q + 2] = f.z; w[4 * q + 3] = f.w;
+            }
+          } else {
+            float m[16], g[16];
+            const uint4 wq = *reinterpret_cast<const uint4*>(data + v * 16);
+            const uint4 mq = *reinterpret_cast<const uint4*>(data + cp + v * 16);
+            dequant4(wq.x, dw, w); dequant4(wq.y, dw, w + 4);
+            dequant4(wq.z, dw, w + 8); dequant4(wq.w, dw, w + 12);
+            dequant4(mq.x, dm, m); dequant4(mq.y, dm, m + 4);
+            dequant4(mq.z, dm, m + 8); dequant4(mq.w, dm, m + 12);
+            if (GK == G_U8) {
+              const uint4 gq = *reinterpret_cast<const uint4*>(data + 2 * cp + v * 16);
+              dequant4(gq.x, dg, g); dequant4(gq.y, dg, g + 4);
+              dequant4(gq.z, dg, g + 8); dequant4(gq.w, dg, g + 12);
+            } else {
+              float graw[16];
+#pragma unroll
+              for (int e = 0; e < 16; ++e)
+                graw[e] = (e < nvalid) ? load_graw<GK>(data + 2 * cp, v * 16 + e) : 0.0f;
+              float em = 0.0f;
+              uint32_t gc[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) gc[q] = quant4_fast(graw + 4 * q, qg, em);
+              if (!qg.fast || !(em < qg.thr)) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) gc[q] = quant4_exact(graw + 4 * q, qg);
+              }
+#pragma unroll
+              for (int q = 0; q < 4; ++q) dequant4(gc[q], dg, g + 4 * q);
+            }
+            const uint32_t o16 = bits16(obits, v);
+            if (o16) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e)
+                if (o16 & (1u << e))
+                  w[e] = old_value(ocols, ovals, old_n, old_begin, v * 16 + e, a.col_in,
+                                   a.val_in);
+            }
+#pragma unroll
+            for (int p = 0; p < 8; ++p) {
+              float2 W = make_float2(w[2 * p], w[2 * p + 1]);
+              float2 M = make_float2(m[2 * p], m[2 * p + 1]);
+              lion2(W, M, make_float2(g[2 * p], g[2 * p + 1]), h);
+              w[2 * p] = W.x; w[2 * p + 1] = W.y;
+              m[2 * p] = M.x; m[2 * p + 1] = M.y;
+            }
+            if (v == 0 && isnan(m[0])) mnan0 = 1;
+            if (valid != 0xFFFFu) {
+#pragma unroll
+              for (int e = 1; e < 16; ++e)
+                if (!(valid & (1u << e))) m[e] = m[0];
+            }
+#pragma unroll
+            for (int p = 0; p < 8; ++p) {
+              float t;
+              asm("min.f32 %0, %1, %2, %3;" : "=f"(t) : "f"(mlo), "f"(m[2 * p]), "f"(m[2 * p + 1]));
+              mlo = t;
+              asm("max.f32 %0, %1, %2, %3;" : "=f"(t) : "f"(mhi), "f"(m[2 * p]), "f"(m[2 * p + 1]));
+              mhi = t;
+            }
+            float4* mp = reinterpret_cast<float4*>(mprime);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              mp[(k * 4 + q) * NCT + ct] =
+                  make_float4(m[4 * q], m[4 * q + 1], m[4 * q + 2], m[4 * q + 3]);
+          }
+          // ---- classify + quantize w'
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            mask |= ((w[e] < tmin) || (w[e] > tmax)) ? (1u << e) : 0u;
+          mask &= valid;
+          float em = 0.0f;
+          uint32_t c[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) c[q] = quant4_fast(w + 4 * q, qw, em);
+          if (!qw.fast || !(em < qw.thr)) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) c[q] = quant4_exact(w + 4 * q, qw);
+          }
+          if (mask) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint32_t bm = nib_to_bytemask((mask >> (4 * q)) & 0xFu);
+              c[q] = (c[q] & ~bm) | (zpay4 & bm);
+            }
+          }
+          uint8_t* wo = cx->w_out + v * 16;
+          if (ALIGNED) {
+            *reinterpret_cast<uint4*>(wo) = make_uint4(c[0], c[1], c[2], c[3]);
+          } else {
+            for (int e = 0; e < nvalid; ++e) wo[e] = (uint8_t)(c[e >> 2] >> ((e & 3) * 8));
+          }
+          masks[v] = (uint16_t)mask;
+        }
+        const int wc = __reduce_add_sync(0xffffffffu, __popc(mask));
+        if (lane == 0) tabs->cnt[par][k][cw] = wc;
+      }
+
+      // ================= row reduction =================
+      if (MODE == MODE_STEP) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          mlo = fminf(mlo, __shfl_xor_sync(0xffffffffu, mlo, o));
+          mhi = fmaxf(mhi, __shfl_xor_sync(0xffffffffu, mhi, o));
+          mnan0 |= __shfl_xor_sync(0xffffffffu, mnan0, o);
+        }
+        if (lane == 0) {
+          tabs->red_lo[par][cw] = mlo;
+          tabs->red_hi[par][cw] = mhi;
+          tabs->red_nan[par][cw] = mnan0;
+        }
+      }
+      named_bar_sync(1, NCT);  // ---- sync C
+
+      QuantRow qm;
+      if (MODE == MODE_STEP) {
+        float lo = tabs->red_lo[par][0], hi = tabs->red_hi[par][0];
+        int nan0 = tabs->red_nan[par][0];
+#pragma unroll
+        for (int w2 = 1; w2 < NCW; ++w2) {
+          lo = fminf(lo, tabs->red_lo[par][w2]);
+          hi = fmaxf(hi, tabs->red_hi[par][w2]);
+          nan0 |= tabs->red_nan[par][w2];
+        }
+        if (nan0) lo = hi = __int_as_float(0x7fc00000);
+        float smv; int32_t zmv;
+        if (!affine_from_bounds(lo, hi, a.bit_width, smv, zmv)) {
+          if (ct == 0) atomicOr(&a.hdr->err, ERR_MPARAMS);
+          smv = 1.0f; zmv = 0;
+        }
+        qm = make_quant_row(smv, zmv, a.bit_width);
+        if (ct == 0) {
+          cx->m_scale_out[cx->lrow] = smv;
+          cx->m_zp_out[cx->lrow] = zmv;
+        }
+      }
+
+      if (cw == 0) {
+        // ---- per-(chunk,warp) exclusive prefix table + row total
+        const int ne = nch * NCW;
+        int loc[4];
+        int sum = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int e = lane * 4 + j;
+          loc[j] = (e < ne) ? tabs->cnt[par][e / NCW][e % NCW] : 0;
+          sum += loc[j];
+        }
+        int incl = sum;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, incl, d);
+          if (lane >= d) incl += t;
+        }
+        const uint32_t total = (uint32_t)__shfl_sync(0xffffffffu, incl, 31);
+        int run = incl - sum;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int e = lane * 4 + j;
+          if (e < ne) tabs->pre[par][e / NCW][e % NCW] = run;
+          run += loc[j];
+        }
+        // ---- decoupled look-back over the per-row status words
+        uint32_t excl = 0;
+        if (row > 0) {
+          if (lane == 0) st_relaxed_u64(a.status + row, pack_status(epoch, FLAG_A, total));
+          int base = row - 1;
+          while (true) {
+            const int idx = base - lane;
+            uint32_t flag = FLAG_P, val = 0;
+            if (idx >= 0) {
+              const unsigned long long wd = ld_relaxed_u64(a.status + idx);
+              flag = ((uint32_t)(wd >> 32) == epoch) ? (uint32_t)(wd >> 30) & 3u : 0u;
+              val = (uint32_t)wd & VAL_MASK;
+            }
+            const uint32_t pm = __ballot_sync(0xffffffffu, flag == FLAG_P);
+            const uint32_t nm = __ballot_sync(0xffffffffu, flag == 0u);
+            const int lim = pm ? __ffs(pm) - 1 : 31;
+            const uint32_t need = (lim >= 31) ? 0xffffffffu : ((2u << lim) - 1u);
+            if (nm & need) {
+              __nanosleep(32);
+              continue;
+            }
+            excl += __reduce_add_sync(0xffffffffu, lane <= lim ? val : 0u);
+            if (pm) break;
+            base -= 32;
+          }
+        }
+        const uint32_t inclusive = excl + total;
+        if (lane == 0) {
+          st_relaxed_u64(a.status + row, pack_status(epoch, FLAG_P, inclusive & VAL_MASK));
+          if (inclusive > VAL_MASK) atomicOr(&a.hdr->err, ERR_PREFIX);
+          tabs->prefix[par] = (int32_t)excl;
+          cx->row_ptr_out[cx->lrow] = (int32_t)excl;
+          if (cx->is_last) cx->row_ptr_out[cx->lrow + 1] = (int32_t)inclusive;
+          if (row == a.total_rows - 1) {
+            a.hdr->total_nnz = (int64_t)inclusive;
+            if ((int64_t)inclusive > a.cap_out) atomicOr(&a.hdr->overflow, 1u);
+          }
+        }
+      }
+
+      // ================= pass 2: quantize m' with the fresh row params =================
+      if (MODE == MODE_STEP) {
+        const float4* mp = reinterpret_cast<const float4*>(mprime);
+        for (int k = 0; k < nch; ++k) {
+          const int v = k * NCT + ct;
+          if (v >= nvec) break;
+          float m[16];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float4 f = mp[(k * 4 + q) * NCT + ct];
+            m[4 * q] = f.x; m[4 * q + 1] = f.y; m[4 * q + 2] = f.z; m[4 * q + 3] = f.w;
+          }
+          float em = 0.0f;
+          uint32_t c[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) c[q] = quant4_fast(m + 4 * q, qm, em);
+          if (!qm.fast || !(em < qm.thr)) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) c[q] = quant4_exact(m + 4 * q, qm);
+          }
+          uint8_t* mo = cx->m_out + v * 16;
+          if (ALIGNED) {
+            *reinterpret_cast<uint4*>(mo) = make_uint4(c[0], c[1], c[2], c[3]);
+          } else {
+            const int nvalid = min(16, cols - v * 16);
+            for (int e = 0; e < nvalid; ++e) mo[e] = (uint8_t)(c[e >> 2] >> ((e & 3) * 8));
+          }
+        }
+      }
+
+      named_bar_sync(2, NCT);  // ---- sync D: row CSR offset known
+
+      // ================= ordered CSR write =================
+      {
+        const int prefix = tabs->prefix[par];
+        for (int k = 0; k < nch; ++k) {
+          if (tabs->cnt[par][k][cw] == 0) continue;  // warp-uniform
+          const int v = k * NCT + ct;
+          uint32_t mask = (v < nvec) ? (uint32_t)masks[v] : 0u;
+          const int c = __popc(mask);
+          int incl = c;
+#pragma unroll
+          for (int d = 1; d < 32; d <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += t;
+          }
+          int pos = prefix + tabs->pre[par][k][cw] + incl - c;
+          while (mask) {
+            const int e = __ffs(mask) - 1;
+            mask &= mask - 1u;
+            const int col = v * 16 + e;
+            float val;
+            if (MODE == MODE_DECOMPOSE) {
+              val = reinterpret_cast<const float*>(data)[col];
+            } else {
+              // recompute w' for this element exactly as pass 1 did
+              float wv = (dw.fast)
+                             ? __fmul_rn(__fadd_rn(magic_byte(data[col], 0), dw.negc), dw.s)
+                             : dequant_exact(data[col], dw.s, dw.z);
+              if (bits16(obits, v) & (1u << e))
+                wv = old_value(ocols, ovals, old_n, old_begin, col, a.col_in, a.val_in);
+              const uint32_t mc = data[cp + col];
+              float mv = dm.fast ? __fmul_rn(__fadd_rn(magic_byte(mc, 0), dm.negc), dm.s)
+                                 : dequant_exact(mc, dm.s, dm.z);
+              float gv;
+              if (GK == G_U8) {
+                const uint32_t gc = data[2 * cp + col];
+                gv = dg.fast ? __fmul_rn(__fadd_rn(magic_byte(gc, 0), dg.negc), dg.s)
+                             : dequant_exact(gc, dg.s, dg.z);
+              } else {
+                const float gr = load_graw<GK>(data + 2 * cp, col);
+                const uint32_t gc = quant_exact(gr, qg.s, qg.z, qg.qmax);
+                gv = dg.fast ? __fmul_rn(__fadd_rn(magic_byte(gc, 0), dg.negc), dg.s)
+                             : dequant_exact(gc, dg.s, dg.z);
+              }
+              lion1(wv, mv, gv, h);
+              val = wv;
+            }
+            if (pos < a.cap_out) {
+              a.col_out[pos] = col;
+              a.val_out[pos] = val;
+            }
+            ++pos;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+  }
+
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t prev = atomicAdd(&a.hdr->done, 1u);
+    if (prev == gridDim.x - 1) {
+      a.hdr->ticket = 0u;
+      a.hdr->done = 0u;
+      a.hdr->epoch = a.hdr->epoch + 1u;
+      __threadfence();
+    }
+  }
+}
+
+// ----------------------------------------------------------------------------
+// host-side launcher
+// ----------------------------------------------------------------------------
+template <int MODE, int GK, bool AL>
+static cudaError_t launch_t(const LaunchArgs& a, size_t smem, cudaStream_t st, int* grid_out) {
+  auto k = row_engine_kernel<MODE, GK, AL>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  int grid = sms * per_sm;
+  if (grid > a.total_rows) grid = a.total_rows;
+  if (grid < 1) grid = 1;
+  k<<<grid, NT, smem, st>>>(a);
+  if (grid_out) *grid_out = grid;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_row_engine(int mode, int gk, const LaunchArgs& a, cudaStream_t st,
+                              int* grid_out) {
+  const size_t smem = row_engine_smem(mode, gk, a.cols_p, a.stages);
+  const bool al = a.use_bulk != 0;
+#define QFT_L(M, G)                                                            \
+  return al ? launch_t<M, G, true>(a, smem, st, grid_out)                      \
+            : launch_t<M, G, false>(a, smem, st, grid_out)
+  switch (mode) {
+    case MODE_STEP:
+      if (gk == G_U8) QFT_L(MODE_STEP, G_U8);
+      if (gk == G_F32) QFT_L(MODE_STEP, G_F32);
+      QFT_L(MODE_STEP, G_BF16);
+    case MODE_DECOMPOSE: QFT_L(MODE_DECOMPOSE, G_U8);
+    case MODE_RECON_F32: QFT_L(MODE_RECON_F32, G_U8);
+    default: QFT_L(MODE_RECON_BF16, G_U8);
+  }
+#undef QFT_L
+}
+
+}  // namespace qftk

@@ -1,0 +1,77 @@
+"""CPU: the C-ABI library loads, exports every entry point include/qft_b200.h
+declares, validates arguments in the reference's order, and -- on a host with
+no GPU -- refuses compute calls instead of falling back to the CPU."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "qft_b200.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(qftc_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_path():
+    names = declared_functions()
+    for must in ("qftc_quantize_state", "qftc_dequantize", "qftc_outlier_thresholds",
+                 "qftc_decompose_dense_sparse", "qftc_reconstruct", "qftc_reconstruct_bf16",
+                 "qftc_plan_create", "qftc_plan_step", "qftc_lion_step", "qftc_lion_apply"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2310_07147_b200 import _native as N
+    out = subprocess.run(["nm", "-D", "--defined-only", N.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r" T (qftc_\w+)", out))
+    missing = [f for f in declared_functions() if f not in exported]
+    assert not missing, f"declared but not exported: {missing}"
+    # and the ctypes binding covers exactly the declared surface
+    assert set(N.EXPORTS) == set(declared_functions())
+
+
+def test_library_is_sm100a():
+    from paper_2310_07147_b200 import _native as N
+    out = subprocess.run(["cuobjdump", "--list-elf", N.LIB_PATH], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_validation_precedes_device_check():
+    from paper_2310_07147_b200 import _native as N
+    assert N.lib.qftc_quantize_state(None, 2, 2, 9, None, None, None, 0, None) == N.QFTC_EINVAL
+    assert "bit width" in N.last_error()
+    assert N.lib.qftc_outlier_thresholds(None, 2, 2, 0.5, 0, None, None, None) == N.QFTC_EINVAL
+    assert "fraction" in N.last_error()
+    assert N.lib.qftc_dequantize(None, 0, 4, None, None, 1, None, None) == N.QFTC_EINVAL
+    with pytest.raises(ValueError):
+        N.check(N.QFTC_EINVAL)
+    with pytest.raises(IndexError):
+        N.check(N.QFTC_ERANGE)
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_no_cpu_fallback_without_gpu():
+    from paper_2310_07147_b200 import _native as N
+    rc = N.lib.qftc_synth(None, 16, 1, 1.0, 0.0, None)
+    assert rc == N.QFTC_ECUDA and "no CPU fallback" in N.last_error()
+    rc = N.lib.qftc_quantize_state(None, 2, 2, 8, None, None, None, 0, None)
+    assert rc == N.QFTC_ECUDA
+
+
+def test_gradient_stack_semantics():
+    # gradflow.hpp:15-47: FILO, pop on empty -> std::out_of_range (IndexError)
+    from paper_2310_07147_b200 import GradientStack
+    s = GradientStack()
+    with pytest.raises(IndexError):
+        s.pop()
+    s.push(2, "g2")
+    s.push(1, "g1")
+    assert s.pop().layer_index == 1 and s.pop().layer_index == 2 and s.empty()

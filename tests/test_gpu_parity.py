@@ -1,0 +1,279 @@
+"""GPU parity: every sm_100a kernel against the CPU oracle on identical inputs.
+
+Bar: codes, zero points, row_ptr, col_idx bit-exact; scales,
+thresholds, CSR values and post-step fp32 tensors bit-exact (the reference
+arithmetic is reproduced, not approximated); bf16 outputs equal the RNE of the
+oracle's fp32 value.  Calls go through the C-ABI (via the package's ctypes
+binding).
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _eq(a, b, what):
+    a, b = np.asarray(a), np.asarray(b)
+    assert a.shape == b.shape, f"{what}: shape {a.shape} vs {b.shape}"
+    if a.dtype.kind == "f":
+        bad = ~((a == b) | (np.isnan(a) & np.isnan(b)))
+    else:
+        bad = a != b
+    n = int(bad.sum())
+    assert n == 0, f"{what}: {n} mismatches, first at {np.argwhere(bad)[:5].tolist()}"
+
+
+def _rows_zoo(rng, rows, cols, bit_width=8):
+    """random rows + the edge cases the reference tests exercise"""
+    x = rng.uniform(-2, 2, size=(rows, cols)).astype(np.float32)
+    x[0] = 0.0                                   # all-zero channel (acceptance.cpp:173-176)
+    x[1] = 3.5                                   # constant channel
+    x[2] = 1000.0 + rng.uniform(0, 1e-3, cols).astype(np.float32)   # narrow, far from zero
+    x[3] = -7.0 + rng.uniform(0, 1e-4, cols).astype(np.float32)     # |z| huge -> fp64 path
+    x[4] = rng.normal(0, 1, cols).astype(np.float32) * 1e-30        # tiny scale
+    if rows > 6:
+        # planted near-ties: values on (k+0.5)*s grid of the row's own params
+        lo, hi = -1.0, 1.0
+        qmax = (1 << bit_width) - 1
+        s = np.float32((hi - lo) / qmax)
+        k = rng.integers(-qmax // 2, qmax // 2, cols)
+        v = ((k + 0.5) * s.astype(np.float64)).astype(np.float32)
+        jitter = rng.integers(-2, 3, cols)
+        v = np.array([np.nextafter(a, np.float32(np.inf) if j > 0 else np.float32(-np.inf))
+                      if j else a for a, j in zip(v, jitter)], np.float32)
+        v[0], v[1] = lo, hi
+        x[5] = v
+    return x
+
+
+def test_synth_device_matches_host(cuda, port):
+    for seed, sig, sp in [(1234, 0.02, 0.005), (7, 1e-3, 0.0), (99, 1.0, 0.5)]:
+        d = _np(cuda.synth((37, 129), seed, sig, sp))
+        h = port.synth((37, 129), seed, sig, sp)
+        _eq(d, h, f"synth seed {seed}")
+
+
+@pytest.mark.parametrize("bw", [2, 3, 4, 8])
+@pytest.mark.parametrize("shape", [(64, 256), (33, 100), (7, 4096), (9, 3)])
+def test_quantize_state_bitexact(cuda, port, bw, shape):
+    rng = np.random.default_rng(bw * 1000 + shape[1])
+    x = _rows_zoo(rng, *shape, bit_width=bw) if shape[0] > 5 else \
+        rng.normal(size=shape).astype(np.float32)
+    q = cuda.quantize_state(torch.from_numpy(x).cuda(), bw)
+    cq, cs, cz = port.quantize_state(x, bw)
+    _eq(_np(q.params.scale), cs, "scale")
+    _eq(_np(q.params.zero_point), cz, "zero_point")
+    _eq(_np(q.data), cq, "codes")
+    # dequantize f32 and bf16
+    deq = cuda.dequantize(q)
+    ref = port.dequantize(cq, cs, cz)
+    _eq(_np(deq), ref, "dequantize")
+    b16 = cuda.dequantize(q, torch.bfloat16)
+    _eq(_np(b16.float()), _np(torch.from_numpy(ref).to(torch.bfloat16).float()), "dequant bf16")
+
+
+@pytest.mark.parametrize("bw", [2, 4, 8])
+def test_quantize_given_params_ties(cuda, port, bw):
+    """half-away rounding on planted exact ties and +-1..3 ulp neighbours (test_quantize.cpp:102-114)"""
+    rng = np.random.default_rng(bw)
+    rows, cols = 16, 512
+    qmax = (1 << bw) - 1
+    scale = rng.uniform(1e-3, 2.0, rows).astype(np.float32)
+    zp = rng.integers(-3, qmax + 3, rows).astype(np.int32)
+    zp[0] = 3_000_000     # forces the exact fp64 row path (|z| >= 2^21)
+    x = np.empty((rows, cols), np.float32)
+    for r in range(rows):
+        k = rng.integers(-zp[r] - 2, qmax - zp[r] + 2, cols).astype(np.float64)
+        v = ((k + 0.5) * np.float64(scale[r])).astype(np.float32)
+        steps = rng.integers(-3, 4, cols)
+        for j in range(cols):
+            for _ in range(abs(int(steps[j]))):
+                v[j] = np.nextafter(v[j], np.float32(np.inf if steps[j] > 0 else -np.inf))
+        x[r] = v
+    x[1, :4] = [np.nan, np.inf, -np.inf, 0.0]
+    q = cuda.quantize(torch.from_numpy(x).cuda(),
+                      cuda.AffineParams(torch.from_numpy(scale).cuda(),
+                                        torch.from_numpy(zp).cuda(), bw))
+    _eq(_np(q.data), port.quantize(x, scale, zp, bw), "codes")
+
+
+def test_half_away_kat(cuda):
+    """test_quantize.cpp:102-114: s=1, z=128: 0.5->129, 1.5->130, -0.5->127, -1.5->126, 2.5->131"""
+    x = torch.tensor([[0.5, 1.5, -0.5, -1.5, 2.5]], device="cuda")
+    p = cuda.AffineParams(torch.tensor([1.0], device="cuda"),
+                          torch.tensor([128], dtype=torch.int32, device="cuda"), 8)
+    assert _np(cuda.quantize(x, p).data).tolist() == [[129, 130, 127, 126, 131]]
+
+
+def test_hand_params_kat(cuda):
+    """test_quantize.cpp:42-60: [-1,0,2] -> s=3/255, z=85, codes [0,85,255]"""
+    q = cuda.quantize_state(torch.tensor([[-1.0, 0.0, 2.0]], device="cuda"), 8)
+    assert _np(q.params.zero_point).tolist() == [85]
+    assert abs(float(q.params.scale[0]) - 3 / 255) < 1e-8
+    assert _np(q.data).tolist() == [[0, 85, 255]]
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("fraction", [0.0, 0.0005, 0.01, 0.05, 0.3])
+@pytest.mark.parametrize("shape", [(48, 4096), (17, 100), (5, 1), (3, 2)])
+def test_thresholds(cuda, port, kind, fraction, shape):
+    w = port.synth(shape, 11 + shape[1], 0.02, 0.005)
+    if shape[0] > 4:
+        w[4, ::3] = 0.0                           # duplicates / zeros
+    lo, hi = cuda.compute_outlier_thresholds(torch.from_numpy(w).cuda(), fraction, kind)
+    elo, ehi = port.outlier_thresholds(w, fraction, kind)
+    _eq(_np(lo), elo, "t_min")
+    _eq(_np(hi), ehi, "t_max")
+
+
+@pytest.mark.parametrize("bw", [3, 4, 8])
+@pytest.mark.parametrize("shape", [(64, 4096), (40, 11008), (13, 80), (6, 7)])
+def test_decompose_and_reconstruct(cuda, port, bw, shape):
+    w = port.synth(shape, 5 + shape[0], 0.02, 0.005)
+    dev = cuda.decompose_weight(torch.from_numpy(w).cuda(), 0.01, bw)
+    ref = port.decompose_weight(w, 0.01, bw)
+    _eq(_np(dev.t_min), ref.t_min, "t_min")
+    _eq(_np(dev.t_max), ref.t_max, "t_max")
+    _eq(_np(dev.dense.params.scale), ref.scale, "scale")
+    _eq(_np(dev.dense.params.zero_point), ref.zero_point, "zero_point")
+    _eq(_np(dev.dense.data), ref.codes, "codes")
+    _eq(_np(dev.sparse.row_ptr), ref.row_ptr, "row_ptr")
+    _eq(_np(dev.sparse.col_idx), ref.col_idx, "col_idx")
+    _eq(_np(dev.sparse.values), ref.values, "values")
+    rec = port.reconstruct(ref)
+    _eq(_np(cuda.reconstruct(dev)), rec, "reconstruct")
+    _eq(_np(cuda.reconstruct(dev, torch.bfloat16).float()),
+        _np(torch.from_numpy(rec).to(torch.bfloat16).float()), "reconstruct bf16")
+    assert cuda.byte_size(dev) == ref.byte_size()
+
+
+def test_decompose_hand_csr(cuda):
+    """test_quantize.cpp:218-235: row_ptr [0,0,1], col [1], val [100]"""
+    w = torch.tensor([[0.1, 0.2], [0.3, 100.0]], device="cuda")
+    d = cuda.decompose_dense_sparse(w, torch.tensor([0.1, 0.3]), torch.tensor([0.2, 0.4]), 8)
+    assert _np(d.sparse.row_ptr).tolist() == [0, 0, 1]
+    assert _np(d.sparse.col_idx).tolist() == [1]
+    assert _np(d.sparse.values).tolist() == [100.0]
+    assert float(cuda.reconstruct(d)[1, 1]) == 100.0
+    assert cuda.byte_size(d) == 56
+
+
+def _layer(port, shape, seed, bw, frac):
+    w = port.synth(shape, seed, 0.02, 0.005)
+    dsw = port.decompose_weight(w, frac, bw)
+    m = port.quantize_state(np.zeros(shape, np.float32), bw)
+    return dsw, m
+
+
+@pytest.mark.parametrize("bw,frac", [(8, 0.01), (4, 0.01), (3, 0.0045), (8, 0.05)])
+@pytest.mark.parametrize("shape", [(64, 4096), (24, 11008), (16, 48), (5, 13)])
+def test_lion_step_trajectory(cuda, port, bw, frac, shape):
+    """10 quantized Lion steps through the C-ABI single-layer entry, byte-compared each step
+    (exercises CSR drift: nnz moves while thresholds stay cached)."""
+    dsw, m = _layer(port, shape, 100 + shape[1], bw, frac)
+    dw = cuda.DenseSparseWeight(
+        cuda.QuantizedTensor(shape[0], shape[1], torch.from_numpy(dsw.codes).cuda(),
+                             cuda.AffineParams(torch.from_numpy(dsw.scale).cuda(),
+                                               torch.from_numpy(dsw.zero_point).cuda(), bw)),
+        cuda.SparseOutliers(torch.from_numpy(dsw.row_ptr).cuda(),
+                            torch.from_numpy(dsw.col_idx).cuda(),
+                            torch.from_numpy(dsw.values).cuda()),
+        torch.from_numpy(dsw.t_min).cuda(), torch.from_numpy(dsw.t_max).cuda(), frac)
+    st = cuda.LionState([cuda.QuantizedTensor(shape[0], shape[1], torch.from_numpy(m[0]).cuda(),
+                                              cuda.AffineParams(torch.from_numpy(m[1]).cuda(),
+                                                                torch.from_numpy(m[2]).cuda(),
+                                                                bw))])
+    h = cuda.LionHyper(lr=2e-3, beta1=0.9, beta2=0.99, weight_decay=0.01)
+    for step in range(10):
+        g = port.synth(shape, 7000 + step, 1e-2, 0.0)
+        gq = port.quantize_state(g, bw)
+        stack = cuda.GradientStack()
+        stack.push(1, cuda.QuantizedTensor(shape[0], shape[1], torch.from_numpy(gq[0]).cuda(),
+                                           cuda.AffineParams(torch.from_numpy(gq[1]).cuda(),
+                                                             torch.from_numpy(gq[2]).cuda(), bw)))
+        cuda.lion_step_quantized([dw], st, stack, h, bw)
+        dsw, m, _ = port.lion_step_layer(dsw, *m, *gq, lr=h.lr, beta1=h.beta1, beta2=h.beta2,
+                                         wd=h.weight_decay)
+        tag = f"step {step}"
+        _eq(_np(st.momentum[0].params.scale), m[1], tag + " m scale")
+        _eq(_np(st.momentum[0].params.zero_point), m[2], tag + " m zp")
+        _eq(_np(st.momentum[0].data), m[0], tag + " m codes")
+        _eq(_np(dw.dense.data), dsw.codes, tag + " w codes")
+        _eq(_np(dw.sparse.row_ptr), dsw.row_ptr, tag + " row_ptr")
+        _eq(_np(dw.sparse.col_idx), dsw.col_idx, tag + " col_idx")
+        _eq(_np(dw.sparse.values), dsw.values, tag + " values")
+
+
+def test_engine_grouped_step_matches_oracle(cuda, port):
+    """A mixed-width model (two width classes, an RMSNorm-like 1xC row) stepped by the
+    grouped persistent launch; every tensor byte-compared with the per-layer oracle."""
+    shapes = [(32, 4096), (1, 4096), (96, 1024), (16, 4096), (48, 1024)]
+    bw, frac = 8, 0.01
+    tensors, oracle_state = [], []
+    for i, sh in enumerate(shapes):
+        dsw, m = _layer(port, sh, 300 + i, bw, frac)
+        tensors.append(dict(codes=dsw.codes, scale=dsw.scale, zero_point=dsw.zero_point,
+                            t_min=dsw.t_min, t_max=dsw.t_max, row_ptr=dsw.row_ptr,
+                            col_idx=dsw.col_idx, values=dsw.values))
+        oracle_state.append([dsw, m])
+    eng = cuda.QftModelState(shapes, bit_width=bw)
+    eng.init_from_host(tensors)
+    for step in range(4):
+        for i, sh in enumerate(shapes):
+            g = port.synth(sh, 9000 + 10 * step + i, 1e-2, 0.0)
+            gq = port.quantize_state(g, bw)
+            c, s, z = eng.grad_views(i)
+            c.copy_(torch.from_numpy(gq[0]))
+            s.copy_(torch.from_numpy(gq[1]))
+            z.copy_(torch.from_numpy(gq[2]))
+            dsw, m = oracle_state[i]
+            dsw, m, _ = port.lion_step_layer(dsw, *m, *gq, lr=1e-3, wd=0.0)
+            oracle_state[i] = [dsw, m]
+        eng.step(lr=1e-3, check=True)
+        for i in range(len(shapes)):
+            got = eng.export_tensor(i)
+            dsw, m = oracle_state[i]
+            tag = f"step {step} tensor {i}"
+            _eq(got["codes"], dsw.codes, tag + " w codes")
+            _eq(got["row_ptr"], dsw.row_ptr, tag + " row_ptr")
+            _eq(got["col_idx"], dsw.col_idx, tag + " col_idx")
+            _eq(got["values"], dsw.values, tag + " values")
+            _eq(got["m_codes"], m[0], tag + " m codes")
+            _eq(got["m_scale"], m[1], tag + " m scale")
+            _eq(got["m_zero_point"], m[2], tag + " m zp")
+
+
+def test_lion_apply_passthrough_bitwise(cuda, port):
+    """QuantMode::passthrough pipeline == lion_step_reference bitwise (test_optimizer.cpp:160-187)"""
+    rng = np.random.default_rng(5)
+    w = rng.uniform(-1, 1, 10001).astype(np.float32)
+    m = np.zeros_like(w)
+    dw, dm = torch.from_numpy(w).cuda(), torch.from_numpy(m).cuda()
+    h = cuda.LionHyper(lr=3e-3, weight_decay=0.01)
+    for step in range(25):
+        g = rng.uniform(-1, 1, w.size).astype(np.float32)
+        cuda.lion_apply(dw, dm, torch.from_numpy(g).cuda(), h)
+        w, m = port.lion_apply(w, m, g, lr=3e-3, wd=0.01)
+    _eq(_np(dw), w, "w")
+    _eq(_np(dm), m, "m")
+
+
+def test_validation_errors(cuda):
+    with pytest.raises(ValueError):
+        cuda.quantize_state(torch.zeros(2, 2, device="cuda"), 9)
+    with pytest.raises(ValueError):
+        cuda.compute_outlier_thresholds(torch.zeros(2, 2, device="cuda"), 0.5)
+    with pytest.raises(ValueError):
+        cuda.decompose_dense_sparse(torch.zeros(2, 2, device="cuda"), torch.tensor([1.0, 0.0]),
+                                    torch.tensor([0.0, 0.0]))
+    with pytest.raises(IndexError):
+        cuda.GradientStack().pop()
+    x = torch.zeros(2, 2, device="cuda")
+    x[0, 0] = float("nan")      # NaN in column 0 sticks as the bound -> min > max
+    with pytest.raises(ValueError):
+        cuda.quantize_state(x, 8)
