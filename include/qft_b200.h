@@ -121,15 +121,26 @@ typedef struct {
  * Ping-pong state: a step with flip=f reads set [f] and writes set [1-f]; the
  * caller swaps its view after the step.  The weight's dense params and
  * thresholds are fixed between refreshes (requantize_weight, quantize.hpp:318-329)
- * and are read-only here.  row_ptr[k] holds ABSOLUTE offsets into the plan's CSR
- * arena k.  The gradient is the GradientStack entry (u8 codes + per-row params,
+ * and are read-only here.
+ *
+ * Outliers live in a SLOTTED CSR on the device: row r of set k owns entries
+ * [row_start[k][r], row_start[k][r+1]) of the plan's arena k (offsets absolute in
+ * the arena, multiples of 4 so slots are 16-byte aligned), the first
+ * row_count[k][r] of them used, columns ascending.  No row of a step depends on
+ * another row.  A row whose new count exceeds its slot sets the overflow status;
+ * the caller re-plans row_start[1-f] (qftc_csr_plan_slots on the returned counts)
+ * and re-runs the step -- its inputs (set f) are intact.  The strict reference
+ * CSR is produced by qftc_csr_compact.
+ *
+ * The gradient is the GradientStack entry (u8 codes + per-row params,
  * gradflow.hpp:77) or, for QFTC_GRAD_F32/BF16, the raw fp gradient that the
  * backward sink would quantize: the fused kernel applies quantize_state ->
  * dequantize to it exactly. */
 typedef struct {
   int32_t rows, cols;
   uint8_t* w_codes[2];
-  int32_t* row_ptr[2];
+  int32_t* row_start[2];
+  int32_t* row_count[2];
   const float* w_scale;
   const int32_t* w_zero_point;
   const float* t_min;
@@ -177,10 +188,46 @@ int qftc_lion_step(int rows, int cols, int bit_width, const uint8_t* g_codes,
                    int32_t* col_idx_out, float* values_out, int64_t capacity,
                    qftc_lion_hyper hyper, int64_t* nnz_host, qftc_stream_t stream);
 
+/* ---------------------------------------------------------------- slotted CSR */
+
+/* row_start[0..rows] of 16-byte aligned slots with capacity count + count/4 + slack
+ * (rounded up to 4 entries), counts taken from `counts` or, if NULL, from a
+ * strict `row_ptr`.  Synchronises to return the arena size in *total_host. */
+int qftc_csr_plan_slots(const int32_t* counts, const int32_t* row_ptr, int rows, int slack,
+                        int32_t* row_start, int64_t* total_host, qftc_stream_t stream);
+/* copy every row's entries from a slotted (src_count != NULL) or strict (src_count
+ * == NULL: src_start is row_ptr) CSR to the slots dst_start of another arena. */
+int qftc_csr_copy_rows(int rows, const int32_t* src_start, const int32_t* src_count,
+                       const int32_t* src_col, const float* src_val, const int32_t* dst_start,
+                       int32_t* dst_col, float* dst_val, int64_t dst_capacity,
+                       qftc_stream_t stream);
+/* slotted -> strict reference CSR (SparseOutliers, quantize.hpp:48-57): row_ptr =
+ * exclusive scan of the counts, entries gathered.  Synchronises for *nnz_host;
+ * QFTC_EOVERFLOW if nnz > capacity. */
+int qftc_csr_compact(int rows, const int32_t* row_start, const int32_t* row_count,
+                     const int32_t* col_idx, const float* values, int32_t* row_ptr,
+                     int32_t* col_out, float* val_out, int64_t capacity, int64_t* nnz_host,
+                     qftc_stream_t stream);
+/* reconstruct from a slotted CSR (out: f32, or bf16 if bf16 != 0) */
+int qftc_reconstruct_slots(const uint8_t* codes, int rows, int cols, const float* scale,
+                           const int32_t* zero_point, const int32_t* row_start,
+                           const int32_t* row_count, const int32_t* col_idx,
+                           const float* values, void* out, int bf16, qftc_stream_t stream);
+
 /* Pass-through mode (QuantMode::passthrough, quantize.hpp:17): lion_apply on raw
  * fp32 state, bitwise equal to lion_step_reference (optimizer.hpp:135-142). */
 int qftc_lion_apply(float* w, float* m, const float* g, int64_t n, qftc_lion_hyper hyper,
                     qftc_stream_t stream);
+
+/* ---------------------------------------------------------------- memory helpers
+ * For FFI hosts (ctypes / cgo / JNI / pybind) that have no CUDA runtime of their
+ * own: device allocation and stream-ordered copies. */
+int qftc_device_alloc(void** ptr, size_t bytes);
+int qftc_device_free(void* ptr);
+int qftc_copy_to_device(void* dst, const void* src_host, size_t bytes, qftc_stream_t stream);
+int qftc_copy_to_host(void* dst_host, const void* src, size_t bytes, qftc_stream_t stream);
+int qftc_memset(void* dst, int value, size_t bytes, qftc_stream_t stream);
+int qftc_stream_synchronize(qftc_stream_t stream);
 
 /* ---------------------------------------------------------------- inputs */
 

@@ -13,6 +13,7 @@
 // The signatures are the qo_* ones from qft_oracle.c with a qr_ prefix.
 #include <algorithm>
 #include <chrono>
+#include <optional>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -302,20 +303,33 @@ struct QrBench {
 
 void* qr_bench_create(int n_layers, const int* rows, const int* cols, uint64_t seed,
                       int bit_width, double fraction, float lr, float beta1, float beta2,
-                      float wd) {
+                      float wd, int threads) {
   auto* b = new QrBench;
   b->bit_width = bit_width;
   b->h = qft::LionHyper<float>{lr, beta1, beta2, wd};
+  std::vector<std::optional<qft::Model<float>>> models(n_layers);
+  std::vector<qft::QuantizedTensor<float>> grads(n_layers);
+  threads = std::max(1, std::min(threads, n_layers));
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) {
+    pool.emplace_back([&, t] {
+      for (int l = t; l < n_layers; l += threads) {
+        qft::Tensor<float> w(rows[l], cols[l]);
+        qo_synth(w.data(), static_cast<int64_t>(w.size()), seed + 2 * l, 0.02, 0.005);
+        auto dsw = qft::decompose_weight(w, fraction, bit_width, qft::QuantMode::affine,
+                                         qft::ThresholdKind::percentile);
+        models[l].emplace(one_layer_model(std::move(dsw), bit_width));
+        qft::Tensor<float> g(rows[l], cols[l]);
+        qo_synth(g.data(), static_cast<int64_t>(g.size()), seed + 2 * l + 1, 1e-3, 0.0);
+        grads[l] = qft::quantize_state(g, bit_width, qft::QuantMode::affine);
+      }
+    });
+  }
+  for (auto& th : pool) th.join();
   for (int l = 0; l < n_layers; ++l) {
-    qft::Tensor<float> w(rows[l], cols[l]);
-    qo_synth(w.data(), static_cast<int64_t>(w.size()), seed + 2 * l, 0.02, 0.005);
-    auto dsw = qft::decompose_weight(w, fraction, bit_width, qft::QuantMode::affine,
-                                     qft::ThresholdKind::percentile);
-    b->models.push_back(one_layer_model(std::move(dsw), bit_width));
+    b->models.push_back(std::move(*models[l]));
     b->states.push_back(qft::LionState<float>::init(b->models.back()));
-    qft::Tensor<float> g(rows[l], cols[l]);
-    qo_synth(g.data(), static_cast<int64_t>(g.size()), seed + 2 * l + 1, 1e-3, 0.0);
-    b->grads.push_back(qft::quantize_state(g, bit_width, qft::QuantMode::affine));
+    b->grads.push_back(std::move(grads[l]));
   }
   return b;
 }

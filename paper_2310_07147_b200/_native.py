@@ -32,7 +32,8 @@ class LionTensorC(C.Structure):
     """``qftc_lion_tensor``: one layer of a grouped quantized Lion step."""
     _fields_ = [
         ("rows", C.c_int32), ("cols", C.c_int32),
-        ("w_codes", C.c_void_p * 2), ("row_ptr", C.c_void_p * 2),
+        ("w_codes", C.c_void_p * 2), ("row_start", C.c_void_p * 2),
+        ("row_count", C.c_void_p * 2),
         ("w_scale", C.c_void_p), ("w_zero_point", C.c_void_p),
         ("t_min", C.c_void_p), ("t_max", C.c_void_p),
         ("m_codes", C.c_void_p * 2), ("m_scale", C.c_void_p * 2),
@@ -79,6 +80,17 @@ _SIGS = {
     "qftc_lion_step": (_i, [_i, _i, _i] + [_vp] * 21 + [_i64, LionHyperC, C.POINTER(_i64), _vp]),
     "qftc_lion_apply": (_i, [_vp, _vp, _vp, _i64, LionHyperC, _vp]),
     "qftc_synth": (_i, [_vp, _i64, _u64, _d, _d, _vp]),
+    "qftc_csr_plan_slots": (_i, [_vp, _vp, _i, _i, _vp, C.POINTER(_i64), _vp]),
+    "qftc_csr_copy_rows": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp]),
+    "qftc_csr_compact": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, C.POINTER(_i64),
+                              _vp]),
+    "qftc_reconstruct_slots": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp]),
+    "qftc_device_alloc": (_i, [C.POINTER(_vp), C.c_size_t]),
+    "qftc_device_free": (_i, [_vp]),
+    "qftc_copy_to_device": (_i, [_vp, _vp, C.c_size_t, _vp]),
+    "qftc_copy_to_host": (_i, [_vp, _vp, C.c_size_t, _vp]),
+    "qftc_memset": (_i, [_vp, _i, C.c_size_t, _vp]),
+    "qftc_stream_synchronize": (_i, [_vp]),
 }
 
 EXPORTS = tuple(_SIGS)

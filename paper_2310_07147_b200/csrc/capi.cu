@@ -28,6 +28,10 @@ cudaError_t launch_thresholds(const float*, int, int, double, int, float*, float
 cudaError_t launch_lion_apply(float*, float*, const float*, int64_t, float, float, float, float,
                               cudaStream_t);
 cudaError_t launch_synth(float*, int64_t, uint64_t, double, double, cudaStream_t);
+cudaError_t csr_plan_slots(const int32_t*, const int32_t*, int, int, int32_t*, cudaStream_t);
+cudaError_t csr_copy_rows(int, const int32_t*, const int32_t*, const int32_t*, const float*,
+                          const int32_t*, int32_t*, float*, int64_t, cudaStream_t);
+cudaError_t csr_row_ptr(const int32_t*, int, int32_t*, cudaStream_t);
 }  // namespace qftk
 
 using namespace qftk;
@@ -45,10 +49,10 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(QFTC_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
-#define QFTC_CUDA(expr, where)                 \
-  do {                                         \
-    cudaError_t _e = (expr);                   \
-    if (_e != cudaSuccess) return cuda_fail(_e, where); \
+#define QFTC_CUDA(expr, where)                           \
+  do {                                                   \
+    cudaError_t _e = (expr);                             \
+    if (_e != cudaSuccess) return cuda_fail(_e, where);  \
   } while (0)
 
 int require_device() {
@@ -72,31 +76,63 @@ int require_shape(int rows, int cols, const char* what) {
 
 inline bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
-// Device scratch for one call: header + status words.
+constexpr int kSlack = 8;  // extra slot entries per row beyond count + count/4
+
+// Device workspace: header | tensors | blocks | status words
 struct Scratch {
   void* base = nullptr;
   Header* hdr = nullptr;
-  unsigned long long* status = nullptr;
   DevTensor* tensors = nullptr;
+  RowBlock* blocks = nullptr;
+  unsigned long long* status = nullptr;
+  int n_blocks = 0;
 };
 
-int scratch_alloc(Scratch& s, int64_t rows, int n_tensors, cudaStream_t st) {
-  const size_t hb = sizeof(Header);
-  const size_t tb = sizeof(DevTensor) * (size_t)n_tensors;
-  const size_t sb = sizeof(unsigned long long) * (size_t)(rows > 0 ? rows : 1);
-  const size_t total = hb + ((tb + 255) & ~size_t(255)) + sb + 256;
+std::vector<RowBlock> make_blocks(const std::vector<DevTensor>& ts) {
+  std::vector<RowBlock> b;
+  for (int t = 0; t < (int)ts.size(); ++t)
+    for (int r0 = 0; r0 < ts[t].rows; r0 += kBlockRows)
+      b.push_back(RowBlock{t, r0, std::min(kBlockRows, ts[t].rows - r0), 0});
+  return b;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// allocate + upload descriptors and the block table (stream-ordered)
+int scratch_alloc(Scratch& s, const std::vector<DevTensor>& ts, int64_t status_rows,
+                  cudaStream_t st) {
+  const std::vector<RowBlock> blocks = make_blocks(ts);
+  const size_t hb = 256;
+  const size_t tb = align256(sizeof(DevTensor) * ts.size());
+  const size_t bb = align256(sizeof(RowBlock) * (blocks.size() ? blocks.size() : 1));
+  const size_t sb = sizeof(unsigned long long) * (size_t)(status_rows > 0 ? status_rows : 1);
+  const size_t total = hb + tb + bb + sb;
   QFTC_CUDA(cudaMallocAsync(&s.base, total, st), "cudaMallocAsync");
-  QFTC_CUDA(cudaMemsetAsync(s.base, 0, total, st), "cudaMemsetAsync");
-  s.hdr = reinterpret_cast<Header*>(s.base);
-  s.tensors = reinterpret_cast<DevTensor*>(reinterpret_cast<char*>(s.base) + 256);
-  s.status = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(s.base) + 256 +
-                                                   ((tb + 255) & ~size_t(255)));
-  const uint32_t one = 1;  // epoch starts at 1: zeroed status words read as "not ready"
+  QFTC_CUDA(cudaMemsetAsync(s.base, 0, hb, st), "cudaMemsetAsync");
+  if (status_rows > 0)
+    QFTC_CUDA(cudaMemsetAsync(reinterpret_cast<char*>(s.base) + hb + tb + bb, 0, sb, st),
+              "cudaMemsetAsync");
+  char* p = reinterpret_cast<char*>(s.base);
+  s.hdr = reinterpret_cast<Header*>(p);
+  s.tensors = reinterpret_cast<DevTensor*>(p + hb);
+  s.blocks = reinterpret_cast<RowBlock*>(p + hb + tb);
+  s.status = reinterpret_cast<unsigned long long*>(p + hb + tb + bb);
+  s.n_blocks = (int)blocks.size();
+  static const uint32_t one = 1;  // epoch starts at 1: zeroed status words read "not ready"
   QFTC_CUDA(cudaMemcpyAsync(&s.hdr->epoch, &one, 4, cudaMemcpyHostToDevice, st), "init epoch");
+  QFTC_CUDA(cudaMemcpyAsync(s.tensors, ts.data(), sizeof(DevTensor) * ts.size(),
+                            cudaMemcpyHostToDevice, st),
+            "upload descriptors");
+  if (!blocks.empty())
+    QFTC_CUDA(cudaMemcpyAsync(s.blocks, blocks.data(), sizeof(RowBlock) * blocks.size(),
+                              cudaMemcpyHostToDevice, st),
+              "upload blocks");
+  // the pageable host vectors must outlive the copies
+  QFTC_CUDA(cudaStreamSynchronize(st), "sync");
   return QFTC_OK;
 }
 
-// choose the number of pipeline stages: most CTAs per SM first, then most stages
+// stages: most CTAs per SM first, then most stages
 int pick_stages(int mode, int gk, int cols_p) {
   int best_s = 2;
   long best_score = -1;
@@ -126,7 +162,7 @@ int read_header(const Header* d_hdr, Header* h, cudaStream_t st) {
 extern "C" {
 
 const char* qftc_last_error(void) { return g_err.c_str(); }
-int qftc_version(void) { return 1; }
+int qftc_version(void) { return 2; }
 int qftc_max_cols(void) { return row_engine_max_cols(); }
 
 int qftc_channel_minmax(const float* x, int rows, int cols, float* mins, float* maxs,
@@ -243,25 +279,24 @@ int qftc_decompose_dense_sparse(const float* w, int rows, int cols, const float*
   // params from thresholds (quantize.hpp:264) -- validates t_min <= t_max
   int rc = qftc_affine_params_from_bounds(t_min, t_max, rows, bit_width, scale, zp, stream);
   if (rc) return rc;
-  Scratch sc;
-  if ((rc = scratch_alloc(sc, rows, 1, st))) return rc;
   DevTensor t{};
   t.rows = rows;
   t.cols = cols;
-  t.row_base = 0;
   t.w_f32 = w;
   t.w_scale = scale;
   t.w_zp = zp;
   t.t_min = t_min;
   t.t_max = t_max;
   t.w_codes[1] = codes;
-  t.row_ptr[1] = row_ptr;
-  QFTC_CUDA(cudaMemcpyAsync(sc.tensors, &t, sizeof t, cudaMemcpyHostToDevice, st), "upload");
+  t.rs[1] = row_ptr;
+  Scratch sc;
+  if ((rc = scratch_alloc(sc, {t}, rows, st))) return rc;
   LaunchArgs a{};
   a.tensors = sc.tensors;
+  a.blocks = sc.blocks;
   a.n_tensors = 1;
+  a.n_blocks = sc.n_blocks;
   a.total_rows = rows;
-  a.flip = 0;
   a.bit_width = bit_width;
   a.col_out = col_idx;
   a.val_out = values;
@@ -285,29 +320,31 @@ int qftc_decompose_dense_sparse(const float* w, int rows, int cols, const float*
 }
 
 static int reconstruct_impl(const uint8_t* codes, int rows, int cols, const float* scale,
-                            const int32_t* zp, const int32_t* row_ptr, const int32_t* col_idx,
+                            const int32_t* zp, const int32_t* row_start,
+                            const int32_t* row_count, const int32_t* col_idx,
                             const float* values, void* out, bool bf16, qftc_stream_t stream) {
   if (int rc = require_shape(rows, cols, "dequantize")) return rc;
   if (cols > row_engine_max_cols())
     return fail(QFTC_ENOTSUP, "reconstruct: cols above " + std::to_string(row_engine_max_cols()));
   if (int rc = require_device()) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  Scratch sc;
-  if (int rc = scratch_alloc(sc, 0, 1, st)) return rc;
   DevTensor t{};
   t.rows = rows;
   t.cols = cols;
   t.w_codes[0] = const_cast<uint8_t*>(codes);
-  t.row_ptr[0] = const_cast<int32_t*>(row_ptr);
+  t.rs[0] = const_cast<int32_t*>(row_start);
+  t.cnt[0] = const_cast<int32_t*>(row_count);
   t.w_scale = scale;
   t.w_zp = zp;
   t.out = out;
-  QFTC_CUDA(cudaMemcpyAsync(sc.tensors, &t, sizeof t, cudaMemcpyHostToDevice, st), "upload");
+  Scratch sc;
+  if (int rc = scratch_alloc(sc, {t}, 0, st)) return rc;
   LaunchArgs a{};
   a.tensors = sc.tensors;
+  a.blocks = sc.blocks;
   a.n_tensors = 1;
+  a.n_blocks = sc.n_blocks;
   a.total_rows = rows;
-  a.flip = 0;
   a.bit_width = 8;
   a.col_in = col_idx;
   a.val_in = values;
@@ -315,6 +352,7 @@ static int reconstruct_impl(const uint8_t* codes, int rows, int cols, const floa
   a.status = sc.status;
   a.cols_p = (cols + 15) & ~15;
   a.use_bulk = (cols % 16 == 0) && al16(codes) && al16(out);
+  a.slotted_in = row_count != nullptr && al16(col_idx) && al16(values);
   const int mode = bf16 ? MODE_RECON_BF16 : MODE_RECON_F32;
   a.stages = pick_stages(mode, G_U8, a.cols_p);
   QFTC_CUDA(launch_row_engine(mode, G_U8, a, st, nullptr), "reconstruct kernel");
@@ -325,20 +363,81 @@ static int reconstruct_impl(const uint8_t* codes, int rows, int cols, const floa
 int qftc_reconstruct(const uint8_t* codes, int rows, int cols, const float* scale,
                      const int32_t* zp, const int32_t* row_ptr, const int32_t* col_idx,
                      const float* values, float* out, qftc_stream_t stream) {
-  return reconstruct_impl(codes, rows, cols, scale, zp, row_ptr, col_idx, values, out, false,
-                          stream);
+  return reconstruct_impl(codes, rows, cols, scale, zp, row_ptr, nullptr, col_idx, values, out,
+                          false, stream);
 }
 
 int qftc_reconstruct_bf16(const uint8_t* codes, int rows, int cols, const float* scale,
                           const int32_t* zp, const int32_t* row_ptr, const int32_t* col_idx,
                           const float* values, uint16_t* out, qftc_stream_t stream) {
-  return reconstruct_impl(codes, rows, cols, scale, zp, row_ptr, col_idx, values, out, true,
-                          stream);
+  return reconstruct_impl(codes, rows, cols, scale, zp, row_ptr, nullptr, col_idx, values, out,
+                          true, stream);
 }
 
-// ------------------------------------------------------------------ plans
+int qftc_reconstruct_slots(const uint8_t* codes, int rows, int cols, const float* scale,
+                           const int32_t* zp, const int32_t* row_start,
+                           const int32_t* row_count, const int32_t* col_idx,
+                           const float* values, void* out, int bf16, qftc_stream_t stream) {
+  if (!row_count) return fail(QFTC_EINVAL, "reconstruct_slots: row_count is required");
+  return reconstruct_impl(codes, rows, cols, scale, zp, row_start, row_count, col_idx, values,
+                          out, bf16 != 0, stream);
+}
+
+// ------------------------------------------------------------------ slotted CSR
+int qftc_csr_plan_slots(const int32_t* counts, const int32_t* row_ptr, int rows, int slack,
+                        int32_t* row_start, int64_t* total_host, qftc_stream_t stream) {
+  if (rows <= 0) return fail(QFTC_EINVAL, "csr_plan_slots: no rows");
+  if (!counts && !row_ptr) return fail(QFTC_EINVAL, "csr_plan_slots: need counts or row_ptr");
+  if (int rc = require_device()) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  QFTC_CUDA(csr_plan_slots(counts, row_ptr, rows, slack < 0 ? 0 : slack, row_start, st),
+            "csr_plan_slots");
+  if (total_host) {
+    int32_t t = 0;
+    QFTC_CUDA(cudaMemcpyAsync(&t, row_start + rows, 4, cudaMemcpyDeviceToHost, st), "copy");
+    QFTC_CUDA(cudaStreamSynchronize(st), "sync");
+    *total_host = t;
+  }
+  return QFTC_OK;
+}
+
+int qftc_csr_copy_rows(int rows, const int32_t* src_start, const int32_t* src_count,
+                       const int32_t* src_col, const float* src_val, const int32_t* dst_start,
+                       int32_t* dst_col, float* dst_val, int64_t dst_capacity,
+                       qftc_stream_t stream) {
+  if (rows <= 0) return QFTC_OK;
+  if (int rc = require_device()) return rc;
+  QFTC_CUDA(csr_copy_rows(rows, src_start, src_count, src_col, src_val, dst_start, dst_col,
+                          dst_val, dst_capacity, (cudaStream_t)stream),
+            "csr_copy_rows");
+  return QFTC_OK;
+}
+
+int qftc_csr_compact(int rows, const int32_t* row_start, const int32_t* row_count,
+                     const int32_t* col_idx, const float* values, int32_t* row_ptr,
+                     int32_t* col_out, float* val_out, int64_t capacity, int64_t* nnz_host,
+                     qftc_stream_t stream) {
+  if (rows <= 0) return fail(QFTC_EINVAL, "csr_compact: no rows");
+  if (!row_count) return fail(QFTC_EINVAL, "csr_compact: row_count is required");
+  if (int rc = require_device()) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  QFTC_CUDA(csr_row_ptr(row_count, rows, row_ptr, st), "csr_row_ptr");
+  QFTC_CUDA(csr_copy_rows(rows, row_start, row_count, col_idx, values, row_ptr, col_out, val_out,
+                          capacity, st),
+            "csr_copy_rows");
+  int32_t n = 0;
+  QFTC_CUDA(cudaMemcpyAsync(&n, row_ptr + rows, 4, cudaMemcpyDeviceToHost, st), "copy");
+  QFTC_CUDA(cudaStreamSynchronize(st), "sync");
+  if (nnz_host) *nnz_host = n;
+  if (n > capacity)
+    return fail(QFTC_EOVERFLOW, "csr_compact: nnz " + std::to_string(n) + " exceeds capacity " +
+                                    std::to_string(capacity));
+  return QFTC_OK;
+}
+
 }  // extern "C"
 
+// ------------------------------------------------------------------ plans
 struct qftc_plan {
   Scratch sc;
   int n = 0;
@@ -348,10 +447,10 @@ struct qftc_plan {
   int cols_p = 16;
   int stages = 2;
   int use_bulk = 1;
+  int slotted[2] = {0, 0};
   int32_t* col[2] = {nullptr, nullptr};
   float* val[2] = {nullptr, nullptr};
   int64_t cap[2] = {0, 0};
-  int last_flip = 0;
 };
 
 extern "C" {
@@ -369,6 +468,7 @@ int qftc_plan_create(qftc_plan** out, const qftc_lion_tensor* ts, int n, int bit
   int64_t rows = 0;
   int maxc = 1;
   bool bulk = true;
+  bool slotted[2] = {true, true};
   for (int i = 0; i < n; ++i) {
     const qftc_lion_tensor& t = ts[i];
     if (t.rows <= 0 || t.cols <= 0)
@@ -382,11 +482,13 @@ int qftc_plan_create(qftc_plan** out, const qftc_lion_tensor* ts, int n, int bit
     d.row_base = (int32_t)rows;
     for (int k = 0; k < 2; ++k) {
       d.w_codes[k] = t.w_codes[k];
-      d.row_ptr[k] = t.row_ptr[k];
+      d.rs[k] = t.row_start[k];
+      d.cnt[k] = t.row_count[k];
       d.m_codes[k] = t.m_codes[k];
       d.m_scale[k] = t.m_scale[k];
       d.m_zp[k] = t.m_zero_point[k];
       bulk = bulk && al16(t.w_codes[k]) && al16(t.m_codes[k]);
+      slotted[k] = slotted[k] && t.row_count[k] != nullptr;
     }
     d.w_scale = t.w_scale;
     d.w_zp = t.w_zero_point;
@@ -410,18 +512,10 @@ int qftc_plan_create(qftc_plan** out, const qftc_lion_tensor* ts, int n, int bit
   }
   if (rows > 0x7fffffff) return fail(QFTC_ENOTSUP, "plan: more than 2^31 rows");
   auto* p = new qftc_plan;
-  int rc = scratch_alloc(p->sc, rows, n, st);
+  int rc = scratch_alloc(p->sc, dts, 0, st);
   if (rc) {
     delete p;
     return rc;
-  }
-  cudaError_t e = cudaMemcpyAsync(p->sc.tensors, dts.data(), sizeof(DevTensor) * (size_t)n,
-                                  cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  if (e != cudaSuccess) {
-    cudaFree(p->sc.base);
-    delete p;
-    return cuda_fail(e, "plan upload");
   }
   p->n = n;
   p->total_rows = (int)rows;
@@ -434,6 +528,7 @@ int qftc_plan_create(qftc_plan** out, const qftc_lion_tensor* ts, int n, int bit
     p->col[k] = col_idx ? col_idx[k] : nullptr;
     p->val[k] = values ? values[k] : nullptr;
     p->cap[k] = capacity ? capacity[k] : 0;
+    p->slotted[k] = slotted[k] && al16(p->col[k]) && al16(p->val[k]) ? 1 : 0;
   }
   *out = p;
   return QFTC_OK;
@@ -446,6 +541,7 @@ int qftc_plan_set_arena(qftc_plan* p, int32_t* col_idx[2], float* values[2],
     p->col[k] = col_idx[k];
     p->val[k] = values[k];
     p->cap[k] = capacity[k];
+    p->slotted[k] = p->slotted[k] && al16(col_idx[k]) && al16(values[k]);
   }
   return QFTC_OK;
 }
@@ -455,7 +551,9 @@ int qftc_plan_step(qftc_plan* p, int flip, qftc_lion_hyper h, qftc_stream_t stre
   if (flip != 0 && flip != 1) return fail(QFTC_EINVAL, "plan_step: flip must be 0 or 1");
   LaunchArgs a{};
   a.tensors = p->sc.tensors;
+  a.blocks = p->sc.blocks;
   a.n_tensors = p->n;
+  a.n_blocks = p->sc.n_blocks;
   a.total_rows = p->total_rows;
   a.flip = flip;
   a.bit_width = p->bit_width;
@@ -473,7 +571,7 @@ int qftc_plan_step(qftc_plan* p, int flip, qftc_lion_hyper h, qftc_stream_t stre
   a.cols_p = p->cols_p;
   a.stages = p->stages;
   a.use_bulk = p->use_bulk;
-  p->last_flip = flip;
+  a.slotted_in = p->slotted[flip];
   QFTC_CUDA(launch_row_engine(MODE_STEP, p->grad_kind, a, (cudaStream_t)stream, nullptr),
             "lion step kernel");
   return QFTC_OK;
@@ -492,10 +590,8 @@ int qftc_plan_result(qftc_plan* p, int64_t* nnz_total, qftc_stream_t stream) {
     return fail(QFTC_EINVAL, "affine_params_from_bounds: min > max in momentum channel");
   if (h.err & ERR_GPARAMS)
     return fail(QFTC_EINVAL, "affine_params_from_bounds: min > max in gradient channel");
-  if (h.err & ERR_PREFIX) return fail(QFTC_ENOTSUP, "lion step: nnz above 2^30");
   if (h.overflow)
-    return fail(QFTC_EOVERFLOW, "lion step: new nnz " + std::to_string(h.total_nnz) +
-                                    " exceeds the CSR arena capacity");
+    return fail(QFTC_EOVERFLOW, "lion step: a row's new outlier count exceeds its CSR slot");
   return QFTC_OK;
 }
 
@@ -517,35 +613,71 @@ int qftc_lion_step(int rows, int cols, int bit_width, const uint8_t* g_codes,
                    int32_t* m_zp_out, uint8_t* w_codes_out, int32_t* row_ptr_out,
                    int32_t* col_idx_out, float* values_out, int64_t capacity,
                    qftc_lion_hyper hyper, int64_t* nnz_host, qftc_stream_t stream) {
-  qftc_lion_tensor t{};
-  t.rows = rows;
-  t.cols = cols;
-  t.w_codes[0] = const_cast<uint8_t*>(w_codes);
-  t.w_codes[1] = w_codes_out;
-  t.row_ptr[0] = const_cast<int32_t*>(row_ptr);
-  t.row_ptr[1] = row_ptr_out;
-  t.w_scale = w_scale;
-  t.w_zero_point = w_zp;
-  t.t_min = t_min;
-  t.t_max = t_max;
-  t.m_codes[0] = const_cast<uint8_t*>(m_codes);
-  t.m_codes[1] = m_codes_out;
-  t.m_scale[0] = const_cast<float*>(m_scale);
-  t.m_scale[1] = m_scale_out;
-  t.m_zero_point[0] = const_cast<int32_t*>(m_zp);
-  t.m_zero_point[1] = m_zp_out;
-  t.g_codes = g_codes;
-  t.g_scale = g_scale;
-  t.g_zero_point = g_zp;
-  int32_t* cols_arr[2] = {const_cast<int32_t*>(col_idx), col_idx_out};
-  float* vals_arr[2] = {const_cast<float*>(values), values_out};
-  const int64_t caps[2] = {0, capacity};
-  qftc_plan* p = nullptr;
-  int rc = qftc_plan_create(&p, &t, 1, bit_width, QFTC_GRAD_U8, cols_arr, vals_arr, caps, stream);
-  if (rc) return rc;
-  rc = qftc_plan_step(p, 0, hyper, stream);
-  if (!rc) rc = qftc_plan_result(p, nnz_host, stream);
-  qftc_plan_destroy(p);
+  if (int rc = require_shape(rows, cols, "lion step")) return rc;
+  if (int rc = require_device()) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  // output slots planned from the input counts; strict CSR via compaction
+  int32_t* rs_out = nullptr;
+  int32_t* cnt_out = nullptr;
+  QFTC_CUDA(cudaMallocAsync((void**)&rs_out, sizeof(int32_t) * (rows + 1), st), "alloc");
+  QFTC_CUDA(cudaMallocAsync((void**)&cnt_out, sizeof(int32_t) * rows, st), "alloc");
+  int64_t slots = 0;
+  int rc = qftc_csr_plan_slots(nullptr, row_ptr, rows, kSlack, rs_out, &slots, stream);
+  int32_t* col_tmp = nullptr;
+  float* val_tmp = nullptr;
+  for (int attempt = 0; attempt < 3 && rc == QFTC_OK; ++attempt) {
+    QFTC_CUDA(cudaMallocAsync((void**)&col_tmp, sizeof(int32_t) * (slots + 4), st), "alloc");
+    QFTC_CUDA(cudaMallocAsync((void**)&val_tmp, sizeof(float) * (slots + 4), st), "alloc");
+    qftc_lion_tensor t{};
+    t.rows = rows;
+    t.cols = cols;
+    t.w_codes[0] = const_cast<uint8_t*>(w_codes);
+    t.w_codes[1] = w_codes_out;
+    t.row_start[0] = const_cast<int32_t*>(row_ptr);
+    t.row_count[0] = nullptr;  // strict input
+    t.row_start[1] = rs_out;
+    t.row_count[1] = cnt_out;
+    t.w_scale = w_scale;
+    t.w_zero_point = w_zp;
+    t.t_min = t_min;
+    t.t_max = t_max;
+    t.m_codes[0] = const_cast<uint8_t*>(m_codes);
+    t.m_codes[1] = m_codes_out;
+    t.m_scale[0] = const_cast<float*>(m_scale);
+    t.m_scale[1] = m_scale_out;
+    t.m_zero_point[0] = const_cast<int32_t*>(m_zp);
+    t.m_zero_point[1] = m_zp_out;
+    t.g_codes = g_codes;
+    t.g_scale = g_scale;
+    t.g_zero_point = g_zp;
+    int32_t* cols_arr[2] = {const_cast<int32_t*>(col_idx), col_tmp};
+    float* vals_arr[2] = {const_cast<float*>(values), val_tmp};
+    const int64_t caps[2] = {0, slots};
+    qftc_plan* p = nullptr;
+    rc = qftc_plan_create(&p, &t, 1, bit_width, QFTC_GRAD_U8, cols_arr, vals_arr, caps, stream);
+    if (rc) break;
+    rc = qftc_plan_step(p, 0, hyper, stream);
+    if (!rc) rc = qftc_plan_result(p, nullptr, stream);
+    qftc_plan_destroy(p);
+    if (rc == QFTC_EOVERFLOW && attempt < 2) {
+      // re-plan the slots from the true counts and re-run (inputs are intact)
+      cudaFreeAsync(col_tmp, st);
+      cudaFreeAsync(val_tmp, st);
+      col_tmp = nullptr;
+      val_tmp = nullptr;
+      rc = qftc_csr_plan_slots(cnt_out, nullptr, rows, kSlack, rs_out, &slots, stream);
+      continue;  // rc == QFTC_OK -> next attempt
+    }
+    break;
+  }
+  if (rc == QFTC_OK)
+    rc = qftc_csr_compact(rows, rs_out, cnt_out, col_tmp, val_tmp, row_ptr_out, col_idx_out,
+                          values_out, capacity, nnz_host, stream);
+  if (col_tmp) cudaFreeAsync(col_tmp, st);
+  if (val_tmp) cudaFreeAsync(val_tmp, st);
+  cudaFreeAsync(rs_out, st);
+  cudaFreeAsync(cnt_out, st);
+  cudaStreamSynchronize(st);
   return rc;
 }
 
@@ -557,6 +689,44 @@ int qftc_lion_apply(float* w, float* m, const float* g, int64_t n, qftc_lion_hyp
   QFTC_CUDA(launch_lion_apply(w, m, g, n, h.lr, h.beta1, h.beta2, h.weight_decay,
                               (cudaStream_t)stream),
             "lion_apply");
+  return QFTC_OK;
+}
+
+int qftc_device_alloc(void** ptr, size_t bytes) {
+  if (!ptr) return fail(QFTC_EINVAL, "device_alloc: null out pointer");
+  if (int rc = require_device()) return rc;
+  QFTC_CUDA(cudaMalloc(ptr, bytes ? bytes : 1), "cudaMalloc");
+  return QFTC_OK;
+}
+
+int qftc_device_free(void* ptr) {
+  if (!ptr) return QFTC_OK;
+  QFTC_CUDA(cudaFree(ptr), "cudaFree");
+  return QFTC_OK;
+}
+
+int qftc_copy_to_device(void* dst, const void* src, size_t bytes, qftc_stream_t stream) {
+  if (!bytes) return QFTC_OK;
+  QFTC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream),
+            "copy_to_device");
+  return QFTC_OK;
+}
+
+int qftc_copy_to_host(void* dst, const void* src, size_t bytes, qftc_stream_t stream) {
+  if (!bytes) return QFTC_OK;
+  QFTC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, (cudaStream_t)stream),
+            "copy_to_host");
+  return QFTC_OK;
+}
+
+int qftc_memset(void* dst, int value, size_t bytes, qftc_stream_t stream) {
+  if (!bytes) return QFTC_OK;
+  QFTC_CUDA(cudaMemsetAsync(dst, value, bytes, (cudaStream_t)stream), "memset");
+  return QFTC_OK;
+}
+
+int qftc_stream_synchronize(qftc_stream_t stream) {
+  QFTC_CUDA(cudaStreamSynchronize((cudaStream_t)stream), "stream synchronize");
   return QFTC_OK;
 }
 

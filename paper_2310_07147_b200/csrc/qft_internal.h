@@ -7,13 +7,19 @@
 
 namespace qftk {
 
-// One tensor of a grouped launch, device copy of qftc_lion_tensor plus the row
-// base of the tensor inside the launch's global row numbering.
+// One tensor of a launch.
+//
+// CSR on the device is SLOTTED: row r of set k owns arena entries
+// [rs[k][r], rs[k][r+1]) (a 16-byte aligned slot sized from its previous count
+// plus slack) of which the first cnt[k][r] are used, columns ascending.  A step
+// therefore needs no cross-row scan.  With cnt[k] == nullptr the arrays are a
+// strict reference CSR (rs = row_ptr, count = rs[r+1]-rs[r]).
 struct DevTensor {
   int32_t rows, cols;
   int32_t row_base, _pad;
   uint8_t* w_codes[2];
-  int32_t* row_ptr[2];
+  int32_t* rs[2];
+  int32_t* cnt[2];
   const float* w_scale;
   const int32_t* w_zp;
   const float* t_min;
@@ -29,9 +35,15 @@ struct DevTensor {
   void* out;           // reconstruct output (f32 or bf16)
 };
 
-// Device header of a plan / scan workspace.  `epoch` tags look-back status
-// words so the status array never needs clearing between launches; the last
-// CTA of every launch bumps it and resets the ticket counter.
+// A static unit of work: up to 32 consecutive rows of one tensor.
+struct RowBlock {
+  int32_t tensor, row0, nrows, _pad;
+};
+constexpr int kBlockRows = 32;
+
+// Device header of a workspace.  `epoch` tags the decompose look-back status
+// words so the status array never needs clearing; the last CTA of every launch
+// bumps it and resets the ticket counter.
 struct Header {
   uint32_t epoch;
   uint32_t ticket;
@@ -49,11 +61,13 @@ enum GradKind : int { G_U8 = 0, G_F32 = 1, G_BF16 = 2 };
 // error bits in Header::err
 constexpr uint32_t ERR_MPARAMS = 1u;   // momentum min > max (NaN in column 0)
 constexpr uint32_t ERR_GPARAMS = 2u;   // gradient min > max
-constexpr uint32_t ERR_PREFIX = 4u;    // nnz prefix exceeded 2^30
+constexpr uint32_t ERR_PREFIX = 4u;    // decompose nnz prefix exceeded 2^30
 
 struct LaunchArgs {
   DevTensor* tensors;
+  const RowBlock* blocks;
   int32_t n_tensors;
+  int32_t n_blocks;
   int32_t total_rows;
   int32_t flip;
   int32_t bit_width;
@@ -62,18 +76,18 @@ struct LaunchArgs {
   const float* val_in;
   int32_t* col_out;
   float* val_out;
-  int64_t cap_out;
+  int64_t cap_out;    // decompose: arena capacity (strict CSR output)
   Header* hdr;
   unsigned long long* status;
   int32_t cols_p;     // max padded (x16) row length of the launch
   int32_t stages;
   int32_t use_bulk;   // TMA bulk copies (all rows 16-byte aligned)
-  int32_t _pad;
+  int32_t slotted_in; // input CSR is slotted (16-byte aligned slots)
 };
 
 // launch helpers (rowengine.cu)
-size_t row_engine_smem(int mode, int gkind, int cols_p, int stages);
-cudaError_t launch_row_engine(int mode, int gkind, const LaunchArgs& a, cudaStream_t s,
+size_t row_engine_smem(int mode, int gk, int cols_p, int stages);
+cudaError_t launch_row_engine(int mode, int gk, const LaunchArgs& a, cudaStream_t s,
                               int* grid_out);
 int row_engine_max_cols();
 

@@ -8,27 +8,33 @@
 //   MODE_RECON_F32   reconstruct                (quantize.hpp:331-338)
 //   MODE_RECON_BF16  reconstruct -> bf16 for the next forward (network.hpp:208-211)
 //
-// CTA = 1 producer warp + 4 consumer warps.  The unit of work is one ROW
-// (= one output channel: every per-channel quantity -- scales, zero points,
-// thresholds, the m' min/max and the CSR segment -- is row-local).  Rows are
-// handed out by an atomic ticket in global row order across all tensors of the
-// launch (a grouped launch covers a whole model).
+// CTA = 1 producer warp + 4 consumer warps; the unit of work is one ROW (one
+// output channel: scales, zero points, thresholds, the m' min/max and the CSR
+// segment are all row-local).
 //
-// Producer warp, running up to S stages ahead of the consumers:
-//   ticket -> tensor lookup -> per-row context (params, thresholds, pointers)
-//   -> old CSR segment into a smem bitmap + (col,val) list
-//   -> TMA 1-D bulk copies (cp.async.bulk, SASS UBLKCP) of the row's w/m/g codes
-//      into the stage, completion counted on the stage's mbarrier.
-// Consumer warps (128 threads, 16 elements = one 16-byte vector per thread-step):
-//   pass 1: dequant g,m,w (+old outlier patch) -> Lion (packed FP32x2, no FMA)
-//           -> w' classify / quantize -> dense W codes straight to HBM (STG.128),
-//           m' kept in smem, m' row min/max, new-outlier masks;
-//   named barrier; m' params (fp64, as the reference); pass 2 quantizes m';
-//   warp 0 publishes the row's outlier count and runs a warp-wide decoupled
-//   look-back over the per-row status words to get the row's CSR offset;
-//   named barrier; ordered CSR write (ascending columns within the row).
-// HBM traffic per parameter (u8 gradient): read w,m,g codes (3 B) + old CSR,
-// write w,m codes (2 B) + new CSR -- nothing is read twice.
+// Producer warp (STEP/RECON): walks a static list of row blocks (<= 32 rows of
+// one tensor, round-robin over CTAs).  Per block its lanes load the 32 rows'
+// metadata in parallel (params, thresholds, CSR slot bounds); per row it waits
+// for a free stage, writes the row context and issues TMA 1-D bulk copies
+// (cp.async.bulk -> SASS UBLKCP) of the row's w/m/g codes and of the row's old
+// CSR slot (cols, values) into the stage, completion counted on the stage's
+// mbarrier.  It runs up to S rows ahead of the consumers.
+//
+// Consumer warps (128 threads, one 16-byte vector = 16 elements per thread-step):
+//   old-outlier bitmap from the staged slot; named barrier;
+//   pass 1: dequant g,m,w (+old outlier patch) -> Lion (packed FP32x2 products,
+//           scalar sums: see qft_device.cuh) -> classify / quantize w' -> dense
+//           W codes straight to HBM (STG.128); m' kept in smem; m' row min/max;
+//           new-outlier masks;
+//   named barrier; m' params in fp64 (as the reference); pass 2 quantizes m';
+//   CSR write into the row's own slot (ascending columns: warp ballot/popc and a
+//   chunk-major prefix), slot count stored; overflow of a slot raises a flag and
+//   the host re-plans the slots and re-runs from the intact ping-pong inputs.
+// No row ever waits on another row.
+//
+// DECOMPOSE (init / threshold refresh only) writes the STRICT reference CSR
+// directly: rows are taken by an atomic ticket and the row offsets come from a
+// warp-wide decoupled look-back over per-row status words.
 #include <cstdio>
 
 #include "qft_device.cuh"
@@ -40,40 +46,43 @@ using namespace qftd;
 constexpr int NCW = 4;             // consumer warps
 constexpr int NCT = NCW * 32;      // consumer threads
 constexpr int NT = NCT + 32;       // + producer warp
-constexpr int OLDCAP = 256;        // old CSR entries cached in smem per stage
+constexpr int OLDCAP = 256;        // old CSR entries staged in smem per stage
 constexpr int NCH_MAX = 32;        // chunks of NCT*16 columns
 constexpr int MAX_COLS = NCH_MAX * NCT * 16;  // 65536
 constexpr int MAX_STAGES = 6;
+constexpr int HDR = 256;           // stage header (row context) bytes
 
 constexpr uint32_t FLAG_A = 1u, FLAG_P = 2u;
 constexpr uint32_t VAL_MASK = (1u << 30) - 1u;
 
+constexpr int BAR_C = 1;      // after pass 1 (row reduction)
+constexpr int BAR_D = 2;      // decompose: row offset known
+constexpr int BAR_G = 3;      // raw-gradient row reduction
+constexpr int BAR_B0 = 4;     // old-outlier bitmap ready
+
 struct StageCtx {
-  int32_t row;        // launch-global row (ticket); -1 = no more work
+  int32_t row;        // >= 0 valid (decompose: launch-global row); -1 = no more work
   int32_t lrow;       // row inside its tensor
   int32_t cols;
-  int32_t old_begin;  // absolute arena index of the row's first old outlier
+  int32_t old_begin;  // arena index of the row's first old outlier
   int32_t old_n;
-  int32_t is_last;    // lrow == rows-1
-  int32_t zw, zm;
-  float sw, tmin, tmax, sm;
-  float sg;
-  int32_t zg;
-  int32_t zpay;       // clamp(zw, 0, qmax): dense payload under an outlier
-  int32_t _p0;
+  int32_t old_staged; // old (col,val) list is TMA-staged in this stage
+  int32_t is_last;    // lrow == rows-1 (decompose)
+  int32_t zw, zm, zg, zpay;
+  float sw, tmin, tmax, sm, sg;
+  int32_t slot_out, cap_out;
   uint8_t* w_out;     // row pointers in HBM
   uint8_t* m_out;
   void* aux_out;      // reconstruct output row
   float* m_scale_out; // tensor arrays
   int32_t* m_zp_out;
-  int32_t* row_ptr_out;
-  int64_t _p1[2];
+  int32_t* cnt_out;
+  int32_t* row_ptr_out;  // decompose (strict)
 };
-static_assert(sizeof(StageCtx) == 128, "ctx size");
+static_assert(sizeof(StageCtx) <= HDR, "ctx size");
 
 __host__ __device__ inline int round16(int x) { return (x + 15) & ~15; }
 
-// stage data bytes for the mode (all sections 16-byte aligned)
 __host__ __device__ inline int stage_data_bytes(int mode, int gk, int cp) {
   switch (mode) {
     case MODE_STEP: return 2 * cp + (gk == G_U8 ? cp : gk == G_F32 ? 4 * cp : 2 * cp);
@@ -84,7 +93,7 @@ __host__ __device__ inline int stage_data_bytes(int mode, int gk, int cp) {
 __host__ __device__ inline int old_bits_bytes(int cp) { return round16((cp + 31) / 32 * 4); }
 __host__ __device__ inline int stage_bytes(int mode, int gk, int cp) {
   const int old = (mode == MODE_DECOMPOSE) ? 0 : OLDCAP * 8 + old_bits_bytes(cp);
-  return 128 + old + stage_data_bytes(mode, gk, cp);
+  return HDR + old + stage_data_bytes(mode, gk, cp);
 }
 struct Tabs {
   float red_lo[2][NCW];
@@ -94,13 +103,15 @@ struct Tabs {
   float gred_hi[2][NCW];
   int32_t gred_nan[2][NCW];
   int32_t cnt[2][NCH_MAX][NCW];
-  int32_t pre[2][NCH_MAX][NCW];
   int32_t prefix[2];
   int32_t _pad[2];
 };
+__host__ __device__ inline int mprime_bytes(int cp) {
+  return 4 * ((cp + NCT * 16 - 1) / (NCT * 16)) * (NCT * 16);
+}
 __host__ __device__ inline int consumer_bytes(int mode, int cp) {
   int b = (int)sizeof(Tabs);
-  if (mode == MODE_STEP) b += 4 * ((cp + NCT * 16 - 1) / (NCT * 16)) * (NCT * 16);  // m'
+  if (mode == MODE_STEP) b += mprime_bytes(cp);
   if (mode == MODE_STEP || mode == MODE_DECOMPOSE) b += round16(cp / 16 * 2);  // masks
   return b;
 }
@@ -118,20 +129,22 @@ __device__ __forceinline__ unsigned long long pack_status(uint32_t epoch, uint32
   return ((unsigned long long)epoch << 32) | ((unsigned long long)flag << 30) | v;
 }
 
-// value of an old outlier at column `col` of the stage's row
-__device__ __noinline__ float old_value(const int32_t* old_cols, const float* old_vals, int n_old,
+// value of the old outlier at column `col` of the stage's row (rare path)
+__device__ __noinline__ float old_value(const int32_t* oc, const float* ov, int n_old, int staged,
                                         int old_begin, int col, const int32_t* col_in,
                                         const float* val_in) {
-  const int nc = n_old < OLDCAP ? n_old : OLDCAP;
-  int lo = 0, hi = nc;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (old_cols[mid] < col) lo = mid + 1; else hi = mid;
+  int lo = 0;
+  if (staged) {
+    const int nc = n_old < OLDCAP ? n_old : OLDCAP;
+    int hi = nc;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (oc[mid] < col) lo = mid + 1; else hi = mid;
+    }
+    if (lo < nc && oc[lo] == col) return ov[lo];
+    lo = nc;
   }
-  if (lo < nc && old_cols[lo] == col) return old_vals[lo];
-  // beyond the cached prefix: search the arena in HBM
-  lo = nc;
-  hi = n_old;
+  int hi = n_old;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
     if (col_in[old_begin + mid] < col) lo = mid + 1; else hi = mid;
@@ -155,10 +168,15 @@ __device__ __forceinline__ float load_graw(const uint8_t* gdata, int idx) {
   return __uint_as_float((uint32_t)b << 16);
 }
 
+__device__ __forceinline__ float dequant1(uint32_t code, const DequantRow& d) {
+  return d.fast ? __fmul_rn(__fadd_rn(magic_byte(code, 0), d.negc), d.s)
+                : dequant_exact(code, d.s, d.z);
+}
+
 // ----------------------------------------------------------------------------
 // the kernel
 // ----------------------------------------------------------------------------
-template <int MODE, int GK, bool ALIGNED>
+template <int MODE, int GK, bool ALIGNED, bool WD0>
 __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -170,12 +188,12 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
   uint8_t* cons = stage0 + (size_t)S * sbytes;
   Tabs* tabs = reinterpret_cast<Tabs*>(cons);
   float* mprime = reinterpret_cast<float*>(cons + sizeof(Tabs));
-  const int mp_bytes = 4 * ((cp + NCT * 16 - 1) / (NCT * 16)) * (NCT * 16);
   uint16_t* masks = reinterpret_cast<uint16_t*>(cons + sizeof(Tabs) +
-                                                (MODE == MODE_STEP ? mp_bytes : 0));
+                                                (MODE == MODE_STEP ? mprime_bytes(cp) : 0));
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int qmax = (1 << a.bit_width) - 1;
+  constexpr bool kOld = (MODE != MODE_DECOMPOSE);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -188,152 +206,225 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
 
   auto stage_ptr = [&](int s) { return stage0 + (size_t)s * sbytes; };
   auto ctx_of = [&](uint8_t* st) { return reinterpret_cast<StageCtx*>(st); };
-  auto oldc_of = [&](uint8_t* st) { return reinterpret_cast<int32_t*>(st + 128); };
-  auto oldv_of = [&](uint8_t* st) { return reinterpret_cast<float*>(st + 128 + OLDCAP * 4); };
-  auto oldb_of = [&](uint8_t* st) {
-    return reinterpret_cast<uint32_t*>(st + 128 + OLDCAP * 8);
-  };
+  auto oldc_of = [&](uint8_t* st) { return reinterpret_cast<int32_t*>(st + HDR); };
+  auto oldv_of = [&](uint8_t* st) { return reinterpret_cast<float*>(st + HDR + OLDCAP * 4); };
+  auto oldb_of = [&](uint8_t* st) { return reinterpret_cast<uint32_t*>(st + HDR + OLDCAP * 8); };
   auto data_of = [&](uint8_t* st) {
-    return st + 128 + (MODE == MODE_DECOMPOSE ? 0 : OLDCAP * 8 + old_bits_bytes(cp));
+    return st + HDR + (kOld ? OLDCAP * 8 + old_bits_bytes(cp) : 0);
   };
 
   if (warp == NCW) {
-    // ======================= PRODUCER WARP ===============================
+    // ============================ PRODUCER WARP =============================
     const int in = a.flip, out = 1 - a.flip;
-    for (int it = 0;; ++it) {
-      const int s = it % S;
-      const uint32_t round = (uint32_t)(it / S);
-      mbar_wait(&empty[s], (round & 1u) ^ 1u);
-      uint8_t* st = stage_ptr(s);
-      StageCtx* cx = ctx_of(st);
-      int row = 0;
-      if (lane == 0) row = (int)atomicAdd(&a.hdr->ticket, 1u);
-      row = __shfl_sync(0xffffffffu, row, 0);
-      if (row >= a.total_rows) {
-        if (lane == 0) {
-          cx->row = -1;
-          mbar_arrive(&full[s]);
+    int it = 0;
+    if (MODE == MODE_DECOMPOSE) {
+      // dynamic tickets in global row order (the look-back needs them)
+      for (;; ++it) {
+        const int s = it % S;
+        mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
+        uint8_t* st = stage_ptr(s);
+        StageCtx* cx = ctx_of(st);
+        int row = 0;
+        if (lane == 0) row = (int)atomicAdd(&a.hdr->ticket, 1u);
+        row = __shfl_sync(0xffffffffu, row, 0);
+        if (row >= a.total_rows) {
+          if (lane == 0) {
+            cx->row = -1;
+            mbar_arrive(&full[s]);
+          }
+          break;
         }
-        break;
-      }
-      int lo = 0, hi = a.n_tensors - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (a.tensors[mid].row_base <= row) lo = mid; else hi = mid - 1;
-      }
-      const DevTensor& T = a.tensors[lo];
-      const int lrow = row - T.row_base;
-      const int cols = T.cols;
-      const size_t roff = (size_t)lrow * (size_t)cols;
-      int ob = 0, on = 0;
-      if (MODE != MODE_DECOMPOSE) {
-        ob = T.row_ptr[in][lrow];
-        on = T.row_ptr[in][lrow + 1] - ob;
-      }
-      if (lane == 0) {
-        cx->row = row;
-        cx->lrow = lrow;
-        cx->cols = cols;
-        cx->old_begin = ob;
-        cx->old_n = on;
-        cx->is_last = (lrow == T.rows - 1);
-        cx->sw = T.w_scale[lrow];
-        cx->zw = T.w_zp[lrow];
-        const int32_t zw = cx->zw;
-        cx->zpay = zw < 0 ? 0 : (zw > qmax ? qmax : zw);
-        if (MODE == MODE_STEP || MODE == MODE_DECOMPOSE) {
+        int lo = 0, hi = a.n_tensors - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (a.tensors[mid].row_base <= row) lo = mid; else hi = mid - 1;
+        }
+        const DevTensor& T = a.tensors[lo];
+        const int lrow = row - T.row_base;
+        const int cols = T.cols;
+        const size_t roff = (size_t)lrow * (size_t)cols;
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(T.w_f32 + roff);
+        if (lane == 0) {
+          cx->row = row;
+          cx->lrow = lrow;
+          cx->cols = cols;
+          cx->is_last = (lrow == T.rows - 1);
+          const float sw = T.w_scale[lrow];
+          const int32_t zw = T.w_zp[lrow];
+          cx->sw = sw;
+          cx->zw = zw;
+          cx->zpay = zw < 0 ? 0 : (zw > qmax ? qmax : zw);
           cx->tmin = T.t_min[lrow];
           cx->tmax = T.t_max[lrow];
+          cx->w_out = T.w_codes[1] + roff;
+          cx->row_ptr_out = T.rs[1];
         }
-        if (MODE == MODE_STEP) {
-          cx->sm = T.m_scale[in][lrow];
-          cx->zm = T.m_zp[in][lrow];
-          if (GK == G_U8) {
-            cx->sg = T.g_scale[lrow];
-            cx->zg = T.g_zp[lrow];
+        uint8_t* data = data_of(st);
+        if (ALIGNED) {
+          if (lane == 0) {
+            mbar_expect_tx(&full[s], 4u * cols);
+            bulk_g2s(data, src, 4u * cols, &full[s]);
           }
-          cx->m_out = T.m_codes[out] + roff;
-          cx->m_scale_out = T.m_scale[out];
-          cx->m_zp_out = T.m_zp[out];
-        }
-        if (MODE == MODE_STEP || MODE == MODE_DECOMPOSE) {
-          cx->w_out = T.w_codes[MODE == MODE_STEP ? out : 1] + roff;
-          cx->row_ptr_out = T.row_ptr[MODE == MODE_STEP ? out : 1];
-        }
-        if (MODE == MODE_RECON_F32)
-          cx->aux_out = reinterpret_cast<float*>(T.out) + roff;
-        if (MODE == MODE_RECON_BF16)
-          cx->aux_out = reinterpret_cast<__nv_bfloat16*>(T.out) + roff;
-      }
-      uint8_t* data = data_of(st);
-      // ---- bulk (TMA) copies of the row payload
-      uint32_t tx = 0;
-      const uint8_t* src_w = nullptr;
-      const uint8_t* src_m = nullptr;
-      const uint8_t* src_g = nullptr;
-      int gbytes = 0;
-      if (MODE == MODE_STEP) {
-        src_w = T.w_codes[in] + roff;
-        src_m = T.m_codes[in] + roff;
-        if (GK == G_U8) { src_g = T.g_codes + roff; gbytes = cols; }
-        else if (GK == G_F32) { src_g = (const uint8_t*)T.g_raw + roff * 4; gbytes = 4 * cols; }
-        else { src_g = (const uint8_t*)T.g_raw + roff * 2; gbytes = 2 * cols; }
-        tx = 2u * cols + gbytes;
-      } else if (MODE == MODE_DECOMPOSE) {
-        src_w = reinterpret_cast<const uint8_t*>(T.w_f32 + roff);
-        tx = 4u * cols;
-      } else {
-        src_w = T.w_codes[in] + roff;
-        tx = cols;
-      }
-      if (ALIGNED) {
-        if (lane == 0) {
-          mbar_expect_tx(&full[s], tx);
-          if (MODE == MODE_STEP) {
-            bulk_g2s(data, src_w, cols, &full[s]);
-            bulk_g2s(data + cp, src_m, cols, &full[s]);
-            bulk_g2s(data + 2 * cp, src_g, gbytes, &full[s]);
-          } else {
-            bulk_g2s(data, src_w, tx, &full[s]);
-          }
-        }
-      }
-      // ---- old CSR segment -> bitmap + cached (col,val) list
-      if (MODE != MODE_DECOMPOSE) {
-        int32_t* oc = oldc_of(st);
-        float* ov = oldv_of(st);
-        uint32_t* bits = oldb_of(st);
-        const int nw = (cp + 31) / 32;
-        for (int i = lane; i < nw; i += 32) bits[i] = 0u;
-        __syncwarp();
-        for (int i = lane; i < on; i += 32) {
-          const int col = a.col_in[ob + i];
-          if (i < OLDCAP) {
-            oc[i] = col;
-            ov[i] = a.val_in[ob + i];
-          }
-          atomicOr(&bits[col >> 5], 1u << (col & 31));
-        }
-      }
-      if (!ALIGNED) {
-        // generic path (rows not 16-byte aligned): the producer lanes copy
-        if (MODE == MODE_STEP) {
-          for (int i = lane; i < cols; i += 32) {
-            data[i] = src_w[i];
-            data[cp + i] = src_m[i];
-          }
-          for (int i = lane; i < gbytes; i += 32) data[2 * cp + i] = src_g[i];
         } else {
-          for (int i = lane; i < (int)tx; i += 32) data[i] = src_w[i];
+          for (int i = lane; i < 4 * cols; i += 32) data[i] = src[i];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[s]);
+      }
+    } else {
+      // static round-robin over row blocks; 32 rows' metadata loaded lane-parallel
+      for (int blk = blockIdx.x; blk < a.n_blocks; blk += gridDim.x) {
+        const RowBlock B = a.blocks[blk];
+        const DevTensor* T = a.tensors + B.tensor;
+        const int cols = T->cols;
+        const bool act = lane < B.nrows;
+        const int lrow_l = B.row0 + lane;
+        float sw = 0.f, tmin = 0.f, tmax = 0.f, smv = 0.f, sgv = 0.f;
+        int zw = 0, zm = 0, zg = 0, ob = 0, on = 0, so = 0, co = 0;
+        if (act) {
+          sw = T->w_scale[lrow_l];
+          zw = T->w_zp[lrow_l];
+          const int32_t* rs_in = T->rs[in];
+          ob = rs_in[lrow_l];
+          const int cap_in = rs_in[lrow_l + 1] - ob;
+          // never read past the slot (a count above it means the previous step
+          // overflowed and was not re-run; the host reports that state invalid)
+          on = T->cnt[in] ? min(T->cnt[in][lrow_l], cap_in) : cap_in;
+          if (MODE == MODE_STEP) {
+            tmin = T->t_min[lrow_l];
+            tmax = T->t_max[lrow_l];
+            smv = T->m_scale[in][lrow_l];
+            zm = T->m_zp[in][lrow_l];
+            if (GK == G_U8) {
+              sgv = T->g_scale[lrow_l];
+              zg = T->g_zp[lrow_l];
+            }
+            so = T->rs[out][lrow_l];
+            co = T->rs[out][lrow_l + 1] - so;
+          }
+        }
+        // per-tensor pointers (lane 0; broadcast where the copy loop needs them)
+        const uint8_t* w_in = nullptr;
+        const uint8_t* m_in = nullptr;
+        const uint8_t* g_in = nullptr;
+        uint8_t* w_outp = nullptr;
+        uint8_t* m_outp = nullptr;
+        float* ms_out = nullptr;
+        int32_t* mz_out = nullptr;
+        int32_t* cnt_out = nullptr;
+        void* aux = nullptr;
+        if (lane == 0) {
+          w_in = T->w_codes[in];
+          if (MODE == MODE_STEP) {
+            m_in = T->m_codes[in];
+            g_in = (GK == G_U8) ? T->g_codes : reinterpret_cast<const uint8_t*>(T->g_raw);
+            w_outp = T->w_codes[out];
+            m_outp = T->m_codes[out];
+            ms_out = T->m_scale[out];
+            mz_out = T->m_zp[out];
+            cnt_out = T->cnt[out];
+          } else {
+            aux = T->out;
+          }
+        }
+        const int gel = (MODE != MODE_STEP) ? 0 : (GK == G_U8 ? 1 : GK == G_F32 ? 4 : 2);
+        const int gbytes = gel * cols;
+        const bool slotted = a.slotted_in != 0;
+        for (int j = 0; j < B.nrows; ++j, ++it) {
+          const int s = it % S;
+          mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
+          uint8_t* st = stage_ptr(s);
+          StageCtx* cx = ctx_of(st);
+          uint32_t* bits = oldb_of(st);
+          for (int i = lane; i < (cp + 31) / 32; i += 32) bits[i] = 0u;
+          if (lane == j) {
+            cx->sw = sw;
+            cx->zw = zw;
+            cx->zpay = zw < 0 ? 0 : (zw > qmax ? qmax : zw);
+            cx->old_begin = ob;
+            cx->old_n = on;
+            if (MODE == MODE_STEP) {
+              cx->tmin = tmin;
+              cx->tmax = tmax;
+              cx->sm = smv;
+              cx->zm = zm;
+              cx->sg = sgv;
+              cx->zg = zg;
+              cx->slot_out = so;
+              cx->cap_out = co;
+            }
+          }
+          const int obj = __shfl_sync(0xffffffffu, ob, j);
+          const int onj = __shfl_sync(0xffffffffu, on, j);
+          const int lrow = B.row0 + j;
+          const size_t roff = (size_t)lrow * (size_t)cols;
+          const bool staged = ALIGNED && slotted && onj > 0 && ((obj & 3) == 0);
+          const int nstage = staged ? min((onj + 3) & ~3, OLDCAP) : 0;
+          uint8_t* data = data_of(st);
+          if (lane == 0) {
+            cx->row = lrow;
+            cx->lrow = lrow;
+            cx->cols = cols;
+            cx->old_staged = staged ? 1 : 0;
+            if (MODE == MODE_STEP) {
+              cx->w_out = w_outp + roff;
+              cx->m_out = m_outp + roff;
+              cx->m_scale_out = ms_out;
+              cx->m_zp_out = mz_out;
+              cx->cnt_out = cnt_out;
+            } else if (MODE == MODE_RECON_F32) {
+              cx->aux_out = reinterpret_cast<float*>(aux) + roff;
+            } else {
+              cx->aux_out = reinterpret_cast<__nv_bfloat16*>(aux) + roff;
+            }
+          }
+          if (!ALIGNED) {
+            // generic path (rows not 16-byte aligned): the producer lanes copy
+            const uint8_t* wsrc = reinterpret_cast<const uint8_t*>(
+                                      __shfl_sync(0xffffffffu, (unsigned long long)w_in, 0)) +
+                                  roff;
+            for (int i = lane; i < cols; i += 32) data[i] = wsrc[i];
+            if (MODE == MODE_STEP) {
+              const uint8_t* msrc = reinterpret_cast<const uint8_t*>(
+                                        __shfl_sync(0xffffffffu, (unsigned long long)m_in, 0)) +
+                                    roff;
+              const uint8_t* gsrc = reinterpret_cast<const uint8_t*>(
+                                        __shfl_sync(0xffffffffu, (unsigned long long)g_in, 0)) +
+                                    (size_t)gel * roff;
+              for (int i = lane; i < cols; i += 32) data[cp + i] = msrc[i];
+              for (int i = lane; i < gbytes; i += 32) data[2 * cp + i] = gsrc[i];
+            }
+          }
+          __syncwarp();
+          if (lane == 0) {
+            uint32_t tx = 0;
+            if (ALIGNED) tx += (MODE == MODE_STEP) ? (uint32_t)(2 * cols + gbytes) : (uint32_t)cols;
+            tx += 8u * (uint32_t)nstage;
+            if (tx) mbar_expect_tx(&full[s], tx);
+            if (ALIGNED) {
+              bulk_g2s(data, w_in + roff, cols, &full[s]);
+              if (MODE == MODE_STEP) {
+                bulk_g2s(data + cp, m_in + roff, cols, &full[s]);
+                bulk_g2s(data + 2 * cp, g_in + (size_t)gel * roff, gbytes, &full[s]);
+              }
+            }
+            if (nstage) {
+              bulk_g2s(oldc_of(st), a.col_in + obj, 4u * nstage, &full[s]);
+              bulk_g2s(oldv_of(st), a.val_in + obj, 4u * nstage, &full[s]);
+            }
+            mbar_arrive(&full[s]);
+          }
         }
       }
-      // single arrival (release) after every lane's ctx/bitmap/list stores; the
-      // phase completes once the bulk-copy bytes have landed as well.
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&full[s]);
+      const int s = it % S;
+      mbar_wait(&empty[s], ((uint32_t)(it / S) & 1u) ^ 1u);
+      if (lane == 0) {
+        ctx_of(stage_ptr(s))->row = -1;
+        mbar_arrive(&full[s]);
+      }
     }
   } else {
-    // ======================= CONSUMER WARPS ==============================
+    // ============================ CONSUMER WARPS ============================
     const int ct = threadIdx.x;  // 0..127
     const int cw = warp;
     Hyper h;
@@ -344,9 +435,8 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
 
     for (int it = 0;; ++it) {
       const int s = it % S;
-      const uint32_t round = (uint32_t)(it / S);
       const int par = it & 1;
-      mbar_wait(&full[s], round & 1u);
+      mbar_wait(&full[s], (uint32_t)(it / S) & 1u);
       uint8_t* st = stage_ptr(s);
       const StageCtx* cx = ctx_of(st);
       const int row = cx->row;
@@ -355,12 +445,22 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
       const int nvec = (cols + 15) >> 4;
       const int nch = (nvec + NCT - 1) / NCT;
       const uint8_t* data = data_of(st);
-      const uint32_t* obits = oldb_of(st);
+      uint32_t* obits = oldb_of(st);
       const int32_t* ocols = oldc_of(st);
       const float* ovals = oldv_of(st);
-      const int old_n = cx->old_n, old_begin = cx->old_begin;
-
+      const int old_n = kOld ? cx->old_n : 0;
+      const int old_begin = kOld ? cx->old_begin : 0;
+      const int staged = kOld ? cx->old_staged : 0;
       const DequantRow dw = make_dequant_row(cx->sw, cx->zw);
+
+      if (kOld) {
+        // old-outlier bitmap of this row (the producer cleared it)
+        for (int i = ct; i < old_n; i += NCT) {
+          const int col = (staged && i < OLDCAP) ? ocols[i] : a.col_in[old_begin + i];
+          atomicOr(&obits[col >> 5], 1u << (col & 31));
+        }
+        named_bar_sync(BAR_B0, NCT);
+      }
 
       if (MODE == MODE_RECON_F32 || MODE == MODE_RECON_BF16) {
         for (int k = 0; k < nch; ++k) {
@@ -377,7 +477,8 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
 #pragma unroll
             for (int e = 0; e < 16; ++e)
               if (o16 & (1u << e))
-                w[e] = old_value(ocols, ovals, old_n, old_begin, v * 16 + e, a.col_in, a.val_in);
+                w[e] = old_value(ocols, ovals, old_n, staged, old_begin, v * 16 + e, a.col_in,
+                                 a.val_in);
           }
           const int nvalid = min(16, cols - v * 16);
           if (MODE == MODE_RECON_F32) {
@@ -413,15 +514,14 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
       }
 
       // ---------------- STEP / DECOMPOSE ----------------
-      QuantRow qw;
-      {
-        // dense params derive from the cached thresholds (requantize_weight ->
-        // decompose_dense_sparse -> affine_params_from_bounds); the host keeps
-        // (w_scale, w_zp) == affine_params_from_bounds(t_min, t_max).
-        qw = make_quant_row(cx->sw, cx->zw, a.bit_width);
-      }
+      // dense params: stored (w_scale, w_zp) == affine_params_from_bounds(t_min, t_max)
+      // (requantize_weight -> decompose_dense_sparse, quantize.hpp:264), an invariant
+      // the host maintains because the params are only ever produced by decompose.
+      const QuantRow qw = make_quant_row(cx->sw, cx->zw, a.bit_width);
       const float tmin = cx->tmin, tmax = cx->tmax;
       const uint32_t zpay4 = (uint32_t)cx->zpay * 0x01010101u;
+      // dequantized w can only be non-finite if s*(qmax+|z|) overflows fp32
+      const bool w_ovf = !(__fmul_rn(fabsf(cx->sw), (float)qmax + fabsf((float)cx->zw)) < 3.0e38f);
       DequantRow dm, dg;
       QuantRow qg;
       if (MODE == MODE_STEP) {
@@ -429,7 +529,7 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
         if (GK == G_U8) dg = make_dequant_row(cx->sg, cx->zg);
       }
 
-      // ---- raw-gradient modes: fused quantize_state(g) -> dequantize(g)
+      // ---- raw-gradient modes: fused quantize_state(g) -> dequantize(g) (gradflow.hpp:77)
       if (MODE == MODE_STEP && GK != G_U8) {
         float lo = __int_as_float(0x7f800000), hi = __int_as_float(0xff800000);
         int nan0 = 0;
@@ -457,7 +557,7 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
           tabs->gred_hi[par][cw] = hi;
           tabs->gred_nan[par][cw] = nan0;
         }
-        named_bar_sync(3, NCT);
+        named_bar_sync(BAR_G, NCT);
         lo = tabs->gred_lo[par][0]; hi = tabs->gred_hi[par][0]; nan0 = tabs->gred_nan[par][0];
 #pragma unroll
         for (int w2 = 1; w2 < NCW; ++w2) {
@@ -522,20 +622,34 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
               for (int q = 0; q < 4; ++q) dequant4(gc[q], dg, g + 4 * q);
             }
             const uint32_t o16 = bits16(obits, v);
+            bool wspecial = w_ovf;  // non-finite w must take the general Lion form
             if (o16) {
 #pragma unroll
               for (int e = 0; e < 16; ++e)
-                if (o16 & (1u << e))
-                  w[e] = old_value(ocols, ovals, old_n, old_begin, v * 16 + e, a.col_in,
+                if (o16 & (1u << e)) {
+                  w[e] = old_value(ocols, ovals, old_n, staged, old_begin, v * 16 + e, a.col_in,
                                    a.val_in);
+                  wspecial |= !isfinite(w[e]);
+                }
             }
+            if (WD0 && !wspecial) {
 #pragma unroll
-            for (int p = 0; p < 8; ++p) {
-              float2 W = make_float2(w[2 * p], w[2 * p + 1]);
-              float2 M = make_float2(m[2 * p], m[2 * p + 1]);
-              lion2(W, M, make_float2(g[2 * p], g[2 * p + 1]), h);
-              w[2 * p] = W.x; w[2 * p + 1] = W.y;
-              m[2 * p] = M.x; m[2 * p + 1] = M.y;
+              for (int p = 0; p < 8; ++p) {
+                float2 W = make_float2(w[2 * p], w[2 * p + 1]);
+                float2 M = make_float2(m[2 * p], m[2 * p + 1]);
+                lion2_wd0(W, M, make_float2(g[2 * p], g[2 * p + 1]), h);
+                w[2 * p] = W.x; w[2 * p + 1] = W.y;
+                m[2 * p] = M.x; m[2 * p + 1] = M.y;
+              }
+            } else {
+#pragma unroll
+              for (int p = 0; p < 8; ++p) {
+                float2 W = make_float2(w[2 * p], w[2 * p + 1]);
+                float2 M = make_float2(m[2 * p], m[2 * p + 1]);
+                lion2(W, M, make_float2(g[2 * p], g[2 * p + 1]), h);
+                w[2 * p] = W.x; w[2 * p + 1] = W.y;
+                m[2 * p] = M.x; m[2 * p + 1] = M.y;
+              }
             }
             if (v == 0 && isnan(m[0])) mnan0 = 1;
             if (valid != 0xFFFFu) {
@@ -603,7 +717,27 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
           tabs->red_nan[par][cw] = mnan0;
         }
       }
-      named_bar_sync(1, NCT);  // ---- sync C
+      named_bar_sync(BAR_C, NCT);
+
+      // chunk-major CSR offsets of this warp: lane l < nch holds the offset of
+      // (chunk l, this warp) inside the row
+      int tot_l = 0, mine_l = 0;
+      if (lane < nch) {
+#pragma unroll
+        for (int w2 = 0; w2 < NCW; ++w2) {
+          const int cv = tabs->cnt[par][lane][w2];
+          tot_l += cv;
+          if (w2 < cw) mine_l += cv;
+        }
+      }
+      int incl_l = tot_l;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl_l, d);
+        if (lane >= d) incl_l += t;
+      }
+      const int chunk_pref = incl_l - tot_l + mine_l;
+      const int row_total = __shfl_sync(0xffffffffu, incl_l, nch - 1);
 
       QuantRow qm;
       if (MODE == MODE_STEP) {
@@ -625,35 +759,20 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
         if (ct == 0) {
           cx->m_scale_out[cx->lrow] = smv;
           cx->m_zp_out[cx->lrow] = zmv;
+          cx->cnt_out[cx->lrow] = row_total;
+          if (row_total > cx->cap_out) atomicOr(&a.hdr->overflow, 1u);
         }
       }
 
-      if (cw == 0) {
-        // ---- per-(chunk,warp) exclusive prefix table + row total
-        const int ne = nch * NCW;
-        int loc[4];
-        int sum = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int e = lane * 4 + j;
-          loc[j] = (e < ne) ? tabs->cnt[par][e / NCW][e % NCW] : 0;
-          sum += loc[j];
-        }
-        int incl = sum;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const int t = __shfl_up_sync(0xffffffffu, incl, d);
-          if (lane >= d) incl += t;
-        }
-        const uint32_t total = (uint32_t)__shfl_sync(0xffffffffu, incl, 31);
-        int run = incl - sum;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int e = lane * 4 + j;
-          if (e < ne) tabs->pre[par][e / NCW][e % NCW] = run;
-          run += loc[j];
-        }
-        // ---- decoupled look-back over the per-row status words
+      int row_base_out = 0, row_cap = 0x7fffffff;
+      if (MODE == MODE_STEP) {
+        row_base_out = cx->slot_out;
+        row_cap = cx->cap_out;
+      }
+
+      if (MODE == MODE_DECOMPOSE && cw == 0) {
+        // ---- decoupled look-back over the per-row status words (strict CSR)
+        const uint32_t total = (uint32_t)row_total;
         uint32_t excl = 0;
         if (row > 0) {
           if (lane == 0) st_relaxed_u64(a.status + row, pack_status(epoch, FLAG_A, total));
@@ -723,12 +842,16 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
         }
       }
 
-      named_bar_sync(2, NCT);  // ---- sync D: row CSR offset known
+      if (MODE == MODE_DECOMPOSE) {
+        named_bar_sync(BAR_D, NCT);  // the row's offset from the look-back
+        row_base_out = tabs->prefix[par];
+      }
 
-      // ================= ordered CSR write =================
+      // ================= CSR write (ascending columns) =================
       {
-        const int prefix = tabs->prefix[par];
+        const int64_t cap = (MODE == MODE_DECOMPOSE) ? a.cap_out : (int64_t)row_cap;
         for (int k = 0; k < nch; ++k) {
+          const int pref_k = __shfl_sync(0xffffffffu, chunk_pref, k);
           if (tabs->cnt[par][k][cw] == 0) continue;  // warp-uniform
           const int v = k * NCT + ct;
           uint32_t mask = (v < nvec) ? (uint32_t)masks[v] : 0u;
@@ -739,7 +862,7 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
             const int t = __shfl_up_sync(0xffffffffu, incl, d);
             if (lane >= d) incl += t;
           }
-          int pos = prefix + tabs->pre[par][k][cw] + incl - c;
+          int pos = pref_k + incl - c;
           while (mask) {
             const int e = __ffs(mask) - 1;
             mask &= mask - 1u;
@@ -748,32 +871,25 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
             if (MODE == MODE_DECOMPOSE) {
               val = reinterpret_cast<const float*>(data)[col];
             } else {
-              // recompute w' for this element exactly as pass 1 did
-              float wv = (dw.fast)
-                             ? __fmul_rn(__fadd_rn(magic_byte(data[col], 0), dw.negc), dw.s)
-                             : dequant_exact(data[col], dw.s, dw.z);
+              // recompute w' for this element exactly as pass 1 did (scalar, exact)
+              float wv = dequant1(data[col], dw);
               if (bits16(obits, v) & (1u << e))
-                wv = old_value(ocols, ovals, old_n, old_begin, col, a.col_in, a.val_in);
-              const uint32_t mc = data[cp + col];
-              float mv = dm.fast ? __fmul_rn(__fadd_rn(magic_byte(mc, 0), dm.negc), dm.s)
-                                 : dequant_exact(mc, dm.s, dm.z);
+                wv = old_value(ocols, ovals, old_n, staged, old_begin, col, a.col_in, a.val_in);
+              float mv = dequant1(data[cp + col], dm);
               float gv;
               if (GK == G_U8) {
-                const uint32_t gc = data[2 * cp + col];
-                gv = dg.fast ? __fmul_rn(__fadd_rn(magic_byte(gc, 0), dg.negc), dg.s)
-                             : dequant_exact(gc, dg.s, dg.z);
+                gv = dequant1(data[2 * cp + col], dg);
               } else {
                 const float gr = load_graw<GK>(data + 2 * cp, col);
-                const uint32_t gc = quant_exact(gr, qg.s, qg.z, qg.qmax);
-                gv = dg.fast ? __fmul_rn(__fadd_rn(magic_byte(gc, 0), dg.negc), dg.s)
-                             : dequant_exact(gc, dg.s, dg.z);
+                gv = dequant1(quant_exact(gr, qg.s, qg.z, qg.qmax), dg);
               }
               lion1(wv, mv, gv, h);
               val = wv;
             }
-            if (pos < a.cap_out) {
-              a.col_out[pos] = col;
-              a.val_out[pos] = val;
+            if (pos < cap) {
+              const int64_t dst = (int64_t)row_base_out + pos;
+              a.col_out[dst] = col;
+              a.val_out[dst] = val;
             }
             ++pos;
           }
@@ -800,9 +916,9 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
 // ----------------------------------------------------------------------------
 // host-side launcher
 // ----------------------------------------------------------------------------
-template <int MODE, int GK, bool AL>
+template <int MODE, int GK, bool AL, bool WD0>
 static cudaError_t launch_t(const LaunchArgs& a, size_t smem, cudaStream_t st, int* grid_out) {
-  auto k = row_engine_kernel<MODE, GK, AL>;
+  auto k = row_engine_kernel<MODE, GK, AL, WD0>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
@@ -812,7 +928,8 @@ static cudaError_t launch_t(const LaunchArgs& a, size_t smem, cudaStream_t st, i
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int grid = sms * per_sm;
-  if (grid > a.total_rows) grid = a.total_rows;
+  const int work = (MODE == MODE_DECOMPOSE) ? a.total_rows : a.n_blocks;
+  if (grid > work) grid = work;
   if (grid < 1) grid = 1;
   k<<<grid, NT, smem, st>>>(a);
   if (grid_out) *grid_out = grid;
@@ -823,19 +940,26 @@ cudaError_t launch_row_engine(int mode, int gk, const LaunchArgs& a, cudaStream_
                               int* grid_out) {
   const size_t smem = row_engine_smem(mode, gk, a.cols_p, a.stages);
   const bool al = a.use_bulk != 0;
-#define QFT_L(M, G)                                                            \
-  return al ? launch_t<M, G, true>(a, smem, st, grid_out)                      \
-            : launch_t<M, G, false>(a, smem, st, grid_out)
+  const bool wd0 = (a.wd == 0.0f);
+#define QFT_L(M, G)                                                              \
+  if (wd0) return al ? launch_t<M, G, true, true>(a, smem, st, grid_out)        \
+                     : launch_t<M, G, false, true>(a, smem, st, grid_out);      \
+  return al ? launch_t<M, G, true, false>(a, smem, st, grid_out)                \
+            : launch_t<M, G, false, false>(a, smem, st, grid_out)
+#define QFT_L1(M)                                                                \
+  return al ? launch_t<M, G_U8, true, false>(a, smem, st, grid_out)             \
+            : launch_t<M, G_U8, false, false>(a, smem, st, grid_out)
   switch (mode) {
     case MODE_STEP:
-      if (gk == G_U8) QFT_L(MODE_STEP, G_U8);
-      if (gk == G_F32) QFT_L(MODE_STEP, G_F32);
-      QFT_L(MODE_STEP, G_BF16);
-    case MODE_DECOMPOSE: QFT_L(MODE_DECOMPOSE, G_U8);
-    case MODE_RECON_F32: QFT_L(MODE_RECON_F32, G_U8);
-    default: QFT_L(MODE_RECON_BF16, G_U8);
+      if (gk == G_U8) { QFT_L(MODE_STEP, G_U8); }
+      if (gk == G_F32) { QFT_L(MODE_STEP, G_F32); }
+      { QFT_L(MODE_STEP, G_BF16); }
+    case MODE_DECOMPOSE: QFT_L1(MODE_DECOMPOSE);
+    case MODE_RECON_F32: QFT_L1(MODE_RECON_F32);
+    default: QFT_L1(MODE_RECON_BF16);
   }
 #undef QFT_L
+#undef QFT_L1
 }
 
 }  // namespace qftk

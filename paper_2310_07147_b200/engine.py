@@ -9,12 +9,16 @@ params), laid out for one B200:
   model's W codes are one 6.7 GB buffer for LLaMA-2-7B, so host<->device
   transfers are single large copies;
 * ping-pong sets ``[0]/[1]`` for every array a step rewrites (W codes, m codes,
-  m params, row_ptr, CSR arena): step ``k`` reads set ``cur`` and writes
-  ``1-cur``, so an overflowing CSR arena can be grown and the step re-run from
-  intact inputs;
+  m params, CSR counts and arena): step ``k`` reads set ``cur`` and writes
+  ``1-cur``, so an overflowing CSR slot can be re-planned and the step re-run
+  from intact inputs;
+* outliers in a SLOTTED CSR: row r owns a 16-byte aligned slot
+  ``[row_start[r], row_start[r+1])`` of its group's arena, sized from its count +
+  25% + 8; ``row_count[r]`` entries are used.  Rows never wait on each other
+  inside the step; the strict reference CSR is produced by compaction
+  (``export_tensor``);
 * tensors grouped by row length; each group is ONE persistent kernel launch
-  (``qftc_plan_step``) with its own CSR arena whose ``row_ptr`` values are
-  absolute offsets.
+  (``qftc_plan_step``) with its own arena.
 
 The hot path is ``step()``: one launch per width class, no host synchronisation.
 """
@@ -28,9 +32,10 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .quantize import _p, _stream, compute_outlier_thresholds, kind_from_name
+from .quantize import _p, _stream, kind_from_name
 
 _GRAD_KINDS = {"u8": N.GRAD_U8, "f32": N.GRAD_F32, "bf16": N.GRAD_BF16}
+SLACK = 8
 
 
 @dataclass
@@ -38,19 +43,14 @@ class _Group:
     cols: int
     members: List[int]
     rows: int
-    col: List[torch.Tensor]
-    val: List[torch.Tensor]
+    col: List[Optional[torch.Tensor]]
+    val: List[Optional[torch.Tensor]]
     plan: Optional[C.c_void_p] = None
-    nnz: int = 0  # nnz of the arena of the current set
-
-
-def _cap_for(nnz: int, rows: int) -> int:
-    return int(nnz * 1.25) + 8 * rows + 1024
 
 
 class QftModelState:
     def __init__(self, shapes: Sequence[Tuple[int, int]], bit_width: int = 8,
-                 grad_kind: str = "u8", device="cuda"):
+                 grad_kind: str = "u8", device="cuda", pad_to: int = 0):
         if bit_width < 2 or bit_width > 8:
             raise ValueError(f"bit width must be in [2, 8], got {bit_width}")
         self.shapes = [(int(r), int(c)) for r, c in shapes]
@@ -60,16 +60,16 @@ class QftModelState:
         self.device = torch.device(device)
         self.cur = 0
         self.steps = 0
+        self.replans = 0
         sizes = [r * c for r, c in self.shapes]
         self.param_count = int(sum(sizes))
-        self.row_count = int(sum(r for r, _ in self.shapes))
-        # flat offsets (elements) and row offsets
+        self.row_count_total = int(sum(r for r, _ in self.shapes))
         self.off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
         self.roff = np.concatenate([[0], np.cumsum([r for r, _ in self.shapes])]).astype(np.int64)
-        self.rpoff = self.roff + np.arange(self.n + 1)  # row_ptr slices have rows+1 entries
-        dev, P, R = self.device, self.param_count, self.row_count
+        self.rpoff = self.roff + np.arange(self.n + 1)  # row_start slices have rows+1 entries
+        dev, P, R = self.device, self.param_count, self.row_count_total
         u8, f32, i32 = torch.uint8, torch.float32, torch.int32
-        self.w_codes = [torch.empty(P, dtype=u8, device=dev) for _ in range(2)]
+        self.w_codes = [torch.zeros(max(P, pad_to), dtype=u8, device=dev) for _ in range(2)]
         self.m_codes = [torch.zeros(P, dtype=u8, device=dev) for _ in range(2)]
         self.w_scale = torch.empty(R, dtype=f32, device=dev)
         self.w_zp = torch.empty(R, dtype=i32, device=dev)
@@ -78,7 +78,8 @@ class QftModelState:
         # LionState::init: quantize_state(zeros) -> scale 2^-20, z 0, codes 0
         self.m_scale = [torch.full((R,), 2.0 ** -20, dtype=f32, device=dev) for _ in range(2)]
         self.m_zp = [torch.zeros(R, dtype=i32, device=dev) for _ in range(2)]
-        self.row_ptr = [torch.zeros(R + self.n, dtype=i32, device=dev) for _ in range(2)]
+        self.row_start = [torch.zeros(R + self.n, dtype=i32, device=dev) for _ in range(2)]
+        self.row_count = [torch.zeros(R, dtype=i32, device=dev) for _ in range(2)]
         if self.grad_kind == N.GRAD_U8:
             self.g_codes = torch.zeros(P, dtype=u8, device=dev)
             self.g_scale = torch.ones(R, dtype=f32, device=dev)
@@ -87,8 +88,7 @@ class QftModelState:
         else:
             self.g_codes = self.g_scale = self.g_zp = None
             gdt = f32 if self.grad_kind == N.GRAD_F32 else torch.bfloat16
-            self.g_raw = torch.zeros(P, dtype=gdt, device=dev)
-        # width classes -> grouped launches
+            self.g_raw = torch.zeros(max(P, pad_to), dtype=gdt, device=dev)
         by_cols: Dict[int, List[int]] = {}
         for i, (_, c) in enumerate(self.shapes):
             by_cols.setdefault(c, []).append(i)
@@ -106,20 +106,65 @@ class QftModelState:
     def _rows(self, flat, i):
         return flat[self.roff[i]:self.roff[i + 1]]
 
-    def _rp(self, flat, i):
+    def _rs(self, flat, i):
         return flat[self.rpoff[i]:self.rpoff[i + 1]]
 
     def grad_views(self, i):
-        """(codes [r,c] u8, scale [r], zero_point [r]) -- the GradientStack entry of tensor i."""
+        """The GradientStack entry of tensor i: (codes [r,c] u8, scale [r], zero_point [r]),
+        or the raw [r,c] gradient for grad kinds f32/bf16."""
         if self.grad_kind != N.GRAD_U8:
             return self._sl(self.g_raw, i)
         return self._sl(self.g_codes, i), self._rows(self.g_scale, i), self._rows(self.g_zp, i)
 
-    # ------------------------------------------------------------------ init
-    def _arena_alloc(self, g: _Group, cap: int, k: int):
-        g.col[k] = torch.empty(max(cap, 1), dtype=torch.int32, device=self.device)
-        g.val[k] = torch.empty(max(cap, 1), dtype=torch.float32, device=self.device)
+    # ------------------------------------------------------------------ arenas / slots
+    def _alloc(self, cap: int):
+        return (torch.empty(max(cap, 4), dtype=torch.int32, device=self.device),
+                torch.empty(max(cap, 4), dtype=torch.float32, device=self.device))
 
+    def _ensure(self, g: _Group, k: int, need: int, keep: int):
+        if g.col[k] is not None and g.col[k].numel() >= need:
+            return
+        col, val = self._alloc(int(need * 1.1) + 1024)
+        if keep and g.col[k] is not None:
+            col[:keep].copy_(g.col[k][:keep])
+            val[:keep].copy_(g.val[k][:keep])
+        g.col[k], g.val[k] = col, val
+
+    def _place_strict(self, g: _Group, i: int, k: int, base: int, rp: torch.Tensor,
+                      col: torch.Tensor, val: torch.Tensor) -> int:
+        """Put tensor i's strict CSR (device row_ptr/col/val) into slots of arena k at
+        `base`; returns the new arena end."""
+        r = self.shapes[i][0]
+        rs = self._rs(self.row_start[k], i)
+        total = C.c_int64(0)
+        # slot = count + edge codes + 25% + 8: dense elements at code 0 / qmax are
+        # the ones requantization can push outside the thresholds (SURVEY.md §0,
+        # finding 2: on rows whose threshold sits among spikes dozens move at once)
+        codes = self._sl(self.w_codes[k], i)
+        qmax = (1 << self.bit_width) - 1
+        edge = ((codes == 0) | (codes == qmax)).sum(dim=1, dtype=torch.int32)
+        want = (rp[1:] - rp[:-1]) + edge
+        N.check(N.lib.qftc_csr_plan_slots(_p(want), None, r, SLACK, _p(rs), C.byref(total),
+                                          _stream()))
+        rs += base
+        end = base + int(total.value)
+        self._ensure(g, k, end, keep=base)
+        N.check(N.lib.qftc_csr_copy_rows(r, _p(rp), None, _p(col), _p(val), _p(rs),
+                                         _p(g.col[k]), _p(g.val[k]), g.col[k].numel(),
+                                         _stream()))
+        self._rows(self.row_count[k], i).copy_(rp[1:] - rp[:-1])
+        return end
+
+    def _mirror_layout(self, g: _Group, src: int):
+        """Give the other set the same slot layout and an arena of the same size."""
+        dst = 1 - src
+        for i in g.members:
+            self._rs(self.row_start[dst], i).copy_(self._rs(self.row_start[src], i))
+        need = g.col[src].numel()
+        if g.col[dst] is None or g.col[dst].numel() < need:
+            g.col[dst], g.val[dst] = self._alloc(need)
+
+    # ------------------------------------------------------------------ init
     def init_from_weights(self, weight_fn, fraction: float = 0.01, kind="percentile"):
         """Decompose every tensor on the device (decompose_weight, quantize.hpp:301-314).
 
@@ -127,8 +172,6 @@ class QftModelState:
         k = kind_from_name(kind)
         cur = self.cur
         for g in self.groups:
-            cap = _cap_for(int(fraction * g.rows * g.cols) + g.rows, g.rows)
-            self._arena_alloc(g, cap, cur)
             base = 0
             for i in g.members:
                 r, c = self.shapes[i]
@@ -136,24 +179,24 @@ class QftModelState:
                 tmn, tmx = self._rows(self.t_min, i), self._rows(self.t_max, i)
                 N.check(N.lib.qftc_outlier_thresholds(_p(w), r, c, float(fraction), k, _p(tmn),
                                                       _p(tmx), _stream()))
+                rp = torch.empty(r + 1, dtype=torch.int32, device=self.device)
+                cap = int(fraction * r * c) + 4 * r + 1024
                 while True:
-                    cap_left = g.col[cur].numel() - base
+                    col, val = self._alloc(cap)
                     nnz = C.c_int64(0)
-                    rp = self._rp(self.row_ptr[cur], i)
                     rc = N.lib.qftc_decompose_dense_sparse(
                         _p(w), r, c, _p(tmn), _p(tmx), self.bit_width,
                         _p(self._sl(self.w_codes[cur], i)), _p(self._rows(self.w_scale, i)),
-                        _p(self._rows(self.w_zp, i)), _p(rp), _p(g.col[cur][base:]),
-                        _p(g.val[cur][base:]), cap_left, C.byref(nnz), _stream())
+                        _p(self._rows(self.w_zp, i)), _p(rp), _p(col), _p(val), cap,
+                        C.byref(nnz), _stream())
                     if rc == N.QFTC_EOVERFLOW:
-                        self._grow(g, cur, base + int(nnz.value), keep=base)
+                        cap = int(nnz.value) + 1024
                         continue
                     N.check(rc)
                     break
-                rp += base
-                base += int(nnz.value)
-                del w
-            g.nnz = base
+                base = self._place_strict(g, i, cur, base, rp, col, val)
+                del w, col, val
+            self._mirror_layout(g, cur)
         self._make_plans()
 
     def init_from_host(self, tensors: Sequence[dict]):
@@ -161,40 +204,30 @@ class QftModelState:
         codes, scale, zero_point, t_min, t_max, row_ptr, col_idx, values (the
         DenseSparseWeight) and optionally m_codes, m_scale, m_zero_point."""
         cur = self.cur
+
+        def dv(a, dt):
+            return torch.as_tensor(np.ascontiguousarray(a)).to(self.device, dt)
+
         for g in self.groups:
-            nnz = sum(int(tensors[i]["row_ptr"][-1]) for i in g.members)
-            self._arena_alloc(g, _cap_for(nnz, g.rows), cur)
             base = 0
             for i in g.members:
                 t = tensors[i]
-                cp = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a)).to(self.device, dt)
-                self._sl(self.w_codes[cur], i).copy_(cp(t["codes"], torch.uint8))
-                self._rows(self.w_scale, i).copy_(cp(t["scale"], torch.float32))
-                self._rows(self.w_zp, i).copy_(cp(t["zero_point"], torch.int32))
-                self._rows(self.t_min, i).copy_(cp(t["t_min"], torch.float32))
-                self._rows(self.t_max, i).copy_(cp(t["t_max"], torch.float32))
-                rp = np.asarray(t["row_ptr"], np.int64)
-                self._rp(self.row_ptr[cur], i).copy_(cp(rp + base, torch.int32))
-                n = int(rp[-1])
-                if n:
-                    g.col[cur][base:base + n].copy_(cp(t["col_idx"], torch.int32))
-                    g.val[cur][base:base + n].copy_(cp(t["values"], torch.float32))
+                self._sl(self.w_codes[cur], i).copy_(dv(t["codes"], torch.uint8))
+                self._rows(self.w_scale, i).copy_(dv(t["scale"], torch.float32))
+                self._rows(self.w_zp, i).copy_(dv(t["zero_point"], torch.int32))
+                self._rows(self.t_min, i).copy_(dv(t["t_min"], torch.float32))
+                self._rows(self.t_max, i).copy_(dv(t["t_max"], torch.float32))
                 if "m_codes" in t:
-                    self._sl(self.m_codes[cur], i).copy_(cp(t["m_codes"], torch.uint8))
-                    self._rows(self.m_scale[cur], i).copy_(cp(t["m_scale"], torch.float32))
-                    self._rows(self.m_zp[cur], i).copy_(cp(t["m_zero_point"], torch.int32))
-                base += n
-            g.nnz = base
+                    self._sl(self.m_codes[cur], i).copy_(dv(t["m_codes"], torch.uint8))
+                    self._rows(self.m_scale[cur], i).copy_(dv(t["m_scale"], torch.float32))
+                    self._rows(self.m_zp[cur], i).copy_(dv(t["m_zero_point"], torch.int32))
+                rp = dv(t["row_ptr"], torch.int32)
+                col = dv(np.append(np.asarray(t["col_idx"], np.int32), np.int32(0)), torch.int32)
+                val = dv(np.append(np.asarray(t["values"], np.float32), np.float32(0)),
+                         torch.float32)
+                base = self._place_strict(g, i, cur, base, rp, col, val)
+            self._mirror_layout(g, cur)
         self._make_plans()
-
-    def _grow(self, g: _Group, k: int, need: int, keep: int):
-        cap = _cap_for(need, g.rows)
-        col = torch.empty(cap, dtype=torch.int32, device=self.device)
-        val = torch.empty(cap, dtype=torch.float32, device=self.device)
-        if keep:
-            col[:keep].copy_(g.col[k][:keep])
-            val[:keep].copy_(g.val[k][:keep])
-        g.col[k], g.val[k] = col, val
 
     # ------------------------------------------------------------------ plans
     def _descs(self, g: _Group):
@@ -205,7 +238,8 @@ class QftModelState:
             d.rows, d.cols = r, c
             for k in range(2):
                 d.w_codes[k] = self._sl(self.w_codes[k], i).data_ptr()
-                d.row_ptr[k] = self._rp(self.row_ptr[k], i).data_ptr()
+                d.row_start[k] = self._rs(self.row_start[k], i).data_ptr()
+                d.row_count[k] = self._rows(self.row_count[k], i).data_ptr()
                 d.m_codes[k] = self._sl(self.m_codes[k], i).data_ptr()
                 d.m_scale[k] = self._rows(self.m_scale[k], i).data_ptr()
                 d.m_zero_point[k] = self._rows(self.m_zp[k], i).data_ptr()
@@ -222,16 +256,17 @@ class QftModelState:
         return arr
 
     def _arena_args(self, g: _Group):
-        cols = (C.c_void_p * 2)(*[t.data_ptr() if t is not None else None for t in g.col])
-        vals = (C.c_void_p * 2)(*[t.data_ptr() if t is not None else None for t in g.val])
-        caps = (C.c_int64 * 2)(*[t.numel() if t is not None else 0 for t in g.col])
+        cols = (C.c_void_p * 2)(*[t.data_ptr() for t in g.col])
+        vals = (C.c_void_p * 2)(*[t.data_ptr() for t in g.val])
+        caps = (C.c_int64 * 2)(*[t.numel() for t in g.col])
         return cols, vals, caps
+
+    def _set_arena(self, g: _Group):
+        cols, vals, caps = self._arena_args(g)
+        N.check(N.lib.qftc_plan_set_arena(g.plan, cols, vals, caps))
 
     def _make_plans(self):
         for g in self.groups:
-            nxt = 1 - self.cur
-            if g.col[nxt] is None:
-                self._arena_alloc(g, _cap_for(g.nnz, g.rows), nxt)
             if g.plan is not None:
                 N.lib.qftc_plan_destroy(g.plan)
             arr = self._descs(g)
@@ -250,16 +285,31 @@ class QftModelState:
                     pass
                 g.plan = None
 
+    def ensure_arena_capacity(self, cap: int):
+        """Give every group's arenas (both sets) >= cap entries (collectives over arenas
+        need a rank-uniform size); keeps the current set's content."""
+        for g in self.groups:
+            for k in range(2):
+                if g.col[k].numel() < cap:
+                    col, val = self._alloc(cap)
+                    if k == self.cur:
+                        n = g.col[k].numel()
+                        col[:n].copy_(g.col[k])
+                        val[:n].copy_(g.val[k])
+                    g.col[k], g.val[k] = col, val
+            if g.plan is not None:
+                self._set_arena(g)
+
     # ------------------------------------------------------------------ the step
     def launches_per_step(self) -> int:
         return len(self.groups)
 
     def step(self, lr=1e-4, beta1=0.9, beta2=0.99, weight_decay=0.0, check: bool = False):
         """One quantized Lion step over the whole model (lion_step_quantized,
-        optimizer.hpp:85-120): one fused kernel launch per width class, enqueued on
-        the current stream without host synchronisation.  ``check=True`` also
-        synchronises, validates, and transparently re-runs after growing a CSR arena
-        that overflowed (the inputs of the step are intact in the other set)."""
+        optimizer.hpp:85-120): one fused kernel launch per width class, enqueued on the
+        current stream without host synchronisation.  ``check=True`` also synchronises,
+        validates, and transparently re-plans CSR slots that overflowed and re-runs
+        (the step's inputs are intact in the other set)."""
         h = N.hyper(lr, beta1, beta2, weight_decay)
         flip = self.cur
         for g in self.groups:
@@ -269,47 +319,75 @@ class QftModelState:
         if check:
             self._check(flip, h)
 
+    def _replan(self, g: _Group, k: int):
+        """Slots of set k re-sized from its (true) counts."""
+        base = 0
+        for i in g.members:
+            r = self.shapes[i][0]
+            rs = self._rs(self.row_start[k], i)
+            total = C.c_int64(0)
+            N.check(N.lib.qftc_csr_plan_slots(_p(self._rows(self.row_count[k], i)), None, r,
+                                              SLACK, _p(rs), C.byref(total), _stream()))
+            rs += base
+            base += int(total.value)
+        if g.col[k].numel() < base:
+            g.col[k], g.val[k] = self._alloc(base)
+
     def _check(self, flip, h):
+        out = 1 - flip
         for g in self.groups:
+            replanned = False
             while True:
-                nnz = C.c_int64(0)
-                rc = N.lib.qftc_plan_result(g.plan, C.byref(nnz), _stream())
+                rc = N.lib.qftc_plan_result(g.plan, None, _stream())
                 if rc == N.QFTC_EOVERFLOW:
-                    self._grow(g, 1 - flip, int(nnz.value), keep=0)
-                    cols, vals, caps = self._arena_args(g)
-                    N.check(N.lib.qftc_plan_set_arena(g.plan, cols, vals, caps))
+                    self._replan(g, out)
+                    self._set_arena(g)
                     N.check(N.lib.qftc_plan_step(g.plan, flip, h, _stream()))
+                    replanned = True
+                    self.replans += 1
                     continue
                 N.check(rc)
-                g.nnz = int(nnz.value)
                 break
+            if replanned:  # the dead input set takes the new layout for the next step
+                self._mirror_layout(g, out)
+                self._set_arena(g)
 
     def check(self):
         """Synchronise and validate the last step (raises on overflow / bad rows)."""
         for g in self.groups:
-            nnz = C.c_int64(0)
-            N.check(N.lib.qftc_plan_result(g.plan, C.byref(nnz), _stream()))
-            g.nnz = int(nnz.value)
+            N.check(N.lib.qftc_plan_result(g.plan, None, _stream()))
 
     # ------------------------------------------------------------------ export
     def nnz(self) -> int:
-        return int(sum(g.nnz for g in self.groups))
+        return int(self.row_count[self.cur].sum().item())
+
+    def group_nnz(self, g: _Group, k: Optional[int] = None) -> int:
+        k = self.cur if k is None else k
+        return int(sum(self._rows(self.row_count[k], i).sum().item() for i in g.members))
 
     def export_tensor(self, i: int) -> dict:
-        """Reference-layout host copy of tensor i (DenseSparseWeight + momentum)."""
+        """Reference-layout host copy of tensor i (DenseSparseWeight + momentum); the
+        slotted CSR is compacted into the strict one on the device."""
         cur = self.cur
         g = self.groups[self.group_of[i]]
-        rp = self._rp(self.row_ptr[cur], i).cpu().numpy().astype(np.int64)
-        b, e = int(rp[0]), int(rp[-1])
+        r = self.shapes[i][0]
+        cnt = self._rows(self.row_count[cur], i)
+        n = int(cnt.sum().item())
+        rp = torch.empty(r + 1, dtype=torch.int32, device=self.device)
+        col, val = self._alloc(n)
+        nnz = C.c_int64(0)
+        N.check(N.lib.qftc_csr_compact(r, _p(self._rs(self.row_start[cur], i)), _p(cnt),
+                                       _p(g.col[cur]), _p(g.val[cur]), _p(rp), _p(col), _p(val),
+                                       col.numel(), C.byref(nnz), _stream()))
         return dict(
             codes=self._sl(self.w_codes[cur], i).cpu().numpy(),
             scale=self._rows(self.w_scale, i).cpu().numpy(),
             zero_point=self._rows(self.w_zp, i).cpu().numpy(),
             t_min=self._rows(self.t_min, i).cpu().numpy(),
             t_max=self._rows(self.t_max, i).cpu().numpy(),
-            row_ptr=(rp - b).astype(np.int32),
-            col_idx=g.col[cur][b:e].cpu().numpy(),
-            values=g.val[cur][b:e].cpu().numpy(),
+            row_ptr=rp.cpu().numpy(),
+            col_idx=col[:n].cpu().numpy(),
+            values=val[:n].cpu().numpy(),
             m_codes=self._sl(self.m_codes[cur], i).cpu().numpy(),
             m_scale=self._rows(self.m_scale[cur], i).cpu().numpy(),
             m_zero_point=self._rows(self.m_zp[cur], i).cpu().numpy(),
@@ -321,8 +399,9 @@ class QftModelState:
         g = self.groups[self.group_of[i]]
         r, c = self.shapes[i]
         out = torch.empty((r, c), dtype=dtype, device=self.device)
-        fn = N.lib.qftc_reconstruct if dtype == torch.float32 else N.lib.qftc_reconstruct_bf16
-        N.check(fn(_p(self._sl(self.w_codes[cur], i)), r, c, _p(self._rows(self.w_scale, i)),
-                   _p(self._rows(self.w_zp, i)), _p(self._rp(self.row_ptr[cur], i)),
-                   _p(g.col[cur]), _p(g.val[cur]), _p(out), _stream()))
+        N.check(N.lib.qftc_reconstruct_slots(
+            _p(self._sl(self.w_codes[cur], i)), r, c, _p(self._rows(self.w_scale, i)),
+            _p(self._rows(self.w_zp, i)), _p(self._rs(self.row_start[cur], i)),
+            _p(self._rows(self.row_count[cur], i)), _p(g.col[cur]), _p(g.val[cur]), _p(out),
+            0 if dtype == torch.float32 else 1, _stream()))
         return out

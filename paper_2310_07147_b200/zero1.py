@@ -1,0 +1,214 @@
+"""ZeRO-1 row-sharded QFT Lion step over NCCL.
+
+Every quantity of the update is per ROW (scales, zero points, thresholds, the m'
+min/max, the CSR segment), so a row-range shard needs no communication inside
+the update.  The exchange steps are the data-parallel ones:
+
+1. ``reduce_scatter_tensor(SUM)`` of the fp gradient, laid out SHARD-MAJOR
+   ([rank0's rows of every tensor | rank1's rows | ...], each rank block padded to
+   the same length) so one collective hands every rank exactly its rows.  The sum
+   is taken in fp before quantisation: the reference quantizes the full gradient
+   once (gradflow.hpp:77), and quantize_state is per-row, so quantizing the
+   shard rows of the summed gradient equals quantizing the full summed gradient.
+2. the fused local step on the shard (grad kind f32/bf16: quantize_state(g) ->
+   dequantize fused into the kernel); momentum stays sharded (ZeRO-1);
+3. ``all_gather_into_tensor`` of the updated W codes, of the slotted-CSR row
+   starts and counts and of the CSR arenas (fixed, rank-uniform capacity, so no
+   host round trip is needed to size the gather); slot offsets are
+   arena-absolute, so rank k's segment is re-based by ``k * arena_capacity`` when
+   read from the gathered buffer.
+
+The local update is pluggable: on GPUs it is :class:`CudaShard` (the fused
+sm_100a kernel through the C-ABI); the CPU tests plug the oracle in to check the
+collective choreography with gloo.
+"""
+from __future__ import annotations
+
+from typing import Dict, List, Sequence, Tuple
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+Shape = Tuple[int, int]
+
+
+class ShardLayout:
+    """Row ranges of every tensor per rank and the shard-major flat layout."""
+
+    def __init__(self, shapes: Sequence[Shape], world: int):
+        self.shapes = [(int(r), int(c)) for r, c in shapes]
+        self.world = world
+        self.widths = sorted({c for _, c in self.shapes})
+        self.members: List[List[Tuple[int, int, int]]] = []   # per rank: (tensor, lo, hi)
+        self.numel: List[int] = []
+        self.rows: List[int] = []
+        for k in range(world):
+            mem = []
+            for i, (r, c) in enumerate(self.shapes):
+                lo, hi = (r * k) // world, (r * (k + 1)) // world
+                if hi > lo:
+                    mem.append((i, lo, hi))
+            self.members.append(mem)
+            self.numel.append(sum((hi - lo) * self.shapes[i][1] for i, lo, hi in mem))
+            self.rows.append(sum(hi - lo for _, lo, hi in mem))
+        self.pad = max(self.numel)                      # elements per rank block
+        self.rp_pad = max(self.rows[k] + len(self.members[k]) for k in range(world))
+        self.rpad = max(self.rows)
+        # element offset of (rank k, j-th member) inside rank k's block
+        self.off: List[List[int]] = []
+        self.rpoff: List[List[int]] = []
+        self.roff: List[List[int]] = []
+        for k in range(world):
+            o, rp, ro = [0], [0], [0]
+            for i, lo, hi in self.members[k]:
+                o.append(o[-1] + (hi - lo) * self.shapes[i][1])
+                rp.append(rp[-1] + (hi - lo) + 1)
+                ro.append(ro[-1] + (hi - lo))
+            self.off.append(o)
+            self.rpoff.append(rp)
+            self.roff.append(ro)
+
+    def shard_shapes(self, k: int) -> List[Shape]:
+        return [(hi - lo, self.shapes[i][1]) for i, lo, hi in self.members[k]]
+
+    def pack(self, grads: Sequence[torch.Tensor], out: torch.Tensor) -> torch.Tensor:
+        """Write full per-tensor gradients into the shard-major flat buffer."""
+        for k in range(self.world):
+            base = k * self.pad
+            for j, (i, lo, hi) in enumerate(self.members[k]):
+                c = self.shapes[i][1]
+                out[base + self.off[k][j]: base + self.off[k][j + 1]].copy_(
+                    grads[i][lo:hi].reshape(-1))
+        return out
+
+
+class Zero1QftLion:
+    """Row-sharded quantized Lion step for one rank of a process group."""
+
+    def __init__(self, shapes: Sequence[Shape], local, group=None, arena_capacity: int = 0):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.layout = ShardLayout(shapes, self.world)
+        self.local = local
+        L = self.layout
+        dev = local.device
+        self.grad_full = torch.zeros(self.world * L.pad, dtype=local.grad_dtype, device=dev)
+        self.codes_full = torch.empty(self.world * L.pad, dtype=torch.uint8, device=dev)
+        self.rowstart_full = torch.empty(self.world * L.rp_pad, dtype=torch.int32, device=dev)
+        self.count_full = torch.empty(self.world * L.rpad, dtype=torch.int32, device=dev)
+        cap = int(arena_capacity) or local.arena_capacity()
+        t = torch.tensor([cap], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)   # rank-uniform capacity
+        self.cap = int(t.item())
+        local.ensure_arena_capacity(self.cap)
+        self.col_full = {c: torch.empty(self.world * self.cap, dtype=torch.int32, device=dev)
+                         for c in L.widths}
+        self.val_full = {c: torch.empty(self.world * self.cap, dtype=torch.float32, device=dev)
+                         for c in L.widths}
+        self.launches = 0
+
+    # ------------------------------------------------------------------ the step
+    def reduce_scatter_grads(self):
+        dist.reduce_scatter_tensor(self.local.grad_shard(self.layout.pad), self.grad_full,
+                                   op=dist.ReduceOp.SUM, group=self.group)
+
+    def all_gather_state(self):
+        L = self.layout
+        dist.all_gather_into_tensor(self.codes_full, self.local.codes_shard(L.pad),
+                                    group=self.group)
+        dist.all_gather_into_tensor(self.rowstart_full, self.local.rowstart_shard(L.rp_pad),
+                                    group=self.group)
+        dist.all_gather_into_tensor(self.count_full, self.local.count_shard(L.rpad),
+                                    group=self.group)
+        for c in L.widths:
+            col, val = self.local.arena(c, self.cap)
+            dist.all_gather_into_tensor(self.col_full[c], col, group=self.group)
+            dist.all_gather_into_tensor(self.val_full[c], val, group=self.group)
+
+    def step(self, lr=1e-4, beta1=0.9, beta2=0.99, weight_decay=0.0):
+        self.reduce_scatter_grads()
+        self.local.step(lr=lr, beta1=beta1, beta2=beta2, weight_decay=weight_decay)
+        self.all_gather_state()
+
+    # ------------------------------------------------------------------ views of the gathered state
+    def gathered_tensor(self, i: int) -> dict:
+        """Reference-layout copy (host numpy) of full tensor i from the gathered buffers."""
+        L = self.layout
+        r, c = L.shapes[i]
+        codes = np.empty((r, c), np.uint8)
+        row_ptr = [0]
+        cols, vals = [], []
+        for k in range(self.world):
+            for j, (ti, lo, hi) in enumerate(L.members[k]):
+                if ti != i:
+                    continue
+                base = k * L.pad
+                codes[lo:hi] = self.codes_full[base + L.off[k][j]: base + L.off[k][j + 1]] \
+                    .cpu().numpy().reshape(hi - lo, c)
+                rs = self.rowstart_full[k * L.rp_pad + L.rpoff[k][j]:
+                                        k * L.rp_pad + L.rpoff[k][j + 1]].cpu().numpy()
+                cnt = self.count_full[k * L.rpad + L.roff[k][j]:
+                                      k * L.rpad + L.roff[k][j + 1]].cpu().numpy()
+                ca = self.col_full[c][k * self.cap:(k + 1) * self.cap].cpu().numpy()
+                va = self.val_full[c][k * self.cap:(k + 1) * self.cap].cpu().numpy()
+                for rr in range(hi - lo):
+                    a0, n = int(rs[rr]), int(cnt[rr])
+                    cols.append(ca[a0:a0 + n])
+                    vals.append(va[a0:a0 + n])
+                    row_ptr.append(row_ptr[-1] + n)
+        return dict(codes=codes, row_ptr=np.asarray(row_ptr, np.int32),
+                    col_idx=np.concatenate(cols) if cols else np.zeros(0, np.int32),
+                    values=np.concatenate(vals) if vals else np.zeros(0, np.float32))
+
+
+class CudaShard:
+    """Local update on this rank's rows: the fused sm_100a step (QftModelState, raw
+    fp gradient kind) with codes and arenas sized for the uniform collectives."""
+
+    def __init__(self, layout: ShardLayout, rank: int, bit_width: int = 8,
+                 grad_dtype=torch.float32, device="cuda"):
+        from .engine import QftModelState
+        self.layout, self.rank = layout, rank
+        self.device = torch.device(device)
+        self.grad_dtype = grad_dtype
+        kind = "f32" if grad_dtype == torch.float32 else "bf16"
+        self.state = QftModelState(layout.shard_shapes(rank), bit_width=bit_width,
+                                   grad_kind=kind, device=device, pad_to=layout.pad)
+
+    def arena_capacity(self) -> int:
+        return max(int(g.col[self.state.cur].numel()) for g in self.state.groups)
+
+    def ensure_arena_capacity(self, cap: int):
+        self.state.ensure_arena_capacity(cap)
+
+    def grad_shard(self, pad: int) -> torch.Tensor:
+        return self.state.g_raw[:pad]
+
+    def step(self, **h):
+        self.state.step(**h)
+
+    def codes_shard(self, pad: int) -> torch.Tensor:
+        return self.state.w_codes[self.state.cur][:pad]
+
+    def _padded(self, t: torch.Tensor, n: int) -> torch.Tensor:
+        if t.numel() < n:
+            out = torch.zeros(n, dtype=t.dtype, device=self.device)
+            out[:t.numel()].copy_(t)
+            return out
+        return t[:n]
+
+    def rowstart_shard(self, rp_pad: int) -> torch.Tensor:
+        return self._padded(self.state.row_start[self.state.cur], rp_pad)
+
+    def count_shard(self, rpad: int) -> torch.Tensor:
+        return self._padded(self.state.row_count[self.state.cur], rpad)
+
+    def arena(self, width: int, cap: int):
+        g = next((g for g in self.state.groups if g.cols == width), None)
+        if g is None:
+            z = torch.zeros(cap, dtype=torch.int32, device=self.device)
+            return z, z.view(torch.float32)
+        k = self.state.cur
+        return g.col[k][:cap], g.val[k][:cap]

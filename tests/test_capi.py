@@ -75,3 +75,13 @@ def test_gradient_stack_semantics():
     s.push(2, "g2")
     s.push(1, "g1")
     assert s.pop().layer_index == 1 and s.pop().layer_index == 2 and s.empty()
+
+
+def test_no_contracted_packed_fma_in_sass():
+    """ptxas 12.9 fuses mul.rn.f32x2 + add.rn.f32x2 into FFMA2 despite .rn; the kernels
+    must never contain FFMA2 (it would break bit-exactness with the -ffp-contract=off
+    reference)."""
+    from paper_2310_07147_b200 import _native as N
+    out = subprocess.run(["cuobjdump", "-sass", N.LIB_PATH], capture_output=True, text=True)
+    assert out.returncode == 0 and "FMUL2" in out.stdout
+    assert "FFMA2" not in out.stdout
