@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libqft_b200.so")
+LIB_PATH = os.environ.get("QFT_B200_LIB") or os.path.join(_HERE, "_lib", "libqft_b200.so")
 
 QFTC_OK, QFTC_EINVAL, QFTC_ERANGE, QFTC_ECUDA, QFTC_EOVERFLOW, QFTC_ENOTSUP = 0, -1, -2, -3, -4, -5
 GRAD_U8, GRAD_F32, GRAD_BF16 = 0, 1, 2

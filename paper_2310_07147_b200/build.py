@@ -40,20 +40,23 @@ def _run(cmd, verbose):
     subprocess.run(cmd, check=True)
 
 
-def build_lib(verbose=False, force=False):
-    os.makedirs(LIBDIR, exist_ok=True)
+def build_lib(verbose=False, force=False, extra_flags=(), libdir=LIBDIR):
+    """Compile every csrc/*.cu for sm_100a and link libqft_b200.so into `libdir`
+    (`extra_flags`/`libdir` build tuning variants, e.g. -DQFT_MIN_CTAS=4)."""
+    os.makedirs(libdir, exist_ok=True)
+    lib = os.path.join(libdir, "libqft_b200.so")
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     hdrs = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
         glob.glob(os.path.join(INCLUDE, "*.h"))
     objs = []
     for s in srcs:
-        o = os.path.join(LIBDIR, os.path.basename(s)[:-3] + ".o")
+        o = os.path.join(libdir, os.path.basename(s)[:-3] + ".o")
         if force or _stale(o, [s] + hdrs):
-            _run([NVCC] + NVCC_FLAGS + ["-c", s, "-o", o], verbose)
+            _run([NVCC] + NVCC_FLAGS + list(extra_flags) + ["-c", s, "-o", o], verbose)
         objs.append(o)
-    if force or _stale(LIB, objs):
-        _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", LIB] + objs, verbose)
-    return LIB
+    if force or _stale(lib, objs):
+        _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", lib] + objs, verbose)
+    return lib
 
 
 def build_pyext(verbose=False, force=False):

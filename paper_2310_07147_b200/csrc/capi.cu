@@ -132,22 +132,65 @@ int scratch_alloc(Scratch& s, const std::vector<DevTensor>& ts, int64_t status_r
   return QFTC_OK;
 }
 
-// stages: most CTAs per SM first, then most stages
-int pick_stages(int mode, int gk, int cols_p) {
-  int best_s = 2;
+// launch shape: most CTAs per SM first, then keeping m' in smem (no recompute),
+// then most pipeline stages
+struct Cfg {
+  int stages, mrec;
+};
+Cfg pick_config(int mode, int gk, int cols_p, bool allow_mrec) {
+  Cfg best{2, 0};
   long best_score = -1;
-  for (int S = 2; S <= 4; ++S) {
-    const size_t smem = row_engine_smem(mode, gk, cols_p, S);
-    if (smem > 227 * 1024) break;
-    const long per_sm = (long)((228 * 1024) / (smem + 1024));
-    const long blocks = per_sm < 3 ? per_sm : 3;  // register limit (launch_bounds(160,3))
-    const long score = blocks * 16 + S;
-    if (blocks >= 1 && score > best_score) {
-      best_score = score;
-      best_s = S;
+  for (int m = 0; m <= (allow_mrec ? 1 : 0); ++m) {
+    for (int S = 2; S <= 4; ++S) {
+      const size_t smem = row_engine_smem(mode, gk, cols_p, S, m != 0);
+      if (smem > 227 * 1024) break;
+      const long per_sm = (long)((228 * 1024) / (smem + 1024));
+      const long blocks = per_sm < QFT_MIN_CTAS ? per_sm : QFT_MIN_CTAS;  // register limit
+      const long score = blocks * 64 + (m ? 0 : 16) + S;
+      if (blocks >= 1 && score > best_score) {
+        best_score = score;
+        best = Cfg{S, m};
+      }
     }
   }
-  return best_s;
+  return best;
+}
+int pick_stages(int mode, int gk, int cols_p) { return pick_config(mode, gk, cols_p, false).stages; }
+
+// step kernel shape: most CTAs per SM (registers cap it at QFT_STEP_MIN_CTAS), then
+// m' kept in smem, then pipeline depth, then parked-outlier slots.  QFT_STEP_CFG="S,K,mrec"
+// overrides it (tuning / A-B runs).
+struct StepCfg {
+  int S, K, mrec, oldcap;
+};
+StepCfg pick_step_config(int gk, int cols_p, bool allow_mrec) {
+  const int oldcap = cols_p <= 4096 ? 128 : 256;
+  if (const char* env = getenv("QFT_STEP_CFG")) {
+    StepCfg c{3, 1, 0, oldcap};
+    if (sscanf(env, "%d,%d,%d", &c.S, &c.K, &c.mrec) == 3) {
+      c.mrec = (c.mrec && allow_mrec) ? 1 : 0;
+      if (c.S >= 2 && c.S <= 8 && c.K >= 1 && c.K <= 3 &&
+          step_kernel_smem(gk, cols_p, c.S, oldcap, c.K, c.mrec) <= 227 * 1024)
+        return c;
+    }
+  }
+  StepCfg best{2, 1, allow_mrec ? 1 : 0, oldcap};
+  long best_score = -1;
+  for (int m = 0; m <= (allow_mrec ? 1 : 0); ++m)
+    for (int S = 2; S <= 6; ++S)
+      for (int K = 1; K <= 2; ++K) {
+        const size_t smem = step_kernel_smem(gk, cols_p, S, oldcap, K, m != 0);
+        if (smem > 227 * 1024) continue;
+        long ctas = (long)((228 * 1024) / (smem + 1024));
+        if (ctas > QFT_STEP_MIN_CTAS) ctas = QFT_STEP_MIN_CTAS;
+        if (ctas < 1) continue;
+        const long score = ctas * 1000 + (m ? 0 : 100) + (S > 4 ? 4 : S) * 10 + K;
+        if (score > best_score) {
+          best_score = score;
+          best = StepCfg{S, K, m, oldcap};
+        }
+      }
+  return best;
 }
 
 int read_header(const Header* d_hdr, Header* h, cudaStream_t st) {
@@ -446,6 +489,9 @@ struct qftc_plan {
   int grad_kind = 0;
   int cols_p = 16;
   int stages = 2;
+  int mrec = 0;
+  int oldcap = 128;
+  int slots = 1;
   int use_bulk = 1;
   int slotted[2] = {0, 0};
   int32_t* col[2] = {nullptr, nullptr};
@@ -523,7 +569,14 @@ int qftc_plan_create(qftc_plan** out, const qftc_lion_tensor* ts, int n, int bit
   p->grad_kind = grad_kind;
   p->cols_p = (maxc + 15) & ~15;
   p->use_bulk = bulk ? 1 : 0;
-  p->stages = pick_stages(MODE_STEP, grad_kind, p->cols_p);
+  {
+    const StepCfg cfg = pick_step_config(grad_kind, p->cols_p,
+                                         grad_kind == QFTC_GRAD_U8 && p->use_bulk);
+    p->stages = cfg.S;
+    p->mrec = cfg.mrec;
+    p->oldcap = cfg.oldcap;
+    p->slots = cfg.K;
+  }
   for (int k = 0; k < 2; ++k) {
     p->col[k] = col_idx ? col_idx[k] : nullptr;
     p->val[k] = values ? values[k] : nullptr;
@@ -570,10 +623,12 @@ int qftc_plan_step(qftc_plan* p, int flip, qftc_lion_hyper h, qftc_stream_t stre
   a.status = p->sc.status;
   a.cols_p = p->cols_p;
   a.stages = p->stages;
+  a.mrec = p->mrec;
+  a.oldcap = p->oldcap;
+  a.slots = p->slots;
   a.use_bulk = p->use_bulk;
   a.slotted_in = p->slotted[flip];
-  QFTC_CUDA(launch_row_engine(MODE_STEP, p->grad_kind, a, (cudaStream_t)stream, nullptr),
-            "lion step kernel");
+  QFTC_CUDA(launch_step_kernel(p->grad_kind, a, (cudaStream_t)stream), "lion step kernel");
   return QFTC_OK;
 }
 

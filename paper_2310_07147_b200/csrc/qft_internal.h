@@ -5,6 +5,15 @@
 
 #include "qft_b200.h"
 
+// CTAs per SM the row engine's register budget is sized for (launch bounds)
+#ifndef QFT_MIN_CTAS
+#define QFT_MIN_CTAS 3
+#endif
+// CTAs per SM the 128-thread step kernel is sized for
+#ifndef QFT_STEP_MIN_CTAS
+#define QFT_STEP_MIN_CTAS 4
+#endif
+
 namespace qftk {
 
 // One tensor of a launch.
@@ -83,10 +92,17 @@ struct LaunchArgs {
   int32_t stages;
   int32_t use_bulk;   // TMA bulk copies (all rows 16-byte aligned)
   int32_t slotted_in; // input CSR is slotted (16-byte aligned slots)
+  int32_t mrec;       // step: recompute m' in pass 2 instead of a 4*cols smem buffer
+  int32_t oldcap;     // step: old CSR entries staged per stage (multiple of 4)
+  int32_t slots;      // step: per-thread parked-outlier vector slots
+  int32_t _pad;
 };
 
+size_t step_kernel_smem(int gk, int cols_p, int stages, int oldcap, int slots, bool mrec);
+cudaError_t launch_step_kernel(int gk, const LaunchArgs& a, cudaStream_t s);
+
 // launch helpers (rowengine.cu)
-size_t row_engine_smem(int mode, int gk, int cols_p, int stages);
+size_t row_engine_smem(int mode, int gk, int cols_p, int stages, bool mrec);
 cudaError_t launch_row_engine(int mode, int gk, const LaunchArgs& a, cudaStream_t s,
                               int* grid_out);
 int row_engine_max_cols();

@@ -91,8 +91,10 @@ __host__ __device__ inline int stage_data_bytes(int mode, int gk, int cp) {
   }
 }
 __host__ __device__ inline int old_bits_bytes(int cp) { return round16((cp + 31) / 32 * 4); }
+__host__ __device__ inline int frank_bytes(int cp) { return round16((cp + 31) / 32 * 2); }
 __host__ __device__ inline int stage_bytes(int mode, int gk, int cp) {
-  const int old = (mode == MODE_DECOMPOSE) ? 0 : OLDCAP * 8 + old_bits_bytes(cp);
+  const int old =
+      (mode == MODE_DECOMPOSE) ? 0 : OLDCAP * 8 + old_bits_bytes(cp) + frank_bytes(cp);
   return HDR + old + stage_data_bytes(mode, gk, cp);
 }
 struct Tabs {
@@ -109,15 +111,15 @@ struct Tabs {
 __host__ __device__ inline int mprime_bytes(int cp) {
   return 4 * ((cp + NCT * 16 - 1) / (NCT * 16)) * (NCT * 16);
 }
-__host__ __device__ inline int consumer_bytes(int mode, int cp) {
+__host__ __device__ inline int consumer_bytes(int mode, int cp, bool mrec) {
   int b = (int)sizeof(Tabs);
-  if (mode == MODE_STEP) b += mprime_bytes(cp);
+  if (mode == MODE_STEP && !mrec) b += mprime_bytes(cp);
   if (mode == MODE_STEP || mode == MODE_DECOMPOSE) b += round16(cp / 16 * 2);  // masks
   return b;
 }
-size_t row_engine_smem(int mode, int gk, int cols_p, int stages) {
+size_t row_engine_smem(int mode, int gk, int cols_p, int stages, bool mrec) {
   return 128 /*barriers*/ + (size_t)stages * stage_bytes(mode, gk, cols_p) +
-         consumer_bytes(mode, cols_p);
+         consumer_bytes(mode, cols_p, mrec);
 }
 int row_engine_max_cols() { return MAX_COLS; }
 
@@ -129,27 +131,14 @@ __device__ __forceinline__ unsigned long long pack_status(uint32_t epoch, uint32
   return ((unsigned long long)epoch << 32) | ((unsigned long long)flag << 30) | v;
 }
 
-// value of the old outlier at column `col` of the stage's row (rare path)
-__device__ __noinline__ float old_value(const int32_t* oc, const float* ov, int n_old, int staged,
-                                        int old_begin, int col, const int32_t* col_in,
-                                        const float* val_in) {
-  int lo = 0;
-  if (staged) {
-    const int nc = n_old < OLDCAP ? n_old : OLDCAP;
-    int hi = nc;
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (oc[mid] < col) lo = mid + 1; else hi = mid;
-    }
-    if (lo < nc && oc[lo] == col) return ov[lo];
-    lo = nc;
-  }
-  int hi = n_old;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (col_in[old_begin + mid] < col) lo = mid + 1; else hi = mid;
-  }
-  return val_in[old_begin + lo];
+// value of the old outlier at column `col` (its bit is set): the entry's rank in
+// the row's sorted list is first_rank[word] + popc(lower bits of the word) -- O(1)
+__device__ __forceinline__ float old_value(const uint32_t* bits, const uint16_t* frank,
+                                           const float* ov, int staged, int old_begin, int col,
+                                           const float* val_in) {
+  const int w = col >> 5;
+  const int r = (int)frank[w] + __popc(bits[w] & ((1u << (col & 31)) - 1u));
+  return (staged && r < OLDCAP) ? ov[r] : val_in[old_begin + r];
 }
 
 __device__ __forceinline__ uint32_t bits16(const uint32_t* bits, int v) {
@@ -176,8 +165,8 @@ __device__ __forceinline__ float dequant1(uint32_t code, const DequantRow& d) {
 // ----------------------------------------------------------------------------
 // the kernel
 // ----------------------------------------------------------------------------
-template <int MODE, int GK, bool ALIGNED, bool WD0>
-__global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
+template <int MODE, int GK, bool ALIGNED, bool WD0, bool MREC>
+__global__ void __launch_bounds__(NT, QFT_MIN_CTAS) row_engine_kernel(const LaunchArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + MAX_STAGES;
@@ -189,7 +178,8 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
   Tabs* tabs = reinterpret_cast<Tabs*>(cons);
   float* mprime = reinterpret_cast<float*>(cons + sizeof(Tabs));
   uint16_t* masks = reinterpret_cast<uint16_t*>(cons + sizeof(Tabs) +
-                                                (MODE == MODE_STEP ? mprime_bytes(cp) : 0));
+                                                (MODE == MODE_STEP && !MREC ? mprime_bytes(cp)
+                                                                            : 0));
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int qmax = (1 << a.bit_width) - 1;
@@ -209,8 +199,11 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
   auto oldc_of = [&](uint8_t* st) { return reinterpret_cast<int32_t*>(st + HDR); };
   auto oldv_of = [&](uint8_t* st) { return reinterpret_cast<float*>(st + HDR + OLDCAP * 4); };
   auto oldb_of = [&](uint8_t* st) { return reinterpret_cast<uint32_t*>(st + HDR + OLDCAP * 8); };
+  auto frank_of = [&](uint8_t* st) {
+    return reinterpret_cast<uint16_t*>(st + HDR + OLDCAP * 8 + old_bits_bytes(cp));
+  };
   auto data_of = [&](uint8_t* st) {
-    return st + HDR + (kOld ? OLDCAP * 8 + old_bits_bytes(cp) : 0);
+    return st + HDR + (kOld ? OLDCAP * 8 + old_bits_bytes(cp) + frank_bytes(cp) : 0);
   };
 
   if (warp == NCW) {
@@ -446,6 +439,7 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
       const int nch = (nvec + NCT - 1) / NCT;
       const uint8_t* data = data_of(st);
       uint32_t* obits = oldb_of(st);
+      uint16_t* frank = frank_of(st);
       const int32_t* ocols = oldc_of(st);
       const float* ovals = oldv_of(st);
       const int old_n = kOld ? cx->old_n : 0;
@@ -454,10 +448,16 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
       const DequantRow dw = make_dequant_row(cx->sw, cx->zw);
 
       if (kOld) {
-        // old-outlier bitmap of this row (the producer cleared it)
+        // old-outlier bitmap of this row (the producer cleared it) and, for every
+        // bitmap word holding an outlier, the rank of its first entry
         for (int i = ct; i < old_n; i += NCT) {
           const int col = (staged && i < OLDCAP) ? ocols[i] : a.col_in[old_begin + i];
-          atomicOr(&obits[col >> 5], 1u << (col & 31));
+          const int wd = col >> 5;
+          atomicOr(&obits[wd], 1u << (col & 31));
+          const int prev = (i == 0) ? -1
+                           : ((staged && i - 1 < OLDCAP) ? ocols[i - 1]
+                                                         : a.col_in[old_begin + i - 1]);
+          if (i == 0 || (prev >> 5) != wd) frank[wd] = (uint16_t)i;
         }
         named_bar_sync(BAR_B0, NCT);
       }
@@ -477,8 +477,7 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
 #pragma unroll
             for (int e = 0; e < 16; ++e)
               if (o16 & (1u << e))
-                w[e] = old_value(ocols, ovals, old_n, staged, old_begin, v * 16 + e, a.col_in,
-                                 a.val_in);
+                w[e] = old_value(obits, frank, ovals, staged, old_begin, v * 16 + e, a.val_in);
           }
           const int nvalid = min(16, cols - v * 16);
           if (MODE == MODE_RECON_F32) {
@@ -520,6 +519,7 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
       const QuantRow qw = make_quant_row(cx->sw, cx->zw, a.bit_width);
       const float tmin = cx->tmin, tmax = cx->tmax;
       const uint32_t zpay4 = (uint32_t)cx->zpay * 0x01010101u;
+      const uint32_t wz_bits = __float_as_uint(__fmul_rn(cx->sw, (float)(cx->zpay - cx->zw)));
       // dequantized w can only be non-finite if s*(qmax+|z|) overflows fp32
       const bool w_ovf = !(__fmul_rn(fabsf(cx->sw), (float)qmax + fabsf((float)cx->zw)) < 3.0e38f);
       DequantRow dm, dg;
@@ -627,8 +627,7 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
 #pragma unroll
               for (int e = 0; e < 16; ++e)
                 if (o16 & (1u << e)) {
-                  w[e] = old_value(ocols, ovals, old_n, staged, old_begin, v * 16 + e, a.col_in,
-                                   a.val_in);
+                  w[e] = old_value(obits, frank, ovals, staged, old_begin, v * 16 + e, a.val_in);
                   wspecial |= !isfinite(w[e]);
                 }
             }
@@ -665,30 +664,38 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
               asm("max.f32 %0, %1, %2, %3;" : "=f"(t) : "f"(mhi), "f"(m[2 * p]), "f"(m[2 * p + 1]));
               mhi = t;
             }
-            float4* mp = reinterpret_cast<float4*>(mprime);
+            if (!MREC) {
+              float4* mp = reinterpret_cast<float4*>(mprime);
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              mp[(k * 4 + q) * NCT + ct] =
-                  make_float4(m[4 * q], m[4 * q + 1], m[4 * q + 2], m[4 * q + 3]);
+              for (int q = 0; q < 4; ++q)
+                mp[(k * 4 + q) * NCT + ct] =
+                    make_float4(m[4 * q], m[4 * q + 1], m[4 * q + 2], m[4 * q + 3]);
+            }
           }
-          // ---- classify + quantize w'
+          // ---- classify + quantize w'.  Outliers are replaced by wz = s*(zpay-z)
+          // before quantizing, which quantizes exactly to the payload zpay
+          // (decompose_dense_sparse stores clamp(z) under an outlier, quantize.hpp:279).
+          float wq[16];
 #pragma unroll
-          for (int e = 0; e < 16; ++e)
-            mask |= ((w[e] < tmin) || (w[e] > tmax)) ? (1u << e) : 0u;
+          for (int e = 0; e < 16; ++e) {
+            const uint32_t d = outside_mask(w[e], tmin, tmax);
+            mask |= d & (1u << e);
+            wq[e] = __uint_as_float((__float_as_uint(w[e]) & ~d) | (wz_bits & d));
+          }
           mask &= valid;
           float em = 0.0f;
           uint32_t c[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) c[q] = quant4_fast(w + 4 * q, qw, em);
+          for (int q = 0; q < 4; ++q) c[q] = quant4_fast(wq + 4 * q, qw, em);
           if (!qw.fast || !(em < qw.thr)) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) c[q] = quant4_exact(w + 4 * q, qw);
-          }
-          if (mask) {
+            if (mask) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const uint32_t bm = nib_to_bytemask((mask >> (4 * q)) & 0xFu);
-              c[q] = (c[q] & ~bm) | (zpay4 & bm);
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t bm = nib_to_bytemask((mask >> (4 * q)) & 0xFu);
+                c[q] = (c[q] & ~bm) | (zpay4 & bm);
+              }
             }
           }
           uint8_t* wo = cx->w_out + v * 16;
@@ -819,10 +826,29 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
           const int v = k * NCT + ct;
           if (v >= nvec) break;
           float m[16];
+          if (MREC) {
+            // recompute m' = b2*m + (1-b2)*g from the staged codes (same expression
+            // as pass 1, so the same bits) instead of keeping a 4*cols smem buffer
+            float g[16];
+            const uint4 mq = *reinterpret_cast<const uint4*>(data + cp + v * 16);
+            const uint4 gq = *reinterpret_cast<const uint4*>(data + 2 * cp + v * 16);
+            dequant4(mq.x, dm, m); dequant4(mq.y, dm, m + 4);
+            dequant4(mq.z, dm, m + 8); dequant4(mq.w, dm, m + 12);
+            dequant4(gq.x, dg, g); dequant4(gq.y, dg, g + 4);
+            dequant4(gq.z, dg, g + 8); dequant4(gq.w, dg, g + 12);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float4 f = mp[(k * 4 + q) * NCT + ct];
-            m[4 * q] = f.x; m[4 * q + 1] = f.y; m[4 * q + 2] = f.z; m[4 * q + 3] = f.w;
+            for (int p = 0; p < 8; ++p) {
+              const float2 M = sadd2(mul2(f2(h.b2), make_float2(m[2 * p], m[2 * p + 1])),
+                                     mul2(f2(h.c2), make_float2(g[2 * p], g[2 * p + 1])));
+              m[2 * p] = M.x;
+              m[2 * p + 1] = M.y;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 f = mp[(k * 4 + q) * NCT + ct];
+              m[4 * q] = f.x; m[4 * q + 1] = f.y; m[4 * q + 2] = f.z; m[4 * q + 3] = f.w;
+            }
           }
           float em = 0.0f;
           uint32_t c[4];
@@ -874,7 +900,7 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
               // recompute w' for this element exactly as pass 1 did (scalar, exact)
               float wv = dequant1(data[col], dw);
               if (bits16(obits, v) & (1u << e))
-                wv = old_value(ocols, ovals, old_n, staged, old_begin, col, a.col_in, a.val_in);
+                wv = old_value(obits, frank, ovals, staged, old_begin, col, a.val_in);
               float mv = dequant1(data[cp + col], dm);
               float gv;
               if (GK == G_U8) {
@@ -916,9 +942,9 @@ __global__ void __launch_bounds__(NT, 3) row_engine_kernel(const LaunchArgs a) {
 // ----------------------------------------------------------------------------
 // host-side launcher
 // ----------------------------------------------------------------------------
-template <int MODE, int GK, bool AL, bool WD0>
+template <int MODE, int GK, bool AL, bool WD0, bool MREC = false>
 static cudaError_t launch_t(const LaunchArgs& a, size_t smem, cudaStream_t st, int* grid_out) {
-  auto k = row_engine_kernel<MODE, GK, AL, WD0>;
+  auto k = row_engine_kernel<MODE, GK, AL, WD0, MREC>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
@@ -938,9 +964,14 @@ static cudaError_t launch_t(const LaunchArgs& a, size_t smem, cudaStream_t st, i
 
 cudaError_t launch_row_engine(int mode, int gk, const LaunchArgs& a, cudaStream_t st,
                               int* grid_out) {
-  const size_t smem = row_engine_smem(mode, gk, a.cols_p, a.stages);
+  const bool mrec = a.mrec && mode == MODE_STEP && gk == G_U8 && a.use_bulk;
+  const size_t smem = row_engine_smem(mode, gk, a.cols_p, a.stages, mrec);
   const bool al = a.use_bulk != 0;
   const bool wd0 = (a.wd == 0.0f);
+  if (mrec) {
+    return wd0 ? launch_t<MODE_STEP, G_U8, true, true, true>(a, smem, st, grid_out)
+               : launch_t<MODE_STEP, G_U8, true, false, true>(a, smem, st, grid_out);
+  }
 #define QFT_L(M, G)                                                              \
   if (wd0) return al ? launch_t<M, G, true, true>(a, smem, st, grid_out)        \
                      : launch_t<M, G, false, true>(a, smem, st, grid_out);      \

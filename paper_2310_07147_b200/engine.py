@@ -50,7 +50,12 @@ class _Group:
 
 class QftModelState:
     def __init__(self, shapes: Sequence[Tuple[int, int]], bit_width: int = 8,
-                 grad_kind: str = "u8", device="cuda", pad_to: int = 0):
+                 grad_kind: str = "u8", device="cuda", pad_to: int = 0,
+                 group_contiguous: bool = True):
+        """`group_contiguous`: lay the flat buffers out width class by width class (so a
+        run of tensors of one launch group is one contiguous range of every array, which
+        the chunked host pipeline needs); False keeps the given order (ZeRO-1 shards,
+        whose gradient layout is fixed by the reduce-scatter)."""
         if bit_width < 2 or bit_width > 8:
             raise ValueError(f"bit width must be in [2, 8], got {bit_width}")
         self.shapes = [(int(r), int(c)) for r, c in shapes]
@@ -61,12 +66,19 @@ class QftModelState:
         self.cur = 0
         self.steps = 0
         self.replans = 0
-        sizes = [r * c for r, c in self.shapes]
+        order = list(range(self.n))
+        if group_contiguous:
+            order.sort(key=lambda i: (self.shapes[i][1], i))
+        self.order = order                       # flat position -> tensor index
+        self.pos = {i: p for p, i in enumerate(order)}
+        sizes = [self.shapes[i][0] * self.shapes[i][1] for i in order]
+        rows_l = [self.shapes[i][0] for i in order]
         self.param_count = int(sum(sizes))
-        self.row_count_total = int(sum(r for r, _ in self.shapes))
+        self.row_count_total = int(sum(rows_l))
         self.off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
-        self.roff = np.concatenate([[0], np.cumsum([r for r, _ in self.shapes])]).astype(np.int64)
+        self.roff = np.concatenate([[0], np.cumsum(rows_l)]).astype(np.int64)
         self.rpoff = self.roff + np.arange(self.n + 1)  # row_start slices have rows+1 entries
+        self.chunks: List[dict] = []
         dev, P, R = self.device, self.param_count, self.row_count_total
         u8, f32, i32 = torch.uint8, torch.float32, torch.int32
         self.w_codes = [torch.zeros(max(P, pad_to), dtype=u8, device=dev) for _ in range(2)]
@@ -90,8 +102,8 @@ class QftModelState:
             gdt = f32 if self.grad_kind == N.GRAD_F32 else torch.bfloat16
             self.g_raw = torch.zeros(max(P, pad_to), dtype=gdt, device=dev)
         by_cols: Dict[int, List[int]] = {}
-        for i, (_, c) in enumerate(self.shapes):
-            by_cols.setdefault(c, []).append(i)
+        for i in order:
+            by_cols.setdefault(self.shapes[i][1], []).append(i)
         self.groups: List[_Group] = []
         for c, mem in sorted(by_cols.items()):
             rows = sum(self.shapes[i][0] for i in mem)
@@ -101,13 +113,16 @@ class QftModelState:
     # ------------------------------------------------------------------ views
     def _sl(self, flat, i):
         r, c = self.shapes[i]
-        return flat[self.off[i]:self.off[i + 1]].view(r, c)
+        p = self.pos[i]
+        return flat[self.off[p]:self.off[p + 1]].view(r, c)
 
     def _rows(self, flat, i):
-        return flat[self.roff[i]:self.roff[i + 1]]
+        p = self.pos[i]
+        return flat[self.roff[p]:self.roff[p + 1]]
 
     def _rs(self, flat, i):
-        return flat[self.rpoff[i]:self.rpoff[i + 1]]
+        p = self.pos[i]
+        return flat[self.rpoff[p]:self.rpoff[p + 1]]
 
     def grad_views(self, i):
         """The GradientStack entry of tensor i: (codes [r,c] u8, scale [r], zero_point [r]),
@@ -163,6 +178,12 @@ class QftModelState:
         need = g.col[src].numel()
         if g.col[dst] is None or g.col[dst].numel() < need:
             g.col[dst], g.val[dst] = self._alloc(need)
+
+    def _mirror_all(self):
+        for g in self.groups:
+            self._mirror_layout(g, self.cur)
+            if g.plan is not None:
+                self._set_arena(g)
 
     # ------------------------------------------------------------------ init
     def init_from_weights(self, weight_fn, fraction: float = 0.01, kind="percentile"):
@@ -230,9 +251,10 @@ class QftModelState:
         self._make_plans()
 
     # ------------------------------------------------------------------ plans
-    def _descs(self, g: _Group):
-        arr = (N.LionTensorC * len(g.members))()
-        for j, i in enumerate(g.members):
+    def _descs(self, g: _Group, members: Optional[List[int]] = None):
+        members = g.members if members is None else members
+        arr = (N.LionTensorC * len(members))()
+        for j, i in enumerate(members):
             r, c = self.shapes[i]
             d = arr[j]
             d.rows, d.cols = r, c
@@ -264,6 +286,50 @@ class QftModelState:
     def _set_arena(self, g: _Group):
         cols, vals, caps = self._arena_args(g)
         N.check(N.lib.qftc_plan_set_arena(g.plan, cols, vals, caps))
+        for ch in self.chunks:
+            if ch["group"] is g:
+                N.check(N.lib.qftc_plan_set_arena(ch["plan"], cols, vals, caps))
+
+    def make_chunk_plans(self, max_params: int = 256 << 20) -> List[dict]:
+        """Split every launch group into runs of consecutive tensors of <= max_params
+        (one plan each).  A chunk is one contiguous range of every flat array, so a host
+        pipeline can stream chunk i+1 in while chunk i steps and chunk i-1 streams out."""
+        for ch in self.chunks:
+            N.lib.qftc_plan_destroy(ch["plan"])
+        self.chunks = []
+        for g in self.groups:
+            run, acc = [], 0
+            runs = []
+            for i in g.members:
+                sz = self.shapes[i][0] * self.shapes[i][1]
+                if run and acc + sz > max_params:
+                    runs.append(run)
+                    run, acc = [], 0
+                run.append(i)
+                acc += sz
+            if run:
+                runs.append(run)
+            for run in runs:
+                arr = self._descs(g, run)
+                cols, vals, caps = self._arena_args(g)
+                plan = C.c_void_p()
+                N.check(N.lib.qftc_plan_create(C.byref(plan), arr, len(run), self.bit_width,
+                                               self.grad_kind, cols, vals, caps, _stream()))
+                p0, p1 = self.pos[run[0]], self.pos[run[-1]] + 1
+                self.chunks.append(dict(group=g, members=run, plan=plan, p0=p0, p1=p1))
+        return self.chunks
+
+    def chunk_ranges(self, ch: dict, k: int) -> dict:
+        """Flat-array ranges of a chunk (element offsets) and its arena range in set k."""
+        p0, p1 = ch["p0"], ch["p1"]
+        a0 = int(self.row_start[k][int(self.rpoff[p0])].item())
+        a1 = int(self.row_start[k][int(self.rpoff[p1]) - 1].item())
+        return dict(code=(int(self.off[p0]), int(self.off[p1])),
+                    row=(int(self.roff[p0]), int(self.roff[p1])),
+                    rs=(int(self.rpoff[p0]), int(self.rpoff[p1])), arena=(a0, a1))
+
+    def step_chunk(self, ch: dict, flip: int, h, stream_handle):
+        N.check(N.lib.qftc_plan_step(ch["plan"], flip, h, stream_handle))
 
     def _make_plans(self):
         for g in self.groups:
@@ -277,6 +343,12 @@ class QftModelState:
             g.plan = plan
 
     def __del__(self):
+        for ch in getattr(self, "chunks", []):
+            try:
+                N.lib.qftc_plan_destroy(ch["plan"])
+            except Exception:
+                pass
+        self.chunks = []
         for g in getattr(self, "groups", []):
             if g.plan is not None:
                 try:

@@ -175,7 +175,8 @@ class CudaShard:
         self.grad_dtype = grad_dtype
         kind = "f32" if grad_dtype == torch.float32 else "bf16"
         self.state = QftModelState(layout.shard_shapes(rank), bit_width=bit_width,
-                                   grad_kind=kind, device=device, pad_to=layout.pad)
+                                   grad_kind=kind, device=device, pad_to=layout.pad,
+                                   group_contiguous=False)
 
     def arena_capacity(self) -> int:
         return max(int(g.col[self.state.cur].numel()) for g in self.state.groups)

@@ -277,3 +277,124 @@ def test_validation_errors(cuda):
     x[0, 0] = float("nan")      # NaN in column 0 sticks as the bound -> min > max
     with pytest.raises(ValueError):
         cuda.quantize_state(x, 8)
+
+
+@pytest.mark.parametrize("gkind", ["f32", "bf16"])
+def test_engine_raw_gradient_fused_quantize(cuda, port, gkind):
+    """grad kind f32/bf16: the kernel applies the backward sink's quantize_state(g)
+    (gradflow.hpp:77) and dequantize in-register; bytes equal the oracle fed the
+    quantized gradient."""
+    shapes = [(40, 1024), (8, 2048)]
+    bw = 8
+    eng = cuda.QftModelState(shapes, bit_width=bw, grad_kind=gkind)
+    host, ora = [], []
+    for i, sh in enumerate(shapes):
+        d = port.decompose_weight(port.synth(sh, 40 + i, 0.02, 0.005), 0.01, bw)
+        host.append(dict(codes=d.codes, scale=d.scale, zero_point=d.zero_point, t_min=d.t_min,
+                         t_max=d.t_max, row_ptr=d.row_ptr, col_idx=d.col_idx, values=d.values))
+        ora.append([d, port.quantize_state(np.zeros(sh, np.float32), bw)])
+    eng.init_from_host(host)
+    for step in range(3):
+        for i, sh in enumerate(shapes):
+            g = port.synth(sh, 700 + 10 * step + i, 1e-2, 0.0)
+            gt = torch.from_numpy(g)
+            if gkind == "bf16":
+                gt = gt.to(torch.bfloat16)
+                g = gt.float().numpy()
+            eng.grad_views(i).copy_(gt)
+            gq = port.quantize_state(g, bw)
+            d, m = ora[i]
+            ora[i] = list(port.lion_step_layer(d, *m, *gq, lr=1e-3, wd=0.01)[:2])
+        eng.step(lr=1e-3, weight_decay=0.01, check=True)
+        for i in range(len(shapes)):
+            got = eng.export_tensor(i)
+            d, m = ora[i]
+            for k, ref in (("codes", d.codes), ("row_ptr", d.row_ptr), ("col_idx", d.col_idx),
+                           ("values", d.values), ("m_codes", m[0]), ("m_scale", m[1])):
+                _eq(got[k], ref, f"{gkind} step {step} tensor {i} {k}")
+
+
+def test_engine_slot_overflow_replans(cuda, port):
+    """A spike-dominated row moves dozens of edge codes into the sparse set in one step
+    (SURVEY finding 2); undersized slots must be re-planned and the step re-run from the
+    intact ping-pong inputs, with results still equal to the oracle."""
+    sh = (64, 256)
+    d = port.decompose_weight(port.synth(sh, 1240, 0.02, 0.02), 0.01, 8)
+    eng = cuda.QftModelState([sh], bit_width=8)
+    eng.init_from_host([dict(codes=d.codes, scale=d.scale, zero_point=d.zero_point,
+                             t_min=d.t_min, t_max=d.t_max, row_ptr=d.row_ptr,
+                             col_idx=d.col_idx, values=d.values)])
+    # shrink every slot to the bare count: the first step must overflow somewhere
+    n = eng.n
+    rp = torch.from_numpy(d.row_ptr.astype(np.int64))
+    cnt = (rp[1:] - rp[:-1])
+    starts = torch.zeros(sh[0] + 1, dtype=torch.int64)
+    starts[1:] = torch.cumsum((cnt + 3) // 4 * 4, 0)
+    g = eng.groups[0]
+    for k in range(2):
+        eng.row_start[k][:sh[0] + 1].copy_(starts.to(torch.int32))
+    eng.row_count[eng.cur].copy_(cnt.to(torch.int32))
+    nnz_slots = int(starts[-1])
+    for r in range(sh[0]):
+        a, b = int(d.row_ptr[r]), int(d.row_ptr[r + 1])
+        s0 = int(starts[r])
+        g.col[eng.cur][s0:s0 + b - a].copy_(torch.from_numpy(d.col_idx[a:b]))
+        g.val[eng.cur][s0:s0 + b - a].copy_(torch.from_numpy(d.values[a:b]))
+    m = port.quantize_state(np.zeros(sh, np.float32), 8)
+    gq = port.quantize_state(port.synth(sh, 9, 1e-3, 0.0), 8)
+    c, s, z = eng.grad_views(0)
+    c.copy_(torch.from_numpy(gq[0]))
+    s.copy_(torch.from_numpy(gq[1]))
+    z.copy_(torch.from_numpy(gq[2]))
+    eng.step(lr=2e-5, check=True)
+    d2, m2, _ = port.lion_step_layer(d, *m, *gq, lr=2e-5)
+    assert eng.replans >= 1 and d2.nnz > d.nnz and nnz_slots < 2 ** 31
+    got = eng.export_tensor(0)
+    for k in ("codes", "row_ptr", "col_idx", "values"):
+        _eq(got[k], getattr(d2, k), k)
+    _eq(got["m_codes"], m2[0], "m_codes")
+
+
+def test_zero1_world1_nccl_cuda_shard(cuda, port):
+    """ZeRO-1 path with the real CUDA local update on a world-size-1 NCCL group:
+    reduce-scatter -> fused f32-gradient step -> all-gather of codes/slots/arenas."""
+    import socket
+    import torch.distributed as dist
+    from paper_2310_07147_b200.zero1 import CudaShard, ShardLayout, Zero1QftLion
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port_no = s_.getsockname()[1]
+    s_.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port_no}", rank=0,
+                            world_size=1)
+    try:
+        shapes = [(24, 512), (1, 512), (12, 256)]
+        layout = ShardLayout(shapes, 1)
+        local = CudaShard(layout, 0, bit_width=8)
+        host, ora = [], []
+        for i, sh in enumerate(shapes):
+            d = port.decompose_weight(port.synth(sh, 60 + i, 0.02, 0.005), 0.01, 8)
+            host.append(dict(codes=d.codes, scale=d.scale, zero_point=d.zero_point,
+                             t_min=d.t_min, t_max=d.t_max, row_ptr=d.row_ptr,
+                             col_idx=d.col_idx, values=d.values))
+            ora.append([d, port.quantize_state(np.zeros(sh, np.float32), 8)])
+        local.state.init_from_host(host)
+        z = Zero1QftLion(shapes, local)
+        for step in range(2):
+            grads = []
+            for i, sh in enumerate(shapes):
+                g = port.synth(sh, 800 + 10 * step + i, 1e-2, 0.0)
+                grads.append(torch.from_numpy(g).cuda())
+                d, m = ora[i]
+                ora[i] = list(port.lion_step_layer(d, *m, *port.quantize_state(g, 8),
+                                                   lr=1e-3)[:2])
+            layout.pack(grads, z.grad_full)
+            z.step(lr=1e-3)
+            local.state.check()
+            for i in range(len(shapes)):
+                got = z.gathered_tensor(i)
+                d = ora[i][0]
+                for k in ("codes", "row_ptr", "col_idx", "values"):
+                    _eq(got[k], getattr(d, k), f"zero1 step {step} tensor {i} {k}")
+    finally:
+        dist.destroy_process_group()
