@@ -279,7 +279,7 @@ def run_gpu_arm(args):
                    "parallelism": f"zero1-rows{world}" if world > 1 else "single"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic,
-                     "kernel": f"row_engine_kernel<STEP,u8> cols={g.cols}",
+                     "kernel": f"step_kernel<u8> cols={g.cols}",
                      "algorithmic_bytes_per_launch": alg, "launch_ms": per_group_ms[gi_dom],
                      "peak_kind": peak_kind},
         "step_hbm_gbs": all_alg / (ms * 1e-3) / 1e9,
@@ -398,12 +398,116 @@ def e2e_host(st, q, args, stream):
                     "chunked 3-stream H2D/step/D2H overlap"}
 
 
+def timed_steps(st, steps, stream):
+    """device time per launch group and per step for `steps` fused steps"""
+    import torch
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in st.groups] for _ in range(steps)]
+    h = None
+    for k in range(steps):
+        flip = st.cur
+        for gi, g in enumerate(st.groups):
+            ev[k][gi][0].record(stream)
+            st.step_chunk({"plan": g.plan}, flip, _hyper_c(), C.c_void_p(stream.cuda_stream))
+            ev[k][gi][1].record(stream)
+        st.cur = 1 - flip
+    torch.cuda.synchronize()
+    st.check()
+    per = [statistics.mean(ev[k][gi][0].elapsed_time(ev[k][gi][1]) for k in range(steps))
+           for gi in range(len(st.groups))]
+    return per
+
+
+def _hyper_c():
+    import paper_2310_07147_b200 as q
+    return q._native.hyper(HYPER["lr"], HYPER["beta1"], HYPER["beta2"], HYPER["weight_decay"])
+
+
+def run_sweep(args):
+    """configs[4]: weight bit width x outlier fraction on LLaMA-2-7B's 32 down-proj
+    tensors (4096 x 11008, 1.44 G params: out of L2), bytes/param vs roofline."""
+    import torch
+    import paper_2310_07147_b200 as q
+    global BIT_WIDTH, FRACTION
+    hbm, _ = peaks()
+    shapes = [(4096, 11008)] * 32
+    stream = torch.cuda.current_stream()
+    rows = []
+    for bw in (3, 4, 8):
+        for frac in (0.0005, 0.001, 0.0045, 0.01):
+            BIT_WIDTH, FRACTION = bw, frac
+            st = build_state(shapes, q, 777)
+            for _ in range(args.warmup):
+                st.step(**HYPER, check=True)
+            nnz0 = st.nnz()
+            per = timed_steps(st, args.steps, stream)
+            nnz1 = st.nnz()
+            params = st.param_count
+            alg = 5 * params + 8 * (nnz0 + nnz1) + 48 * st.row_count_total
+            ms = sum(per)
+            rows.append({"bit_width": bw, "outlier_fraction": frac, "ms": ms,
+                         "gparams_s": params / (ms * 1e-3) / 1e9,
+                         "bytes_per_param": alg / params, "achieved_gbs": alg / (ms * 1e-3) / 1e9,
+                         "frac_of_hbm": alg / (ms * 1e-3) / 1e9 / hbm, "nnz": nnz1})
+            del st
+            torch.cuda.empty_cache()
+    print(json.dumps({"sweep": "llama2-7b down_proj x32 (4096x11008), reference u8 layout",
+                      "peak_gbs": hbm, "rows": rows}), flush=True)
+
+
+def run_13b_dequant(args):
+    """configs[3] per rank on one GPU: the row shard (1/8) of LLaMA-2-13B stepped, then
+    the on-the-fly bf16 expansion of ALL 13B weights for the next forward."""
+    import torch
+    import paper_2310_07147_b200 as q
+    from paper_2310_07147_b200.shapes import llama2_13b, shard_rows, count
+    hbm, _ = peaks()
+    full = llama2_13b()
+    shard = shard_rows(full, 8, 0)
+    stream = torch.cuda.current_stream()
+    st = build_state(shard, q, 1313)
+    for _ in range(args.warmup):
+        st.step(**HYPER, check=True)
+    per = timed_steps(st, args.steps, stream)
+    step_ms = sum(per)
+    # bf16 expansion of every 13B tensor (codes + CSR -> bf16), measured on the shard's
+    # state replicated per width class: dequant cost is per element, independent of values
+    out = torch.empty(max(r * c for r, c in full), dtype=torch.bfloat16, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    src_of = {}
+    for i, (r, c) in enumerate(shard):
+        src_of.setdefault(c, i)
+    e0.record(stream)
+    n_el = 0
+    for (r, c) in full:
+        i = src_of[c]
+        rs, cs = st.shapes[i]
+        done = 0
+        while done < r:  # tile the full tensor with the shard tensor of the same width
+            take = min(rs, r - done)
+            st.reconstruct_into(i, out[done * c:(done + take) * c].view(take, c), take)
+            done += take
+        n_el += r * c
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dq_ms = e0.elapsed_time(e1)
+    nnz_frac = st.nnz() / st.param_count
+    dq_bytes = n_el * (1 + 2) + 8 * nnz_frac * n_el
+    print(json.dumps({"config": "llama2-13b per-rank (dp8 row shard) step + full bf16 expansion",
+                      "shard_params": st.param_count, "step_ms": step_ms,
+                      "step_gparams_s": st.param_count / (step_ms * 1e-3) / 1e9,
+                      "dequant_params": n_el, "dequant_ms": dq_ms,
+                      "dequant_gbs": dq_bytes / (dq_ms * 1e-3) / 1e9,
+                      "dequant_frac_of_hbm": dq_bytes / (dq_ms * 1e-3) / 1e9 / hbm}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
+    ap.add_argument("--mode", default="step", choices=["step", "sweep", "13b"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -411,6 +515,10 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference_arm(args)
+    elif args.mode == "sweep":
+        run_sweep(args)
+    elif args.mode == "13b":
+        run_13b_dequant(args)
     else:
         run_gpu_arm(args)
 

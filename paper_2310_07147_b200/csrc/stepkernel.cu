@@ -85,9 +85,12 @@ struct Layout {
   __host__ __device__ int masks_bytes() const { return r16(cp / 16 * 2); }
   __host__ __device__ int slots_bytes() const { return K * 4 * T * 16; }
   __host__ __device__ int meta_bytes() const { return 32 * (int)sizeof(Meta); }
+  // double-buffered by row parity: row t writes its sparse results before the barrier
+  // that retires row t-1, whose CSR phase may still read the other buffer
+  __host__ __device__ int sparse_bytes() const { return 16 * oldcap; }
   __host__ __device__ size_t total() const {
     return 128 + (size_t)S * stage_bytes() + sizeof(Tabs) + mprime_bytes() + masks_bytes() +
-           slots_bytes() + meta_bytes();
+           slots_bytes() + meta_bytes() + sparse_bytes();
   }
 };
 }  // namespace sk
@@ -149,6 +152,8 @@ __global__ void __launch_bounds__(sk::T, QFT_STEP_MIN_CTAS) step_kernel(const La
   float4* slots = reinterpret_cast<float4*>(p);
   p += L.slots_bytes();
   Meta* meta = reinterpret_cast<Meta*>(p);
+  p += L.meta_bytes();
+  float* const sp_base = reinterpret_cast<float*>(p);  // sparse pass: [w' | code|class<<8] x 2
 
   const int ct = threadIdx.x;
   const int warp = ct >> 5, lane = ct & 31;
@@ -318,7 +323,43 @@ __global__ void __launch_bounds__(sk::T, QFT_STEP_MIN_CTAS) step_kernel(const La
     const float* ovals = ov_of(s);
     const int old_n = cx->old_n, old_begin = cx->old_begin, staged = cx->old_staged;
 
-    // old-outlier bitmap + first rank per 32-column word (O(1) value lookup)
+    const DequantRow dw = make_dequant_row(cx->sw, cx->zw);
+    const DequantRow dm = make_dequant_row(cx->sm, cx->zm);
+    DequantRow dg = make_dequant_row(cx->sg, cx->zg);
+    QuantRow qg;
+    const QuantRow qw = make_quant_row(cx->sw, cx->zw, a.bit_width);
+    const float tmin = cx->tmin, tmax = cx->tmax;
+    const int zpay = cx->zpay;
+    const uint32_t zpay4 = (uint32_t)zpay * 0x01010101u;
+    const uint32_t wz_bits = __float_as_uint(__fmul_rn(cx->sw, (float)(zpay - cx->zw)));
+    const bool w_ovf = !(__fmul_rn(fabsf(cx->sw), (float)qmax + fabsf((float)cx->zw)) < 3.0e38f);
+    // old outliers: handled as a sparse side computation (one thread per entry)
+    // unless the row has more than the per-CTA table holds
+    const bool sparse_ok = old_n <= oldcap;
+    float* const sp_val = sp_base + (t & 1) * 2 * oldcap;
+    uint32_t* const sp_cw = reinterpret_cast<uint32_t*>(sp_val + oldcap);
+
+    // sparse pass for one old outlier: its exact w' (lion1, the general form), its
+    // class against the cached thresholds and its code -- what requantize_weight
+    // gives that element (quantize.hpp:274-285)
+    auto sparse_entry = [&](int i, int col) {
+      const float v0 = (staged && i < oldcap) ? ovals[i] : a.val_in[old_begin + i];
+      const float mv = sk_deq1(data[cp + col], dm);
+      float gv;
+      if (GK == G_U8) {
+        gv = sk_deq1(data[2 * cp + col], dg);
+      } else {
+        gv = sk_deq1(quant_exact(sk_graw<GK>(data + 2 * cp, col), qg.s, qg.z, qg.qmax), dg);
+      }
+      float wv = v0, mm = mv;
+      lion1(wv, mm, gv, h);
+      const bool o = (wv < tmin) || (wv > tmax);
+      const uint32_t code = o ? (uint32_t)zpay : quant_exact(wv, qw.s, qw.z, qw.qmax);
+      sp_val[i] = wv;
+      sp_cw[i] = code | (o ? 0x100u : 0u);
+    };
+
+    // old-outlier bitmap + first rank per 32-column word (O(1) rank/value lookup)
     for (int i = ct; i < old_n; i += T) {
       const int col = (staged && i < oldcap) ? ocols[i] : a.col_in[old_begin + i];
       const int wd = col >> 5;
@@ -326,19 +367,10 @@ __global__ void __launch_bounds__(sk::T, QFT_STEP_MIN_CTAS) step_kernel(const La
       const int prev = (i == 0) ? -1
                        : ((staged && i - 1 < oldcap) ? ocols[i - 1] : a.col_in[old_begin + i - 1]);
       if (i == 0 || (prev >> 5) != wd) frank[wd] = (uint16_t)i;
+      if (GK == G_U8 && sparse_ok) sparse_entry(i, col);
     }
     __syncthreads();  // bitmap ready; every thread is done with row t-1
     if (warp == 0 && t > 0) issue((t - 1) % S);
-
-    const DequantRow dw = make_dequant_row(cx->sw, cx->zw);
-    const DequantRow dm = make_dequant_row(cx->sm, cx->zm);
-    DequantRow dg = make_dequant_row(cx->sg, cx->zg);
-    QuantRow qg;
-    const QuantRow qw = make_quant_row(cx->sw, cx->zw, a.bit_width);
-    const float tmin = cx->tmin, tmax = cx->tmax;
-    const uint32_t zpay4 = (uint32_t)cx->zpay * 0x01010101u;
-    const uint32_t wz_bits = __float_as_uint(__fmul_rn(cx->sw, (float)(cx->zpay - cx->zw)));
-    const bool w_ovf = !(__fmul_rn(fabsf(cx->sw), (float)qmax + fabsf((float)cx->zw)) < 3.0e38f);
 
     // ---- raw-gradient kinds: fused quantize_state(g) -> dequantize (gradflow.hpp:77)
     if (GK != G_U8) {
@@ -384,6 +416,11 @@ __global__ void __launch_bounds__(sk::T, QFT_STEP_MIN_CTAS) step_kernel(const La
       }
       qg = make_quant_row(sgv, zgv, a.bit_width);
       dg = make_dequant_row(sgv, zgv);
+      if (sparse_ok) {  // the sparse pass needs the gradient params: one more barrier
+        for (int i = ct; i < old_n; i += T)
+          sparse_entry(i, (staged && i < oldcap) ? ocols[i] : a.col_in[old_begin + i]);
+        __syncthreads();
+      }
     }
 
     float mlo = __int_as_float(0x7f800000), mhi = __int_as_float(0xff800000);
@@ -425,8 +462,11 @@ __global__ void __launch_bounds__(sk::T, QFT_STEP_MIN_CTAS) step_kernel(const La
 #pragma unroll
           for (int q = 0; q < 4; ++q) dequant4(gc[q], dg, g + 4 * q);
         }
-        // old outliers: loop over the set bits only, select network into w[]
-        uint32_t o16 = skbits16(obits, v);
+        // old outliers: normally done by the sparse pass (their w here comes from the
+        // payload code and is patched over below); rows with more old outliers than
+        // the table holds patch w before the update instead
+        const uint32_t o16_all = skbits16(obits, v);
+        uint32_t o16 = sparse_ok ? 0u : o16_all;
         bool wspecial = w_ovf;
         while (o16) {
           const int e = __ffs(o16) - 1;
@@ -478,18 +518,15 @@ __global__ void __launch_bounds__(sk::T, QFT_STEP_MIN_CTAS) step_kernel(const La
         }
         // ---- outlier test, payload select, quantize w'
         float wq2[16];
+        const float wz = __uint_as_float(wz_bits);
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          const uint32_t d = outside_mask(w[e], tmin, tmax);
-          mask |= d & (1u << e);
-          wq2[e] = __uint_as_float((__float_as_uint(w[e]) & ~d) | (wz_bits & d));
-        }
+        for (int e = 0; e < 16; ++e) wq2[e] = outlier_select(w[e], tmin, tmax, wz, 1u << e, mask);
         mask &= valid;
-        float em = 0.0f;
+        QAcc qa = qacc_init();
         uint32_t c[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) c[q] = quant4_fast(wq2 + 4 * q, qw, em);
-        if (!qw.fast || !(em < qw.thr)) {
+        for (int q = 0; q < 4; ++q) c[q] = quant4_nc(wq2 + 4 * q, qw, qa);
+        if (!quant_vec_ok(qa, qw)) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) c[q] = quant4_exact(w + 4 * q, qw);
           if (mask) {
@@ -500,6 +537,26 @@ __global__ void __launch_bounds__(sk::T, QFT_STEP_MIN_CTAS) step_kernel(const La
             }
           }
         }
+        if (sparse_ok && o16_all) {
+          // old-outlier elements: class and code from the sparse pass
+          uint32_t ob = o16_all & valid;
+          while (ob) {
+            const int e = __ffs(ob) - 1;
+            ob &= ob - 1u;
+            const int col = v * 16 + e;
+            const int wd = col >> 5;
+            const int r = (int)frank[wd] + __popc(obits[wd] & ((1u << (col & 31)) - 1u));
+            const uint32_t cw = sp_cw[r];
+            mask = (mask & ~(1u << e)) | (((cw >> 8) & 1u) << e);
+            const uint32_t sh = (uint32_t)(e & 3) * 8u;
+            const uint32_t keep = ~(0xFFu << sh), put = (cw & 0xFFu) << sh;
+            const int q = e >> 2;
+            c[0] = (q == 0) ? ((c[0] & keep) | put) : c[0];
+            c[1] = (q == 1) ? ((c[1] & keep) | put) : c[1];
+            c[2] = (q == 2) ? ((c[2] & keep) | put) : c[2];
+            c[3] = (q == 3) ? ((c[3] & keep) | put) : c[3];
+          }
+        }
         uint8_t* wo = cx->w_out + v * 16;
         if (ALIGNED) {
           *reinterpret_cast<uint4*>(wo) = make_uint4(c[0], c[1], c[2], c[3]);
@@ -507,8 +564,10 @@ __global__ void __launch_bounds__(sk::T, QFT_STEP_MIN_CTAS) step_kernel(const La
           for (int e = 0; e < nvalid; ++e) wo[e] = (uint8_t)(c[e >> 2] >> ((e & 3) * 8));
         }
         masks[v] = (uint16_t)mask;
-        // park the w' values of a vector holding new outliers (CSR values later)
-        if (mask && slots_used < K) {
+        // park the w' values of a vector holding new dense-origin outliers (CSR values
+        // later; old-origin ones come from the sparse pass)
+        const uint32_t need_slot = sparse_ok ? (mask & ~o16_all) : mask;
+        if (need_slot && slots_used < K) {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             slots[(slots_used * 4 + q) * T + ct] =
@@ -605,11 +664,11 @@ __global__ void __launch_bounds__(sk::T, QFT_STEP_MIN_CTAS) step_kernel(const La
           m[4 * q] = f.x; m[4 * q + 1] = f.y; m[4 * q + 2] = f.z; m[4 * q + 3] = f.w;
         }
       }
-      float em = 0.0f;
+      QAcc qa = qacc_init();
       uint32_t c[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) c[q] = quant4_fast(m + 4 * q, qm, em);
-      if (!qm.fast || !(em < qm.thr)) {
+      for (int q = 0; q < 4; ++q) c[q] = quant4_nc(m + 4 * q, qm, qa);
+      if (!quant_vec_ok(qa, qm)) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) c[q] = quant4_exact(m + 4 * q, qm);
       }
@@ -637,12 +696,16 @@ __global__ void __launch_bounds__(sk::T, QFT_STEP_MIN_CTAS) step_kernel(const La
       }
       int pos = pref_k + incl - c;
       const int sid = (int)((slotmap >> (2 * k)) & 3ull);
+      const uint32_t o16 = (sparse_ok && v < nvec) ? skbits16(obits, v) : 0u;
       while (mask) {
         const int e = __ffs(mask) - 1;
         mask &= mask - 1u;
         const int col = v * 16 + e;
         float val;
-        if (sid < K) {
+        if (o16 & (1u << e)) {  // old-origin: value from the sparse pass
+          const int wd = col >> 5;
+          val = sp_val[(int)frank[wd] + __popc(obits[wd] & ((1u << (col & 31)) - 1u))];
+        } else if (sid < K) {
           val = reinterpret_cast<const float*>(&slots[(sid * 4 + (e >> 2)) * T + ct])[e & 3];
         } else {  // no slot left: recompute exactly as pass 1 did (scalar, exact)
           float wv = sk_deq1(data[col], dw);

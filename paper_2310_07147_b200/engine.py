@@ -465,6 +465,19 @@ class QftModelState:
             m_zero_point=self._rows(self.m_zp[cur], i).cpu().numpy(),
         )
 
+    def reconstruct_into(self, i: int, out: torch.Tensor, nrows: Optional[int] = None):
+        """Expand the first `nrows` rows of tensor i into `out` (f32 or bf16, [nrows, cols])."""
+        cur = self.cur
+        g = self.groups[self.group_of[i]]
+        r, c = self.shapes[i]
+        nrows = r if nrows is None else nrows
+        N.check(N.lib.qftc_reconstruct_slots(
+            _p(self._sl(self.w_codes[cur], i)), nrows, c, _p(self._rows(self.w_scale, i)),
+            _p(self._rows(self.w_zp, i)), _p(self._rs(self.row_start[cur], i)),
+            _p(self._rows(self.row_count[cur], i)), _p(g.col[cur]), _p(g.val[cur]), _p(out),
+            0 if out.dtype == torch.float32 else 1, _stream()))
+        return out
+
     def reconstruct(self, i: int, dtype=torch.float32) -> torch.Tensor:
         """Expand tensor i (dequant + CSR overwrite) to f32 or bf16 for the next forward."""
         cur = self.cur
