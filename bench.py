@@ -456,11 +456,12 @@ def run_sweep(args):
 
 
 def run_13b_dequant(args):
-    """configs[3] per rank on one GPU: the row shard (1/8) of LLaMA-2-13B stepped, then
-    the on-the-fly bf16 expansion of ALL 13B weights for the next forward."""
+    """configs[3] per rank on one GPU: rank 0's row shard (1/8) of LLaMA-2-13B stepped,
+    then the on-the-fly bf16 expansion of ALL 13B weights (what every rank does after the
+    all-gather, for its next forward) in one grouped launch (qftc_expand)."""
     import torch
     import paper_2310_07147_b200 as q
-    from paper_2310_07147_b200.shapes import llama2_13b, shard_rows, count
+    from paper_2310_07147_b200.shapes import llama2_13b, shard_rows
     hbm, _ = peaks()
     full = llama2_13b()
     shard = shard_rows(full, 8, 0)
@@ -470,35 +471,39 @@ def run_13b_dequant(args):
         st.step(**HYPER, check=True)
     per = timed_steps(st, args.steps, stream)
     step_ms = sum(per)
-    # bf16 expansion of every 13B tensor (codes + CSR -> bf16), measured on the shard's
-    # state replicated per width class: dequant cost is per element, independent of values
-    out = torch.empty(max(r * c for r, c in full), dtype=torch.bfloat16, device="cuda")
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    src_of = {}
-    for i, (r, c) in enumerate(shard):
-        src_of.setdefault(c, i)
-    e0.record(stream)
-    n_el = 0
-    for (r, c) in full:
-        i = src_of[c]
-        rs, cs = st.shapes[i]
-        done = 0
-        while done < r:  # tile the full tensor with the shard tensor of the same width
-            take = min(rs, r - done)
-            st.reconstruct_into(i, out[done * c:(done + take) * c].view(take, c), take)
-            done += take
-        n_el += r * c
-    e1.record(stream)
+    shard_params = st.param_count
+    del st
+    torch.cuda.empty_cache()
+    # the gathered full-model state: every 13B tensor's codes + params + CSR
+    fst = build_state(full, q, 2626)
+    outs = [torch.empty((r, c), dtype=torch.bfloat16, device="cuda") for r, c in full]
+    table = fst.expand_table(outs)
+    for _ in range(2):
+        fst.expand(outs, table=table)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
     torch.cuda.synchronize()
-    dq_ms = e0.elapsed_time(e1)
-    nnz_frac = st.nnz() / st.param_count
-    dq_bytes = n_el * (1 + 2) + 8 * nnz_frac * n_el
+    for e0, e1 in ev:
+        e0.record(stream)
+        fst.expand(outs, table=table)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    dq_ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in ev)
+    n_el = fst.param_count
+    nnz = fst.nnz()
+    # algorithmic bytes: 1 B code read + 2 B bf16 written per param, 8 B per CSR entry
+    # read (+2 B scattered bf16 write), 16 B per row (scale, zp, row_start, row_count)
+    dq_bytes = 3 * n_el + 10 * nnz + 16 * fst.row_count_total
+    launches = (len(full) + 223) // 224
     print(json.dumps({"config": "llama2-13b per-rank (dp8 row shard) step + full bf16 expansion",
-                      "shard_params": st.param_count, "step_ms": step_ms,
-                      "step_gparams_s": st.param_count / (step_ms * 1e-3) / 1e9,
-                      "dequant_params": n_el, "dequant_ms": dq_ms,
+                      "shard_params": shard_params, "step_ms": step_ms,
+                      "step_gparams_s": shard_params / (step_ms * 1e-3) / 1e9,
+                      "dequant_params": n_el, "dequant_nnz": nnz, "dequant_ms": dq_ms,
+                      "dequant_launches": launches,
+                      "dequant_gparams_s": n_el / (dq_ms * 1e-3) / 1e9,
                       "dequant_gbs": dq_bytes / (dq_ms * 1e-3) / 1e9,
-                      "dequant_frac_of_hbm": dq_bytes / (dq_ms * 1e-3) / 1e9 / hbm}), flush=True)
+                      "dequant_frac_of_hbm": dq_bytes / (dq_ms * 1e-3) / 1e9 / hbm,
+                      "peak_gbs": hbm}), flush=True)
 
 
 def main():

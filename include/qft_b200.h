@@ -214,6 +214,26 @@ int qftc_reconstruct_slots(const uint8_t* codes, int rows, int cols, const float
                            const int32_t* row_count, const int32_t* col_idx,
                            const float* values, void* out, int bf16, qftc_stream_t stream);
 
+/* Grouped weight expansion for the next forward (quantize.hpp:331-338 reconstruct of
+ * every tensor of a model, network.hpp:208-211): one launch per up to 224 tensors, no
+ * host synchronisation, no device allocation.  Each tensor: codes [rows, cols] u8, its
+ * per-row scale/zero_point, its CSR as row_start (+ row_count for a slotted CSR; NULL
+ * means strict, count = row_start[r+1]-row_start[r]) indexing col_idx/values, and out
+ * [rows, cols] f32 or (bf16 != 0) bf16 bits, RNE of the f32 reconstruction. */
+typedef struct qftc_expand_tensor {
+  int32_t rows, cols;
+  const uint8_t* codes;
+  const float* scale;
+  const int32_t* zero_point;
+  const int32_t* row_start;
+  const int32_t* row_count;
+  const int32_t* col_idx;
+  const float* values;
+  void* out;
+} qftc_expand_tensor;
+int qftc_expand(const qftc_expand_tensor* tensors, int n_tensors, int bf16,
+                qftc_stream_t stream);
+
 /* Pass-through mode (QuantMode::passthrough, quantize.hpp:17): lion_apply on raw
  * fp32 state, bitwise equal to lion_step_reference (optimizer.hpp:135-142). */
 int qftc_lion_apply(float* w, float* m, const float* g, int64_t n, qftc_lion_hyper hyper,

@@ -43,6 +43,16 @@ class LionTensorC(C.Structure):
     ]
 
 
+class ExpandTensorC(C.Structure):
+    """``qftc_expand_tensor``: one tensor of a grouped weight expansion."""
+    _fields_ = [
+        ("rows", C.c_int32), ("cols", C.c_int32),
+        ("codes", C.c_void_p), ("scale", C.c_void_p), ("zero_point", C.c_void_p),
+        ("row_start", C.c_void_p), ("row_count", C.c_void_p),
+        ("col_idx", C.c_void_p), ("values", C.c_void_p), ("out", C.c_void_p),
+    ]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -85,6 +95,7 @@ _SIGS = {
     "qftc_csr_compact": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, C.POINTER(_i64),
                               _vp]),
     "qftc_reconstruct_slots": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp]),
+    "qftc_expand": (_i, [_vp, _i, _i, _vp]),
     "qftc_device_alloc": (_i, [C.POINTER(_vp), C.c_size_t]),
     "qftc_device_free": (_i, [_vp]),
     "qftc_copy_to_device": (_i, [_vp, _vp, C.c_size_t, _vp]),

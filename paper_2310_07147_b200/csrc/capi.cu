@@ -132,31 +132,6 @@ int scratch_alloc(Scratch& s, const std::vector<DevTensor>& ts, int64_t status_r
   return QFTC_OK;
 }
 
-// launch shape: most CTAs per SM first, then keeping m' in smem (no recompute),
-// then most pipeline stages
-struct Cfg {
-  int stages, mrec;
-};
-Cfg pick_config(int mode, int gk, int cols_p, bool allow_mrec) {
-  Cfg best{2, 0};
-  long best_score = -1;
-  for (int m = 0; m <= (allow_mrec ? 1 : 0); ++m) {
-    for (int S = 2; S <= 4; ++S) {
-      const size_t smem = row_engine_smem(mode, gk, cols_p, S, m != 0);
-      if (smem > 227 * 1024) break;
-      const long per_sm = (long)((228 * 1024) / (smem + 1024));
-      const long blocks = per_sm < QFT_MIN_CTAS ? per_sm : QFT_MIN_CTAS;  // register limit
-      const long score = blocks * 64 + (m ? 0 : 16) + S;
-      if (blocks >= 1 && score > best_score) {
-        best_score = score;
-        best = Cfg{S, m};
-      }
-    }
-  }
-  return best;
-}
-int pick_stages(int mode, int gk, int cols_p) { return pick_config(mode, gk, cols_p, false).stages; }
-
 // step kernel shape: most CTAs per SM (registers cap it at QFT_STEP_MIN_CTAS), then
 // m' kept in smem, then pipeline depth, then parked-outlier slots.  QFT_STEP_CFG="S,K,mrec"
 // overrides it (tuning / A-B runs).
@@ -206,7 +181,7 @@ extern "C" {
 
 const char* qftc_last_error(void) { return g_err.c_str(); }
 int qftc_version(void) { return 2; }
-int qftc_max_cols(void) { return row_engine_max_cols(); }
+int qftc_max_cols(void) { return step_kernel_max_cols(); }
 
 int qftc_channel_minmax(const float* x, int rows, int cols, float* mins, float* maxs,
                         qftc_stream_t stream) {
@@ -315,50 +290,32 @@ int qftc_decompose_dense_sparse(const float* w, int rows, int cols, const float*
                                 int64_t capacity, int64_t* nnz_host, qftc_stream_t stream) {
   if (int rc = require_shape(rows, cols, "decompose_dense_sparse")) return rc;
   if (int rc = require_bit_width(bit_width)) return rc;
-  if (cols > row_engine_max_cols())
-    return fail(QFTC_ENOTSUP, "decompose: cols above " + std::to_string(row_engine_max_cols()));
+  if (!w || !codes || !row_ptr) return fail(QFTC_EINVAL, "decompose: null pointer");
   if (int rc = require_device()) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   // params from thresholds (quantize.hpp:264) -- validates t_min <= t_max
   int rc = qftc_affine_params_from_bounds(t_min, t_max, rows, bit_width, scale, zp, stream);
   if (rc) return rc;
-  DevTensor t{};
-  t.rows = rows;
-  t.cols = cols;
-  t.w_f32 = w;
-  t.w_scale = scale;
-  t.w_zp = zp;
-  t.t_min = t_min;
-  t.t_max = t_max;
-  t.w_codes[1] = codes;
-  t.rs[1] = row_ptr;
-  Scratch sc;
-  if ((rc = scratch_alloc(sc, {t}, rows, st))) return rc;
-  LaunchArgs a{};
-  a.tensors = sc.tensors;
-  a.blocks = sc.blocks;
-  a.n_tensors = 1;
-  a.n_blocks = sc.n_blocks;
-  a.total_rows = rows;
-  a.bit_width = bit_width;
-  a.col_out = col_idx;
-  a.val_out = values;
-  a.cap_out = capacity;
-  a.hdr = sc.hdr;
-  a.status = sc.status;
-  a.cols_p = (cols + 15) & ~15;
-  a.use_bulk = (cols % 16 == 0) && al16(w) && al16(codes);
-  a.stages = pick_stages(MODE_DECOMPOSE, G_U8, a.cols_p);
-  QFTC_CUDA(launch_row_engine(MODE_DECOMPOSE, G_U8, a, st, nullptr), "decompose kernel");
-  Header h{};
-  rc = read_header(sc.hdr, &h, st);
-  cudaFreeAsync(sc.base, st);
-  if (rc) return rc;
-  if (nnz_host) *nnz_host = h.total_nnz;
-  if (h.err & ERR_PREFIX) return fail(QFTC_ENOTSUP, "decompose: nnz above 2^30");
-  if (h.overflow)
-    return fail(QFTC_EOVERFLOW, "decompose: nnz " + std::to_string(h.total_nnz) +
-                                    " exceeds capacity " + std::to_string(capacity));
+  int32_t* counts = nullptr;
+  QFTC_CUDA(cudaMallocAsync((void**)&counts, (size_t)rows * 4, st), "alloc");
+  cudaError_t e = decompose_codes(w, rows, cols, scale, zp, t_min, t_max, bit_width, codes,
+                                  counts, st);
+  if (e == cudaSuccess) e = csr_row_ptr(counts, rows, row_ptr, st);
+  int32_t nnz = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&nnz, row_ptr + rows, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFreeAsync(counts, st);
+  QFTC_CUDA(e, "decompose codes");
+  if (nnz_host) *nnz_host = nnz;
+  if (nnz < 0) return fail(QFTC_ENOTSUP, "decompose: nnz above 2^31");
+  if ((int64_t)nnz > capacity)
+    return fail(QFTC_EOVERFLOW, "decompose: nnz " + std::to_string(nnz) + " exceeds capacity " +
+                                    std::to_string(capacity));
+  if (nnz > 0) {
+    if (!col_idx || !values) return fail(QFTC_EINVAL, "decompose: null CSR arrays");
+    QFTC_CUDA(decompose_csr(w, rows, cols, t_min, t_max, row_ptr, col_idx, values, st),
+              "decompose csr");
+  }
   return QFTC_OK;
 }
 
@@ -366,40 +323,38 @@ static int reconstruct_impl(const uint8_t* codes, int rows, int cols, const floa
                             const int32_t* zp, const int32_t* row_start,
                             const int32_t* row_count, const int32_t* col_idx,
                             const float* values, void* out, bool bf16, qftc_stream_t stream) {
-  if (int rc = require_shape(rows, cols, "dequantize")) return rc;
-  if (cols > row_engine_max_cols())
-    return fail(QFTC_ENOTSUP, "reconstruct: cols above " + std::to_string(row_engine_max_cols()));
+  if (int rc = require_shape(rows, cols, "reconstruct")) return rc;
+  if (!codes || !scale || !zp || !row_start || !out)
+    return fail(QFTC_EINVAL, "reconstruct: null pointer");
   if (int rc = require_device()) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
-  DevTensor t{};
+  qftc_expand_tensor t{};
   t.rows = rows;
   t.cols = cols;
-  t.w_codes[0] = const_cast<uint8_t*>(codes);
-  t.rs[0] = const_cast<int32_t*>(row_start);
-  t.cnt[0] = const_cast<int32_t*>(row_count);
-  t.w_scale = scale;
-  t.w_zp = zp;
+  t.codes = codes;
+  t.scale = scale;
+  t.zero_point = zp;
+  t.row_start = row_start;
+  t.row_count = row_count;
+  t.col_idx = col_idx;
+  t.values = values;
   t.out = out;
-  Scratch sc;
-  if (int rc = scratch_alloc(sc, {t}, 0, st)) return rc;
-  LaunchArgs a{};
-  a.tensors = sc.tensors;
-  a.blocks = sc.blocks;
-  a.n_tensors = 1;
-  a.n_blocks = sc.n_blocks;
-  a.total_rows = rows;
-  a.bit_width = 8;
-  a.col_in = col_idx;
-  a.val_in = values;
-  a.hdr = sc.hdr;
-  a.status = sc.status;
-  a.cols_p = (cols + 15) & ~15;
-  a.use_bulk = (cols % 16 == 0) && al16(codes) && al16(out);
-  a.slotted_in = row_count != nullptr && al16(col_idx) && al16(values);
-  const int mode = bf16 ? MODE_RECON_BF16 : MODE_RECON_F32;
-  a.stages = pick_stages(mode, G_U8, a.cols_p);
-  QFTC_CUDA(launch_row_engine(mode, G_U8, a, st, nullptr), "reconstruct kernel");
-  QFTC_CUDA(cudaFreeAsync(sc.base, st), "free");
+  QFTC_CUDA(launch_expand(&t, 1, bf16, (cudaStream_t)stream), "reconstruct kernel");
+  return QFTC_OK;
+}
+
+int qftc_expand(const qftc_expand_tensor* tensors, int n_tensors, int bf16,
+                qftc_stream_t stream) {
+  if (n_tensors < 0 || (n_tensors > 0 && !tensors))
+    return fail(QFTC_EINVAL, "expand: bad tensor list");
+  for (int i = 0; i < n_tensors; ++i) {
+    const qftc_expand_tensor& t = tensors[i];
+    if (int rc = require_shape(t.rows, t.cols, "expand")) return rc;
+    if (!t.codes || !t.scale || !t.zero_point || !t.row_start || !t.out)
+      return fail(QFTC_EINVAL, "expand: null pointer in tensor " + std::to_string(i));
+  }
+  if (n_tensors == 0) return QFTC_OK;
+  if (int rc = require_device()) return rc;
+  QFTC_CUDA(launch_expand(tensors, n_tensors, bf16 != 0, (cudaStream_t)stream), "expand kernel");
   return QFTC_OK;
 }
 
@@ -519,8 +474,8 @@ int qftc_plan_create(qftc_plan** out, const qftc_lion_tensor* ts, int n, int bit
     const qftc_lion_tensor& t = ts[i];
     if (t.rows <= 0 || t.cols <= 0)
       return fail(QFTC_EINVAL, "lion step: empty tensor " + std::to_string(i));
-    if (t.cols > row_engine_max_cols())
-      return fail(QFTC_ENOTSUP, "lion step: cols above " + std::to_string(row_engine_max_cols()));
+    if (t.cols > step_kernel_max_cols())
+      return fail(QFTC_ENOTSUP, "lion step: cols above " + std::to_string(step_kernel_max_cols()));
     DevTensor& d = dts[(size_t)i];
     d = DevTensor{};
     d.rows = t.rows;

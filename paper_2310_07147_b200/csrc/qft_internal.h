@@ -64,13 +64,11 @@ struct Header {
   int64_t _pad2[5];
 };
 
-enum Mode : int { MODE_STEP = 0, MODE_DECOMPOSE = 1, MODE_RECON_F32 = 2, MODE_RECON_BF16 = 3 };
 enum GradKind : int { G_U8 = 0, G_F32 = 1, G_BF16 = 2 };
 
 // error bits in Header::err
 constexpr uint32_t ERR_MPARAMS = 1u;   // momentum min > max (NaN in column 0)
 constexpr uint32_t ERR_GPARAMS = 2u;   // gradient min > max
-constexpr uint32_t ERR_PREFIX = 4u;    // decompose nnz prefix exceeded 2^30
 
 struct LaunchArgs {
   DevTensor* tensors;
@@ -101,10 +99,19 @@ struct LaunchArgs {
 size_t step_kernel_smem(int gk, int cols_p, int stages, int oldcap, int slots, bool mrec);
 cudaError_t launch_step_kernel(int gk, const LaunchArgs& a, cudaStream_t s);
 
-// launch helpers (rowengine.cu)
-size_t row_engine_smem(int mode, int gk, int cols_p, int stages, bool mrec);
-cudaError_t launch_row_engine(int mode, int gk, const LaunchArgs& a, cudaStream_t s,
-                              int* grid_out);
-int row_engine_max_cols();
+int step_kernel_max_cols();
+
+// decomposition with given thresholds (decompose.cu)
+cudaError_t decompose_codes(const float* w, int rows, int cols, const float* scale,
+                            const int32_t* zp, const float* t_min, const float* t_max,
+                            int bit_width, uint8_t* codes, int32_t* counts, cudaStream_t s);
+cudaError_t decompose_csr(const float* w, int rows, int cols, const float* t_min,
+                          const float* t_max, const int32_t* row_ptr, int32_t* col_idx,
+                          float* values, cudaStream_t s);
+cudaError_t csr_row_ptr(const int32_t* counts, int rows, int32_t* row_ptr, cudaStream_t s);
+
+// weight expansion (expand.cu): one launch per expand_max_tensors() tensors
+int expand_max_tensors();
+cudaError_t launch_expand(const qftc_expand_tensor* ts, int n, bool bf16, cudaStream_t s);
 
 }  // namespace qftk

@@ -95,6 +95,8 @@ struct Layout {
 };
 }  // namespace sk
 
+int step_kernel_max_cols() { return sk::NCH_MAX * sk::T * 16; }
+
 size_t step_kernel_smem(int gk, int cols_p, int stages, int oldcap, int slots, bool mrec) {
   sk::Layout L{cols_p, oldcap, stages, slots, mrec, gk};
   return L.total();
@@ -326,7 +328,7 @@ __global__ void __launch_bounds__(sk::T, QFT_STEP_MIN_CTAS) step_kernel(const La
     const DequantRow dw = make_dequant_row(cx->sw, cx->zw);
     const DequantRow dm = make_dequant_row(cx->sm, cx->zm);
     DequantRow dg = make_dequant_row(cx->sg, cx->zg);
-    QuantRow qg;
+    QuantRow qg{};
     const QuantRow qw = make_quant_row(cx->sw, cx->zw, a.bit_width);
     const float tmin = cx->tmin, tmax = cx->tmax;
     const int zpay = cx->zpay;

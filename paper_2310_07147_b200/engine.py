@@ -478,6 +478,45 @@ class QftModelState:
             0 if out.dtype == torch.float32 else 1, _stream()))
         return out
 
+    def expand_table(self, outs: Sequence[torch.Tensor], rows: Optional[Sequence[int]] = None):
+        """ctypes table (qftc_expand_tensor[n]) expanding tensor i's first rows[i] rows into
+        outs[i] from the CURRENT state; reusable while `cur` and the buffers are unchanged."""
+        cur = self.cur
+        n = len(self.shapes)
+        tab = (N.ExpandTensorC * n)()
+        bf16 = None
+        for i, (r, c) in enumerate(self.shapes):
+            o = outs[i]
+            isb = o.dtype == torch.bfloat16
+            if bf16 is None:
+                bf16 = isb
+            if isb != bf16 or o.dtype not in (torch.float32, torch.bfloat16):
+                raise ValueError("expand: every output must be f32, or every output bf16")
+            g = self.groups[self.group_of[i]]
+            t = tab[i]
+            t.rows = r if rows is None else int(rows[i])
+            t.cols = c
+            if o.numel() < t.rows * c:
+                raise ValueError(f"expand: output {i} holds {o.numel()} < {t.rows * c} elements")
+            t.codes = self._sl(self.w_codes[cur], i).data_ptr()
+            t.scale = self._rows(self.w_scale, i).data_ptr()
+            t.zero_point = self._rows(self.w_zp, i).data_ptr()
+            t.row_start = self._rs(self.row_start[cur], i).data_ptr()
+            t.row_count = self._rows(self.row_count[cur], i).data_ptr()
+            t.col_idx = g.col[cur].data_ptr()
+            t.values = g.val[cur].data_ptr()
+            t.out = o.data_ptr()
+        return tab, 1 if bf16 else 0
+
+    def expand(self, outs: Sequence[torch.Tensor], rows: Optional[Sequence[int]] = None,
+               table=None):
+        """Reconstruct every tensor (dense dequant + CSR overwrite, quantize.hpp:331-338)
+        into outs (all f32 or all bf16) with one grouped launch -- the weight expansion
+        for the next forward (network.hpp:208-211)."""
+        tab, bf16 = table if table is not None else self.expand_table(outs, rows)
+        N.check(N.lib.qftc_expand(C.cast(tab, C.c_void_p), len(tab), bf16, _stream()))
+        return outs
+
     def reconstruct(self, i: int, dtype=torch.float32) -> torch.Tensor:
         """Expand tensor i (dequant + CSR overwrite) to f32 or bf16 for the next forward."""
         cur = self.cur

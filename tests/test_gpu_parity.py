@@ -248,6 +248,57 @@ def test_engine_grouped_step_matches_oracle(cuda, port):
             _eq(got["m_zero_point"], m[2], tag + " m zp")
 
 
+def test_engine_expand_grouped(cuda, port):
+    """Grouped weight expansion (qftc_expand, one launch for the model) after a step:
+    f32 bit-exact with the oracle's reconstruct, bf16 = RNE of it; covers the vector
+    path, unaligned widths, a 1xC row and the exact (|z| >= 2^22) dequant rows."""
+    shapes = [(32, 4096), (1, 4096), (96, 1024), (9, 100), (6, 7), (8, 1024)]
+    bw = 8
+    rng = np.random.default_rng(7)
+    oracle_state, tensors = [], []
+    for i, sh in enumerate(shapes):
+        if i == len(shapes) - 1:
+            w = _rows_zoo(rng, sh[0], sh[1], bw)
+            dsw = port.decompose_weight(w, 0.01, bw)
+            m = port.quantize_state(np.zeros(sh, np.float32), bw)
+        else:
+            dsw, m = _layer(port, sh, 700 + i, bw, 0.01)
+        tensors.append(dict(codes=dsw.codes, scale=dsw.scale, zero_point=dsw.zero_point,
+                            t_min=dsw.t_min, t_max=dsw.t_max, row_ptr=dsw.row_ptr,
+                            col_idx=dsw.col_idx, values=dsw.values))
+        oracle_state.append([dsw, m])
+    eng = cuda.QftModelState(shapes, bit_width=bw)
+    eng.init_from_host(tensors)
+    for i, sh in enumerate(shapes):
+        gq = port.quantize_state(port.synth(sh, 7100 + i, 1e-2, 0.0), bw)
+        c, s, z = eng.grad_views(i)
+        c.copy_(torch.from_numpy(gq[0]))
+        s.copy_(torch.from_numpy(gq[1]))
+        z.copy_(torch.from_numpy(gq[2]))
+        dsw, m = oracle_state[i]
+        oracle_state[i][0] = port.lion_step_layer(dsw, *m, *gq, lr=1e-3)[0]
+    eng.step(lr=1e-3, check=True)
+    f32 = [torch.full(sh, float("nan"), device="cuda") for sh in shapes]
+    b16 = [torch.zeros(sh, dtype=torch.bfloat16, device="cuda") for sh in shapes]
+    eng.expand(f32)
+    eng.expand(b16)
+    for i in range(len(shapes)):
+        rec = port.reconstruct(oracle_state[i][0])
+        _eq(_np(f32[i]), rec, f"expand f32 tensor {i}")
+        _eq(_np(b16[i].float()), _np(torch.from_numpy(rec).to(torch.bfloat16).float()),
+            f"expand bf16 tensor {i}")
+    # a row prefix only (the expansion of a partial tensor leaves the rest untouched)
+    part = [torch.zeros(sh, device="cuda") for sh in shapes]
+    eng.expand(part, rows=[min(2, sh[0]) for sh in shapes])
+    for i, sh in enumerate(shapes):
+        rec = port.reconstruct(oracle_state[i][0])
+        k = min(2, sh[0])
+        _eq(_np(part[i][:k]), rec[:k], f"expand prefix tensor {i}")
+        assert not bool(part[i][k:].any())
+    with pytest.raises(ValueError):
+        eng.expand(f32[:-1] + [b16[-1]])
+
+
 def test_lion_apply_passthrough_bitwise(cuda, port):
     """QuantMode::passthrough pipeline == lion_step_reference bitwise (test_optimizer.cpp:160-187)"""
     rng = np.random.default_rng(5)
