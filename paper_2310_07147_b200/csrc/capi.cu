@@ -144,15 +144,15 @@ StepCfg pick_step_config(int gk, int cols_p, bool allow_mrec) {
     StepCfg c{3, 1, 0, oldcap};
     if (sscanf(env, "%d,%d,%d", &c.S, &c.K, &c.mrec) == 3) {
       c.mrec = (c.mrec && allow_mrec) ? 1 : 0;
-      if (c.S >= 2 && c.S <= 8 && c.K >= 1 && c.K <= 3 &&
+      if (c.S >= 3 && c.S <= 8 && c.K >= 1 && c.K <= 3 &&
           step_kernel_smem(gk, cols_p, c.S, oldcap, c.K, c.mrec) <= 227 * 1024)
         return c;
     }
   }
-  StepCfg best{2, 1, allow_mrec ? 1 : 0, oldcap};
+  StepCfg best{3, 1, allow_mrec ? 1 : 0, oldcap};
   long best_score = -1;
   for (int m = 0; m <= (allow_mrec ? 1 : 0); ++m)
-    for (int S = 2; S <= 6; ++S)
+    for (int S = 3; S <= 6; ++S)  // >= 3: a stage is refilled two rows after its use
       for (int K = 1; K <= 2; ++K) {
         const size_t smem = step_kernel_smem(gk, cols_p, S, oldcap, K, m != 0);
         if (smem > 227 * 1024) continue;

@@ -170,11 +170,13 @@ def _layer(port, shape, seed, bw, frac):
     return dsw, m
 
 
+@pytest.mark.parametrize("wd", [0.0, 0.01])
 @pytest.mark.parametrize("bw,frac", [(8, 0.01), (4, 0.01), (3, 0.0045), (8, 0.05)])
 @pytest.mark.parametrize("shape", [(64, 4096), (24, 11008), (16, 48), (5, 13)])
-def test_lion_step_trajectory(cuda, port, bw, frac, shape):
+def test_lion_step_trajectory(cuda, port, bw, frac, shape, wd):
     """10 quantized Lion steps through the C-ABI single-layer entry, byte-compared each step
-    (exercises CSR drift: nnz moves while thresholds stay cached)."""
+    (exercises CSR drift: nnz moves while thresholds stay cached); wd=0 runs the
+    saturating sign-update form on proven rows, wd>0 the general form."""
     dsw, m = _layer(port, shape, 100 + shape[1], bw, frac)
     dw = cuda.DenseSparseWeight(
         cuda.QuantizedTensor(shape[0], shape[1], torch.from_numpy(dsw.codes).cuda(),
@@ -188,9 +190,64 @@ def test_lion_step_trajectory(cuda, port, bw, frac, shape):
                                               cuda.AffineParams(torch.from_numpy(m[1]).cuda(),
                                                                 torch.from_numpy(m[2]).cuda(),
                                                                 bw))])
-    h = cuda.LionHyper(lr=2e-3, beta1=0.9, beta2=0.99, weight_decay=0.01)
+    h = cuda.LionHyper(lr=2e-3, beta1=0.9, beta2=0.99, weight_decay=wd)
     for step in range(10):
         g = port.synth(shape, 7000 + step, 1e-2, 0.0)
+        gq = port.quantize_state(g, bw)
+        stack = cuda.GradientStack()
+        stack.push(1, cuda.QuantizedTensor(shape[0], shape[1], torch.from_numpy(gq[0]).cuda(),
+                                           cuda.AffineParams(torch.from_numpy(gq[1]).cuda(),
+                                                             torch.from_numpy(gq[2]).cuda(), bw)))
+        cuda.lion_step_quantized([dw], st, stack, h, bw)
+        dsw, m, _ = port.lion_step_layer(dsw, *m, *gq, lr=h.lr, beta1=h.beta1, beta2=h.beta2,
+                                         wd=h.weight_decay)
+        tag = f"step {step}"
+        _eq(_np(st.momentum[0].params.scale), m[1], tag + " m scale")
+        _eq(_np(st.momentum[0].params.zero_point), m[2], tag + " m zp")
+        _eq(_np(st.momentum[0].data), m[0], tag + " m codes")
+        _eq(_np(dw.dense.data), dsw.codes, tag + " w codes")
+        _eq(_np(dw.sparse.row_ptr), dsw.row_ptr, tag + " row_ptr")
+        _eq(_np(dw.sparse.col_idx), dsw.col_idx, tag + " col_idx")
+        _eq(_np(dw.sparse.values), dsw.values, tag + " values")
+
+
+def _dev_layer(cuda, dsw, m, shape, bw, frac):
+    dw = cuda.DenseSparseWeight(
+        cuda.QuantizedTensor(shape[0], shape[1], torch.from_numpy(dsw.codes).cuda(),
+                             cuda.AffineParams(torch.from_numpy(dsw.scale).cuda(),
+                                               torch.from_numpy(dsw.zero_point).cuda(), bw)),
+        cuda.SparseOutliers(torch.from_numpy(dsw.row_ptr).cuda(),
+                            torch.from_numpy(dsw.col_idx).cuda(),
+                            torch.from_numpy(dsw.values).cuda()),
+        torch.from_numpy(dsw.t_min).cuda(), torch.from_numpy(dsw.t_max).cuda(), frac)
+    st = cuda.LionState([cuda.QuantizedTensor(shape[0], shape[1], torch.from_numpy(m[0]).cuda(),
+                                              cuda.AffineParams(torch.from_numpy(m[1]).cuda(),
+                                                                torch.from_numpy(m[2]).cuda(),
+                                                                bw))])
+    return dw, st
+
+
+@pytest.mark.parametrize("wd", [0.0, 0.01])
+@pytest.mark.parametrize("bw", [8, 4])
+def test_lion_step_edge_rows(cuda, port, bw, wd):
+    """Rows that must leave the fast paths, stepped next to ordinary ones: all-zero and
+    constant channels, narrow channels far from zero (|z| >= 2^22), tiny scales, planted
+    ties (the zoo), and gradients that are zero, 1e-30-scaled (Lion sign products below
+    the saturating form's bound), 1e30-scaled or constant per row."""
+    shape = (12, 1024)
+    rng = np.random.default_rng(11 + bw)
+    w = _rows_zoo(rng, shape[0], shape[1], bw)
+    dsw = port.decompose_weight(w, 0.01, bw)
+    m = port.quantize_state(np.zeros(shape, np.float32), bw)
+    dw, st = _dev_layer(cuda, dsw, m, shape, bw, 0.01)
+    h = cuda.LionHyper(lr=1e-3, beta1=0.9, beta2=0.99, weight_decay=wd)
+    for step in range(6):
+        g = port.synth(shape, 8100 + step, 1e-2, 0.0)
+        g[0] = 0.0
+        g[1] *= np.float32(1e-28)
+        g[2] *= np.float32(1e30)
+        g[3] = np.float32(0.25)
+        g[7] *= np.float32(1e-40 if step % 2 else 1.0)
         gq = port.quantize_state(g, bw)
         stack = cuda.GradientStack()
         stack.push(1, cuda.QuantizedTensor(shape[0], shape[1], torch.from_numpy(gq[0]).cuda(),
