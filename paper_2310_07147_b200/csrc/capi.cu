@@ -132,40 +132,21 @@ int scratch_alloc(Scratch& s, const std::vector<DevTensor>& ts, int64_t status_r
   return QFTC_OK;
 }
 
-// step kernel shape: most CTAs per SM (registers cap it at QFT_STEP_MIN_CTAS), then
-// m' kept in smem, then pipeline depth, then parked-outlier slots.  QFT_STEP_CFG="S,K,mrec"
-// overrides it (tuning / A-B runs).
+// step kernel shape (warp-per-row kernel): the old-outlier table per warp, sized for
+// the width class (rows with more old outliers take the general path).
+// QFT_STEP_CFG="oldcap" overrides it (tuning).
 struct StepCfg {
-  int S, K, mrec, oldcap;
+  int oldcap;
 };
-StepCfg pick_step_config(int gk, int cols_p, bool allow_mrec) {
-  const int oldcap = cols_p <= 4096 ? 128 : 256;
+StepCfg pick_step_config(int gk, int cols_p) {
+  StepCfg c{cols_p <= 4096 ? 128 : 256};
   if (const char* env = getenv("QFT_STEP_CFG")) {
-    StepCfg c{3, 1, 0, oldcap};
-    if (sscanf(env, "%d,%d,%d", &c.S, &c.K, &c.mrec) == 3) {
-      c.mrec = (c.mrec && allow_mrec) ? 1 : 0;
-      if (c.S >= 3 && c.S <= 8 && c.K >= 1 && c.K <= 3 &&
-          step_kernel_smem(gk, cols_p, c.S, oldcap, c.K, c.mrec) <= 227 * 1024)
-        return c;
-    }
+    int oc = 0;
+    if (sscanf(env, "%d", &oc) == 1 && oc >= 32 && oc <= 4096 &&
+        step_kernel_smem(gk, cols_p, oc) <= 227 * 1024)
+      c.oldcap = oc;
   }
-  StepCfg best{3, 1, allow_mrec ? 1 : 0, oldcap};
-  long best_score = -1;
-  for (int m = 0; m <= (allow_mrec ? 1 : 0); ++m)
-    for (int S = 3; S <= 6; ++S)  // >= 3: a stage is refilled two rows after its use
-      for (int K = 1; K <= 2; ++K) {
-        const size_t smem = step_kernel_smem(gk, cols_p, S, oldcap, K, m != 0);
-        if (smem > 227 * 1024) continue;
-        long ctas = (long)((228 * 1024) / (smem + 1024));
-        if (ctas > QFT_STEP_MIN_CTAS) ctas = QFT_STEP_MIN_CTAS;
-        if (ctas < 1) continue;
-        const long score = ctas * 1000 + (m ? 0 : 100) + (S > 4 ? 4 : S) * 10 + K;
-        if (score > best_score) {
-          best_score = score;
-          best = StepCfg{S, K, m, oldcap};
-        }
-      }
-  return best;
+  return c;
 }
 
 int read_header(const Header* d_hdr, Header* h, cudaStream_t st) {
@@ -443,10 +424,7 @@ struct qftc_plan {
   int bit_width = 8;
   int grad_kind = 0;
   int cols_p = 16;
-  int stages = 2;
-  int mrec = 0;
   int oldcap = 128;
-  int slots = 1;
   int use_bulk = 1;
   int slotted[2] = {0, 0};
   int32_t* col[2] = {nullptr, nullptr};
@@ -525,12 +503,8 @@ int qftc_plan_create(qftc_plan** out, const qftc_lion_tensor* ts, int n, int bit
   p->cols_p = (maxc + 15) & ~15;
   p->use_bulk = bulk ? 1 : 0;
   {
-    const StepCfg cfg = pick_step_config(grad_kind, p->cols_p,
-                                         grad_kind == QFTC_GRAD_U8 && p->use_bulk);
-    p->stages = cfg.S;
-    p->mrec = cfg.mrec;
+    const StepCfg cfg = pick_step_config(grad_kind, p->cols_p);
     p->oldcap = cfg.oldcap;
-    p->slots = cfg.K;
   }
   for (int k = 0; k < 2; ++k) {
     p->col[k] = col_idx ? col_idx[k] : nullptr;
@@ -577,10 +551,7 @@ int qftc_plan_step(qftc_plan* p, int flip, qftc_lion_hyper h, qftc_stream_t stre
   a.hdr = p->sc.hdr;
   a.status = p->sc.status;
   a.cols_p = p->cols_p;
-  a.stages = p->stages;
-  a.mrec = p->mrec;
   a.oldcap = p->oldcap;
-  a.slots = p->slots;
   a.use_bulk = p->use_bulk;
   a.slotted_in = p->slotted[flip];
   QFTC_CUDA(launch_step_kernel(p->grad_kind, a, (cudaStream_t)stream), "lion step kernel");

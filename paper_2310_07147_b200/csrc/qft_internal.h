@@ -48,7 +48,7 @@ struct DevTensor {
 struct RowBlock {
   int32_t tensor, row0, nrows, _pad;
 };
-constexpr int kBlockRows = 32;
+constexpr int kBlockRows = 8;  // step rows per work item (static round-robin over warps)
 
 // Device header of a workspace.  `epoch` tags the decompose look-back status
 // words so the status array never needs clearing; the last CTA of every launch
@@ -87,16 +87,15 @@ struct LaunchArgs {
   Header* hdr;
   unsigned long long* status;
   int32_t cols_p;     // max padded (x16) row length of the launch
-  int32_t stages;
+  int32_t _pad0;
   int32_t use_bulk;   // TMA bulk copies (all rows 16-byte aligned)
   int32_t slotted_in; // input CSR is slotted (16-byte aligned slots)
-  int32_t mrec;       // step: recompute m' in pass 2 instead of a 4*cols smem buffer
-  int32_t oldcap;     // step: old CSR entries staged per stage (multiple of 4)
-  int32_t slots;      // step: per-thread parked-outlier vector slots
+  int32_t oldcap;     // step: old outliers per row handled by the sparse pass
+  int32_t _pad1;
   int32_t _pad;
 };
 
-size_t step_kernel_smem(int gk, int cols_p, int stages, int oldcap, int slots, bool mrec);
+size_t step_kernel_smem(int gk, int cols_p, int oldcap);
 cudaError_t launch_step_kernel(int gk, const LaunchArgs& a, cudaStream_t s);
 
 int step_kernel_max_cols();
