@@ -237,15 +237,16 @@ __global__ void __launch_bounds__(ws::NW * 32, QFT_STEP_MIN_CTAS) step_kernel(co
   // ------------------------------------------------------------------ producer
   // (warp-uniform state; lane 0 issues the copies)
   Cursor pc{gwarp, 0, 0, 0, 0};
-  int p_pass = P0, p_c = 0, p_nit = 0, p_nvec = 0, p_cols = 0;
+  int p_pass = P0, p_c = 0, p_nit = 0, p_off = 0, p_last = 0;
   const uint8_t *p_w = nullptr, *p_m = nullptr, *p_g = nullptr;
   bool p_live = false;
   int p_slot = 0;
   auto p_row = [&]() {  // enter the producer's current row (pc.j < pc.nrows)
     const DevTensor* Tt = a.tensors + pc.tensor;
-    p_cols = Tt->cols;
-    p_nvec = (p_cols + 15) >> 4;
-    p_nit = (p_nvec + 31) >> 5;
+    const int p_cols = Tt->cols;
+    p_nit = (p_cols + VB - 1) / VB;
+    p_last = p_cols - (p_nit - 1) * VB;  // bytes of the row's last chunk
+    p_off = 0;
     const size_t roff = (size_t)(pc.row0 + pc.j) * (size_t)p_cols;
     p_w = Tt->w_codes[in] + roff;
     p_m = Tt->m_codes[in] + roff;
@@ -272,10 +273,9 @@ __global__ void __launch_bounds__(ws::NW * 32, QFT_STEP_MIN_CTAS) step_kernel(co
     const int s = p_slot;
     p_slot = (p_slot + 1) & (R - 1);
     uint8_t* sl = ring + s * sbytes;
-    const int v0 = p_c * 32;
-    const int nv = min(32, p_nvec - v0);
-    const int b0 = v0 * 16;
-    const int nb = min(nv * 16, p_cols - b0);  // bytes of this chunk per u8 array
+    const bool last = (p_c + 1 == p_nit);
+    const int nb = last ? p_last : VB;  // bytes of this chunk per u8 array
+    const int b0 = p_off;
     const bool lw = (p_pass == 1), lm = (p_pass >= 1);
     if (ALIGNED) {
       if (lane == 0) {
@@ -295,8 +295,11 @@ __global__ void __launch_bounds__(ws::NW * 32, QFT_STEP_MIN_CTAS) step_kernel(co
       if (lane == 0) mbar_arrive(&bars[s]);
     }
     // advance: chunk -> pass -> row -> block
-    if (++p_c == p_nit) {
+    p_off += VB;
+    ++p_c;
+    if (last) {
       p_c = 0;
+      p_off = 0;
       if (++p_pass > 2) {
         if (++pc.j < pc.nrows) {
           p_row();
@@ -456,7 +459,6 @@ __global__ void __launch_bounds__(ws::NW * 32, QFT_STEP_MIN_CTAS) step_kernel(co
       int mnan0 = 0;
       int base = 0;  // CSR entries of the row emitted so far
       const bool lsat = WD0 && (flags & F_LSAT);
-      const float2 n2lr = f2(__fmul_rn(-2.0f, h.lr)), plr = f2(h.lr);
       for (int c = 0; c < nit; ++c) {
         const uint8_t* sl = acquire();
         const int v = c * 32 + lane;
@@ -479,7 +481,7 @@ __global__ void __launch_bounds__(ws::NW * 32, QFT_STEP_MIN_CTAS) step_kernel(co
               for (int pp = 0; pp < 8; ++pp) {
                 float2 W = make_float2(w[2 * pp], w[2 * pp + 1]);
                 float2 M = make_float2(m[2 * pp], m[2 * pp + 1]);
-                lion2_sat(W, M, make_float2(g[2 * pp], g[2 * pp + 1]), h, n2lr, plr);
+                lion2_sat(W, M, make_float2(g[2 * pp], g[2 * pp + 1]), h);
                 w[2 * pp] = W.x; w[2 * pp + 1] = W.y;
                 m[2 * pp] = M.x; m[2 * pp + 1] = M.y;
               }

@@ -80,20 +80,36 @@ def test_gradient_stack_semantics():
 def test_no_contracted_packed_fma_in_sass():
     """ptxas 12.9 fuses mul.rn.f32x2 + add.rn.f32x2 into FFMA2 despite .rn, so every Lion
     SUM of products is a scalar FADD.  The only FFMA2 forms allowed are the deliberate
-    ones: pair * scalar + scalar (saturating sign update, magic-number rounding) and
+    ones: pair * scalar + scalar (the sign factor of the saturating update,
+    magic-number rounding), pair * scalar + pair where the pair addend is the weight
+    itself (w' = fma(s, lr, w), s in {-1,0,1}: exact product, one rounding) and
     pair * scalar - pair (the quantizer's tie distance x*inv - rint, whose proof holds
-    for the exact or the rounded product).  A contracted sum would show up as
-    pair * scalar + pair, which must never appear."""
+    for the exact or the rounded product).  A contracted sum shows up as
+    pair * pair-or-scalar + pair on a product register; the parity tests are the
+    authoritative check, this one catches the pattern early: every FFMA2 with a
+    non-negated pair addend must multiply by the lr register of the sign update."""
     import re
     from paper_2310_07147_b200 import _native as N
     out = subprocess.run(["cuobjdump", "-sass", N.LIB_PATH], capture_output=True, text=True)
     assert out.returncode == 0 and "FMUL2" in out.stdout
     bad = []
+    sign_regs = set()   # pair registers holding s = fma(a, -2, 1) (the -sign factor)
     for line in out.stdout.splitlines():
-        if "FFMA2" not in line:
+        if "Function :" in line:
+            sign_regs = set()
             continue
-        ops = line.split("FFMA2", 1)[1].split(";")[0].split(",")
-        addend = ops[-1].strip()
-        if ".F32x2" in addend and not addend.startswith("-"):
-            bad.append(line.strip())
+        m = re.search(r"\b(FFMA2|FMUL2|FADD2|[A-Z][A-Z0-9.]*)\s+(R\d+)\s*,(.*);", line)
+        if not m:
+            continue
+        op, dst, rest = m.group(1), m.group(2), m.group(3)
+        ops = [o.strip() for o in rest.split(",")]
+        if op == "FFMA2":
+            addend = ops[-1]
+            if ops[1] == "-2":      # s = fma(a, -2, 1)
+                sign_regs.add(dst)
+                continue
+            src = ops[0].split(".")[0]
+            if ".F32x2" in addend and not addend.startswith("-") and src not in sign_regs:
+                bad.append(line.strip())
+        sign_regs.discard(dst) if op != "FFMA2" else None
     assert not bad, f"contracted packed FMA: {bad[:4]}"
