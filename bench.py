@@ -290,6 +290,10 @@ def run_gpu_arm(args):
     }
     if e2e:
         line["e2e"] = e2e
+    if world > 1 or args.zero1:
+        del st
+        torch.cuda.empty_cache()
+        line["zero1_step"] = zero1_run(args, full, world, rank, q)
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
             cb = cpu_reference_run(steps=2, warmup=0)
@@ -301,6 +305,71 @@ def run_gpu_arm(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def zero1_run(args, full, world, rank, q):
+    """configs[2]: the full ZeRO-1 step on this rank -- reduce-scatter of the bf16
+    gradient (shard-major layout), the fused step on the rank's rows (bf16 raw-gradient
+    kind: quantize_state(g) fused in), all-gather of the updated W codes, CSR slot
+    starts/counts and arenas.  Device time, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2310_07147_b200.zero1 import CudaShard, ShardLayout, Zero1QftLion
+    own_group = not dist.is_initialized()
+    if own_group:  # single-process check of the path (bench.py --zero1 at N=1)
+        import socket
+        s_ = socket.socket()
+        s_.bind(("127.0.0.1", 0))
+        port_no = s_.getsockname()[1]
+        s_.close()
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port_no}", rank=0,
+                                world_size=1)
+    try:
+        layout = ShardLayout(full, world)
+        local = CudaShard(layout, rank, bit_width=BIT_WIDTH, grad_dtype=torch.bfloat16)
+        shard = layout.shard_shapes(rank)
+        local.state.init_from_weights(
+            lambda i: q.synth(shard[i], 4321 + 1000 * rank + i, 0.02, 0.005), FRACTION, "percentile")
+        z = Zero1QftLion(full, local)
+        gen = torch.Generator(device="cuda")
+        gen.manual_seed(99 + rank)
+        z.grad_full.normal_(0.0, 1e-3, generator=gen)
+        g0 = z.grad_full.clone()
+        stream = torch.cuda.current_stream()
+        for _ in range(args.warmup):
+            z.grad_full.copy_(g0)
+            z.step(**HYPER)
+        local.state.check()
+        dist.barrier()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        for e0, e1 in ev:
+            z.grad_full.copy_(g0)       # a fresh gradient each step (outside the event pair)
+            e0.record(stream)
+            z.step(**HYPER)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        local.state.check()
+        ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev)
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        params = sum(r * c for r, c in full)
+        f = (world - 1) / world
+        rs_bytes = f * 2 * layout.pad * world
+        ag_bytes = f * (layout.pad + 4 * layout.rp_pad + 4 * layout.rpad +
+                        8 * z.cap * len(layout.widths)) * world
+        return {"ms_per_step": ms, "gparams_s": params / (ms * 1e-3) / 1e9,
+                "what": "reduce_scatter(bf16 grad) + fused bf16-gradient step on the row "
+                        "shard + all_gather(W codes, CSR slots, arenas)",
+                "grad_dtype": "bf16", "world": world,
+                "rs_bytes_per_rank": rs_bytes, "ag_bytes_per_rank": ag_bytes,
+                "nvlink_gbs_per_rank": (rs_bytes + ag_bytes) / (ms * 1e-3) / 1e9}
+    finally:
+        if own_group:
+            dist.destroy_process_group()
 
 
 def e2e_host(st, q, args, stream):
@@ -515,6 +584,8 @@ def main():
     ap.add_argument("--mode", default="step", choices=["step", "sweep", "13b"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--zero1", action="store_true",
+                    help="also time the full ZeRO-1 step (RS + step + AG) at N=1")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "own":
         args.warmup = 3
