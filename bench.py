@@ -284,7 +284,7 @@ def run_gpu_arm(args):
                      "peak_kind": peak_kind},
         "step_hbm_gbs": all_alg / (ms * 1e-3) / 1e9,
         "per_launch_ms": {f"cols{gg.cols}": per_group_ms[i] for i, gg in enumerate(st.groups)},
-        "gpu_launches": args.steps * len(st.groups),
+        "gpu_launches": args.steps * sum(int(q._native.lib.qftc_plan_launches(gg.plan)) for gg in st.groups),
         "clocks": clocks,
         "setup_s": setup_s,
     }

@@ -426,6 +426,11 @@ struct qftc_plan {
   int cols_p = 16;
   int oldcap = 128;
   int use_bulk = 1;
+  int uniform_cols = 0;       // every tensor's row length (0: mixed)
+  bool rows_path = false;     // v6 rows kernel (prep + stable rows + general rows)
+  RowPrep* prep = nullptr;    // per-row records
+  RowBlock* xlist = nullptr;  // general-tier rows
+  int32_t* xcount = nullptr;
   int slotted[2] = {0, 0};
   int32_t* col[2] = {nullptr, nullptr};
   float* val[2] = {nullptr, nullptr};
@@ -446,6 +451,7 @@ int qftc_plan_create(qftc_plan** out, const qftc_lion_tensor* ts, int n, int bit
   std::vector<DevTensor> dts((size_t)n);
   int64_t rows = 0;
   int maxc = 1;
+  int ucols = ts[0].cols;
   bool bulk = true;
   bool slotted[2] = {true, true};
   for (int i = 0; i < n; ++i) {
@@ -488,6 +494,7 @@ int qftc_plan_create(qftc_plan** out, const qftc_lion_tensor* ts, int n, int bit
     bulk = bulk && (t.cols % 16 == 0);
     rows += t.rows;
     if (t.cols > maxc) maxc = t.cols;
+    if (t.cols != ucols) ucols = 0;
   }
   if (rows > 0x7fffffff) return fail(QFTC_ENOTSUP, "plan: more than 2^31 rows");
   auto* p = new qftc_plan;
@@ -505,6 +512,20 @@ int qftc_plan_create(qftc_plan** out, const qftc_lion_tensor* ts, int n, int bit
   {
     const StepCfg cfg = pick_step_config(grad_kind, p->cols_p);
     p->oldcap = cfg.oldcap;
+  }
+  p->uniform_cols = ucols;
+  const char* no_rows = getenv("QFT_NO_ROWS_KERNEL");
+  p->rows_path = rows_kernel_eligible(grad_kind, p->use_bulk, ucols) &&
+                 !(no_rows && no_rows[0] == '1');
+  if (p->rows_path) {
+    cudaError_t e = cudaMallocAsync((void**)&p->prep, sizeof(RowPrep) * (size_t)rows, st);
+    if (e == cudaSuccess)
+      e = cudaMallocAsync((void**)&p->xlist, sizeof(RowBlock) * (size_t)rows, st);
+    if (e == cudaSuccess) e = cudaMallocAsync((void**)&p->xcount, 16, st);
+    if (e != cudaSuccess) {
+      qftc_plan_destroy(p);
+      return fail(QFTC_ECUDA, std::string("plan_create: ") + cudaGetErrorString(e));
+    }
   }
   for (int k = 0; k < 2; ++k) {
     p->col[k] = col_idx ? col_idx[k] : nullptr;
@@ -554,6 +575,15 @@ int qftc_plan_step(qftc_plan* p, int flip, qftc_lion_hyper h, qftc_stream_t stre
   a.oldcap = p->oldcap;
   a.use_bulk = p->use_bulk;
   a.slotted_in = p->slotted[flip];
+  if (p->rows_path) {
+    a.cols_p = p->uniform_cols;
+    a.oldcap6 = rows_kernel_oldcap(p->uniform_cols);
+    a.prep = p->prep;
+    a.xlist = p->xlist;
+    a.xcount = p->xcount;
+    QFTC_CUDA(launch_rows_step(a, (cudaStream_t)stream), "lion step (rows kernel)");
+    return QFTC_OK;
+  }
   QFTC_CUDA(launch_step_kernel(p->grad_kind, a, (cudaStream_t)stream), "lion step kernel");
   return QFTC_OK;
 }
@@ -576,11 +606,14 @@ int qftc_plan_result(qftc_plan* p, int64_t* nnz_total, qftc_stream_t stream) {
   return QFTC_OK;
 }
 
-int qftc_plan_launches(const qftc_plan* p) { return p ? 1 : 0; }
+int qftc_plan_launches(const qftc_plan* p) { return p ? (p->rows_path ? 3 : 1) : 0; }
 
 int qftc_plan_destroy(qftc_plan* p) {
   if (!p) return QFTC_OK;
   cudaFree(p->sc.base);
+  if (p->prep) cudaFree(p->prep);
+  if (p->xlist) cudaFree(p->xlist);
+  if (p->xcount) cudaFree(p->xcount);
   delete p;
   return QFTC_OK;
 }

@@ -91,14 +91,35 @@ struct LaunchArgs {
   int32_t use_bulk;   // TMA bulk copies (all rows 16-byte aligned)
   int32_t slotted_in; // input CSR is slotted (16-byte aligned slots)
   int32_t oldcap;     // step: old outliers per row handled by the sparse pass
-  int32_t _pad1;
-  int32_t _pad;
+  int32_t oldcap6;    // rows kernel: old outliers per row of its sparse table
+  float negzero;      // -0.0f at run time (an FFMA2 addend ptxas cannot fold)
+  struct RowPrep* prep;          // rows kernel: per-row records (k_step_prep)
+  RowBlock* xlist;               // rows outside the stable tier (general kernel)
+  int32_t* xcount;               // their number (device)
+  const int32_t* n_blocks_dev;   // step_kernel: read the block count from the device
+};
+
+// Per-row record of the rows kernel (64 B), written by k_step_prep every step.
+struct RowPrep {
+  uint32_t info;  // bit 0: stable tier; bits 8..15: outlier payload code clamp(z, 0, qmax)
+  int32_t tensor, lrow, ob;
+  int32_t on, so, co, cols;  // old slot start/count, new slot start/capacity, row length
+  float sm;
+  int32_t zm;
+  float sg;
+  int32_t zg;
+  int32_t _pad[4];
 };
 
 size_t step_kernel_smem(int gk, int cols_p, int oldcap);
 cudaError_t launch_step_kernel(int gk, const LaunchArgs& a, cudaStream_t s);
 
 int step_kernel_max_cols();
+
+// v6 rows kernel (rowstep.cu): prep + stable rows + step_kernel over the rest
+bool rows_kernel_eligible(int gk, int use_bulk, int uniform_cols);
+int rows_kernel_oldcap(int cols);
+cudaError_t launch_rows_step(const LaunchArgs& a, cudaStream_t s);
 
 // decomposition with given thresholds (decompose.cu)
 cudaError_t decompose_codes(const float* w, int rows, int cols, const float* scale,

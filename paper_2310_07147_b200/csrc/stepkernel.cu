@@ -222,6 +222,9 @@ __global__ void __launch_bounds__(ws::NW * 32, QFT_STEP_MIN_CTAS) step_kernel(co
   const int gwarp = blockIdx.x * NW + wid;
   const int nwarps = gridDim.x * NW;
   constexpr int P0 = (GK == G_U8) ? 1 : 0;  // first pass (raw kinds: a g-range pass 0)
+  // the row list of the rows kernel's general tier has a device-side length
+  const int n_blocks = a.n_blocks_dev ? *a.n_blocks_dev : a.n_blocks;
+  if (gwarp >= n_blocks) return;  // whole warp idle (warps are independent)
 
   if (lane == 0) {
     for (int s = 0; s < R; ++s) mbar_init(&bars[s], 1);
@@ -256,7 +259,7 @@ __global__ void __launch_bounds__(ws::NW * 32, QFT_STEP_MIN_CTAS) step_kernel(co
     p_c = 0;
   };
   auto p_block = [&]() {  // enter block pc.blk (or finish)
-    if (pc.blk >= a.n_blocks) {
+    if (pc.blk >= n_blocks) {
       p_live = false;
       return;
     }
@@ -328,7 +331,7 @@ __global__ void __launch_bounds__(ws::NW * 32, QFT_STEP_MIN_CTAS) step_kernel(co
     produce();
   };
 
-  for (int blk = gwarp; blk < a.n_blocks; blk += nwarps) {
+  for (int blk = gwarp; blk < n_blocks; blk += nwarps) {
     const RowBlock B = a.blocks[blk];
     const DevTensor* Tt = a.tensors + B.tensor;
     const int cols = Tt->cols;
