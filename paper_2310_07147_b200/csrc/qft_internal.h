@@ -99,17 +99,25 @@ struct LaunchArgs {
   const int32_t* n_blocks_dev;   // step_kernel: read the block count from the device
 };
 
-// Per-row record of the rows kernel (64 B), written by k_step_prep every step.
+// Per-row record of the rows kernel (128 B), written by k_step_prep every step and
+// bulk-copied into shared memory with the row's codes: everything a row needs.
 struct RowPrep {
   uint32_t info;  // bit 0: stable tier; bits 8..15: outlier payload code clamp(z, 0, qmax)
-  int32_t tensor, lrow, ob;
-  int32_t on, so, co, cols;  // old slot start/count, new slot start/capacity, row length
-  float sm;
-  int32_t zm;
-  float sg;
+  int32_t lrow, ob, on;          // local row, old CSR slot start / count
+  int32_t so, co, zw, zm;        // new slot start / capacity, w / m zero points
+  float sm, negc_m, sg, negc_g;  // m / g scale and -(2^23 + z) (the PRMT dequant form)
   int32_t zg;
-  int32_t _pad[4];
+  float sw, tmin, tmax;
+  const uint8_t* w_in;           // row pointers of the step's inputs ...
+  const uint8_t* m_in;
+  const uint8_t* g_in;
+  uint8_t* w_out;                // ... and outputs
+  uint8_t* m_out;
+  float* m_scale_out;            // &m_scale[out][row], &m_zp[out][row], &cnt[out][row]
+  int32_t* m_zp_out;
+  int32_t* cnt_out;
 };
+static_assert(sizeof(RowPrep) == 128, "RowPrep is one 128-byte record");
 
 size_t step_kernel_smem(int gk, int cols_p, int oldcap);
 cudaError_t launch_step_kernel(int gk, const LaunchArgs& a, cudaStream_t s);

@@ -8,20 +8,25 @@
 //
 // Three launches per step (one stream, no host synchronisation):
 //
-//   k_step_prep   one thread per row: the row's tier, its per-row constants and CSR
-//                 slot bounds (RowPrep, 64 B); rows outside the stable tier are
-//                 appended to a device row list for the general kernel.
-//   rows_kernel   (this file) every STABLE row, one CTA per row:
-//                   phase 1  each thread owns V 16-byte vectors of the row: dequant m,
-//                            g (PRMT magic numbers, FADD2/FMUL2) -> m' = b2*m + c2*g,
-//                            kept in registers; m' min/max (FMNMX3, CREDUX); weight
-//                            codes pass through except boundary-code candidates and
-//                            old outliers; STG.128 of the weight codes.
-//                   barrier  warp 0: the row's m' range -> affine_from_bounds (fp64),
-//                            the CSR segment offsets; the other warps run the sparse
-//                            pass of the CTA's NEXT row (one thread per old outlier).
-//                   phase 2  quantize m' (range-proven fast quantizer), STG.128; CSR
-//                            entries appended in column order.
+//   k_step_prep   one thread per row: the row's tier and a self-describing 128-byte
+//                 record (RowPrep: per-row constants, CSR slot bounds, absolute row
+//                 pointers); rows outside the stable tier are appended to a device row
+//                 list for the general kernel.
+//   rows_kernel   every STABLE row, one CTA per row, persistent over a static stride:
+//                   TMA      thread 0 streams the NEXT row -- record, w | m | g codes,
+//                            the old CSR slot -- into a 2-stage shared-memory ring
+//                            (cp.async.bulk on an mbarrier), one row ahead.
+//                   phase 1  each thread owns V=2 16-byte vectors: dequant m, g (PRMT
+//                            magic numbers, FADD2/FMUL2) -> m' = b2*m + c2*g kept in
+//                            registers; m' min/max (FMNMX3, CREDUX); weight codes pass
+//                            through except boundary-code candidates; STG.128.
+//                   barrier A  warp 0: the row's m' range -> affine_from_bounds (fp64),
+//                            CSR segment offsets.  The other warps: the deferred output
+//                            of the PREVIOUS row's old outliers (code bytes, CSR entries)
+//                            and the sparse pass of the NEXT row (one thread per old
+//                            outlier, reading the landed stage).
+//                   barrier B  phase 2: quantize m' (range-proven fast quantizer),
+//                            STG.128; per-vector CSR bases; new-outlier entries.
 //   step_kernel   (stepkernel.cu, v5) the rows of the device list: every row the
 //                 stable-tier proof does not cover (large lr, weight decay that can
 //                 move a code, odd zero points, NaN/Inf, over-full sparse tables).
@@ -36,72 +41,75 @@
 // so this is the normal case), every code in [1, qmax-1] stays strictly inside
 // (t_min, t_max): it can neither become an outlier nor change.  Only codes 0 and qmax
 // ("candidates") and the old outliers need the Lion arithmetic, which they get
-// exactly (fp32 reference order, fp64 quantizer).  (*) is checked per row in fp64
-// (k_step_prep); at the paper's lr = 2e-5 every LLaMA row satisfies it (sw ~ 4e-4 at
-// 8 bits).  The output is byte-identical to the reference either way.
+// exactly (fp32 reference order; the quantizer's fp64 formula or its proven fp32
+// equivalent).  (*) is checked per row in fp64 (k_step_prep); at the paper's lr = 2e-5
+// every LLaMA row satisfies it (sw ~ 4e-4 at 8 bits).  The bytes are the reference's
+// either way: rows without the proof run the general kernel.
 #include "qft_device.cuh"
 #include "qft_internal.h"
+
+#include <cstdlib>
 
 namespace qftk {
 using namespace qftd;
 
 namespace rs6 {
 constexpr uint32_t I_STABLE = 1u;
+constexpr int V = 2;  // 16-byte vectors per thread
 
-struct Smem {  // per-CTA shared-memory layout (runtime sizes)
-  int nvec, oldcap, nw;
-  __device__ __host__ int buf_bytes() const {
-    return ((nvec * 2 + 15) & ~15) + ((nvec * 2 + 15) & ~15) + oldcap * 8;
-  }
-  __device__ __host__ int o_bits(int b) const { return b * buf_bytes(); }
-  __device__ __host__ int o_frank(int b) const { return o_bits(b) + ((nvec * 2 + 15) & ~15); }
-  __device__ __host__ int o_spval(int b) const { return o_frank(b) + ((nvec * 2 + 15) & ~15); }
-  __device__ __host__ int o_spcw(int b) const { return o_spval(b) + oldcap * 4; }
-  __device__ __host__ int o_part() const { return 3 * buf_bytes(); }         // nw x float4
-  __device__ __host__ int o_seg() const { return o_part() + nw * 16; }        // nw x int2
-  __device__ __host__ int o_res() const { return o_seg() + nw * 8; }          // RowRes
-  __device__ __host__ int total() const { return o_res() + 64; }
+// Per-CTA shared memory (runtime sizes).
+//   stage[2]   record (128 B) | w codes | m codes | g codes | old cols | old values
+//   bars[2]    the stages' mbarriers
+//   buf[3]     sparse buffers (row k of the CTA uses buffer k % 3): a 16-byte header
+//              (the row's w_out, so, co), per vector one u32 word -- bits 0..15 the OLD
+//              outlier positions, bits 16..31 the OUTPUT outlier positions (old ones
+//              that stay, new ones from the candidate path) -- and per old outlier its
+//              w' value, code|class, column
+//   vbase      CSR base of every vector with outputs (phase 2 -> next row's old_out)
+//   part, seg, res  warp partials, CSR segment offsets, the m' quantizer
+struct Smem {
+  int nvec, oldcap, nw, cols;
+  __device__ __host__ int stage_bytes() const { return 128 + 3 * cols + 8 * oldcap; }
+  __device__ __host__ int o_stage(int s) const { return s * stage_bytes(); }
+  __device__ __host__ int o_bar() const { return 2 * stage_bytes(); }
+  __device__ __host__ int buf_bytes() const { return 16 + nvec * 4 + oldcap * 12; }
+  __device__ __host__ int o_buf(int b) const { return o_bar() + 16 + b * buf_bytes(); }
+  __device__ __host__ int o_vbase() const { return o_buf(3); }
+  __device__ __host__ int o_part() const { return o_vbase() + nvec * 4; }
+  __device__ __host__ int o_seg() const { return o_part() + nw * 16; }
+  __device__ __host__ int o_res() const { return o_seg() + nw * 8; }
+  __device__ __host__ int total() const { return o_res() + 32; }
+};
+
+struct BufHdr {  // what the deferred output of a row needs after its stage is reused
+  uint8_t* w_out;
+  int32_t so, co;
 };
 
 struct RowRes {  // the row's m' quantizer, published by warp 0
   float s, inv, magic, thr;
-  float ylo, yhi;
-  int32_t z, qmf;
+  int32_t z, qmf, _p0, _p1;
 };
 
-// the row's identity and the pointers of the CTA's current row (uniform)
-struct RowCtx {
-  int gr, tensor, lrow;
-  int ob, on, so, co;
-  uint32_t zpay;
-  DequantRow dm, dg;
-  size_t roff;
+// the fields the CTA needs to ISSUE a row's copies (loaded one row ahead)
+struct RowHead {
+  uint32_t info;
+  int32_t ob, on;
+  const uint8_t *w_in, *m_in, *g_in;
 };
-
-__device__ __forceinline__ RowCtx load_ctx(const LaunchArgs& a, int gr) {
-  RowCtx c;
+__device__ __forceinline__ RowHead load_head(const LaunchArgs& a, int gr) {
+  RowHead h;
   const RowPrep* p = a.prep + gr;
-  const int4 p0 = __ldg(reinterpret_cast<const int4*>(p));
-  const int4 p1 = __ldg(reinterpret_cast<const int4*>(p) + 1);
-  const int4 p2 = __ldg(reinterpret_cast<const int4*>(p) + 2);
-  c.gr = gr;
-  c.zpay = ((uint32_t)p0.x >> 8) & 0xFFu;
-  c.tensor = p0.y;
-  c.lrow = p0.z;
-  c.ob = p0.w;
-  c.on = p1.x;
-  c.so = p1.y;
-  c.co = p1.z;
-  c.dm = make_dequant_row(__int_as_float(p2.x), p2.y);
-  c.dg = make_dequant_row(__int_as_float(p2.z), p2.w);
-  c.roff = (size_t)c.lrow * (size_t)p1.w;  // p1.w = cols
-  return c;
-}
-
-// next row of this CTA's static stride that is in the stable tier
-__device__ __forceinline__ int next_stable(const LaunchArgs& a, int gr) {
-  while (gr < a.total_rows && !(__ldg(&a.prep[gr].info) & I_STABLE)) gr += gridDim.x;
-  return gr;
+  const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(p));
+  const ulonglong2 q4 = __ldg(reinterpret_cast<const ulonglong2*>(p) + 4);
+  const ulonglong2 q5 = __ldg(reinterpret_cast<const ulonglong2*>(p) + 5);
+  h.info = q0.x;
+  h.ob = (int32_t)q0.z;
+  h.on = (int32_t)q0.w;
+  h.w_in = reinterpret_cast<const uint8_t*>(q4.x);
+  h.m_in = reinterpret_cast<const uint8_t*>(q4.y);
+  h.g_in = reinterpret_cast<const uint8_t*>(q5.x);
+  return h;
 }
 
 // m' = RN(RN(b2*m) + RN(c2*g)) for a pair: the products are FFMA2s with a RUNTIME -0
@@ -111,11 +119,10 @@ __device__ __forceinline__ float2 mprime2(float2 m, float2 g, float2 b2, float2 
   return __fadd2_rn(__ffma2_rn(b2, m, nz), __ffma2_rn(c2, g, nz));
 }
 
-// any byte of the 4 words equal to 0 or qmax (b-bit codes: bits >= b are zero):
-// byte in {0, qmax} <=> its low b bits are all equal <=> (x ^ x>>1) & K == 0 on the
-// byte, K = bits 0..b-2; then the classic zero-byte test.  The flag word is exact for
-// "some byte"; per-byte flags may include false positives above a flagged byte
-// (harmless: flagged elements take the exact path).
+// byte in {0, qmax} of b-bit codes (bits >= b are zero) <=> its low b bits are all
+// equal <=> (x ^ x>>1) & K == 0 on the byte, K = bits 0..b-2; then the classic
+// zero-byte test.  Exact for "some byte"; per-byte flags may include false positives
+// above a flagged byte (harmless: flagged elements take the exact path).
 __device__ __forceinline__ uint32_t cand_flags(uint32_t x, uint32_t K) {
   const uint32_t t = (x ^ (x >> 1)) & K;
   return (t - 0x01010101u) & ~t & 0x80808080u;
@@ -143,149 +150,223 @@ __device__ __forceinline__ void set_byte(uint4& q, int e, uint32_t v) {
   q.w = (w == 3) ? ((q.w & keep) | put) : q.w;
 }
 
+// Rare exact paths out of line: their fp64 divides (and the divide's slow-path call)
+// would otherwise set the kernel's register budget while the hot state is live.
+__device__ __noinline__ uint32_t quant_exact_ni(float x, float s, int32_t z, int qmax) {
+  return quant_exact(x, s, z, qmax);
+}
+__device__ __noinline__ void affine_ni(float lo, float hi, int bw, float* s, int32_t* z) {
+  affine_from_bounds(lo, hi, bw, *s, *z);
+}
+
+// code of an INLIER weight of a stable row (its exact code lies in [0, qmax], proven
+// by code(t_min) == 0 and code(t_max) == qmax): the fast quantizer with its tie proof,
+// the reference's fp64 formula when the proof fails
+__device__ __forceinline__ uint32_t quant_inlier(float x, float sw, int32_t zw, int bw) {
+  const QuantRow q = make_quant_row(sw, zw, bw);
+  const float y = __fmul_rn(x, q.inv_s);
+  const float tt = __fadd_rn(y, q.magic);
+  const float e = __fsub_rn(y, __fsub_rn(tt, q.magic));
+  if (q.fast && fabsf(e) < q.thr && y > q.ylo - 0.5f && y < q.yhi + 0.5f)
+    return __float_as_uint(tt) & 0xFFu;
+  return quant_exact_ni(x, sw, zw, q.qmax);
+}
+
 // exact w' of one dense element from its three codes (lion1: the reference's fp32
-// order; dequantize as quantize.hpp:209)
+// order; dequantize as quantize.hpp:209), the row's record in r
 __device__ __forceinline__ float exact_wprime(uint32_t qw, uint32_t qm, uint32_t qg,
-                                              const DevTensor* T, int lrow, const RowCtx& c,
-                                              const Hyper& h) {
-  float w = dequant_exact(qw, __ldg(T->w_scale + lrow), __ldg(T->w_zp + lrow));
-  float m = dequant_exact(qm, c.dm.s, c.dm.z);
-  const float g = dequant_exact(qg, c.dg.s, c.dg.z);
+                                              const RowPrep& r, const Hyper& h) {
+  float w = dequant_exact(qw, r.sw, r.zw);
+  float m = dequant_exact(qm, r.sm, r.zm);
+  const float g = dequant_exact(qg, r.sg, r.zg);
   lion1(w, m, g, h);
   return w;
 }
 
 }  // namespace rs6
 
-int rows_kernel_nt(int cols, int v) {
+int rows_kernel_nt(int cols) {
   const int nvec = (cols + 15) / 16;
-  const int per = (nvec + v - 1) / v;
+  const int per = (nvec + rs6::V - 1) / rs6::V;
   return ((per + 31) / 32) * 32;
 }
 
-size_t rows_kernel_smem(int cols, int v, int oldcap) {
-  const int nt = rows_kernel_nt(cols, v);
-  rs6::Smem L{nt * v, oldcap, nt / 32};
+int rows_kernel_oldcap(int cols) { return ((cols / 16) + 31) & ~31; }
+
+size_t rows_kernel_smem(int cols, int oldcap) {
+  const int nt = rows_kernel_nt(cols);
+  rs6::Smem L{nt * rs6::V, oldcap, nt / 32, ((cols + 15) / 16) * 16};
   return (size_t)L.total();
 }
 
-template <int V>
-__global__ void __launch_bounds__(512, 1) rows_kernel(const LaunchArgs a) {
+template <int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   using namespace rs6;
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem[];
   const int NT = blockDim.x, NW = NT >> 5;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  const Smem L{NT * V, a.oldcap6, NW};
-  const int qmax = (1 << a.bit_width) - 1;
-  const uint32_t KC = (uint32_t)((1 << (a.bit_width - 1)) - 1) * 0x01010101u;
-  const int in = a.flip, out = 1 - a.flip;
   const int cols = a.cols_p;  // uniform row length of the launch (multiple of 16)
   const int nvec = cols >> 4;
+  const Smem L{NT * V, a.oldcap6, NW, cols};
+  const int qmax = (1 << a.bit_width) - 1;
+  const uint32_t KC = (uint32_t)((1 << (a.bit_width - 1)) - 1) * 0x01010101u;
+  const int G = gridDim.x;
+  const bool slotted = a.slotted_in != 0;
   Hyper h;
   h.lr = a.lr; h.b1 = a.b1; h.b2 = a.b2; h.wd = a.wd;
   h.c1 = __fsub_rn(1.0f, a.b1);
   h.c2 = __fsub_rn(1.0f, a.b2);
   const float2 B2 = f2(h.b2), C2 = f2(h.c2), NZ = f2(a.negzero);
 
-  auto bits16 = [&](int b) { return reinterpret_cast<uint16_t*>(smem + L.o_bits(b)); };
-  auto frank = [&](int b) { return reinterpret_cast<uint16_t*>(smem + L.o_frank(b)); };
-  auto spval = [&](int b) { return reinterpret_cast<float*>(smem + L.o_spval(b)); };
-  auto spcw = [&](int b) { return reinterpret_cast<uint32_t*>(smem + L.o_spcw(b)); };
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.o_bar());
+  auto stage = [&](int s) { return smem + L.o_stage(s); };
+  auto rec = [&](int s) { return reinterpret_cast<const RowPrep*>(stage(s)); };
+  auto hdr = [&](int b) { return reinterpret_cast<BufHdr*>(smem + L.o_buf(b)); };
+  auto words = [&](int b) { return reinterpret_cast<uint32_t*>(smem + L.o_buf(b) + 16); };
+  auto spval = [&](int b) {
+    return reinterpret_cast<float*>(smem + L.o_buf(b) + 16 + L.nvec * 4);
+  };
+  auto spcw = [&](int b) { return reinterpret_cast<uint32_t*>(spval(b) + L.oldcap); };
+  auto spcol = [&](int b) { return reinterpret_cast<int32_t*>(spval(b) + 2 * L.oldcap); };
+  int* vbase = reinterpret_cast<int*>(smem + L.o_vbase());
   float4* part = reinterpret_cast<float4*>(smem + L.o_part());
   int2* seg = reinterpret_cast<int2*>(smem + L.o_seg());
   RowRes* res = reinterpret_cast<RowRes*>(smem + L.o_res());
 
-  // sparse pass over the OLD outliers of row c into buffer b (threads t0.. of the CTA):
-  // the exact w' (general Lion form), its class against the cached thresholds and its
-  // code (quantize.hpp:274-285); bitmap + first-rank table for O(1) lookups
-  auto sparse_pass = [&](const RowCtx& c, int b, int t0) {
-    const DevTensor* T = a.tensors + c.tensor;
-    const uint8_t* m_in = T->m_codes[in] + c.roff;
-    const uint8_t* g_in = T->g_codes + c.roff;
-    const float sw = __ldg(T->w_scale + c.lrow);
-    const int32_t zw = __ldg(T->w_zp + c.lrow);
-    const float tmin = __ldg(T->t_min + c.lrow), tmax = __ldg(T->t_max + c.lrow);
-    uint32_t* bw = reinterpret_cast<uint32_t*>(bits16(b));
-    uint16_t* fr = frank(b);
-    float* sv = spval(b);
-    uint32_t* sc = spcw(b);
-    for (int i = t - t0; i < c.on; i += NT - t0) {
-      const int col = __ldg(a.col_in + c.ob + i);
-      atomicOr(&bw[col >> 5], 1u << (col & 31));
-      const int vv = col >> 4;
-      if (i == 0 || (__ldg(a.col_in + c.ob + i - 1) >> 4) != vv) fr[vv] = (uint16_t)i;
-      float wv = __ldg(a.val_in + c.ob + i);
-      float mv = dequant_exact(m_in[col], c.dm.s, c.dm.z);
-      const float gv = dequant_exact(g_in[col], c.dg.s, c.dg.z);
-      lion1(wv, mv, gv, h);
-      const bool o = (wv < tmin) || (wv > tmax);
-      const uint32_t code = o ? c.zpay : quant_exact(wv, sw, zw, qmax);
-      sv[i] = wv;
-      sc[i] = code | (o ? 0x100u : 0u);
+  // thread 0: the row's record, codes and old CSR slot into stage s (TMA bulk copies)
+  auto issue_row = [&](int grow, const RowHead& hd, int s) {
+    uint8_t* dst = stage(s);
+    const uint32_t n = (uint32_t)cols;
+    const uint32_t cb = (slotted && hd.on > 0) ? (uint32_t)((hd.on * 4 + 15) & ~15) : 0u;
+    mbar_arrive_expect_tx(&bars[s], 128u + 3u * n + 2u * cb);
+    bulk_g2s(dst, a.prep + grow, 128u, &bars[s]);
+    bulk_g2s(dst + 128, hd.w_in, n, &bars[s]);
+    bulk_g2s(dst + 128 + n, hd.m_in, n, &bars[s]);
+    bulk_g2s(dst + 128 + 2 * n, hd.g_in, n, &bars[s]);
+    if (cb) {
+      bulk_g2s(dst + 128 + 3 * n, a.col_in + hd.ob, cb, &bars[s]);
+      bulk_g2s(dst + 128 + 3 * n + 4 * L.oldcap, a.val_in + hd.ob, cb, &bars[s]);
     }
   };
-  auto clear_bits = [&](int b) {
-#pragma unroll
-    for (int j = 0; j < V; ++j) bits16(b)[t + j * NT] = 0;
+  // Sparse pass over the OLD outliers of the row in stage s into buffer b (threads t0..
+  // of the CTA): the exact w' (general Lion form), its class against the cached
+  // thresholds and its code (quantize.hpp:274-285); marks bit e (old) and bit 16+e
+  // (stays an outlier) of its vector's word.
+  auto sparse_pass = [&](int s, int b, int t0) {
+    const RowPrep& r = *rec(s);
+    const uint8_t* st = stage(s);
+    const int32_t* cin = slotted ? reinterpret_cast<const int32_t*>(st + 128 + 3 * cols)
+                                 : a.col_in + r.ob;
+    const float* vin = slotted ? reinterpret_cast<const float*>(st + 128 + 3 * cols + 4 * L.oldcap)
+                               : a.val_in + r.ob;
+    const uint32_t zpay = (r.info >> 8) & 0xFFu;
+    uint32_t* wd = words(b);
+    if (t == t0) *hdr(b) = BufHdr{r.w_out, r.so, r.co};
+    for (int i = t - t0; i < r.on; i += NT - t0) {
+      const int col = cin[i];
+      float wv = vin[i];
+      float mv = dequant_exact(st[128 + cols + col], r.sm, r.zm);
+      const float gv = dequant_exact(st[128 + 2 * cols + col], r.sg, r.zg);
+      lion1(wv, mv, gv, h);
+      const bool o = (wv < r.tmin) || (wv > r.tmax);
+      const uint32_t code = o ? zpay : quant_inlier(wv, r.sw, r.zw, a.bit_width);
+      atomicOr(&wd[col >> 4], (1u << (col & 15)) | (o ? (0x10000u << (col & 15)) : 0u));
+      spval(b)[i] = wv;
+      spcw(b)[i] = code | (o ? 0x100u : 0u);
+      spcol(b)[i] = col;
+    }
   };
-
-  int gr = next_stable(a, blockIdx.x);
-  if (gr >= a.total_rows) return;
-  RowCtx cur = load_ctx(a, gr);
-  uint4 cw[V], cm[V], cg[V];
-  auto load_codes = [&](const RowCtx& c, uint4* wv, uint4* mv, uint4* gv) {
-    const DevTensor* T = a.tensors + c.tensor;
-    const uint4* w4 = reinterpret_cast<const uint4*>(T->w_codes[in] + c.roff);
-    const uint4* m4 = reinterpret_cast<const uint4*>(T->m_codes[in] + c.roff);
-    const uint4* g4 = reinterpret_cast<const uint4*>(T->g_codes + c.roff);
-#pragma unroll
-    for (int j = 0; j < V; ++j) {
-      const int v = t + j * NT;
-      if (v < nvec) {
-        wv[j] = __ldg(w4 + v);
-        mv[j] = __ldg(m4 + v);
-        gv[j] = __ldg(g4 + v);
+  // Deferred output of a row's old outliers (after its phase 2 published vbase): the
+  // weight code byte over the payload left by the dense pass and, for those that stay
+  // outliers, the CSR entry at its column-ordered position.
+  auto old_out = [&](int b, int on, int t0) {
+    const BufHdr hd = *hdr(b);
+    const uint32_t* wd = words(b);
+    for (int i = t - t0; i < on; i += NT - t0) {
+      const uint32_t cw = spcw(b)[i];
+      const int col = spcol(b)[i];
+      hd.w_out[col] = (uint8_t)(cw & 0xFFu);
+      if (cw & 0x100u) {
+        const int v = col >> 4, e = col & 15;
+        const int pos = vbase[v] + __popc((wd[v] >> 16) & ((1u << e) - 1u));
+        if (pos < hd.co) {
+          a.col_out[hd.so + pos] = col;
+          a.val_out[hd.so + pos] = spval(b)[i];
+        }
       }
     }
   };
-  load_codes(cur, cw, cm, cg);
-  clear_bits(0);
+  auto clear_words = [&](int b) {
+#pragma unroll
+    for (int j = 0; j < V; ++j) words(b)[t + j * NT] = 0u;
+  };
+  auto first_stable = [&](int g) {
+    while (g < a.total_rows && !(__ldg(&a.prep[g].info) & I_STABLE)) g += G;
+    return g;
+  };
+
+  // ---------------------------------------------------------------- prologue
+  int gr = first_stable(blockIdx.x);
+  if (gr >= a.total_rows) return;
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    mbar_fence_init();
+  }
+  clear_words(0);
   __syncthreads();
-  sparse_pass(cur, 0, 0);
+  if (t == 0) issue_row(gr, load_head(a, gr), 0);
+  int gn = first_stable(gr + G);
+  RowHead hn{};
+  if (gn < a.total_rows) hn = load_head(a, gn);
+  RowHead hs{};  // speculative: the row after gn in the stride
+  if (gn + G < a.total_rows) hs = load_head(a, gn + G);
+  mbar_wait(&bars[0], 0u);
+  sparse_pass(0, 0, 0);
+  int on_prev = rec(0)->on;
   __syncthreads();
 
-  for (int it = 0;; ++it) {
-    const int b = it % 3, bn = (it + 1) % 3;
-    const int gn = next_stable(a, gr + gridDim.x);
+  const int tw = NW > 1 ? 32 : 0;  // first thread of the deferred / sparse work
+  int it = 0;
+  for (;; ++it) {
+    const int b = it % 3, bn = (it + 1) % 3, bp = (it + 2) % 3;
+    const int s = it & 1, sn = s ^ 1;
     const bool has_next = gn < a.total_rows;
-    RowCtx nxt;
-    if (has_next) nxt = load_ctx(a, gn);
-    clear_bits(bn);
-    const DevTensor* T = a.tensors + cur.tensor;
-    uint8_t* w_out = T->w_codes[out] + cur.roff;
+    if (t == 0 && has_next) issue_row(gn, hn, sn);
+    clear_words(bn);
+    mbar_wait(&bars[s], (uint32_t)((it >> 1) & 1));
+    const RowPrep& R = *rec(s);
+    const uint8_t* st = stage(s);
+    const float negc_m = R.negc_m, sm = R.sm, negc_g = R.negc_g, sg = R.sg;
+    uint8_t* const m_out = R.m_out;
+    const int so = R.so, co = R.co, on_cur = R.on;
 
     // ================================ phase 1 ================================
     float mp[V][16];
-    uint32_t mask[V], o16[V];
+    uint32_t nmask[V], out16[V];
     float mlo = __int_as_float(0x7f800000), mhi = __int_as_float(0xff800000);
+    uint32_t cnt = 0;
 #pragma unroll
     for (int j = 0; j < V; ++j) {
       const int v = t + j * NT;
-      mask[j] = 0;
-      o16[j] = 0;
+      nmask[j] = 0;
+      out16[j] = 0;
       if (v < nvec) {
-        const uint32_t mw[4] = {cm[j].x, cm[j].y, cm[j].z, cm[j].w};
-        const uint32_t gw[4] = {cg[j].x, cg[j].y, cg[j].z, cg[j].w};
+        const uint4 cwj = *reinterpret_cast<const uint4*>(st + 128 + v * 16);
+        const uint4 cmj = *reinterpret_cast<const uint4*>(st + 128 + cols + v * 16);
+        const uint4 cgj = *reinterpret_cast<const uint4*>(st + 128 + 2 * cols + v * 16);
+        const uint32_t mw[4] = {cmj.x, cmj.y, cmj.z, cmj.w};
+        const uint32_t gw[4] = {cgj.x, cgj.y, cgj.z, cgj.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           float2 a0 = make_float2(magic_byte(mw[i], 0), magic_byte(mw[i], 1));
           float2 a1 = make_float2(magic_byte(mw[i], 2), magic_byte(mw[i], 3));
           float2 b0 = make_float2(magic_byte(gw[i], 0), magic_byte(gw[i], 1));
           float2 b1 = make_float2(magic_byte(gw[i], 2), magic_byte(gw[i], 3));
-          a0 = mul2(add2(a0, f2(cur.dm.negc)), f2(cur.dm.s));
-          a1 = mul2(add2(a1, f2(cur.dm.negc)), f2(cur.dm.s));
-          b0 = mul2(add2(b0, f2(cur.dg.negc)), f2(cur.dg.s));
-          b1 = mul2(add2(b1, f2(cur.dg.negc)), f2(cur.dg.s));
+          a0 = mul2(add2(a0, f2(negc_m)), f2(sm));
+          a1 = mul2(add2(a1, f2(negc_m)), f2(sm));
+          b0 = mul2(add2(b0, f2(negc_g)), f2(sg));
+          b1 = mul2(add2(b1, f2(negc_g)), f2(sg));
           const float2 r0 = mprime2(a0, b0, B2, C2, NZ);
           const float2 r1 = mprime2(a1, b1, B2, C2, NZ);
           mp[j][4 * i] = r0.x; mp[j][4 * i + 1] = r0.y;
@@ -299,58 +380,43 @@ __global__ void __launch_bounds__(512, 1) rows_kernel(const LaunchArgs a) {
           asm("max.f32 %0, %1, %2, %3;" : "=f"(tt) : "f"(mhi), "f"(mp[j][2 * pp]), "f"(mp[j][2 * pp + 1]));
           mhi = tt;
         }
-        // weight codes: pass through, except candidates (codes 0 / qmax) and old outliers
-        uint4 wq = cw[j];
-        const uint32_t any = (cand_flags(wq.x, KC) | cand_flags(wq.y, KC) |
-                              cand_flags(wq.z, KC) | cand_flags(wq.w, KC));
-        const uint32_t ob16 = bits16(b)[v];
-        o16[j] = ob16;
-        if (any | ob16) {
-          uint32_t cmask = any ? (flags16(wq, KC) & ~ob16) : 0u;
-          uint32_t msk = 0;
+        // weight codes pass through; candidates (codes 0 / qmax, not old outliers) get
+        // the exact Lion step; old-outlier bytes are rewritten by old_out()
+        uint4 wq = cwj;
+        const uint32_t wrd = words(b)[v];
+        const uint32_t any = cand_flags(wq.x, KC) | cand_flags(wq.y, KC) |
+                             cand_flags(wq.z, KC) | cand_flags(wq.w, KC);
+        uint32_t o16 = wrd >> 16;
+        if (any) {
+          uint32_t cmask = flags16(wq, KC) & ~(wrd & 0xFFFFu);
           if (cmask) {
             const uint4 q0 = wq;
-            const float tmin = __ldg(T->t_min + cur.lrow), tmax = __ldg(T->t_max + cur.lrow);
-            const float sw = __ldg(T->w_scale + cur.lrow);
-            const int32_t zw = __ldg(T->w_zp + cur.lrow);
+            const uint32_t zpay = (R.info >> 8) & 0xFFu;
+            uint32_t nm = 0;
             while (cmask) {
               const int e = __ffs(cmask) - 1;
               cmask &= cmask - 1u;
-              const float wv = exact_wprime(byte_of(q0, e), byte_of(cm[j], e), byte_of(cg[j], e), T,
-                                            cur.lrow, cur, h);
-              const bool o = (wv < tmin) || (wv > tmax);
-              set_byte(wq, e, o ? cur.zpay : quant_exact(wv, sw, zw, qmax));
-              msk |= (o ? 1u : 0u) << e;
+              const float wv = exact_wprime(byte_of(q0, e), byte_of(cmj, e), byte_of(cgj, e), R, h);
+              const bool o = (wv < R.tmin) || (wv > R.tmax);
+              set_byte(wq, e, o ? zpay : quant_inlier(wv, R.sw, R.zw, a.bit_width));
+              nm |= (o ? 1u : 0u) << e;
+            }
+            if (nm) {
+              atomicOr(&words(b)[v], nm << 16);
+              o16 |= nm;
+              nmask[j] = nm;
             }
           }
-          uint32_t om = ob16;
-          while (om) {
-            const int e = __ffs(om) - 1;
-            om &= om - 1u;
-            const int rank = frank(b)[v] + __popc(ob16 & ((1u << e) - 1u));
-            const uint32_t c = spcw(b)[rank];
-            set_byte(wq, e, c);
-            msk |= ((c >> 8) & 1u) << e;
-          }
-          mask[j] = msk;
         }
-        __stcs(reinterpret_cast<uint4*>(w_out) + v, wq);
+        out16[j] = o16;
+        cnt |= (uint32_t)__popc(o16) << (16 * j);
+        __stcs(reinterpret_cast<uint4*>(R.w_out) + v, wq);
       }
     }
-    // prefetch the next row's codes (in flight during the barriers and phase 2)
-    if (has_next) load_codes(nxt, cw, cm, cg);
 
     // warp partials: m' range, CSR counts (packed j=0 | j=1 << 16, prefix-scanned)
-    {
-      float wlo, whi;
-      asm("redux.sync.min.f32 %0, %1, 0xffffffff;" : "=f"(wlo) : "f"(mlo));
-      asm("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(whi) : "f"(mhi));
-      mlo = wlo;
-      mhi = whi;
-    }
-    uint32_t cnt = 0;
-#pragma unroll
-    for (int j = 0; j < V; ++j) cnt |= (uint32_t)__popc(mask[j]) << (16 * j);
+    asm("redux.sync.min.f32 %0, %1, 0xffffffff;" : "=f"(mlo) : "f"(mlo));
+    asm("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(mhi) : "f"(mhi));
     uint32_t incl = cnt;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -391,33 +457,50 @@ __global__ void __launch_bounds__(512, 1) rows_kernel(const LaunchArgs a) {
         float smv = 1.0f;
         int32_t zmv = 0;
         // stable rows have bounded, finite m' (k_step_prep), so lo <= hi
-        affine_from_bounds(lo, hi, a.bit_width, smv, zmv);
+        affine_ni(lo, hi, a.bit_width, &smv, &zmv);
         const QuantRow qm = make_quant_row(smv, zmv, a.bit_width);
-        const bool qmf = qm.fast && code_unclamped(lo, smv, zmv) >= 0.0 &&
-                         code_unclamped(hi, smv, zmv) <= (double)qmax;
-        RowRes r;
-        r.s = smv; r.inv = qm.inv_s; r.magic = qm.magic; r.thr = qm.thr;
-        r.ylo = qm.ylo; r.yhi = qm.yhi; r.z = zmv; r.qmf = qmf ? 1 : 0;
-        *res = r;
-        T->m_scale[out][cur.lrow] = smv;
-        T->m_zp[out][cur.lrow] = zmv;
+        // every m' lies in [lo, hi]: if their codes need no clip (proven with the fast
+        // quantizer's own tie bound), no code of the row does
+        float em = 0.0f;
+        const float lh[4] = {lo, hi, lo, hi};
+        (void)quant4_e(lh, qm, em);
+        const float ylo = __fmul_rn(lo, qm.inv_s), yhi = __fmul_rn(hi, qm.inv_s);
+        const bool qmf = qm.fast && em < qm.thr && ylo > qm.ylo - 0.5f && yhi < qm.yhi + 0.5f;
+        RowRes rr;
+        rr.s = smv; rr.inv = qm.inv_s; rr.magic = qm.magic; rr.thr = qm.thr;
+        rr.z = zmv; rr.qmf = qmf ? 1 : 0;
+        *res = rr;
+        *R.m_scale_out = smv;
+        *R.m_zp_out = zmv;
         const int total = (int)(tot0 + tot1);
-        T->cnt[out][cur.lrow] = total;
-        if (total > cur.co) atomicOr(&a.hdr->overflow, 1u);
+        *R.cnt_out = total;
+        if (total > co) atomicOr(&a.hdr->overflow, 1u);
       }
-      if (NW == 1 && has_next) sparse_pass(nxt, bn, 0);
-    } else if (has_next) {
-      sparse_pass(nxt, bn, 32);
+      if (NW == 1) {
+        if (it > 0) old_out(bp, on_prev, 0);
+        if (has_next) {
+          mbar_wait(&bars[sn], (uint32_t)(((it + 1) >> 1) & 1));
+          sparse_pass(sn, bn, 0);
+        }
+      }
+    } else {
+      if (it > 0) old_out(bp, on_prev, tw);
+      if (has_next) {  // the next row's old outliers, from its landed stage
+        mbar_wait(&bars[sn], (uint32_t)(((it + 1) >> 1) & 1));
+        sparse_pass(sn, bn, tw);
+      }
     }
     __syncthreads();  // ---------------------------------------------------- B
 
     // ================================ phase 2 ================================
+    // (the stage is not read after B: thread 0 refills it at the next row's start)
     {
       const RowRes r = *res;
       QuantRow qm;
       qm.s = r.s; qm.inv_s = r.inv; qm.magic = r.magic; qm.thr = r.thr;
-      qm.ylo = r.ylo; qm.yhi = r.yhi; qm.z = r.z; qm.qmax = qmax; qm.fast = true;
-      uint8_t* m_out = T->m_codes[out] + cur.roff;
+      qm.z = r.z; qm.qmax = qmax; qm.fast = true;
+      qm.ylo = (float)(-r.z);
+      qm.yhi = (float)(qmax - r.z);
       const int2 sg2 = seg[wid];
 #pragma unroll
       for (int j = 0; j < V; ++j) {
@@ -441,37 +524,46 @@ __global__ void __launch_bounds__(512, 1) rows_kernel(const LaunchArgs a) {
             for (int q = 0; q < 4; ++q) cq[q] = quant4_exact(&mp[j][4 * q], qm);
           }
           __stcs(reinterpret_cast<uint4*>(m_out) + v, make_uint4(cq[0], cq[1], cq[2], cq[3]));
-          // CSR entries of this vector (columns ascending)
-          uint32_t mm = mask[j];
-          if (mm) {
-            int pos = (j == 0 ? sg2.x : sg2.y) + (int)((excl >> (16 * j)) & 0xFFFFu);
-            const uint8_t* w_in = T->w_codes[in] + cur.roff;
-            const uint8_t* m_in = T->m_codes[in] + cur.roff;
-            const uint8_t* g_in = T->g_codes + cur.roff;
-            while (mm) {
-              const int e = __ffs(mm) - 1;
-              mm &= mm - 1u;
-              const int col = v * 16 + e;
-              float val;
-              if (o16[j] & (1u << e)) {
-                val = spval(b)[frank(b)[v] + __popc(o16[j] & ((1u << e) - 1u))];
-              } else {
-                val = exact_wprime(w_in[col], m_in[col], g_in[col], T, cur.lrow, cur, h);
+          if (out16[j]) {
+            const int vb = (j == 0 ? sg2.x : sg2.y) + (int)((excl >> (16 * j)) & 0xFFFFu);
+            vbase[v] = vb;
+            // new outliers (candidate path): CSR entries with the exact w'
+            uint32_t nm = nmask[j];
+            if (nm) {
+              const RowPrep& G0 = a.prep[gr];  // global copy (the stage may be refilled)
+              while (nm) {
+                const int e = __ffs(nm) - 1;
+                nm &= nm - 1u;
+                const int col = v * 16 + e;
+                const int pos = vb + __popc(out16[j] & ((1u << e) - 1u));
+                const float val = exact_wprime(G0.w_in[col], G0.m_in[col], G0.g_in[col], G0, h);
+                if (pos < co) {
+                  a.col_out[so + pos] = col;
+                  a.val_out[so + pos] = val;
+                }
               }
-              if (pos < cur.co) {
-                a.col_out[cur.so + pos] = col;
-                a.val_out[cur.so + pos] = val;
-              }
-              ++pos;
             }
           }
         }
       }
     }
+    on_prev = on_cur;
     if (!has_next) break;
+    // advance: the speculative head is the next row when it is stable (the usual case)
     gr = gn;
-    cur = nxt;
+    int gnn = gn + G;
+    if (gnn < a.total_rows && (hs.info & I_STABLE)) {
+      hn = hs;
+    } else {
+      gnn = first_stable(gnn);
+      if (gnn < a.total_rows) hn = load_head(a, gnn);
+    }
+    gn = gnn;
+    if (gn + G < a.total_rows) hs = load_head(a, gn + G);
   }
+  // the last row's old outliers
+  __syncthreads();
+  old_out(it % 3, on_prev, 0);
 }
 
 // ---------------------------------------------------------------------------- prep
@@ -504,7 +596,7 @@ __global__ void k_step_prep(const LaunchArgs a, int stable_ok) {
   const int co = T.rs[out][r + 1] - so;
   const int zpay = zw < 0 ? 0 : (zw > qmax ? qmax : zw);
 
-  bool ok = stable_ok != 0 && on <= a.oldcap6;
+  bool ok = stable_ok != 0 && on <= a.oldcap6 && T.cols == a.cols_p && T.cnt[out] != nullptr;
   ok = ok && make_dequant_row(sw, zw).fast && make_dequant_row(sm, zm).fast &&
        make_dequant_row(sg, zg).fast;
   // positive, normal scales (so 1/s is finite and the dense values are bounded)
@@ -512,7 +604,7 @@ __global__ void k_step_prep(const LaunchArgs a, int stable_ok) {
        sg >= 0x1.0p-126f && sg <= 0x1.0p100f;
   if (ok) {
     const double K = (double)qmax + fabs((double)zw);
-    // m' = b2*m + c2*g finite: |m|, |g| <= s*(qmax+|z|) <= 2^100 * 2^23, |b2|, |c2| <= 4
+    // m' = b2*m + c2*g finite: |m|, |g| <= s*(qmax+|z|) <= 2^120, |b2|, |c2| <= 4
     const double c2 = (double)__fsub_rn(1.0f, a.b2);
     ok = (double)sm * ((double)qmax + fabs((double)zm)) <= 0x1.0p120 &&
          (double)sg * ((double)qmax + fabs((double)zg)) <= 0x1.0p120 &&
@@ -528,17 +620,30 @@ __global__ void k_step_prep(const LaunchArgs a, int stable_ok) {
   }
   RowPrep p;
   p.info = (ok ? rs6::I_STABLE : 0u) | ((uint32_t)zpay << 8);
-  p.tensor = lo;
   p.lrow = r;
   p.ob = ob;
   p.on = on;
   p.so = so;
   p.co = co;
-  p.cols = T.cols;
-  p.sm = sm;
+  p.zw = zw;
   p.zm = zm;
+  p.sm = sm;
+  p.negc_m = make_dequant_row(sm, zm).negc;
   p.sg = sg;
+  p.negc_g = make_dequant_row(sg, zg).negc;
   p.zg = zg;
+  p.sw = sw;
+  p.tmin = tmin;
+  p.tmax = tmax;
+  const size_t roff = (size_t)r * (size_t)T.cols;
+  p.w_in = T.w_codes[in] + roff;
+  p.m_in = T.m_codes[in] + roff;
+  p.g_in = T.g_codes ? T.g_codes + roff : nullptr;
+  p.w_out = T.w_codes[out] + roff;
+  p.m_out = T.m_codes[out] + roff;
+  p.m_scale_out = T.m_scale[out] + r;
+  p.m_zp_out = T.m_zp[out] + r;
+  p.cnt_out = T.cnt[out] ? T.cnt[out] + r : nullptr;
   a.prep[gr] = p;
   if (!ok) {
     const int k = atomicAdd(a.xcount, 1);
@@ -547,9 +652,9 @@ __global__ void k_step_prep(const LaunchArgs a, int stable_ok) {
 }
 
 // ---------------------------------------------------------------------------- launch
-template <int V>
+template <int MAXT, int MINB>
 static cudaError_t rows_launch_t(const LaunchArgs& a, int nt, size_t smem, cudaStream_t st) {
-  auto k = rows_kernel<V>;
+  auto k = rows_kernel<MAXT, MINB>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
@@ -567,10 +672,17 @@ static cudaError_t rows_launch_t(const LaunchArgs& a, int nt, size_t smem, cudaS
 
 bool rows_kernel_eligible(int gk, int use_bulk, int uniform_cols) {
   return gk == G_U8 && use_bulk && uniform_cols > 0 && uniform_cols % 16 == 0 &&
-         uniform_cols <= 16384;  // <= 512 threads at V = 2
+         uniform_cols <= 16384 &&  // <= 512 threads at V = 2
+         rows_kernel_smem(uniform_cols, rows_kernel_oldcap(uniform_cols)) <= 227 * 1024;
 }
 
-int rows_kernel_oldcap(int cols) { return (cols / 16 + 31) & ~31; }
+// register budget per width class (tuning: -DQFT_ROWS_MINB_S / _M)
+#ifndef QFT_ROWS_MINB_S
+#define QFT_ROWS_MINB_S 4  // rows of <= 4096 columns (<= 128 threads)
+#endif
+#ifndef QFT_ROWS_MINB_M
+#define QFT_ROWS_MINB_M 2  // rows of <= 12288 columns (<= 384 threads)
+#endif
 
 cudaError_t launch_rows_step(const LaunchArgs& a0, cudaStream_t st) {
   LaunchArgs a = a0;
@@ -578,13 +690,17 @@ cudaError_t launch_rows_step(const LaunchArgs& a0, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(a.xcount, 0, sizeof(int32_t), st);
   if (e != cudaSuccess) return e;
   const int pt = 256;
-  const int stable_ok = a.use_bulk ? 1 : 0;
-  k_step_prep<<<(a.total_rows + pt - 1) / pt, pt, 0, st>>>(a, stable_ok);
+  k_step_prep<<<(a.total_rows + pt - 1) / pt, pt, 0, st>>>(a, 1);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  const int V = 2;
-  const int nt = rows_kernel_nt(a.cols_p, V);
-  const size_t smem = rows_kernel_smem(a.cols_p, V, a.oldcap6);
-  if ((e = rows_launch_t<2>(a, nt, smem, st)) != cudaSuccess) return e;
+  const int nt = rows_kernel_nt(a.cols_p);
+  const size_t smem = rows_kernel_smem(a.cols_p, a.oldcap6);
+  if (nt <= 128)
+    e = rows_launch_t<128, QFT_ROWS_MINB_S>(a, nt, smem, st);
+  else if (nt <= 384)
+    e = rows_launch_t<384, QFT_ROWS_MINB_M>(a, nt, smem, st);
+  else
+    e = rows_launch_t<512, 1>(a, nt, smem, st);
+  if (e != cudaSuccess) return e;
   // the general kernel over the device row list
   LaunchArgs x = a;
   x.blocks = a.xlist;
