@@ -300,13 +300,11 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
 #pragma unroll
     for (int j = 0; j < V; ++j) words(b)[t + j * NT] = 0u;
   };
-  auto first_stable = [&](int g) {
-    while (g < a.total_rows && !(__ldg(&a.prep[g].info) & I_STABLE)) g += G;
-    return g;
-  };
 
   // ---------------------------------------------------------------- prologue
-  int gr = first_stable(blockIdx.x);
+  // Static row sequence: row blockIdx.x + k*G.  Rows outside the stable tier still
+  // flow through the pipeline (their record says so) but do no work here.
+  int gr = blockIdx.x;
   if (gr >= a.total_rows) return;
   if (t == 0) {
     mbar_init(&bars[0], 1);
@@ -315,31 +313,35 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   }
   clear_words(0);
   __syncthreads();
-  if (t == 0) issue_row(gr, load_head(a, gr), 0);
-  int gn = first_stable(gr + G);
-  RowHead hn{};
-  if (gn < a.total_rows) hn = load_head(a, gn);
-  RowHead hs{};  // speculative: the row after gn in the stride
-  if (gn + G < a.total_rows) hs = load_head(a, gn + G);
+  RowHead hn{};  // thread 0: the head of the row after the next one (loaded a row ahead)
+  if (t == 0) {
+    issue_row(gr, load_head(a, gr), 0);
+    if (gr + G < a.total_rows) hn = load_head(a, gr + G);
+  }
   mbar_wait(&bars[0], 0u);
-  sparse_pass(0, 0, 0);
-  int on_prev = rec(0)->on;
+  if (rec(0)->info & I_STABLE) sparse_pass(0, 0, 0);
+  int on_prev = (rec(0)->info & I_STABLE) ? rec(0)->on : 0;
   __syncthreads();
 
   const int tw = NW > 1 ? 32 : 0;  // first thread of the deferred / sparse work
   int it = 0;
-  for (;; ++it) {
+  for (;; ++it, gr += G) {
     const int b = it % 3, bn = (it + 1) % 3, bp = (it + 2) % 3;
     const int s = it & 1, sn = s ^ 1;
+    const int gn = gr + G;
     const bool has_next = gn < a.total_rows;
-    if (t == 0 && has_next) issue_row(gn, hn, sn);
+    if (t == 0 && has_next) {
+      issue_row(gn, hn, sn);
+      if (gn + G < a.total_rows) hn = load_head(a, gn + G);
+    }
     clear_words(bn);
     mbar_wait(&bars[s], (uint32_t)((it >> 1) & 1));
     const RowPrep& R = *rec(s);
+    const bool stable = (R.info & I_STABLE) != 0;
     const uint8_t* st = stage(s);
     const float negc_m = R.negc_m, sm = R.sm, negc_g = R.negc_g, sg = R.sg;
     uint8_t* const m_out = R.m_out;
-    const int so = R.so, co = R.co, on_cur = R.on;
+    const int so = R.so, co = R.co, on_cur = stable ? R.on : 0;
 
     // ================================ phase 1 ================================
     float mp[V][16];
@@ -351,7 +353,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
       const int v = t + j * NT;
       nmask[j] = 0;
       out16[j] = 0;
-      if (v < nvec) {
+      if (stable && v < nvec) {
         const uint4 cwj = *reinterpret_cast<const uint4*>(st + 128 + v * 16);
         const uint4 cmj = *reinterpret_cast<const uint4*>(st + 128 + cols + v * 16);
         const uint4 cgj = *reinterpret_cast<const uint4*>(st + 128 + 2 * cols + v * 16);
@@ -428,6 +430,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
     __syncthreads();  // ---------------------------------------------------- A
 
     if (wid == 0) {
+      if (stable) {
       // the row's m' range and CSR segment offsets (segment order: j-major, then warp)
       float lo = __int_as_float(0x7f800000), hi = __int_as_float(0xff800000);
       uint32_t c = 0;
@@ -476,25 +479,26 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
         *R.cnt_out = total;
         if (total > co) atomicOr(&a.hdr->overflow, 1u);
       }
+      }
       if (NW == 1) {
         if (it > 0) old_out(bp, on_prev, 0);
         if (has_next) {
           mbar_wait(&bars[sn], (uint32_t)(((it + 1) >> 1) & 1));
-          sparse_pass(sn, bn, 0);
+          if (rec(sn)->info & I_STABLE) sparse_pass(sn, bn, 0);
         }
       }
     } else {
       if (it > 0) old_out(bp, on_prev, tw);
       if (has_next) {  // the next row's old outliers, from its landed stage
         mbar_wait(&bars[sn], (uint32_t)(((it + 1) >> 1) & 1));
-        sparse_pass(sn, bn, tw);
+        if (rec(sn)->info & I_STABLE) sparse_pass(sn, bn, tw);
       }
     }
     __syncthreads();  // ---------------------------------------------------- B
 
     // ================================ phase 2 ================================
     // (the stage is not read after B: thread 0 refills it at the next row's start)
-    {
+    if (stable) {
       const RowRes r = *res;
       QuantRow qm;
       qm.s = r.s; qm.inv_s = r.inv; qm.magic = r.magic; qm.thr = r.thr;
@@ -549,17 +553,6 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
     }
     on_prev = on_cur;
     if (!has_next) break;
-    // advance: the speculative head is the next row when it is stable (the usual case)
-    gr = gn;
-    int gnn = gn + G;
-    if (gnn < a.total_rows && (hs.info & I_STABLE)) {
-      hn = hs;
-    } else {
-      gnn = first_stable(gnn);
-      if (gnn < a.total_rows) hn = load_head(a, gnn);
-    }
-    gn = gnn;
-    if (gn + G < a.total_rows) hs = load_head(a, gn + G);
   }
   // the last row's old outliers
   __syncthreads();
