@@ -48,6 +48,7 @@
 #include "qft_device.cuh"
 #include "qft_internal.h"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace qftk {
@@ -283,7 +284,10 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   auto issue_row = [&](int grow, const RowHead& hd, int s) {
     uint8_t* dst = stage(s);
     const uint32_t n = (uint32_t)cols;
-    const uint32_t cb = (slotted && hd.on > 0) ? (uint32_t)((hd.on * 4 + 15) & ~15) : 0u;
+    // the old CSR slot only for stable rows (k_step_prep bounds their count by oldcap6;
+    // a general-tier row's slot may not fit the stage)
+    const uint32_t cb = (slotted && (hd.info & I_STABLE) && hd.on > 0)
+                            ? (uint32_t)((hd.on * 4 + 15) & ~15) : 0u;
     mbar_arrive_expect_tx(&bars[s], 128u + 3u * n + 2u * cb);
     bulk_g2s(dst, a.prep + grow, 128u, &bars[s]);
     bulk_g2s(dst + 128, hd.w_in, n, &bars[s]);
@@ -705,6 +709,8 @@ static cudaError_t rows_launch_t(const LaunchArgs& a, int nt, size_t smem, cudaS
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   long grid = (long)sms * per_sm;
   if (grid > a.total_rows) grid = a.total_rows;
+  // QFT_ROWS_GRID caps the grid: the tests use it so every CTA pipelines many rows
+  if (const char* g = getenv("QFT_ROWS_GRID")) grid = std::min(grid, std::max(1L, atol(g)));
   if (grid < 1) grid = 1;
   k<<<(unsigned)grid, nt, smem, st>>>(a);
   return cudaGetLastError();

@@ -539,3 +539,45 @@ def test_zero1_world1_nccl_cuda_shard(cuda, port):
                     _eq(got[k], getattr(d, k), f"zero1 step {step} tensor {i} {k}")
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("grid", [3, 37])
+@pytest.mark.parametrize("lr", [2e-5, 2.2e-4])
+def test_rows_kernel_many_rows_per_cta(cuda, port, monkeypatch, grid, lr):
+    """The rows kernel with a capped grid, so every CTA pipelines many rows through its
+    TMA stages and sparse buffers (the other parity tests are small enough to give each
+    CTA one row); lr near sw/2 mixes stable rows with rows of the general kernel inside
+    one launch.  A small LLaMA-shaped model, 3 steps, every tensor byte-compared with
+    the oracle."""
+    from paper_2310_07147_b200.shapes import llama
+    monkeypatch.setenv("QFT_ROWS_GRID", str(grid))
+    shapes = llama(512, 1376, 1, 512)
+    bw, frac = 8, 0.01
+    st = cuda.QftModelState(shapes, bit_width=bw)
+    st.init_from_weights(lambda i: cuda.synth(shapes[i], 1234 + i, 0.02, 0.005), frac)
+    ora = []
+    for i, sh in enumerate(shapes):
+        w = port.synth(sh, 1234 + i, 0.02, 0.005)
+        ora.append([port.decompose_weight(w, frac, bw),
+                    port.quantize_state(np.zeros(sh, np.float32), bw)])
+    for step in range(3):
+        for i, sh in enumerate(shapes):
+            gq = port.quantize_state(port.synth(sh, 5000 + 100 * step + i, 1e-3, 0.0), bw)
+            c, sc, z = st.grad_views(i)
+            c.copy_(torch.from_numpy(gq[0]))
+            sc.copy_(torch.from_numpy(gq[1]))
+            z.copy_(torch.from_numpy(gq[2]))
+            d, m = ora[i]
+            ora[i] = list(port.lion_step_layer(d, *m, *gq, lr=lr)[:2])
+        st.step(lr=lr, check=True)
+        for i in range(len(shapes)):
+            got = st.export_tensor(i)
+            d, m = ora[i]
+            tag = f"grid {grid} lr {lr} step {step} tensor {i}"
+            _eq(got["codes"], d.codes, tag + " w codes")
+            _eq(got["row_ptr"], d.row_ptr, tag + " row_ptr")
+            _eq(got["col_idx"], d.col_idx, tag + " col_idx")
+            _eq(got["values"], d.values, tag + " values")
+            _eq(got["m_codes"], m[0], tag + " m codes")
+            _eq(got["m_scale"], m[1], tag + " m scale")
+            _eq(got["m_zero_point"], m[2], tag + " m zp")
