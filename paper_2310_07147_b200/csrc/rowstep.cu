@@ -77,7 +77,7 @@ struct Smem {
   __device__ __host__ int o_buf(int b) const { return o_bar() + 16 + b * buf_bytes(); }
   __device__ __host__ int o_vbase() const { return o_buf(3); }
   __device__ __host__ int o_part() const { return o_vbase() + nvec * 4; }
-  __device__ __host__ int o_seg() const { return o_part() + nw * 32; }  // part: 2 x nw float4
+  __device__ __host__ int o_seg() const { return o_part() + nw * 16; }
   __device__ __host__ int o_res() const { return o_seg() + nw * 8; }
   __device__ __host__ int total() const { return o_res() + 32; }
 };
@@ -160,40 +160,6 @@ __device__ __noinline__ void affine_ni(float lo, float hi, int bw, float* s, int
   affine_from_bounds(lo, hi, bw, *s, *z);
 }
 
-// affine_params_from_bounds (quantize.hpp:114-128) for lo < hi at low latency: the
-// divide by qmax via a Markstein-corrected product whose exact remainder proves the
-// correctly rounded quotient (s a power of two or a tie: refused), and the zero point
-// from an approximate reciprocal, accepted only when -lo/s is provably clear of a
-// half-integer.  Returns false (-> the exact fp64 path) whenever a proof fails.
-__device__ __forceinline__ bool affine_fast(float lo_f, float hi_f, double qmax, double rq,
-                                            float& scale, int32_t& zp) {
-  const double lo = (double)lo_f, hi = (double)hi_f;
-  if (!(lo < hi)) return false;
-  const double d = __dsub_rn(hi, lo);
-  const double q0 = __dmul_rn(d, rq);
-  const double s = __fma_rn(__fma_rn(-q0, qmax, d), rq, q0);
-  const double r1 = __fma_rn(-s, qmax, d);  // exact remainder d - s*qmax
-  const long long sb = __double_as_longlong(s);
-  const int ex = (int)((sb >> 52) & 0x7FF);
-  if (ex < 64 || ex > 2000 || (sb & 0x000FFFFFFFFFFFFFLL) == 0) return false;
-  const double half_ulp = __longlong_as_double((long long)(ex - 53) << 52);
-  if (!(fabs(r1) < qmax * half_ulp)) return false;
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(s));
-  y = __fma_rn(y, __fma_rn(-s, y, 1.0), y);
-  y = __fma_rn(y, __fma_rn(-s, y, 1.0), y);
-  const double q = __dmul_rn(-lo, y);  // within a few ulp of -lo/s
-  const double aq = fabs(q);
-  if (!(aq < 2147483000.0)) return false;
-  const double tq = trunc(aq);
-  const double fr = aq - tq;
-  if (fabs(fr - 0.5) <= aq * 0x1.0p-46 + 0x1.0p-1000) return false;
-  const double zz = copysign(fr > 0.5 ? tq + 1.0 : tq, q);
-  scale = __double2float_rn(s);
-  zp = (int32_t)zz;
-  return true;
-}
-
 // code of an INLIER weight of a stable row (its exact code lies in [0, qmax], proven
 // by code(t_min) == 0 and code(t_max) == qmax): the fast quantizer with its tie proof,
 // the reference's fp64 formula when the proof fails
@@ -205,17 +171,6 @@ __device__ __forceinline__ uint32_t quant_inlier(float x, float sw, int32_t zw, 
   if (q.fast && fabsf(e) < q.thr && y > q.ylo - 0.5f && y < q.yhi + 0.5f)
     return __float_as_uint(tt) & 0xFFu;
   return quant_exact_ni(x, sw, zw, q.qmax);
-}
-
-// one code with the reference's clip (quantize.hpp:160-170): the fast quantizer when
-// its tie and range proof holds, the fp64 formula (out of line) otherwise
-__device__ __forceinline__ uint32_t quant_checked(float x, const QuantRow& q) {
-  const float y = __fmul_rn(x, q.inv_s);
-  const float tt = __fadd_rn(y, q.magic);
-  const float e = __fsub_rn(y, __fsub_rn(tt, q.magic));
-  if (q.fast && fabsf(e) < q.thr && y > q.ylo - 0.5f && y < q.yhi + 0.5f)
-    return __float_as_uint(tt) & 0xFFu;
-  return quant_exact_ni(x, q.s, q.z, q.qmax);
 }
 
 // exact w' of one dense element from its three codes (lion1: the reference's fp32
@@ -263,7 +218,6 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   h.c1 = __fsub_rn(1.0f, a.b1);
   h.c2 = __fsub_rn(1.0f, a.b2);
   const float2 B2 = f2(h.b2), C2 = f2(h.c2), NZ = f2(a.negzero);
-  const double rq = __drcp_rn((double)qmax);
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.o_bar());
   auto stage = [&](int s) { return smem + L.o_stage(s); };
@@ -276,7 +230,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   auto spcw = [&](int b) { return reinterpret_cast<uint32_t*>(spval(b) + L.oldcap); };
   auto spcol = [&](int b) { return reinterpret_cast<int32_t*>(spval(b) + 2 * L.oldcap); };
   int* vbase = reinterpret_cast<int*>(smem + L.o_vbase());
-  float4* const part0 = reinterpret_cast<float4*>(smem + L.o_part());
+  float4* part = reinterpret_cast<float4*>(smem + L.o_part());
   int2* seg = reinterpret_cast<int2*>(smem + L.o_seg());
   RowRes* res = reinterpret_cast<RowRes*>(smem + L.o_res());
 
@@ -284,10 +238,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   auto issue_row = [&](int grow, const RowHead& hd, int s) {
     uint8_t* dst = stage(s);
     const uint32_t n = (uint32_t)cols;
-    // the old CSR slot only for stable rows (k_step_prep bounds their count by oldcap6;
-    // a general-tier row's slot may not fit the stage)
-    const uint32_t cb = (slotted && (hd.info & I_STABLE) && hd.on > 0)
-                            ? (uint32_t)((hd.on * 4 + 15) & ~15) : 0u;
+    const uint32_t cb = (slotted && hd.on > 0) ? (uint32_t)((hd.on * 4 + 15) & ~15) : 0u;
     mbar_arrive_expect_tx(&bars[s], 128u + 3u * n + 2u * cb);
     bulk_g2s(dst, a.prep + grow, 128u, &bars[s]);
     bulk_g2s(dst + 128, hd.w_in, n, &bars[s]);
@@ -392,7 +343,6 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
     const float negc_m = R.negc_m, sm = R.sm, negc_g = R.negc_g, sg = R.sg;
     uint8_t* const m_out = R.m_out;
     const int so = R.so, co = R.co, on_cur = stable ? R.on : 0;
-    float4* const part = part0 + (it & 1) * NW;  // warp partials (double-buffered)
 
     // ================================ phase 1 ================================
     float mp[V][16];
@@ -482,21 +432,36 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
 
     if (wid == 0) {
       if (stable) {
-      // the row's m' range
+      // the row's m' range and CSR segment offsets (segment order: j-major, then warp)
       float lo = __int_as_float(0x7f800000), hi = __int_as_float(0xff800000);
+      uint32_t c = 0;
       if (lane < NW) {
         const float4 pp = part[lane];
         lo = pp.x;
         hi = pp.y;
+        c = __float_as_uint(pp.z);
       }
       asm("redux.sync.min.f32 %0, %1, 0xffffffff;" : "=f"(lo) : "f"(lo));
       asm("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(hi) : "f"(hi));
+      uint32_t in0 = c & 0xFFFFu, in1 = c >> 16;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t u0 = __shfl_up_sync(0xffffffffu, in0, d);
+        const uint32_t u1 = __shfl_up_sync(0xffffffffu, in1, d);
+        if (lane >= d) {
+          in0 += u0;
+          in1 += u1;
+        }
+      }
+      const uint32_t tot0 = __shfl_sync(0xffffffffu, in0, 31);
+      const uint32_t tot1 = __shfl_sync(0xffffffffu, in1, 31);
+      if (lane < NW)
+        seg[lane] = make_int2((int)(in0 - (c & 0xFFFFu)), (int)(tot0 + in1 - (c >> 16)));
       if (lane == 0) {
         float smv = 1.0f;
         int32_t zmv = 0;
         // stable rows have bounded, finite m' (k_step_prep), so lo <= hi
-        if (!affine_fast(lo, hi, (double)qmax, rq, smv, zmv))
-          affine_ni(lo, hi, a.bit_width, &smv, &zmv);
+        affine_ni(lo, hi, a.bit_width, &smv, &zmv);
         const QuantRow qm = make_quant_row(smv, zmv, a.bit_width);
         // every m' lies in [lo, hi]: if their codes need no clip (proven with the fast
         // quantizer's own tie bound), no code of the row does
@@ -511,9 +476,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
         *res = rr;
         *R.m_scale_out = smv;
         *R.m_zp_out = zmv;
-        uint32_t tot = 0;
-        for (int w = 0; w < NW; ++w) tot += __float_as_uint(part[w].z);
-        const int total = (int)((tot & 0xFFFFu) + (tot >> 16));
+        const int total = (int)(tot0 + tot1);
         *R.cnt_out = total;
         if (total > co) atomicOr(&a.hdr->overflow, 1u);
       }
@@ -543,17 +506,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
       qm.z = r.z; qm.qmax = qmax; qm.fast = true;
       qm.ylo = (float)(-r.z);
       qm.yhi = (float)(qmax - r.z);
-      // CSR segment bases (segment order: j-major, then warp) from the warp totals
-      int2 sg2 = make_int2(0, 0);
-      {
-        uint32_t before = 0, all0 = 0;
-        for (int w = 0; w < NW; ++w) {
-          const uint32_t c = __float_as_uint(part[w].z);
-          if (w < wid) before += c;
-          all0 += c & 0xFFFFu;
-        }
-        sg2 = make_int2((int)(before & 0xFFFFu), (int)(all0 + (before >> 16)));
-      }
+      const int2 sg2 = seg[wid];
 #pragma unroll
       for (int j = 0; j < V; ++j) {
         const int v = t + j * NT;
@@ -573,10 +526,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
           }
           if (!ok) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              cq[q] = quant_checked(mp[j][4 * q], qm) | (quant_checked(mp[j][4 * q + 1], qm) << 8) |
-                      (quant_checked(mp[j][4 * q + 2], qm) << 16) |
-                      (quant_checked(mp[j][4 * q + 3], qm) << 24);
+            for (int q = 0; q < 4; ++q) cq[q] = quant4_exact(&mp[j][4 * q], qm);
           }
           __stcs(reinterpret_cast<uint4*>(m_out) + v, make_uint4(cq[0], cq[1], cq[2], cq[3]));
           if (out16[j]) {
@@ -666,7 +616,9 @@ __global__ void k_step_prep(const LaunchArgs a, int stable_ok) {
   p.info = (ok ? rs6::I_STABLE : 0u) | ((uint32_t)zpay << 8);
   p.lrow = r;
   p.ob = ob;
-  p.on = on;
+  // the rows kernel copies a row's old CSR slot into its stage: general-tier rows
+  // (whose slot may exceed the stage) get 0 -- the general kernel reads its own bounds
+  p.on = ok ? on : 0;
   p.so = so;
   p.co = co;
   p.zw = zw;
