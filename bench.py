@@ -279,7 +279,8 @@ def run_gpu_arm(args):
                    "parallelism": f"zero1-rows{world}" if world > 1 else "single"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic,
-                     "kernel": f"step_kernel<u8> cols={g.cols}",
+                     "kernel": f"qftc_plan_step cols={g.cols} (k_step_prep + rows_kernel, "
+                               "stable tier + step_kernel, general tier)",
                      "algorithmic_bytes_per_launch": alg, "launch_ms": per_group_ms[gi_dom],
                      "peak_kind": peak_kind},
         "step_hbm_gbs": all_alg / (ms * 1e-3) / 1e9,

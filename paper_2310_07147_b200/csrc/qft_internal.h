@@ -102,8 +102,14 @@ struct LaunchArgs {
 // Per-row record of the rows kernel (128 B), written by k_step_prep every step and
 // bulk-copied into shared memory with the row's codes: everything a row needs.
 struct RowPrep {
-  uint32_t info;  // bit 0: stable tier; bits 8..15: outlier payload code clamp(z, 0, qmax)
-  int32_t lrow, ob, on;          // local row, old CSR slot start / count
+  // info: bit 0 stable tier; bits 1..6 outlier flags of the candidate outcomes below;
+  // bits 8..15 the outlier payload code clamp(z, 0, qmax); bits 16..31 outcomes 4, 5
+  uint32_t info;
+  // cand: the codes of the candidate outcomes 0..3 (a byte each).  Outcome 3*B + S is a
+  // dense weight of code 0 (B=0) or qmax (B=1) after the Lion step with sign(d) < 0,
+  // == 0, > 0 (S = 0, 1, 2): w' = w - lr*(sign(d) + wd*w) takes only these 3 values.
+  uint32_t cand;
+  int32_t ob, on;                // old CSR slot start / count
   int32_t so, co, zw, zm;        // new slot start / capacity, w / m zero points
   float sm, negc_m, sg, negc_g;  // m / g scale and -(2^23 + z) (the PRMT dequant form)
   int32_t zg;

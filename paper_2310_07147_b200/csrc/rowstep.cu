@@ -128,6 +128,10 @@ __device__ __forceinline__ uint32_t cand_flags(uint32_t x, uint32_t K) {
   const uint32_t t = (x ^ (x >> 1)) & K;
   return (t - 0x01010101u) & ~t & 0x80808080u;
 }
+// bytes equal to zero (flag exact for "some byte"; neighbours may be false positives)
+__device__ __forceinline__ uint32_t zero_flags(uint32_t x) {
+  return (x - 0x01010101u) & ~x & 0x80808080u;
+}
 __device__ __forceinline__ uint32_t flags16(uint4 q, uint32_t K) {
   auto f4 = [&](uint32_t x) -> uint32_t {
     const uint32_t f = cand_flags(x, K) >> 7;  // bits 0, 8, 16, 24
@@ -211,6 +215,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   const Smem L{NT * V, a.oldcap6, NW, cols};
   const int qmax = (1 << a.bit_width) - 1;
   const uint32_t KC = (uint32_t)((1 << (a.bit_width - 1)) - 1) * 0x01010101u;
+  const uint32_t QB = (uint32_t)qmax * 0x01010101u;
   const int G = gridDim.x;
   const bool slotted = a.slotted_in != 0;
   Hyper h;
@@ -342,6 +347,12 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
     const uint8_t* st = stage(s);
     const float negc_m = R.negc_m, sm = R.sm, negc_g = R.negc_g, sg = R.sg;
     uint8_t* const m_out = R.m_out;
+    // boundary codes 0 / qmax need the candidate path only if one of their tabulated
+    // outcomes differs from "same code, inlier" (k_step_prep)
+    const uint32_t need =
+        (((R.cand & 0xFFFFFFu) != 0u || (R.info & (7u << 1)) != 0u) ? 1u : 0u) |
+        ((((R.cand >> 24) & 0xFFu) != (uint32_t)qmax || (R.info >> 16) != ((uint32_t)qmax * 0x101u) ||
+          (R.info & (7u << 4)) != 0u) ? 2u : 0u);
     const int so = R.so, co = R.co, on_cur = stable ? R.on : 0;
 
     // ================================ phase 1 ================================
@@ -387,22 +398,40 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
         // the exact Lion step; old-outlier bytes are rewritten by old_out()
         uint4 wq = cwj;
         const uint32_t wrd = words(b)[v];
-        const uint32_t any = cand_flags(wq.x, KC) | cand_flags(wq.y, KC) |
-                             cand_flags(wq.z, KC) | cand_flags(wq.w, KC);
+        // detect only the boundary codes whose step can change them (row-uniform)
+        uint32_t any = 0;
+        if (need == 3u) {
+          any = cand_flags(wq.x, KC) | cand_flags(wq.y, KC) | cand_flags(wq.z, KC) |
+                cand_flags(wq.w, KC);
+        } else if (need == 1u) {
+          any = zero_flags(wq.x) | zero_flags(wq.y) | zero_flags(wq.z) | zero_flags(wq.w);
+        } else if (need == 2u) {
+          any = zero_flags(wq.x ^ QB) | zero_flags(wq.y ^ QB) | zero_flags(wq.z ^ QB) |
+                zero_flags(wq.w ^ QB);
+        }
         uint32_t o16 = wrd >> 16;
         if (any) {
           uint32_t cmask = flags16(wq, KC) & ~(wrd & 0xFFFFu);
           if (cmask) {
+            // a dense code-0 / code-qmax weight has one value per row, so its step has 3
+            // possible outcomes (k_step_prep tabulates them): only sign(d) is needed,
+            // d = b1*m + (1-b1)*g in the reference order (optimizer.hpp:36)
             const uint4 q0 = wq;
-            const uint32_t zpay = (R.info >> 8) & 0xFFu;
             uint32_t nm = 0;
             while (cmask) {
               const int e = __ffs(cmask) - 1;
               cmask &= cmask - 1u;
-              const float wv = exact_wprime(byte_of(q0, e), byte_of(cmj, e), byte_of(cgj, e), R, h);
-              const bool o = (wv < R.tmin) || (wv > R.tmax);
-              set_byte(wq, e, o ? zpay : quant_inlier(wv, R.sw, R.zw, a.bit_width));
-              nm |= (o ? 1u : 0u) << e;
+              const uint32_t c = byte_of(q0, e);
+              // SWAR false positives and boundary codes the step cannot change: stable
+              if (c == 0u ? !(need & 1u) : (c == (uint32_t)qmax ? !(need & 2u) : true)) continue;
+              const float mv = __fmul_rn(__fadd_rn(magic_byte(byte_of(cmj, e), 0), negc_m), sm);
+              const float gv = __fmul_rn(__fadd_rn(magic_byte(byte_of(cgj, e), 0), negc_g), sg);
+              const float d = __fadd_rn(__fmul_rn(h.b1, mv), __fmul_rn(h.c1, gv));
+              const int k = (c ? 3 : 0) + (d > 0.0f ? 2 : (d < 0.0f ? 0 : 1));
+              const uint32_t code = k < 4 ? (R.cand >> (8 * k)) & 0xFFu
+                                          : (R.info >> (16 + 8 * (k - 4))) & 0xFFu;
+              set_byte(wq, e, code);
+              nm |= ((R.info >> (1 + k)) & 1u) << e;
             }
             if (nm) {
               atomicOr(&words(b)[v], nm << 16);
@@ -614,7 +643,25 @@ __global__ void k_step_prep(const LaunchArgs a, int stable_ok) {
   }
   RowPrep p;
   p.info = (ok ? rs6::I_STABLE : 0u) | ((uint32_t)zpay << 8);
-  p.lrow = r;
+  p.cand = 0u;
+  if (ok) {
+    // the candidate outcomes: w = dequant(B), w' = w - lr*(s + wd*w) for s = -1, 0, +1
+    // (lion_apply, optimizer.hpp:38), then the class and code against the cached
+    // thresholds exactly as the step computes them (quantize.hpp:274-285)
+    for (int B = 0; B < 2; ++B) {
+      const float w = dequant_exact(B ? (uint32_t)qmax : 0u, sw, zw);
+      for (int S = 0; S < 3; ++S) {
+        const float sg1 = (float)(S - 1);
+        const float wn = __fsub_rn(w, __fmul_rn(a.lr, __fadd_rn(sg1, __fmul_rn(a.wd, w))));
+        const bool o = (wn < tmin) || (wn > tmax);
+        const uint32_t code = o ? (uint32_t)zpay : quant_exact(wn, sw, zw, qmax);
+        const int k = 3 * B + S;
+        if (o) p.info |= 1u << (1 + k);
+        if (k < 4) p.cand |= code << (8 * k);
+        else p.info |= code << (16 + 8 * (k - 4));
+      }
+    }
+  }
   p.ob = ob;
   // the rows kernel copies a row's old CSR slot into its stage: general-tier rows
   // (whose slot may exceed the stage) get 0 -- the general kernel reads its own bounds

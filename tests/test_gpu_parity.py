@@ -211,16 +211,18 @@ def test_lion_step_trajectory(cuda, port, bw, frac, shape, wd):
         _eq(_np(dw.sparse.values), dsw.values, tag + " values")
 
 
+@pytest.mark.parametrize("bw,frac", [(8, 0.01), (8, 0.0045), (4, 0.0045), (3, 0.0045)])
 @pytest.mark.parametrize("wd", [0.0, 0.01])
 @pytest.mark.parametrize("lr", [2e-5, 1.5e-4, 2.2e-4, 4e-4])
 @pytest.mark.parametrize("shape", [(64, 4096), (24, 11008), (40, 48)])
-def test_lion_step_stable_tier(cuda, port, lr, shape, wd):
+def test_lion_step_stable_tier(cuda, port, lr, shape, wd, bw, frac):
     """The rows kernel's stable tier (rowstep.cu): at the paper's lr = 2e-5 every row is
     proven code-stable; lr near sw/2 (~2.2e-4 at 8 bits) splits a tensor between the
     stable tier and the general kernel row by row.  12 steps byte-compared with the
     oracle; the first steps migrate boundary codes (0 / qmax) into the CSR, so the
-    candidate path and the old-outlier sparse pass both run."""
-    bw, frac = 8, 0.01
+    candidate path and the old-outlier sparse pass both run.  p = 0.45% puts the
+    thresholds inside the spikes, so zero points sit near 0 / qmax and boundary-code
+    candidates are common (the tabulated candidate outcomes)."""
     dsw, m = _layer(port, shape, 500 + shape[1], bw, frac)
     dw, st = _dev_layer(cuda, dsw, m, shape, bw, frac)
     h = cuda.LionHyper(lr=lr, beta1=0.9, beta2=0.99, weight_decay=wd)
@@ -234,7 +236,7 @@ def test_lion_step_stable_tier(cuda, port, lr, shape, wd):
         cuda.lion_step_quantized([dw], st, stack, h, bw)
         dsw, m, _ = port.lion_step_layer(dsw, *m, *gq, lr=h.lr, beta1=h.beta1, beta2=h.beta2,
                                          wd=h.weight_decay)
-        tag = f"lr {lr} step {step}"
+        tag = f"b{bw} p{frac} lr {lr} step {step}"
         _eq(_np(st.momentum[0].params.scale), m[1], tag + " m scale")
         _eq(_np(st.momentum[0].params.zero_point), m[2], tag + " m zp")
         _eq(_np(st.momentum[0].data), m[0], tag + " m codes")
