@@ -164,6 +164,40 @@ __device__ __noinline__ void affine_ni(float lo, float hi, int bw, float* s, int
   affine_from_bounds(lo, hi, bw, *s, *z);
 }
 
+// affine_params_from_bounds (quantize.hpp:114-128) for lo < hi at low latency: the
+// divide by qmax via a Markstein-corrected product whose exact remainder proves the
+// correctly rounded quotient (s a power of two or a tie: refused), and the zero point
+// from an approximate reciprocal, accepted only when -lo/s is provably clear of a
+// half-integer.  Returns false (-> the exact fp64 path) whenever a proof fails.
+__device__ __forceinline__ bool affine_fast(float lo_f, float hi_f, double qmax, double rq,
+                                            float& scale, int32_t& zp) {
+  const double lo = (double)lo_f, hi = (double)hi_f;
+  if (!(lo < hi)) return false;
+  const double d = __dsub_rn(hi, lo);
+  const double q0 = __dmul_rn(d, rq);
+  const double s = __fma_rn(__fma_rn(-q0, qmax, d), rq, q0);
+  const double r1 = __fma_rn(-s, qmax, d);  // exact remainder d - s*qmax
+  const long long sb = __double_as_longlong(s);
+  const int ex = (int)((sb >> 52) & 0x7FF);
+  if (ex < 64 || ex > 2000 || (sb & 0x000FFFFFFFFFFFFFLL) == 0) return false;
+  const double half_ulp = __longlong_as_double((long long)(ex - 53) << 52);
+  if (!(fabs(r1) < qmax * half_ulp)) return false;
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(s));
+  y = __fma_rn(y, __fma_rn(-s, y, 1.0), y);
+  y = __fma_rn(y, __fma_rn(-s, y, 1.0), y);
+  const double q = __dmul_rn(-lo, y);  // within a few ulp of -lo/s
+  const double aq = fabs(q);
+  if (!(aq < 2147483000.0)) return false;
+  const double tq = trunc(aq);
+  const double fr = aq - tq;
+  if (fabs(fr - 0.5) <= aq * 0x1.0p-46 + 0x1.0p-1000) return false;
+  const double zz = copysign(fr > 0.5 ? tq + 1.0 : tq, q);
+  scale = __double2float_rn(s);
+  zp = (int32_t)zz;
+  return true;
+}
+
 // code of an INLIER weight of a stable row (its exact code lies in [0, qmax], proven
 // by code(t_min) == 0 and code(t_max) == qmax): the fast quantizer with its tie proof,
 // the reference's fp64 formula when the proof fails
@@ -223,6 +257,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   h.c1 = __fsub_rn(1.0f, a.b1);
   h.c2 = __fsub_rn(1.0f, a.b2);
   const float2 B2 = f2(h.b2), C2 = f2(h.c2), NZ = f2(a.negzero);
+  const double rq = __drcp_rn((double)qmax);
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.o_bar());
   auto stage = [&](int s) { return smem + L.o_stage(s); };
@@ -490,7 +525,10 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
         float smv = 1.0f;
         int32_t zmv = 0;
         // stable rows have bounded, finite m' (k_step_prep), so lo <= hi
-        affine_ni(lo, hi, a.bit_width, &smv, &zmv);
+        // (the FMA-verified fast divide pays off where more warps wait on this chain:
+        // the wide-row instances; measured same-run, slower on the 128-thread one)
+        if (!(MAXT > 128 && affine_fast(lo, hi, (double)qmax, rq, smv, zmv)))
+          affine_ni(lo, hi, a.bit_width, &smv, &zmv);
         const QuantRow qm = make_quant_row(smv, zmv, a.bit_width);
         // every m' lies in [lo, hi]: if their codes need no clip (proven with the fast
         // quantizer's own tie bound), no code of the row does
