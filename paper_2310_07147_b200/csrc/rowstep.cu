@@ -69,12 +69,12 @@ constexpr int V = 2;  // 16-byte vectors per thread
 //   vbase      CSR base of every vector with outputs (phase 2 -> next row's old_out)
 //   part, seg, res  warp partials, CSR segment offsets, the m' quantizer
 struct Smem {
-  int nvec, oldcap, nw, cols;
+  int nvec, oldcap, nw, cols, ns;  // ns: TMA stages (3 on the 128-thread class)
   __device__ __host__ int stage_bytes() const { return 128 + 3 * cols + 8 * oldcap; }
   __device__ __host__ int o_stage(int s) const { return s * stage_bytes(); }
-  __device__ __host__ int o_bar() const { return 2 * stage_bytes(); }
+  __device__ __host__ int o_bar() const { return ns * stage_bytes(); }
   __device__ __host__ int buf_bytes() const { return 16 + nvec * 4 + oldcap * 12; }
-  __device__ __host__ int o_buf(int b) const { return o_bar() + 16 + b * buf_bytes(); }
+  __device__ __host__ int o_buf(int b) const { return o_bar() + 32 + b * buf_bytes(); }
   __device__ __host__ int o_vbase() const { return o_buf(3); }
   __device__ __host__ int o_part() const { return o_vbase() + nvec * 4; }
   __device__ __host__ int o_seg() const { return o_part() + nw * 16; }
@@ -230,15 +230,20 @@ int rows_kernel_nt(int cols) {
   return ((per + 31) / 32) * 32;
 }
 
-int rows_kernel_oldcap(int cols) { return ((cols / 16) + 31) & ~31; }
+// TMA stages: 3 where the smem budget keeps 4 CTAs/SM (rows <= 4096 columns, old-outlier
+// table cols/32), else 2 (table cols/16)
+static int rows_kernel_ns(int cols) { return rows_kernel_nt(cols) <= 128 ? 3 : 2; }
+int rows_kernel_oldcap(int cols) {
+  return ((rows_kernel_ns(cols) == 3 ? cols / 32 : cols / 16) + 31) & ~31;
+}
 
 size_t rows_kernel_smem(int cols, int oldcap) {
   const int nt = rows_kernel_nt(cols);
-  rs6::Smem L{nt * rs6::V, oldcap, nt / 32, ((cols + 15) / 16) * 16};
+  rs6::Smem L{nt * rs6::V, oldcap, nt / 32, ((cols + 15) / 16) * 16, rows_kernel_ns(cols)};
   return (size_t)L.total();
 }
 
-template <int MAXT, int MINB>
+template <int MAXT, int MINB, int NS>
 __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   using namespace rs6;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -246,7 +251,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int cols = a.cols_p;  // uniform row length of the launch (multiple of 16)
   const int nvec = cols >> 4;
-  const Smem L{NT * V, a.oldcap6, NW, cols};
+  const Smem L{NT * V, a.oldcap6, NW, cols, NS};
   const int qmax = (1 << a.bit_width) - 1;
   const uint32_t KC = (uint32_t)((1 << (a.bit_width - 1)) - 1) * 0x01010101u;
   const uint32_t QB = (uint32_t)qmax * 0x01010101u;
@@ -348,17 +353,20 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   int gr = blockIdx.x;
   if (gr >= a.total_rows) return;
   if (t == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
     mbar_fence_init();
   }
   clear_words(0);
   __syncthreads();
-  RowHead hn{};  // thread 0: the head of the row after the next one (loaded a row ahead)
-  if (t == 0) {
-    issue_row(gr, load_head(a, gr), 0);
-    if (gr + G < a.total_rows) hn = load_head(a, gr + G);
-  }
+  // The issuing thread streams row it+NS-1 each iteration.  With 2 stages that is
+  // thread 0 at the top of the iteration; with 3 it is the last warp's lane 0 inside
+  // the barrier window, where that warp has no other work (off the phase-1 path).
+  const int ti = (NS == 3 && NW > 1) ? NT - 32 : 0;
+  RowHead hn{};  // issuing thread: the head of the row it streams next
+  if (t == 0)
+    for (int i = 0; i < NS - 1; ++i)
+      if (gr + i * G < a.total_rows) issue_row(gr + i * G, load_head(a, gr + i * G), i);
+  if (t == ti && gr + (NS - 1) * G < a.total_rows) hn = load_head(a, gr + (NS - 1) * G);
   mbar_wait(&bars[0], 0u);
   if (rec(0)->info & I_STABLE) sparse_pass(0, 0, 0);
   int on_prev = (rec(0)->info & I_STABLE) ? rec(0)->on : 0;
@@ -368,15 +376,19 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   int it = 0;
   for (;; ++it, gr += G) {
     const int b = it % 3, bn = (it + 1) % 3, bp = (it + 2) % 3;
-    const int s = it & 1, sn = s ^ 1;
+    const int s = it % NS, sn = (it + 1) % NS;
     const int gn = gr + G;
     const bool has_next = gn < a.total_rows;
-    if (t == 0 && has_next) {
-      issue_row(gn, hn, sn);
-      if (gn + G < a.total_rows) hn = load_head(a, gn + G);
-    }
+    const int gi = gr + (NS - 1) * G;  // the row streamed this iteration
+    auto issue_ahead = [&]() {
+      if (t == ti && gi < a.total_rows) {
+        issue_row(gi, hn, (it + NS - 1) % NS);
+        if (gi + G < a.total_rows) hn = load_head(a, gi + G);
+      }
+    };
+    if (NS == 2) issue_ahead();
     clear_words(bn);
-    mbar_wait(&bars[s], (uint32_t)((it >> 1) & 1));
+    mbar_wait(&bars[s], (uint32_t)((it / NS) & 1));
     const RowPrep& R = *rec(s);
     const bool stable = (R.info & I_STABLE) != 0;
     const uint8_t* st = stage(s);
@@ -549,16 +561,18 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
       }
       }
       if (NW == 1) {
+        if (NS == 3) issue_ahead();
         if (it > 0) old_out(bp, on_prev, 0);
         if (has_next) {
-          mbar_wait(&bars[sn], (uint32_t)(((it + 1) >> 1) & 1));
+          mbar_wait(&bars[sn], (uint32_t)(((it + 1) / NS) & 1));
           if (rec(sn)->info & I_STABLE) sparse_pass(sn, bn, 0);
         }
       }
     } else {
+      if (NS == 3) issue_ahead();
       if (it > 0) old_out(bp, on_prev, tw);
       if (has_next) {  // the next row's old outliers, from its landed stage
-        mbar_wait(&bars[sn], (uint32_t)(((it + 1) >> 1) & 1));
+        mbar_wait(&bars[sn], (uint32_t)(((it + 1) / NS) & 1));
         if (rec(sn)->info & I_STABLE) sparse_pass(sn, bn, tw);
       }
     }
@@ -733,9 +747,9 @@ __global__ void k_step_prep(const LaunchArgs a, int stable_ok) {
 }
 
 // ---------------------------------------------------------------------------- launch
-template <int MAXT, int MINB>
+template <int MAXT, int MINB, int NS>
 static cudaError_t rows_launch_t(const LaunchArgs& a, int nt, size_t smem, cudaStream_t st) {
-  auto k = rows_kernel<MAXT, MINB>;
+  auto k = rows_kernel<MAXT, MINB, NS>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
@@ -778,11 +792,11 @@ cudaError_t launch_rows_step(const LaunchArgs& a0, cudaStream_t st) {
   const int nt = rows_kernel_nt(a.cols_p);
   const size_t smem = rows_kernel_smem(a.cols_p, a.oldcap6);
   if (nt <= 128)
-    e = rows_launch_t<128, QFT_ROWS_MINB_S>(a, nt, smem, st);
+    e = rows_launch_t<128, QFT_ROWS_MINB_S, 3>(a, nt, smem, st);
   else if (nt <= 384)
-    e = rows_launch_t<384, QFT_ROWS_MINB_M>(a, nt, smem, st);
+    e = rows_launch_t<384, QFT_ROWS_MINB_M, 2>(a, nt, smem, st);
   else
-    e = rows_launch_t<512, 1>(a, nt, smem, st);
+    e = rows_launch_t<512, 1, 2>(a, nt, smem, st);
   if (e != cudaSuccess) return e;
   // the general kernel over the device row list
   LaunchArgs x = a;
