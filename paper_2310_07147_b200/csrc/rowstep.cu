@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   // of the CTA): the exact w' (general Lion form), its class against the cached
   // thresholds and its code (quantize.hpp:274-285); marks bit e (old) and bit 16+e
   // (stays an outlier) of its vector's word.
-  auto sparse_pass = [&](int s, int b, int t0) {
+  auto sparse_pass = [&](int s, int b, int t0, int t1) {  // threads [t0, t1)
     const RowPrep& r = *rec(s);
     const uint8_t* st = stage(s);
     const int32_t* cin = slotted ? reinterpret_cast<const int32_t*>(st + 128 + 3 * cols)
@@ -308,7 +308,8 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
     const uint32_t zpay = (r.info >> 8) & 0xFFu;
     uint32_t* wd = words(b);
     if (t == t0) *hdr(b) = BufHdr{r.w_out, r.so, r.co};
-    for (int i = t - t0; i < r.on; i += NT - t0) {
+    if (t < t0 || t >= t1) return;
+    for (int i = t - t0; i < r.on; i += t1 - t0) {
       const int col = cin[i];
       float wv = vin[i];
       float mv = dequant_exact(st[128 + cols + col], r.sm, r.zm);
@@ -325,10 +326,11 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   // Deferred output of a row's old outliers (after its phase 2 published vbase): the
   // weight code byte over the payload left by the dense pass and, for those that stay
   // outliers, the CSR entry at its column-ordered position.
-  auto old_out = [&](int b, int on, int t0) {
+  auto old_out = [&](int b, int on, int t0, int t1) {  // threads [t0, t1)
     const BufHdr hd = *hdr(b);
     const uint32_t* wd = words(b);
-    for (int i = t - t0; i < on; i += NT - t0) {
+    if (t < t0 || t >= t1) return;
+    for (int i = t - t0; i < on; i += t1 - t0) {
       const uint32_t cw = spcw(b)[i];
       const int col = spcol(b)[i];
       hd.w_out[col] = (uint8_t)(cw & 0xFFu);
@@ -368,7 +370,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
       if (gr + i * G < a.total_rows) issue_row(gr + i * G, load_head(a, gr + i * G), i);
   if (t == ti && gr + (NS - 1) * G < a.total_rows) hn = load_head(a, gr + (NS - 1) * G);
   mbar_wait(&bars[0], 0u);
-  if (rec(0)->info & I_STABLE) sparse_pass(0, 0, 0);
+  if (rec(0)->info & I_STABLE) sparse_pass(0, 0, 0, NT);
   int on_prev = (rec(0)->info & I_STABLE) ? rec(0)->on : 0;
   __syncthreads();
 
@@ -562,18 +564,21 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
       }
       if (NW == 1) {
         if (NS == 3) issue_ahead();
-        if (it > 0) old_out(bp, on_prev, 0);
+        if (it > 0) old_out(bp, on_prev, 0, NT);
         if (has_next) {
           mbar_wait(&bars[sn], (uint32_t)(((it + 1) / NS) & 1));
-          if (rec(sn)->info & I_STABLE) sparse_pass(sn, bn, 0);
+          if (rec(sn)->info & I_STABLE) sparse_pass(sn, bn, 0, NT);
         }
       }
     } else {
       if (NS == 3) issue_ahead();
-      if (it > 0) old_out(bp, on_prev, tw);
-      if (has_next) {  // the next row's old outliers, from its landed stage
+      // 4+ warps: the next row's sparse pass on warps 1..NW-2, the previous row's CSR
+      // output on the last warp (which also issues the TMA), so no warp runs both
+      const int ts = (NS == 3 && NW >= 4) ? NT - 32 : NT;
+      if (it > 0) old_out(bp, on_prev, ts < NT ? ts : tw, NT);
+      if (has_next && t < ts) {  // the next row's old outliers, from its landed stage
         mbar_wait(&bars[sn], (uint32_t)(((it + 1) / NS) & 1));
-        if (rec(sn)->info & I_STABLE) sparse_pass(sn, bn, tw);
+        if (rec(sn)->info & I_STABLE) sparse_pass(sn, bn, tw, ts);
       }
     }
     __syncthreads();  // ---------------------------------------------------- B
@@ -638,7 +643,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   }
   // the last row's old outliers
   __syncthreads();
-  old_out(it % 3, on_prev, 0);
+  old_out(it % 3, on_prev, 0, NT);
 }
 
 // ---------------------------------------------------------------------------- prep
