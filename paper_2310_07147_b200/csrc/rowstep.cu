@@ -572,9 +572,11 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
       }
     } else {
       if (NS == 3) issue_ahead();
-      // 4+ warps: the next row's sparse pass on warps 1..NW-2, the previous row's CSR
-      // output on the last warp (which also issues the TMA), so no warp runs both
-      const int ts = (NS == 3 && NW >= 4) ? NT - 32 : NT;
+      // The next row's sparse pass and the previous row's CSR output on disjoint warps,
+      // so no warp runs both chains: on the 3-stage class the output takes the last
+      // warp (which also issues the TMA)
+      // (8+ warps: the output on the last 4, one iteration for ~100 old outliers)
+      const int ts = (NS == 3 && NW >= 4) ? NT - 32 : (NW >= 8 ? NT - 128 : NT);
       if (it > 0) old_out(bp, on_prev, ts < NT ? ts : tw, NT);
       if (has_next && t < ts) {  // the next row's old outliers, from its landed stage
         mbar_wait(&bars[sn], (uint32_t)(((it + 1) / NS) & 1));
