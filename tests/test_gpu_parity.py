@@ -583,3 +583,82 @@ def test_rows_kernel_many_rows_per_cta(cuda, port, monkeypatch, grid, lr):
             _eq(got["m_codes"], m[0], tag + " m codes")
             _eq(got["m_scale"], m[1], tag + " m scale")
             _eq(got["m_zero_point"], m[2], tag + " m zp")
+
+
+def _csr_rows(row_ptr, col_idx, values, rows):
+    """The CSR entries of the given rows, as (row_ptr, cols, vals) of that sub-matrix."""
+    rp, cs, vs = [0], [], []
+    for r in rows:
+        a, b = int(row_ptr[r]), int(row_ptr[r + 1])
+        cs.append(np.asarray(col_idx[a:b]))
+        vs.append(np.asarray(values[a:b]))
+        rp.append(rp[-1] + (b - a))
+    return (np.asarray(rp, np.int32), np.concatenate(cs).astype(np.int32),
+            np.concatenate(vs).astype(np.float32))
+
+
+@pytest.mark.parametrize("lr", [2e-5, 2.2e-4])
+def test_full_size_7b_tensors_sampled_rows(cuda, port, lr):
+    """Parity at BASELINE.json's full sizes through row independence: the step has no
+    cross-row dependency (optimizer.hpp:103-118 is per-row quantize/decompose), so any
+    subset of rows stepped by the oracle as its own layer must equal the same rows of
+    the full-size GPU step.  The four LLaMA-2-7B matrix shapes (configs[1]; 238 M
+    parameters, one grouped engine as in bench.py), three steps; 42 sampled rows per
+    tensor (first, last, random) byte-compared -- codes, CSR, momentum -- plus
+    whole-tensor invariants (CSR columns ascending and in range, payload code on every
+    outlier, CSR values outside the thresholds)."""
+    shapes = [(4096, 4096), (11008, 4096), (4096, 11008), (32000, 4096)]
+    bw, frac = 8, 0.01
+    qmax = (1 << bw) - 1
+    st = cuda.QftModelState(shapes, bit_width=bw)
+    st.init_from_weights(lambda i: cuda.synth(shapes[i], 4100 + i, 0.02, 0.005), frac)
+    rng = np.random.default_rng(7)
+    rows = [np.unique(np.r_[0, r - 1, rng.choice(r, 40, replace=False)]) for r, _ in shapes]
+    ora = []
+    for i, sh in enumerate(shapes):
+        w = cuda.synth(sh, 4100 + i, 0.02, 0.005)[torch.from_numpy(rows[i]).cuda()].cpu().numpy()
+        ora.append([port.decompose_weight(w, frac, bw),
+                    port.quantize_state(np.zeros((len(rows[i]), sh[1]), np.float32), bw)])
+        del w
+    for step in range(3):
+        for i, sh in enumerate(shapes):
+            g = cuda.synth(sh, 8100 + 10 * step + i, 1e-3, 0.0)
+            q = cuda.quantize_state(g, bw)
+            c, sc, z = st.grad_views(i)
+            c.copy_(q.data)
+            sc.copy_(q.params.scale)
+            z.copy_(q.params.zero_point)
+            gq = port.quantize_state(g[torch.from_numpy(rows[i]).cuda()].cpu().numpy(), bw)
+            del g, q
+            d, m = ora[i]
+            ora[i] = list(port.lion_step_layer(d, *m, *gq, lr=lr)[:2])
+        st.step(lr=lr, check=True)
+    for i, (r, c) in enumerate(shapes):
+        got = st.export_tensor(i)
+        d, m = ora[i]
+        rs = rows[i]
+        tag = f"lr {lr} {r}x{c}"
+        _eq(got["codes"][rs], d.codes, tag + " w codes")
+        rp, cs, vs = _csr_rows(got["row_ptr"], got["col_idx"], got["values"], rs)
+        _eq(rp, d.row_ptr, tag + " row_ptr")
+        _eq(cs, d.col_idx, tag + " col_idx")
+        _eq(vs, d.values, tag + " values")
+        _eq(got["m_codes"][rs], m[0], tag + " m codes")
+        _eq(got["m_scale"][rs], m[1], tag + " m scale")
+        _eq(got["m_zero_point"][rs], m[2], tag + " m zp")
+        # whole-tensor invariants
+        rp_all = np.asarray(got["row_ptr"], np.int64)
+        col = np.asarray(got["col_idx"], np.int64)
+        val = np.asarray(got["values"], np.float32)
+        assert rp_all[0] == 0 and np.all(np.diff(rp_all) >= 0) and rp_all[-1] == col.size
+        row_of = np.repeat(np.arange(r), np.diff(rp_all))
+        assert col.size == 0 or (col.min() >= 0 and col.max() < c), tag + " column range"
+        same_row = row_of[1:] == row_of[:-1]
+        assert np.all(col[1:][same_row] > col[:-1][same_row]), tag + " columns ascending"
+        tmin = np.asarray(got["t_min"])[row_of]
+        tmax = np.asarray(got["t_max"])[row_of]
+        assert np.all((val < tmin) | (val > tmax)), tag + " CSR value inside thresholds"
+        zp = np.asarray(got["zero_point"], np.int64)[row_of]
+        codes = np.asarray(got["codes"])
+        assert np.array_equal(codes[row_of, col], np.clip(zp, 0, qmax)), tag + " payload code"
+        del got
