@@ -576,13 +576,82 @@ def run_13b_dequant(args):
                       "peak_gbs": hbm}), flush=True)
 
 
+def run_ckpt(args):
+    """QFTC v1 checkpoint of the 7B state: the GPU CRC-32
+    over every array of the file in file order (HBM-resident, ~13.8 GB), zlib.crc32 on
+    one host core over a 256 MB sample for scale, and save + load of one LLaMA-2-7B
+    decoder layer (9 tensors, 202 M params) through paper_2310_07147_b200.checkpoint."""
+    import tempfile
+    import time
+    import zlib
+
+    import torch
+    import paper_2310_07147_b200 as q
+    from paper_2310_07147_b200.checkpoint import _crc_device, load_checkpoint, save_checkpoint
+    from paper_2310_07147_b200.shapes import llama2_7b
+    hbm, _ = peaks()
+    shapes = llama2_7b()
+    st = build_state(shapes, q, 1234)
+    segs = []
+    for i in range(st.n):
+        rp, col, val = st.strict_csr(i)
+        segs += [st._rows(st.t_min, i), st._rows(st.t_max, i), st._rows(st.w_scale, i),
+                 st._rows(st.w_zp, i), st._sl(st.w_codes[st.cur], i), rp, col, val,
+                 st._rows(st.m_scale[st.cur], i), st._rows(st.m_zp[st.cur], i),
+                 st._sl(st.m_codes[st.cur], i)]
+    nbytes = sum(t.numel() * t.element_size() for t in segs)
+    for _ in range(args.warmup):
+        _crc_device(segs)
+    ts, dev_ms = [], []
+    stream = torch.cuda.current_stream()
+    for _ in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        _crc_device(segs)  # synchronises (chunk fold on the host)
+        e1.record(stream)
+        ts.append(time.perf_counter() - t0)
+        torch.cuda.synchronize()
+        dev_ms.append(e0.elapsed_time(e1))
+    crc_s = statistics.median(ts)
+    sample = torch.randint(0, 256, (256 << 20,), dtype=torch.uint8).numpy().tobytes()
+    t0 = time.perf_counter()
+    zlib.crc32(sample)
+    zlib_gbs = len(sample) / (time.perf_counter() - t0) / 1e9
+    del st, segs
+    torch.cuda.empty_cache()
+    one = shapes[1:10]  # one decoder layer: 2 norms + 7 matrices
+    st1 = build_state(one, q, 77)
+    with tempfile.TemporaryDirectory() as d:
+        path = d + "/layer.qftc"
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        save_checkpoint(st1, path)
+        save_s = time.perf_counter() - t0
+        size = os.path.getsize(path)
+        t0 = time.perf_counter()
+        st2, _ = load_checkpoint(path)
+        torch.cuda.synchronize()
+        load_s = time.perf_counter() - t0
+    print(json.dumps({"config": "QFTC v1 checkpoint, llama2-7b state", "bytes": nbytes,
+                      "gpu_crc_ms": crc_s * 1e3, "gpu_crc_gbs": nbytes / crc_s / 1e9,
+                      "gpu_crc_frac_of_hbm": nbytes / crc_s / 1e9 / hbm,
+                      "gpu_crc_device_ms": statistics.median(dev_ms),
+                      "host_zlib_crc_gbs_1core": zlib_gbs,
+                      "save_load_sample": f"{len(one)} tensors, {st1.param_count} params, "
+                                          f"{size} bytes", "save_s": save_s, "load_s": load_s,
+                      "timing": "wall clock around synchronous calls (median of steps)"}),
+          flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
-    ap.add_argument("--mode", default="step", choices=["step", "sweep", "13b"])
+    ap.add_argument("--mode", default="step", choices=["step", "sweep", "13b", "ckpt"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--zero1", action="store_true",
@@ -596,6 +665,8 @@ def main():
         run_sweep(args)
     elif args.mode == "13b":
         run_13b_dequant(args)
+    elif args.mode == "ckpt":
+        run_ckpt(args)
     else:
         run_gpu_arm(args)
 

@@ -239,6 +239,15 @@ int qftc_expand(const qftc_expand_tensor* tensors, int n_tensors, int bf16,
 int qftc_lion_apply(float* w, float* m, const float* g, int64_t n, qftc_lion_hyper hyper,
                     qftc_stream_t stream);
 
+/* ---------------------------------------------------------------- checkpoint CRC */
+
+/* The QFTC v1 checkpoint checksum (checkpoint.cpp:20-33: CRC-32, reflected polynomial
+ * 0xEDB88320, preset 0xFFFFFFFF, final complement) of the concatenation of n DEVICE
+ * byte segments, computed on the GPU (save_checkpoint appends it, load_checkpoint
+ * verifies it, checkpoint.cpp:134/:151-154).  Synchronises; *crc_out on the host. */
+int qftc_crc32(const void* const* segments, const int64_t* lengths, int n, uint32_t* crc_out,
+               qftc_stream_t stream);
+
 /* ---------------------------------------------------------------- memory helpers
  * For FFI hosts (ctypes / cgo / JNI / pybind) that have no CUDA runtime of their
  * own: device allocation and stream-ordered copies. */

@@ -1,0 +1,187 @@
+"""QFTC v1 checkpoints straight from / into the device-resident model state.
+
+Drop-in for ``qft::save_checkpoint`` / ``qft::load_checkpoint`` (checkpoint.cpp:100-211):
+the same byte layout, the same checks in the same order, and the same error texts.
+Files written here are byte-identical to the reference's for the same state
+(tests/golden/ckpt_*.qftc come from the reference itself).
+
+Layout (little-endian): "QFTC", version u16 (1), layer count u16, bit width u8, quant
+mode u8, threshold kind u8, loss u8, one activation u8 per junction, outlier fraction
+f32; per layer: rows u32, cols u32, t_min f32[rows], t_max f32[rows], scale f32[rows],
+zero_point i32[rows], codes u8[rows*cols], nnz u32, row_ptr i32[rows+1], col_idx
+i32[nnz], values f32[nnz], momentum scale f32[rows], zero_point i32[rows], codes
+u8[rows*cols]; then the CRC-32 of everything before it.
+
+B200 side: the state never leaves HBM in pieces the host has to assemble.  The CRC is
+computed on the GPU over the device arrays in file order (``qftc_crc32``).  The arrays
+are streamed device -> pinned host -> file.  On load the whole file is copied to the
+device once and verified there before the state is built.  Pass-through checkpoints
+(raw fp32 weights, ``QuantMode::passthrough``) are outside the quantized path and are
+refused.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import struct
+from dataclasses import dataclass, field
+from typing import List, Optional, Tuple
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .engine import QftModelState
+from .quantize import _stream
+
+MAGIC = b"QFTC"
+VERSION = 1
+AFFINE, PASSTHROUGH = 0, 1
+
+
+@dataclass
+class CheckpointMeta:
+    """The ModelConfig fields a checkpoint records (checkpoint.cpp:106-114)."""
+    bit_width: int = 8
+    quant_mode: int = AFFINE
+    threshold_kind: int = 0          # ThresholdKind: 0 percentile, 1 range_fraction
+    loss: int = 0                    # LossKind: 0 mse, 1 softmax_cross_entropy
+    junctions: Optional[List[int]] = None   # Activation per junction; None: relu (1) everywhere
+    outlier_fraction: float = 0.01
+    layer_dims: List[int] = field(default_factory=list)
+
+
+def _crc_device(segments: List[torch.Tensor]) -> int:
+    ptrs = (C.c_void_p * max(len(segments), 1))(*[t.data_ptr() for t in segments])
+    lens = (C.c_int64 * max(len(segments), 1))(*[t.numel() * t.element_size()
+                                                   for t in segments])
+    out = C.c_uint32(0)
+    N.check(N.lib.qftc_crc32(ptrs, lens, len(segments), C.byref(out), _stream()))
+    return int(out.value)
+
+
+def _dev_bytes(b: bytes, device) -> torch.Tensor:
+    return torch.frombuffer(bytearray(b), dtype=torch.uint8).to(device)
+
+
+def save_checkpoint(state: QftModelState, path: str, meta: Optional[CheckpointMeta] = None):
+    """save_checkpoint(model, state, path) (checkpoint.cpp:100-140) for the whole
+    device-resident state: layer l of the file is tensor l of ``state``."""
+    meta = meta or CheckpointMeta(bit_width=state.bit_width)
+    if meta.quant_mode != AFFINE:
+        raise NotImplementedError("pass-through checkpoints are outside the quantized path")
+    L = state.n
+    junc = meta.junctions if meta.junctions is not None else [1] * max(L - 1, 0)
+    if len(junc) != max(L - 1, 0):
+        raise ValueError("junction count must be num_layers - 1")
+    head = MAGIC + struct.pack("<HHBBBB", VERSION, L, state.bit_width, meta.quant_mode,
+                               meta.threshold_kind, meta.loss)
+    head += bytes(junc) + struct.pack("<f", meta.outlier_fraction)
+    dev = state.device
+    cur = state.cur
+    segs: List[torch.Tensor] = [_dev_bytes(head, dev)]
+    for i in range(L):
+        r, c = state.shapes[i]
+        rp, col, val = state.strict_csr(i)
+        segs += [_dev_bytes(struct.pack("<II", r, c), dev),
+                 state._rows(state.t_min, i), state._rows(state.t_max, i),
+                 state._rows(state.w_scale, i), state._rows(state.w_zp, i),
+                 state._sl(state.w_codes[cur], i),
+                 _dev_bytes(struct.pack("<I", col.numel()), dev), rp, col, val,
+                 state._rows(state.m_scale[cur], i), state._rows(state.m_zp[cur], i),
+                 state._sl(state.m_codes[cur], i)]
+    crc = _crc_device(segs)
+    try:
+        f = open(path, "wb")
+    except OSError:
+        raise RuntimeError(f"cannot open '{path}' for writing") from None
+    with f:
+        for t in segs:
+            if t.numel():
+                f.write(t.contiguous().view(torch.uint8).cpu().numpy().data)
+        f.write(struct.pack("<I", crc))
+
+
+class _Reader:
+    """checkpoint.cpp:54-78: bounds-checked little-endian reads."""
+
+    def __init__(self, buf: np.ndarray, start: int, end: int, path: str):
+        self.buf, self.p, self.end, self.path = buf, start, end, path
+
+    def _take(self, n: int) -> int:
+        if self.p + n > self.end:
+            raise RuntimeError(f"checkpoint '{self.path}' is truncated")
+        p = self.p
+        self.p += n
+        return p
+
+    def get(self, fmt: str):
+        n = struct.calcsize(fmt)
+        return struct.unpack_from(fmt, self.buf, self._take(n))[0]
+
+    def array(self, dtype, n: int) -> np.ndarray:
+        dt = np.dtype(dtype)
+        p = self._take(n * dt.itemsize)
+        a = self.buf[p:p + n * dt.itemsize].view(dt)
+        return a if p % dt.itemsize == 0 else a.copy()  # fields are packed, not aligned
+
+
+def load_checkpoint(path: str, device="cuda") -> Tuple[QftModelState, CheckpointMeta]:
+    """load_checkpoint(path) (checkpoint.cpp:142-211): the same checks, in the same
+    order, with the same messages; returns the device-resident state and the config
+    fields the file records."""
+    try:
+        buf = np.fromfile(path, dtype=np.uint8)
+    except OSError:
+        raise RuntimeError(f"cannot open checkpoint '{path}'") from None
+    if buf.size < 4 + 4:
+        raise RuntimeError(f"checkpoint '{path}' is truncated")
+    if bytes(buf[:4]) != MAGIC:
+        raise RuntimeError(f"'{path}' is not a checkpoint (bad magic)")
+    stored = struct.unpack_from("<I", buf, buf.size - 4)[0]
+    body = torch.from_numpy(buf[:-4]).to(device)  # verified where the state will live
+    if _crc_device([body]) != stored:
+        raise RuntimeError(f"checkpoint '{path}' is corrupt (crc mismatch)")
+    del body
+    r = _Reader(buf, 4, buf.size - 4, path)
+    version = r.get("<H")
+    if version != VERSION:
+        raise RuntimeError(f"checkpoint '{path}' has unsupported version {version}")
+    L = r.get("<H")
+    if L == 0:
+        raise RuntimeError(f"checkpoint '{path}' has no layers")
+    meta = CheckpointMeta()
+    meta.bit_width = r.get("<B")
+    meta.quant_mode = r.get("<B")
+    meta.threshold_kind = r.get("<B")
+    meta.loss = r.get("<B")
+    meta.junctions = [r.get("<B") for _ in range(L - 1)]
+    meta.outlier_fraction = float(r.get("<f"))
+    if meta.quant_mode != AFFINE:
+        raise NotImplementedError("pass-through checkpoints are outside the quantized path")
+    shapes, tensors = [], []
+    for li in range(L):
+        rows, cols = r.get("<I"), r.get("<I")
+        if not (0 < rows < 2 ** 31 and 0 < cols < 2 ** 31):  # static_cast<int> > 0
+            raise RuntimeError(f"checkpoint '{path}' has an empty layer")
+        t = dict(t_min=r.array(np.float32, rows), t_max=r.array(np.float32, rows),
+                 scale=r.array(np.float32, rows), zero_point=r.array(np.int32, rows),
+                 codes=r.array(np.uint8, rows * cols).reshape(rows, cols))
+        nnz = r.get("<I")
+        t["row_ptr"] = r.array(np.int32, rows + 1)
+        t["col_idx"] = r.array(np.int32, nnz)
+        t["values"] = r.array(np.float32, nnz)
+        if int(t["row_ptr"][-1]) != nnz:
+            raise RuntimeError(f"checkpoint '{path}' has inconsistent sparse layout")
+        t["m_scale"] = r.array(np.float32, rows)
+        t["m_zero_point"] = r.array(np.int32, rows)
+        t["m_codes"] = r.array(np.uint8, rows * cols).reshape(rows, cols)
+        if li == 0:
+            meta.layer_dims.append(cols)
+        meta.layer_dims.append(rows)
+        shapes.append((rows, cols))
+        tensors.append(t)
+    if r.p != r.end:
+        raise RuntimeError(f"checkpoint '{path}' has trailing bytes")
+    st = QftModelState(shapes, bit_width=meta.bit_width, device=device)
+    st.init_from_host(tensors)
+    return st, meta

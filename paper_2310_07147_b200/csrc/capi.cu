@@ -706,6 +706,18 @@ int qftc_lion_apply(float* w, float* m, const float* g, int64_t n, qftc_lion_hyp
   return QFTC_OK;
 }
 
+int qftc_crc32(const void* const* segments, const int64_t* lengths, int n, uint32_t* crc_out,
+               qftc_stream_t stream) {
+  if (!crc_out || n < 0 || (n > 0 && (!segments || !lengths)))
+    return fail(QFTC_EINVAL, "crc32: bad arguments");
+  for (int i = 0; i < n; ++i)
+    if (lengths[i] < 0 || (lengths[i] > 0 && !segments[i]))
+      return fail(QFTC_EINVAL, "crc32: bad segment " + std::to_string(i));
+  if (int rc = require_device()) return rc;
+  QFTC_CUDA(crc32_device(segments, lengths, n, crc_out, (cudaStream_t)stream), "crc32");
+  return QFTC_OK;
+}
+
 int qftc_device_alloc(void** ptr, size_t bytes) {
   if (!ptr) return fail(QFTC_EINVAL, "device_alloc: null out pointer");
   if (int rc = require_device()) return rc;

@@ -144,6 +144,10 @@ cudaError_t decompose_csr(const float* w, int rows, int cols, const float* t_min
                           float* values, cudaStream_t s);
 cudaError_t csr_row_ptr(const int32_t* counts, int rows, int32_t* row_ptr, cudaStream_t s);
 
+// checkpoint CRC over device segments (crc32.cu); synchronises
+cudaError_t crc32_device(const void* const* segs, const int64_t* lens, int n, uint32_t* crc_out,
+                         cudaStream_t s);
+
 // weight expansion (expand.cu): one launch per expand_max_tensors() tensors
 int expand_max_tensors();
 cudaError_t launch_expand(const qftc_expand_tensor* ts, int n, bool bf16, cudaStream_t s);

@@ -437,9 +437,10 @@ class QftModelState:
         k = self.cur if k is None else k
         return int(sum(self._rows(self.row_count[k], i).sum().item() for i in g.members))
 
-    def export_tensor(self, i: int) -> dict:
-        """Reference-layout host copy of tensor i (DenseSparseWeight + momentum); the
-        slotted CSR is compacted into the strict one on the device."""
+    def strict_csr(self, i: int):
+        """Tensor i's outliers as the reference's strict CSR (SparseOutliers,
+        quantize.hpp:48-57), compacted from the slotted CSR on the device:
+        (row_ptr [rows+1], col_idx [nnz], values [nnz]) device tensors."""
         cur = self.cur
         g = self.groups[self.group_of[i]]
         r = self.shapes[i][0]
@@ -451,6 +452,14 @@ class QftModelState:
         N.check(N.lib.qftc_csr_compact(r, _p(self._rs(self.row_start[cur], i)), _p(cnt),
                                        _p(g.col[cur]), _p(g.val[cur]), _p(rp), _p(col), _p(val),
                                        col.numel(), C.byref(nnz), _stream()))
+        return rp, col[:n], val[:n]
+
+    def export_tensor(self, i: int) -> dict:
+        """Reference-layout host copy of tensor i (DenseSparseWeight + momentum); the
+        slotted CSR is compacted into the strict one on the device."""
+        cur = self.cur
+        rp, col, val = self.strict_csr(i)
+        n = col.numel()
         return dict(
             codes=self._sl(self.w_codes[cur], i).cpu().numpy(),
             scale=self._rows(self.w_scale, i).cpu().numpy(),
