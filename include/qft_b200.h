@@ -77,6 +77,16 @@ int qftc_quantize(const float* x, int rows, int cols, const float* scale,
 int qftc_quantize_state(const float* x, int rows, int cols, int bit_width, uint8_t* codes,
                         float* scale, int32_t* zero_point, int check, qftc_stream_t stream);
 
+/* accumulate (gradflow.hpp:52-58): the integer-form micro-batch gradient sum,
+ * quantize_state(dequantize(acc) + g_new) with fresh per-row params and acc's bit
+ * width, fused in one row kernel (the fp32 sum never reaches HBM).  May run in place
+ * (codes_out == codes, ...).  Synchronises; a NaN in column 0 of the sum ->
+ * QFTC_EINVAL (the reference's min > max). */
+int qftc_accumulate_state(const uint8_t* codes, const float* scale, const int32_t* zero_point,
+                          int rows, int cols, int bit_width, const float* g_new,
+                          uint8_t* codes_out, float* scale_out, int32_t* zero_point_out,
+                          qftc_stream_t stream);
+
 /* dequantize  (quantize.hpp:195-212) -> f32, and the bf16 expansion (RNE of the f32) */
 int qftc_dequantize(const uint8_t* codes, int rows, int cols, const float* scale,
                     const int32_t* zero_point, int channels, float* out, qftc_stream_t stream);

@@ -100,6 +100,7 @@ class Oracle:
         self._quantize = fn("quantize", _i, [_vp, _i, _i, _vp, _vp, _i, _i, _vp])
         self._qstate = fn("quantize_state", _i, [_vp, _i, _i, _i, _vp, _vp, _vp])
         self._dequant = fn("dequantize", _i, [_vp, _i, _i, _vp, _vp, _i, _vp])
+        self._accum = fn("accumulate", _i, [_vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp])
         self._thresh = fn("outlier_thresholds", _i, [_vp, _i, _i, _d, _i, _vp, _vp])
         self._dds = fn("decompose_dense_sparse", _i64,
                        [_vp, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i64])
@@ -184,6 +185,20 @@ class Oracle:
         self._check(self._dequant(_ptr(codes), r, c, _ptr(scale), _ptr(zero_point), scale.size,
                                   _ptr(out)))
         return out
+
+    def accumulate(self, codes, scale, zero_point, g, bit_width=8):
+        """gradflow.hpp:52-58 -> (codes, scale, zero_point) of the new running sum."""
+        codes = np.ascontiguousarray(codes, np.uint8)
+        scale = np.ascontiguousarray(scale, np.float32)
+        zero_point = np.ascontiguousarray(zero_point, np.int32)
+        g = np.ascontiguousarray(g, np.float32)
+        r, c = codes.shape
+        q = np.empty((r, c), np.uint8)
+        s = np.empty(r, np.float32)
+        z = np.empty(r, np.int32)
+        self._check(self._accum(_ptr(codes), _ptr(scale), _ptr(zero_point), r, c, bit_width,
+                                _ptr(g), _ptr(q), _ptr(s), _ptr(z)))
+        return q, s, z
 
     def outlier_thresholds(self, w, fraction, kind=PERCENTILE):
         w = np.ascontiguousarray(w, np.float32)

@@ -156,6 +156,24 @@ int qo_dequantize(const uint8_t* codes, int rows, int cols, const float* scale,
   return 0;
 }
 
+/* accumulate (gradflow.hpp:52-58): quantize_state(dequantize(acc) + g_new) with the
+ * accumulator's bit width; the sum is fp32 (tensor add, one rounding per element). */
+int qo_accumulate(const uint8_t* codes, const float* scale, const int32_t* zp, int rows,
+                  int cols, int bit_width, const float* g, uint8_t* codes_out,
+                  float* scale_out, int32_t* zp_out) {
+  if (rows <= 0 || cols <= 0) return fail(QO_EINVAL, "accumulate: empty tensor");
+  const size_t n = (size_t)rows * (size_t)cols;
+  float* sum = (float*)malloc(n * sizeof(float));
+  if (!sum) return fail(QO_EINVAL, "accumulate: out of memory");
+  int rc = qo_dequantize(codes, rows, cols, scale, zp, rows, sum);
+  if (!rc) {
+    for (size_t i = 0; i < n; ++i) sum[i] = sum[i] + g[i];
+    rc = qo_quantize_state(sum, rows, cols, bit_width, codes_out, scale_out, zp_out);
+  }
+  free(sum);
+  return rc;
+}
+
 /* ------------------------------------------------------------------------ */
 /* L1: outlier thresholds                    quantize.hpp:76-87, 216-247     */
 /* ------------------------------------------------------------------------ */

@@ -159,6 +159,26 @@ int qr_quantize_state(const float* x, int rows, int cols, int bit_width, uint8_t
   }));
 }
 
+int qr_accumulate(const uint8_t* codes, const float* scale, const int32_t* zp, int rows,
+                  int cols, int bit_width, const float* g, uint8_t* codes_out,
+                  float* scale_out, int32_t* zp_out) {
+  return static_cast<int>(guarded([&] {
+    qft::QuantizedTensor<float> acc;
+    acc.rows = rows;
+    acc.cols = cols;
+    acc.mode = qft::QuantMode::affine;
+    acc.params.bit_width = bit_width;
+    acc.params.scale.assign(scale, scale + rows);
+    acc.params.zero_point.assign(zp, zp + rows);
+    acc.data.assign(codes, codes + (size_t)rows * cols);
+    auto q = qft::accumulate(acc, to_tensor(g, rows, cols));
+    std::memcpy(codes_out, q.data.data(), q.data.size());
+    std::copy(q.params.scale.begin(), q.params.scale.end(), scale_out);
+    std::copy(q.params.zero_point.begin(), q.params.zero_point.end(), zp_out);
+    return int64_t{0};
+  }));
+}
+
 int qr_dequantize(const uint8_t* codes, int rows, int cols, const float* scale, const int32_t* zp,
                   int channels, float* out) {
   return static_cast<int>(guarded([&] {

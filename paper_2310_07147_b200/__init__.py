@@ -8,6 +8,7 @@ fails loudly when the CUDA library has not been built: there is no CPU path.
 from . import _native  # noqa: F401  (raises ImportError if the .so is missing)
 from .engine import QftModelState
 from .quantize import (AffineParams, DenseSparseWeight, GradientStack, LionHyper, LionState,
+                       accumulate,
                        QuantizedTensor, SparseOutliers, affine_params_from_bounds, byte_size,
                        channel_minmax, compute_affine_params, compute_outlier_thresholds,
                        decompose_dense_sparse, decompose_weight, dequantize, lion_apply,
@@ -15,7 +16,7 @@ from .quantize import (AffineParams, DenseSparseWeight, GradientStack, LionHyper
                        requantize_weight, synth)
 
 __all__ = [
-    "QftModelState", "AffineParams", "DenseSparseWeight", "GradientStack", "LionHyper",
+    "QftModelState", "accumulate", "AffineParams", "DenseSparseWeight", "GradientStack", "LionHyper",
     "LionState", "QuantizedTensor", "SparseOutliers", "affine_params_from_bounds", "byte_size",
     "channel_minmax", "compute_affine_params", "compute_outlier_thresholds",
     "decompose_dense_sparse", "decompose_weight", "dequantize", "lion_apply",

@@ -87,6 +87,7 @@ _SIGS = {
     "qftc_plan_result": (_i, [_vp, C.POINTER(_i64), _vp]),
     "qftc_plan_launches": (_i, [_vp]),
     "qftc_crc32": (_i, [_vp, _vp, _i, _vp, _vp]),
+    "qftc_accumulate_state": (_i, [_vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "qftc_plan_destroy": (_i, [_vp]),
     "qftc_lion_step": (_i, [_i, _i, _i] + [_vp] * 21 + [_i64, LionHyperC, C.POINTER(_i64), _vp]),
     "qftc_lion_apply": (_i, [_vp, _vp, _vp, _i64, LionHyperC, _vp]),

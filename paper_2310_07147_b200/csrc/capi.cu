@@ -18,6 +18,9 @@ namespace qftk {
 cudaError_t launch_channel_minmax(const float*, int, int, float*, float*, cudaStream_t);
 cudaError_t launch_affine_params(const float*, const float*, int64_t, int, float*, int32_t*,
                                  uint32_t*, cudaStream_t);
+cudaError_t launch_accumulate_state(const uint8_t*, const float*, const int32_t*, int, int, int,
+                                    const float*, uint8_t*, float*, int32_t*, uint32_t*,
+                                    cudaStream_t);
 cudaError_t launch_quantize_state(const float*, int, int, int, uint8_t*, float*, int32_t*,
                                   uint32_t*, cudaStream_t);
 cudaError_t launch_quantize(const float*, int, int, const float*, const int32_t*, int, int,
@@ -224,6 +227,30 @@ int qftc_quantize_state(const float* x, int rows, int cols, int bit_width, uint8
     QFTC_CUDA(cudaStreamSynchronize(st), "sync");
     if (h) return fail(QFTC_EINVAL, "affine_params_from_bounds: min > max in a channel");
   }
+  return QFTC_OK;
+}
+
+int qftc_accumulate_state(const uint8_t* codes, const float* scale, const int32_t* zero_point,
+                          int rows, int cols, int bit_width, const float* g_new,
+                          uint8_t* codes_out, float* scale_out, int32_t* zero_point_out,
+                          qftc_stream_t stream) {
+  if (int rc = require_shape(rows, cols, "accumulate")) return rc;
+  if (int rc = require_bit_width(bit_width)) return rc;
+  if (!codes || !scale || !zero_point || !g_new || !codes_out || !scale_out || !zero_point_out)
+    return fail(QFTC_EINVAL, "accumulate: null pointer");
+  if (int rc = require_device()) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* err = nullptr;
+  QFTC_CUDA(cudaMallocAsync((void**)&err, 4, st), "cudaMallocAsync");
+  QFTC_CUDA(cudaMemsetAsync(err, 0, 4, st), "memset");
+  QFTC_CUDA(launch_accumulate_state(codes, scale, zero_point, rows, cols, bit_width, g_new,
+                                    codes_out, scale_out, zero_point_out, err, st),
+            "accumulate");
+  uint32_t h = 0;
+  QFTC_CUDA(cudaMemcpyAsync(&h, err, 4, cudaMemcpyDeviceToHost, st), "copy");
+  QFTC_CUDA(cudaFreeAsync(err, st), "free");
+  QFTC_CUDA(cudaStreamSynchronize(st), "sync");
+  if (h) return fail(QFTC_EINVAL, "affine_params_from_bounds: min > max in a channel");
   return QFTC_OK;
 }
 

@@ -145,6 +145,78 @@ __global__ void __launch_bounds__(RT) k_quantize_state(const float* __restrict__
   }
 }
 
+// accumulate (gradflow.hpp:52-58): the micro-batch running sum kept in integer form,
+// sum = dequantize(acc) + g_new in fp32 (quantize.hpp:195-212, then tensor add), then
+// quantize_state(sum) with fresh per-row params.  Fused: the sum never exists in HBM
+// (pass 1: bounds; pass 2: recomputed from the L2-resident row and quantized).  The
+// old params are read before the block barrier, so the update may be in place.
+__device__ __forceinline__ float acc_sum(const uint8_t* c, const float* g, int i,
+                                         const DequantRow& d) {
+  return __fadd_rn(dequant_exact(c[i], d.s, d.z), g[i]);
+}
+__global__ void __launch_bounds__(RT) k_accumulate_state(
+    const uint8_t* codes, const float* scale, const int32_t* zp, int rows, int cols, int bw,
+    const float* __restrict__ g, int vec4, uint8_t* codes_out, float* scale_out,
+    int32_t* zp_out, uint32_t* err) {
+  __shared__ float red[64];
+  for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+    const DequantRow d = make_dequant_row(scale[r], zp[r]);
+    const uint8_t* cr = codes + (size_t)r * cols;
+    const float* gr = g + (size_t)r * cols;
+    float lo = __int_as_float(0x7f800000), hi = __int_as_float(0xff800000);
+    if (vec4) {
+      for (int i = threadIdx.x; i < cols / 4; i += RT) {
+        float v[4];
+        dequant4(reinterpret_cast<const uint32_t*>(cr)[i], d, v);
+        const float4 f = reinterpret_cast<const float4*>(gr)[i];
+        v[0] = __fadd_rn(v[0], f.x); v[1] = __fadd_rn(v[1], f.y);
+        v[2] = __fadd_rn(v[2], f.z); v[3] = __fadd_rn(v[3], f.w);
+        float t;
+        asm("min.f32 %0, %1, %2, %3;" : "=f"(t) : "f"(lo), "f"(v[0]), "f"(v[1])); lo = t;
+        asm("min.f32 %0, %1, %2, %3;" : "=f"(t) : "f"(lo), "f"(v[2]), "f"(v[3])); lo = t;
+        asm("max.f32 %0, %1, %2, %3;" : "=f"(t) : "f"(hi), "f"(v[0]), "f"(v[1])); hi = t;
+        asm("max.f32 %0, %1, %2, %3;" : "=f"(t) : "f"(hi), "f"(v[2]), "f"(v[3])); hi = t;
+      }
+    } else {
+      for (int i = threadIdx.x; i < cols; i += RT) {
+        const float v = acc_sum(cr, gr, i, d);
+        lo = fminf(lo, v);
+        hi = fmaxf(hi, v);
+      }
+    }
+    const float v0 = acc_sum(cr, gr, 0, d);  // read before the barrier (in-place safe)
+    block_minmax(lo, hi, red);  // (barrier: every thread has read the old params)
+    if (isnan(v0)) lo = hi = v0;  // channel_minmax: a NaN in column 0 sticks
+    float s;
+    int32_t z;
+    if (!affine_from_bounds(lo, hi, bw, s, z)) {
+      if (threadIdx.x == 0) atomicOr(err, 1u);
+      s = 1.0f;
+      z = 0;
+    }
+    const QuantRow q = make_quant_row(s, z, bw);
+    uint8_t* out = codes_out + (size_t)r * cols;
+    if (vec4) {
+      for (int i = threadIdx.x; i < cols / 4; i += RT) {
+        float v[4];
+        dequant4(reinterpret_cast<const uint32_t*>(cr)[i], d, v);
+        const float4 f = reinterpret_cast<const float4*>(gr)[i];
+        v[0] = __fadd_rn(v[0], f.x); v[1] = __fadd_rn(v[1], f.y);
+        v[2] = __fadd_rn(v[2], f.z); v[3] = __fadd_rn(v[3], f.w);
+        reinterpret_cast<uint32_t*>(out)[i] = quant4(v, q);
+      }
+    } else {
+      for (int i = threadIdx.x; i < cols; i += RT)
+        out[i] = (uint8_t)quant_exact(acc_sum(cr, gr, i, d), q.s, q.z, q.qmax);
+    }
+    __syncthreads();  // the next row's barrier-free reads vs this row's param write
+    if (threadIdx.x == 0) {
+      scale_out[r] = s;
+      zp_out[r] = z;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(RT) k_quantize(const float* __restrict__ x, int rows, int cols,
                                                  const float* scale, const int32_t* zp,
                                                  int channels, int bw, int vec4,
@@ -388,6 +460,15 @@ cudaError_t launch_quantize_state(const float* x, int rows, int cols, int bw, ui
                                   float* scale, int32_t* zp, uint32_t* err, cudaStream_t s) {
   const int v4 = vec4_ok(x, cols) && al16(codes);
   k_quantize_state<<<row_grid(rows), RT, 0, s>>>(x, rows, cols, bw, v4, codes, scale, zp, err);
+  return cudaGetLastError();
+}
+cudaError_t launch_accumulate_state(const uint8_t* codes, const float* scale, const int32_t* zp,
+                                    int rows, int cols, int bw, const float* g,
+                                    uint8_t* codes_out, float* scale_out, int32_t* zp_out,
+                                    uint32_t* err, cudaStream_t s) {
+  const int v4 = (cols % 4 == 0) && vec4_ok(g, cols) && al16(codes) && al16(codes_out);
+  k_accumulate_state<<<row_grid(rows), RT, 0, s>>>(codes, scale, zp, rows, cols, bw, g, v4,
+                                                   codes_out, scale_out, zp_out, err);
   return cudaGetLastError();
 }
 cudaError_t launch_quantize(const float* x, int rows, int cols, const float* scale,

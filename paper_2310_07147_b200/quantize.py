@@ -310,6 +310,32 @@ class GradientStack:
     def empty(self) -> bool:
         return not self._entries
 
+    def at(self, i: int) -> StackEntry:
+        """gradflow.hpp:40-43 (bounds-checked)."""
+        if i < 0 or i >= len(self._entries):
+            raise IndexError("gradient stack: index out of range")
+        return self._entries[i]
+
+
+def accumulate(acc: QuantizedTensor, g_new, out: Optional[QuantizedTensor] = None
+               ) -> QuantizedTensor:
+    """gradflow.hpp:52-58: the integer-form micro-batch running sum,
+    quantize_state(dequantize(acc) + g_new) with fresh per-row params, in one fused row
+    kernel.  ``out`` may be ``acc`` itself (in-place update of the stack entry)."""
+    g = _dev(g_new)
+    if acc.rows != g.shape[0] or acc.cols != g.shape[1]:
+        raise ValueError("accumulate: shape mismatch")
+    if out is None:
+        out = QuantizedTensor(acc.rows, acc.cols, torch.empty_like(acc.data),
+                              AffineParams(torch.empty_like(acc.params.scale),
+                                           torch.empty_like(acc.params.zero_point),
+                                           acc.params.bit_width))
+    N.check(N.lib.qftc_accumulate_state(
+        _p(acc.data), _p(acc.params.scale), _p(acc.params.zero_point), acc.rows, acc.cols,
+        acc.params.bit_width, _p(g), _p(out.data), _p(out.params.scale),
+        _p(out.params.zero_point), _stream()))
+    return out
+
 
 @dataclass
 class LionState:

@@ -662,3 +662,36 @@ def test_full_size_7b_tensors_sampled_rows(cuda, port, lr):
         codes = np.asarray(got["codes"])
         assert np.array_equal(codes[row_of, col], np.clip(zp, 0, qmax)), tag + " payload code"
         del got
+
+
+@pytest.mark.parametrize("bw", [3, 4, 8])
+@pytest.mark.parametrize("shape", [(40, 300), (17, 101), (64, 4096)])
+@pytest.mark.parametrize("inplace", [False, True])
+def test_accumulate_microbatches(cuda, port, bw, shape, inplace):
+    """gradflow.hpp:52-58 on the device (fused dequant + add + quantize_state, one row
+    kernel), three micro-batches chained, byte-compared with the oracle (itself pinned
+    to qft::accumulate in test_oracle.py); in place like the stack entry update."""
+    from test_oracle import _acc_inputs
+    acc, g = _acc_inputs(port, bw, 5 + shape[1], shape)
+    q = cuda.QuantizedTensor(shape[0], shape[1], torch.from_numpy(acc[0]).cuda(),
+                             cuda.AffineParams(torch.from_numpy(acc[1]).cuda(),
+                                               torch.from_numpy(acc[2]).cuda(), bw))
+    ref = acc
+    for k in range(3):
+        gk = (g * (k + 1)).astype(np.float32)
+        q = cuda.accumulate(q, torch.from_numpy(gk).cuda(), out=q if inplace else None)
+        ref = port.accumulate(*ref, gk, bw)
+        _eq(_np(q.data), ref[0], f"micro-batch {k} codes")
+        _eq(_np(q.params.scale), ref[1], f"micro-batch {k} scale")
+        _eq(_np(q.params.zero_point), ref[2], f"micro-batch {k} zero_point")
+
+
+def test_accumulate_nan_column0_raises(cuda, port):
+    from test_oracle import _acc_inputs
+    acc, g = _acc_inputs(port, 8, 3)
+    g[7, 0] = np.nan
+    q = cuda.QuantizedTensor(40, 300, torch.from_numpy(acc[0]).cuda(),
+                             cuda.AffineParams(torch.from_numpy(acc[1]).cuda(),
+                                               torch.from_numpy(acc[2]).cuda(), 8))
+    with pytest.raises(ValueError, match="min > max"):
+        cuda.accumulate(q, torch.from_numpy(g).cuda())
