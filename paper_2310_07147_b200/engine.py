@@ -131,6 +131,25 @@ class QftModelState:
             return self._sl(self.g_raw, i)
         return self._sl(self.g_codes, i), self._rows(self.g_scale, i), self._rows(self.g_zp, i)
 
+    def sink_grad(self, i: int, g: torch.Tensor, accumulate: bool = False):
+        """The backward's gradient sink for tensor i (gradflow.hpp:70-84), u8 kind: the
+        first micro-batch quantizes its fp32 gradient into the stack entry
+        (quantize_state, :77); later ones fold into it in integer form (accumulate,
+        :52-58, one fused row kernel, in place)."""
+        if self.grad_kind != N.GRAD_U8:
+            raise ValueError("sink_grad: the engine keeps raw gradients (grad kind f32/bf16)")
+        r, c = self.shapes[i]
+        g = g.contiguous()
+        if g.dtype != torch.float32 or tuple(g.shape) != (r, c):
+            raise ValueError("sink_grad: expected a float32 gradient of the tensor's shape")
+        codes, s, z = self.grad_views(i)
+        if accumulate:
+            N.check(N.lib.qftc_accumulate_state(_p(codes), _p(s), _p(z), r, c, self.bit_width,
+                                                _p(g), _p(codes), _p(s), _p(z), _stream()))
+        else:
+            N.check(N.lib.qftc_quantize_state(_p(g), r, c, self.bit_width, _p(codes), _p(s),
+                                              _p(z), 1, _stream()))
+
     # ------------------------------------------------------------------ arenas / slots
     def _alloc(self, cap: int):
         return (torch.empty(max(cap, 4), dtype=torch.int32, device=self.device),

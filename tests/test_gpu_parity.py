@@ -695,3 +695,35 @@ def test_accumulate_nan_column0_raises(cuda, port):
                                                torch.from_numpy(acc[2]).cuda(), 8))
     with pytest.raises(ValueError, match="min > max"):
         cuda.accumulate(q, torch.from_numpy(g).cuda())
+
+
+def test_engine_microbatch_sink_then_step(cuda, port):
+    """Three micro-batches sunk into the engine's gradient entries (quantize_state, then
+    accumulate in integer form, gradflow.hpp:70-84), then the grouped step; against the
+    oracle doing the same per layer (sink + lion_step_layer)."""
+    shapes = [(32, 4096), (1, 4096), (48, 1024)]
+    bw, frac, lr = 8, 0.01, 1e-3
+    eng = cuda.QftModelState(shapes, bit_width=bw)
+    eng.init_from_weights(lambda i: cuda.synth(shapes[i], 600 + i, 0.02, 0.005), frac)
+    ora = []
+    for i, sh in enumerate(shapes):
+        w = port.synth(sh, 600 + i, 0.02, 0.005)
+        ora.append([port.decompose_weight(w, frac, bw),
+                    port.quantize_state(np.zeros(sh, np.float32), bw)])
+    for i, sh in enumerate(shapes):
+        gq = None
+        for mb in range(3):
+            g = port.synth(sh, 7000 + 10 * i + mb, 1e-2, 0.0) / np.float32(3.0)
+            eng.sink_grad(i, torch.from_numpy(g).cuda(), accumulate=mb > 0)
+            gq = port.quantize_state(g, bw) if mb == 0 else port.accumulate(*gq, g, bw)
+        d, m = ora[i]
+        ora[i] = list(port.lion_step_layer(d, *m, *gq, lr=lr)[:2])
+    eng.step(lr=lr, check=True)
+    for i in range(len(shapes)):
+        got = eng.export_tensor(i)
+        d, m = ora[i]
+        _eq(got["codes"], d.codes, f"tensor {i} w codes")
+        _eq(got["col_idx"], d.col_idx, f"tensor {i} col_idx")
+        _eq(got["values"], d.values, f"tensor {i} values")
+        _eq(got["m_codes"], m[0], f"tensor {i} m codes")
+        _eq(got["m_scale"], m[1], f"tensor {i} m scale")
