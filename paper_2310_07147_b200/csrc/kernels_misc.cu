@@ -156,21 +156,24 @@ __device__ __forceinline__ float acc_sum(const uint8_t* c, const float* g, int i
 }
 __global__ void __launch_bounds__(RT) k_accumulate_state(
     const uint8_t* codes, const float* scale, const int32_t* zp, int rows, int cols, int bw,
-    const float* __restrict__ g, int vec4, uint8_t* codes_out, float* scale_out,
+    const float* __restrict__ g, int vec4, int staged, uint8_t* codes_out, float* scale_out,
     int32_t* zp_out, uint32_t* err) {
   __shared__ float red[64];
+  extern __shared__ float4 sums[];  // staged: the row's fp32 sums between the passes
   for (int r = blockIdx.x; r < rows; r += gridDim.x) {
     const DequantRow d = make_dequant_row(scale[r], zp[r]);
     const uint8_t* cr = codes + (size_t)r * cols;
     const float* gr = g + (size_t)r * cols;
     float lo = __int_as_float(0x7f800000), hi = __int_as_float(0xff800000);
     if (vec4) {
+#pragma unroll 4  // independent row loads in flight (the loop is latency-bound otherwise)
       for (int i = threadIdx.x; i < cols / 4; i += RT) {
         float v[4];
         dequant4(reinterpret_cast<const uint32_t*>(cr)[i], d, v);
         const float4 f = reinterpret_cast<const float4*>(gr)[i];
         v[0] = __fadd_rn(v[0], f.x); v[1] = __fadd_rn(v[1], f.y);
         v[2] = __fadd_rn(v[2], f.z); v[3] = __fadd_rn(v[3], f.w);
+        if (staged) sums[i] = make_float4(v[0], v[1], v[2], v[3]);
         float t;
         asm("min.f32 %0, %1, %2, %3;" : "=f"(t) : "f"(lo), "f"(v[0]), "f"(v[1])); lo = t;
         asm("min.f32 %0, %1, %2, %3;" : "=f"(t) : "f"(lo), "f"(v[2]), "f"(v[3])); lo = t;
@@ -196,7 +199,14 @@ __global__ void __launch_bounds__(RT) k_accumulate_state(
     }
     const QuantRow q = make_quant_row(s, z, bw);
     uint8_t* out = codes_out + (size_t)r * cols;
-    if (vec4) {
+    if (vec4 && staged) {  // each thread re-reads only what it staged itself
+#pragma unroll 4
+      for (int i = threadIdx.x; i < cols / 4; i += RT) {
+        const float4 f = sums[i];
+        const float v[4] = {f.x, f.y, f.z, f.w};
+        reinterpret_cast<uint32_t*>(out)[i] = quant4(v, q);
+      }
+    } else if (vec4) {
       for (int i = threadIdx.x; i < cols / 4; i += RT) {
         float v[4];
         dequant4(reinterpret_cast<const uint32_t*>(cr)[i], d, v);
@@ -467,8 +477,12 @@ cudaError_t launch_accumulate_state(const uint8_t* codes, const float* scale, co
                                     uint8_t* codes_out, float* scale_out, int32_t* zp_out,
                                     uint32_t* err, cudaStream_t s) {
   const int v4 = (cols % 4 == 0) && vec4_ok(g, cols) && al16(codes) && al16(codes_out);
-  k_accumulate_state<<<row_grid(rows), RT, 0, s>>>(codes, scale, zp, rows, cols, bw, g, v4,
-                                                   codes_out, scale_out, zp_out, err);
+  // stage the sums in shared memory when the row fits 48 KB (the second pass then
+  // reads no global memory); wider rows re-read the row from L2
+  const size_t sm = (size_t)cols * 4;
+  const int staged = v4 && sm <= 48 * 1024;
+  k_accumulate_state<<<row_grid(rows), RT, staged ? sm : 0, s>>>(
+      codes, scale, zp, rows, cols, bw, g, v4, staged, codes_out, scale_out, zp_out, err);
   return cudaGetLastError();
 }
 cudaError_t launch_quantize(const float* x, int rows, int cols, const float* scale,
