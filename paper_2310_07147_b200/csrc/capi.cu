@@ -240,17 +240,19 @@ int qftc_accumulate_state(const uint8_t* codes, const float* scale, const int32_
     return fail(QFTC_EINVAL, "accumulate: null pointer");
   if (int rc = require_device()) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  uint32_t* err = nullptr;
-  QFTC_CUDA(cudaMallocAsync((void**)&err, 4, st), "cudaMallocAsync");
-  QFTC_CUDA(cudaMemsetAsync(err, 0, 4, st), "memset");
+  // the error flag lives in pinned host memory the kernel writes directly (no device
+  // allocation, memset or copy per call; the call is one launch + one synchronisation)
+  static thread_local uint32_t* flag = nullptr;
+  if (!flag) QFTC_CUDA(cudaHostAlloc((void**)&flag, 4, cudaHostAllocMapped), "cudaHostAlloc");
+  *flag = 0;
+  uint32_t* dflag = nullptr;
+  QFTC_CUDA(cudaHostGetDevicePointer((void**)&dflag, flag, 0), "cudaHostGetDevicePointer");
   QFTC_CUDA(launch_accumulate_state(codes, scale, zero_point, rows, cols, bit_width, g_new,
-                                    codes_out, scale_out, zero_point_out, err, st),
+                                    codes_out, scale_out, zero_point_out, dflag, st),
             "accumulate");
-  uint32_t h = 0;
-  QFTC_CUDA(cudaMemcpyAsync(&h, err, 4, cudaMemcpyDeviceToHost, st), "copy");
-  QFTC_CUDA(cudaFreeAsync(err, st), "free");
   QFTC_CUDA(cudaStreamSynchronize(st), "sync");
-  if (h) return fail(QFTC_EINVAL, "affine_params_from_bounds: min > max in a channel");
+  if (*(volatile uint32_t*)flag)
+    return fail(QFTC_EINVAL, "affine_params_from_bounds: min > max in a channel");
   return QFTC_OK;
 }
 

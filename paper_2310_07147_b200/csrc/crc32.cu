@@ -66,8 +66,21 @@ __global__ void k_crc32_chunks(const ChunkJob* jobs, int n, ShiftMats mats, uint
     }
     const uint8_t* q = J.p + (int64_t)lane * kLaneBytes;
     uint32_t c = 0;
-    if ((reinterpret_cast<uintptr_t>(q) & 3u) == 0) {
+    if ((reinterpret_cast<uintptr_t>(q) & 15u) == 0) {
+      // 16-byte loads, several in flight (the byte chain itself is short-latency LDS)
+      const uint4* q16 = reinterpret_cast<const uint4*>(q);
+#pragma unroll 4
+      for (int i = 0; i < kLaneBytes / 16; ++i) {
+        const uint4 x = __ldg(q16 + i);
+        const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) c = tab[(c ^ (w[k] >> (8 * b))) & 0xFFu] ^ (c >> 8);
+      }
+    } else if ((reinterpret_cast<uintptr_t>(q) & 3u) == 0) {
       const uint32_t* q4 = reinterpret_cast<const uint32_t*>(q);
+#pragma unroll 8
       for (int i = 0; i < kLaneBytes / 4; ++i) {
         const uint32_t x = __ldg(q4 + i);
 #pragma unroll

@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(RT) k_accumulate_state(
     float s;
     int32_t z;
     if (!affine_from_bounds(lo, hi, bw, s, z)) {
-      if (threadIdx.x == 0) atomicOr(err, 1u);
+      if (threadIdx.x == 0) *(volatile uint32_t*)err = 1u;  // may be mapped host memory
       s = 1.0f;
       z = 0;
     }
