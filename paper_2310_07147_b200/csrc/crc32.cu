@@ -6,8 +6,9 @@
 // core.  The CRC register without preset/complement ("raw") is linear over GF(2):
 //     raw(A || B) = X^(8|B|) * raw(A)  ^  raw(B)
 // where X^(8n) is the 32x32 bit matrix "append n zero bytes".  Each warp takes one
-// 64 KB chunk of a segment, each lane a 2 KB slice (table-driven, byte by byte, table in
-// shared memory); the 32 lane values are folded in a 5-level shuffle tree with the
+// 64 KB chunk of a segment, each lane a 2 KB slice (table-driven, byte by byte; the
+// table is replicated per lane in shared memory so lookups never bank-conflict); the
+// 32 lane values are folded in a 5-level shuffle tree with the
 // shift matrices for 2, 4, 8, 16, 32 KB.  A segment's short tail chunk leaves one
 // value per 2 KB slice.  The host folds all values in order (fixed 64 KB / 2 KB
 // matrices, a table of 2^k-byte shifts for the odd lengths) and applies the preset and
@@ -42,15 +43,22 @@ __device__ __forceinline__ uint32_t apply_mat(const uint32_t* m, uint32_t v) {
   return r;
 }
 
-__global__ void k_crc32_chunks(const ChunkJob* jobs, int n, ShiftMats mats, uint32_t* out) {
-  __shared__ uint32_t tab[256];
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
-    uint32_t c = (uint32_t)i;
+// The byte table, one copy per lane interleaved so that lane L's entry i sits at word
+// 32*i + L: every lane reads its own bank, so the random table lookups are
+// conflict-free (32 KB of shared memory per CTA).
+constexpr int kCrcThreads = 512;
+__global__ void __launch_bounds__(kCrcThreads) k_crc32_chunks(const ChunkJob* jobs, int n,
+                                                              ShiftMats mats, uint32_t* out) {
+  extern __shared__ uint32_t tab32[];  // [256][32]
+  for (int i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
+    uint32_t c = (uint32_t)(i >> 5);
     for (int k = 0; k < 8; ++k) c = (c & 1u) ? kPoly ^ (c >> 1) : c >> 1;
-    tab[i] = c;
+    tab32[i] = c;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
+  const uint32_t* tab_l = tab32 + lane;
+#define tab(i) tab_l[(i) << 5]
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n; w += warps) {
     const ChunkJob J = jobs[w];
@@ -59,7 +67,7 @@ __global__ void k_crc32_chunks(const ChunkJob* jobs, int n, ShiftMats mats, uint
       if (a < J.len) {
         const int64_t b = std::min<int64_t>(J.len, a + kLaneBytes);
         uint32_t c = 0;
-        for (int64_t i = a; i < b; ++i) c = tab[(c ^ __ldg(J.p + i)) & 0xFFu] ^ (c >> 8);
+        for (int64_t i = a; i < b; ++i) c = tab((c ^ __ldg(J.p + i)) & 0xFFu) ^ (c >> 8);
         out[J.oidx + lane] = c;
       }
       continue;
@@ -76,7 +84,7 @@ __global__ void k_crc32_chunks(const ChunkJob* jobs, int n, ShiftMats mats, uint
 #pragma unroll
         for (int k = 0; k < 4; ++k)
 #pragma unroll
-          for (int b = 0; b < 4; ++b) c = tab[(c ^ (w[k] >> (8 * b))) & 0xFFu] ^ (c >> 8);
+          for (int b = 0; b < 4; ++b) c = tab((c ^ (w[k] >> (8 * b))) & 0xFFu) ^ (c >> 8);
       }
     } else if ((reinterpret_cast<uintptr_t>(q) & 3u) == 0) {
       const uint32_t* q4 = reinterpret_cast<const uint32_t*>(q);
@@ -84,10 +92,10 @@ __global__ void k_crc32_chunks(const ChunkJob* jobs, int n, ShiftMats mats, uint
       for (int i = 0; i < kLaneBytes / 4; ++i) {
         const uint32_t x = __ldg(q4 + i);
 #pragma unroll
-        for (int b = 0; b < 4; ++b) c = tab[(c ^ (x >> (8 * b))) & 0xFFu] ^ (c >> 8);
+        for (int b = 0; b < 4; ++b) c = tab((c ^ (x >> (8 * b))) & 0xFFu) ^ (c >> 8);
       }
     } else {
-      for (int i = 0; i < kLaneBytes; ++i) c = tab[(c ^ __ldg(q + i)) & 0xFFu] ^ (c >> 8);
+      for (int i = 0; i < kLaneBytes; ++i) c = tab((c ^ __ldg(q + i)) & 0xFFu) ^ (c >> 8);
     }
     // fold: level k joins lane pairs 2^k apart; the left value shifts over the right
     // block of 2 KB << k bytes
@@ -98,6 +106,7 @@ __global__ void k_crc32_chunks(const ChunkJob* jobs, int n, ShiftMats mats, uint
     }
     if (lane == 0) out[J.oidx] = c;
   }
+#undef tab
 }
 
 // ---- host GF(2) helpers (zlib's crc32_combine construction)
@@ -211,10 +220,11 @@ cudaError_t crc32_device(const void* const* segs, const int64_t* lens, int n, ui
       int dev = 0, sms = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      const int threads = 256;
+      const int threads = kCrcThreads;
+      const size_t smem = 256 * 32 * sizeof(uint32_t);
       const long want = ((long)jobs.size() * 32 + threads - 1) / threads;
-      const int grid = (int)std::max(1L, std::min<long>(want, (long)sms * 8));
-      k_crc32_chunks<<<grid, threads, 0, st>>>(djobs, (int)jobs.size(), mats, dout);
+      const int grid = (int)std::max(1L, std::min<long>(want, (long)sms * 4));
+      k_crc32_chunks<<<grid, threads, smem, st>>>(djobs, (int)jobs.size(), mats, dout);
       e = cudaGetLastError();
     }
     if (e == cudaSuccess)
