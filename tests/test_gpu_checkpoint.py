@@ -109,3 +109,37 @@ def test_load_errors_match_reference(cuda, tmp_path):
     fails(with_crc(good[:-4] + b"\0"), "has trailing bytes")
     with pytest.raises(RuntimeError, match="cannot open checkpoint"):
         load_checkpoint(str(tmp_path / "missing.qftc"))
+
+
+def test_engine_state_roundtrip_then_identical_steps(cuda, tmp_path):
+    """A LLaMA-shaped engine state (grouped width classes, slotted CSR) saved, loaded
+    and re-saved byte-identically; the loaded copy and the original then take the same
+    step and export the same bytes."""
+    from paper_2310_07147_b200.checkpoint import CheckpointMeta, load_checkpoint, save_checkpoint
+    from paper_2310_07147_b200.shapes import llama
+    shapes = llama(512, 1376, 2, 1000)
+    st = cuda.QftModelState(shapes, bit_width=8)
+    st.init_from_weights(lambda i: cuda.synth(shapes[i], 31 + i, 0.02, 0.005), 0.01)
+    for i, sh in enumerate(shapes):  # give the momentum real codes
+        q = cuda.quantize_state(cuda.synth(sh, 500 + i, 1e-3, 0.0), 8)
+        c, s, z = st.grad_views(i)
+        c.copy_(q.data); s.copy_(q.params.scale); z.copy_(q.params.zero_point)
+    st.step(lr=2e-4, check=True)
+    junc = [(k + 1) % 2 for k in range(len(shapes) - 1)]  # relu / none alternating
+    meta = CheckpointMeta(bit_width=8, loss=1, outlier_fraction=0.01, junctions=junc)
+    p1, p2 = tmp_path / "a.qftc", tmp_path / "b.qftc"
+    save_checkpoint(st, str(p1), meta)
+    st2, meta2 = load_checkpoint(str(p1))
+    assert meta2.junctions == meta.junctions and meta2.loss == 1
+    save_checkpoint(st2, str(p2), meta2)
+    assert p1.read_bytes() == p2.read_bytes()
+    for s_ in (st, st2):
+        for i, sh in enumerate(shapes):
+            q = cuda.quantize_state(cuda.synth(sh, 900 + i, 1e-3, 0.0), 8)
+            c, s, z = s_.grad_views(i)
+            c.copy_(q.data); s.copy_(q.params.scale); z.copy_(q.params.zero_point)
+        s_.step(lr=2e-4, check=True)
+    for i in range(len(shapes)):
+        a, b = st.export_tensor(i), st2.export_tensor(i)
+        for k in a:
+            assert np.array_equal(a[k], b[k]), f"tensor {i} {k}"
