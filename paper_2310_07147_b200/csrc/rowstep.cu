@@ -243,7 +243,9 @@ size_t rows_kernel_smem(int cols, int oldcap) {
   return (size_t)L.total();
 }
 
-template <int MAXT, int MINB, int NS>
+// FULL: every thread owns V whole vectors of the row (cols == blockDim.x * V * 16), so
+// the per-vector bounds checks vanish at compile time
+template <int MAXT, int MINB, int NS, bool FULL>
 __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   using namespace rs6;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -414,7 +416,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
       const int v = t + j * NT;
       nmask[j] = 0;
       out16[j] = 0;
-      if (stable && v < nvec) {
+      if (stable && (FULL || v < nvec)) {
         const uint4 cwj = *reinterpret_cast<const uint4*>(st + 128 + v * 16);
         const uint4 cmj = *reinterpret_cast<const uint4*>(st + 128 + cols + v * 16);
         const uint4 cgj = *reinterpret_cast<const uint4*>(st + 128 + 2 * cols + v * 16);
@@ -598,7 +600,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
 #pragma unroll
       for (int j = 0; j < V; ++j) {
         const int v = t + j * NT;
-        if (v < nvec) {
+        if (FULL || v < nvec) {
           uint32_t cq[4];
           bool ok;
           if (r.qmf) {
@@ -754,9 +756,9 @@ __global__ void k_step_prep(const LaunchArgs a, int stable_ok) {
 }
 
 // ---------------------------------------------------------------------------- launch
-template <int MAXT, int MINB, int NS>
+template <int MAXT, int MINB, int NS, bool FULL = false>
 static cudaError_t rows_launch_t(const LaunchArgs& a, int nt, size_t smem, cudaStream_t st) {
-  auto k = rows_kernel<MAXT, MINB, NS>;
+  auto k = rows_kernel<MAXT, MINB, NS, FULL>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
@@ -798,7 +800,12 @@ cudaError_t launch_rows_step(const LaunchArgs& a0, cudaStream_t st) {
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const int nt = rows_kernel_nt(a.cols_p);
   const size_t smem = rows_kernel_smem(a.cols_p, a.oldcap6);
-  if (nt <= 128)
+#ifndef QFT_FULL
+#define QFT_FULL 1
+#endif
+  if (QFT_FULL && nt == 128 && a.cols_p == 128 * rs6::V * 16)  // LLaMA's 4096 columns
+    e = rows_launch_t<128, QFT_ROWS_MINB_S, 3, true>(a, nt, smem, st);
+  else if (nt <= 128)
     e = rows_launch_t<128, QFT_ROWS_MINB_S, 3>(a, nt, smem, st);
   else if (nt <= 384)
     e = rows_launch_t<384, QFT_ROWS_MINB_M, 2>(a, nt, smem, st);
