@@ -243,9 +243,10 @@ size_t rows_kernel_smem(int cols, int oldcap) {
   return (size_t)L.total();
 }
 
-// FULL: every thread owns V whole vectors of the row (cols == blockDim.x * V * 16), so
-// the per-vector bounds checks vanish at compile time
-template <int MAXT, int MINB, int NS, bool FULL>
+// FULL (2): every thread owns V whole vectors of the row (cols == blockDim.x * V * 16);
+// FIRST (1): every thread's first vector is inside the row (nvec >= blockDim.x).  The
+// per-vector bounds checks they cover vanish at compile time.
+template <int MAXT, int MINB, int NS, int FULL>
 __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   using namespace rs6;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -416,7 +417,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
       const int v = t + j * NT;
       nmask[j] = 0;
       out16[j] = 0;
-      if (stable && (FULL || v < nvec)) {
+      if (stable && (FULL == 2 || (FULL == 1 && j == 0) || v < nvec)) {
         const uint4 cwj = *reinterpret_cast<const uint4*>(st + 128 + v * 16);
         const uint4 cmj = *reinterpret_cast<const uint4*>(st + 128 + cols + v * 16);
         const uint4 cgj = *reinterpret_cast<const uint4*>(st + 128 + 2 * cols + v * 16);
@@ -600,7 +601,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
 #pragma unroll
       for (int j = 0; j < V; ++j) {
         const int v = t + j * NT;
-        if (FULL || v < nvec) {
+        if (FULL == 2 || (FULL == 1 && j == 0) || v < nvec) {
           uint32_t cq[4];
           bool ok;
           if (r.qmf) {
@@ -756,7 +757,7 @@ __global__ void k_step_prep(const LaunchArgs a, int stable_ok) {
 }
 
 // ---------------------------------------------------------------------------- launch
-template <int MAXT, int MINB, int NS, bool FULL = false>
+template <int MAXT, int MINB, int NS, int FULL = 0>
 static cudaError_t rows_launch_t(const LaunchArgs& a, int nt, size_t smem, cudaStream_t st) {
   auto k = rows_kernel<MAXT, MINB, NS, FULL>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -804,9 +805,14 @@ cudaError_t launch_rows_step(const LaunchArgs& a0, cudaStream_t st) {
 #define QFT_FULL 1
 #endif
   if (QFT_FULL && nt == 128 && a.cols_p == 128 * rs6::V * 16)  // LLaMA's 4096 columns
-    e = rows_launch_t<128, QFT_ROWS_MINB_S, 3, true>(a, nt, smem, st);
+    e = rows_launch_t<128, QFT_ROWS_MINB_S, 3, 2>(a, nt, smem, st);
   else if (nt <= 128)
     e = rows_launch_t<128, QFT_ROWS_MINB_S, 3>(a, nt, smem, st);
+#ifndef QFT_FIRST
+#define QFT_FIRST 1
+#endif
+  else if (QFT_FIRST && nt <= 384 && a.cols_p / 16 >= nt)  // e.g. 11008 columns
+    e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1>(a, nt, smem, st);
   else if (nt <= 384)
     e = rows_launch_t<384, QFT_ROWS_MINB_M, 2>(a, nt, smem, st);
   else
