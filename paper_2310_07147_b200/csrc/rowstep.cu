@@ -243,6 +243,15 @@ size_t rows_kernel_smem(int cols, int oldcap) {
   return (size_t)L.total();
 }
 
+#ifndef QFT_CONST_GEOM
+#define QFT_CONST_GEOM 1
+#endif
+// the old-outlier table of a FULL row (rows_kernel_oldcap of 16*V*MAXT columns, 3 stages)
+template <int MAXT>
+__host__ __device__ constexpr int full_oldcap() {
+  return ((MAXT * rs6::V * 16) / 32 + 31) & ~31;
+}
+
 // FULL (2): every thread owns V whole vectors of the row (cols == blockDim.x * V * 16);
 // FIRST (1): every thread's first vector is inside the row (nvec >= blockDim.x).  The
 // per-vector bounds checks they cover vanish at compile time.
@@ -250,11 +259,15 @@ template <int MAXT, int MINB, int NS, int FULL>
 __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   using namespace rs6;
   extern __shared__ __align__(128) uint8_t smem[];
-  const int NT = blockDim.x, NW = NT >> 5;
+  // FULL: the row geometry is a compile-time constant (MAXT threads, 16*V*MAXT columns,
+  // the 3-stage old-outlier table), so every shared-memory offset folds
+  constexpr bool CG = QFT_CONST_GEOM && FULL == 2;
+  const int NT = CG ? MAXT : (int)blockDim.x, NW = NT >> 5;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  const int cols = a.cols_p;  // uniform row length of the launch (multiple of 16)
+  // uniform row length of the launch (multiple of 16)
+  const int cols = CG ? MAXT * V * 16 : a.cols_p;
   const int nvec = cols >> 4;
-  const Smem L{NT * V, a.oldcap6, NW, cols, NS};
+  const Smem L{NT * V, CG ? full_oldcap<MAXT>() : a.oldcap6, NW, cols, NS};
   const int qmax = (1 << a.bit_width) - 1;
   const uint32_t KC = (uint32_t)((1 << (a.bit_width - 1)) - 1) * 0x01010101u;
   const uint32_t QB = (uint32_t)qmax * 0x01010101u;
@@ -804,7 +817,8 @@ cudaError_t launch_rows_step(const LaunchArgs& a0, cudaStream_t st) {
 #ifndef QFT_FULL
 #define QFT_FULL 1
 #endif
-  if (QFT_FULL && nt == 128 && a.cols_p == 128 * rs6::V * 16)  // LLaMA's 4096 columns
+  if (QFT_FULL && nt == 128 && a.cols_p == 128 * rs6::V * 16 &&
+      a.oldcap6 == full_oldcap<128>())  // LLaMA's 4096 columns
     e = rows_launch_t<128, QFT_ROWS_MINB_S, 3, 2>(a, nt, smem, st);
   else if (nt <= 128)
     e = rows_launch_t<128, QFT_ROWS_MINB_S, 3>(a, nt, smem, st);
