@@ -243,31 +243,31 @@ size_t rows_kernel_smem(int cols, int oldcap) {
   return (size_t)L.total();
 }
 
-#ifndef QFT_CONST_GEOM
-#define QFT_CONST_GEOM 1
-#endif
-// the old-outlier table of a FULL row (rows_kernel_oldcap of 16*V*MAXT columns, 3 stages)
-template <int MAXT>
-__host__ __device__ constexpr int full_oldcap() {
-  return ((MAXT * rs6::V * 16) / 32 + 31) & ~31;
+// compile-time row geometry of a CCOLS-column instance (rows_kernel_nt / _oldcap)
+__host__ __device__ constexpr int geom_nt(int cols) {
+  return ((((cols + 15) / 16 + rs6::V - 1) / rs6::V + 31) / 32) * 32;
+}
+__host__ __device__ constexpr int geom_oldcap(int cols, int ns) {
+  return ((ns >= 3 ? cols / 32 : cols / 16) + 31) & ~31;
 }
 
 // FULL (2): every thread owns V whole vectors of the row (cols == blockDim.x * V * 16);
 // FIRST (1): every thread's first vector is inside the row (nvec >= blockDim.x).  The
 // per-vector bounds checks they cover vanish at compile time.
-template <int MAXT, int MINB, int NS, int FULL>
+// CCOLS > 0: the launch's row length is the compile-time constant CCOLS (LLaMA widths)
+template <int MAXT, int MINB, int NS, int FULL, int CCOLS>
 __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   using namespace rs6;
   extern __shared__ __align__(128) uint8_t smem[];
-  // FULL: the row geometry is a compile-time constant (MAXT threads, 16*V*MAXT columns,
-  // the 3-stage old-outlier table), so every shared-memory offset folds
-  constexpr bool CG = QFT_CONST_GEOM && FULL == 2;
-  const int NT = CG ? MAXT : (int)blockDim.x, NW = NT >> 5;
+  // CCOLS: the row geometry is a compile-time constant (threads, columns, old-outlier
+  // table), so every shared-memory offset folds
+  constexpr bool CG = CCOLS > 0;
+  const int NT = CG ? geom_nt(CCOLS) : (int)blockDim.x, NW = NT >> 5;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   // uniform row length of the launch (multiple of 16)
-  const int cols = CG ? MAXT * V * 16 : a.cols_p;
+  const int cols = CG ? CCOLS : a.cols_p;
   const int nvec = cols >> 4;
-  const Smem L{NT * V, CG ? full_oldcap<MAXT>() : a.oldcap6, NW, cols, NS};
+  const Smem L{NT * V, CG ? geom_oldcap(CCOLS, NS) : a.oldcap6, NW, cols, NS};
   const int qmax = (1 << a.bit_width) - 1;
   const uint32_t KC = (uint32_t)((1 << (a.bit_width - 1)) - 1) * 0x01010101u;
   const uint32_t QB = (uint32_t)qmax * 0x01010101u;
@@ -770,9 +770,9 @@ __global__ void k_step_prep(const LaunchArgs a, int stable_ok) {
 }
 
 // ---------------------------------------------------------------------------- launch
-template <int MAXT, int MINB, int NS, int FULL = 0>
+template <int MAXT, int MINB, int NS, int FULL = 0, int CCOLS = 0>
 static cudaError_t rows_launch_t(const LaunchArgs& a, int nt, size_t smem, cudaStream_t st) {
-  auto k = rows_kernel<MAXT, MINB, NS, FULL>;
+  auto k = rows_kernel<MAXT, MINB, NS, FULL, CCOLS>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
@@ -814,18 +814,21 @@ cudaError_t launch_rows_step(const LaunchArgs& a0, cudaStream_t st) {
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const int nt = rows_kernel_nt(a.cols_p);
   const size_t smem = rows_kernel_smem(a.cols_p, a.oldcap6);
-#ifndef QFT_FULL
-#define QFT_FULL 1
-#endif
-  if (QFT_FULL && nt == 128 && a.cols_p == 128 * rs6::V * 16 &&
-      a.oldcap6 == full_oldcap<128>())  // LLaMA's 4096 columns
-    e = rows_launch_t<128, QFT_ROWS_MINB_S, 3, 2>(a, nt, smem, st);
+  // compile-time geometry for the LLaMA-2 widths (4096 / 11008: 7B; 5120 / 13824: 13B),
+  // used only when the plan's table size is the one that geometry implies
+  const int c = a.cols_p;
+  auto geom_ok = [&](int cc, int ns) { return c == cc && a.oldcap6 == geom_oldcap(cc, ns); };
+  if (nt == 128 && geom_ok(4096, 3))
+    e = rows_launch_t<128, QFT_ROWS_MINB_S, 3, 2, 4096>(a, nt, smem, st);
+  else if (geom_ok(11008, 2))
+    e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1, 11008>(a, nt, smem, st);
+  else if (geom_ok(5120, 2))
+    e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1, 5120>(a, nt, smem, st);
+  else if (geom_ok(13824, 2))
+    e = rows_launch_t<512, 1, 2, 1, 13824>(a, nt, smem, st);
   else if (nt <= 128)
     e = rows_launch_t<128, QFT_ROWS_MINB_S, 3>(a, nt, smem, st);
-#ifndef QFT_FIRST
-#define QFT_FIRST 1
-#endif
-  else if (QFT_FIRST && nt <= 384 && a.cols_p / 16 >= nt)  // e.g. 11008 columns
+  else if (nt <= 384 && c / 16 >= nt)
     e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1>(a, nt, smem, st);
   else if (nt <= 384)
     e = rows_launch_t<384, QFT_ROWS_MINB_M, 2>(a, nt, smem, st);

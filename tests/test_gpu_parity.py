@@ -214,7 +214,7 @@ def test_lion_step_trajectory(cuda, port, bw, frac, shape, wd):
 @pytest.mark.parametrize("bw,frac", [(8, 0.01), (8, 0.0045), (4, 0.0045), (3, 0.0045)])
 @pytest.mark.parametrize("wd", [0.0, 0.01])
 @pytest.mark.parametrize("lr", [2e-5, 1.5e-4, 2.2e-4, 4e-4])
-@pytest.mark.parametrize("shape", [(64, 4096), (24, 11008), (40, 48)])
+@pytest.mark.parametrize("shape", [(64, 4096), (24, 11008), (40, 48), (24, 5120), (12, 13824)])
 def test_lion_step_stable_tier(cuda, port, lr, shape, wd, bw, frac):
     """The rows kernel's stable tier (rowstep.cu): at the paper's lr = 2e-5 every row is
     proven code-stable; lr near sw/2 (~2.2e-4 at 8 bits) splits a tensor between the
@@ -545,7 +545,8 @@ def test_zero1_world1_nccl_cuda_shard(cuda, port):
 
 @pytest.mark.parametrize("grid", [3, 37])
 @pytest.mark.parametrize("lr", [2e-5, 2.2e-4])
-def test_rows_kernel_many_rows_per_cta(cuda, port, monkeypatch, grid, lr):
+@pytest.mark.parametrize("model", ["small", "llama_widths"])
+def test_rows_kernel_many_rows_per_cta(cuda, port, monkeypatch, grid, lr, model):
     """The rows kernel with a capped grid, so every CTA pipelines many rows through its
     TMA stages and sparse buffers (the other parity tests are small enough to give each
     CTA one row); lr near sw/2 mixes stable rows with rows of the general kernel inside
@@ -553,7 +554,9 @@ def test_rows_kernel_many_rows_per_cta(cuda, port, monkeypatch, grid, lr):
     the oracle."""
     from paper_2310_07147_b200.shapes import llama
     monkeypatch.setenv("QFT_ROWS_GRID", str(grid))
-    shapes = llama(512, 1376, 1, 512)
+    # llama_widths: the compile-time-geometry instances (7B and 13B row lengths)
+    shapes = llama(512, 1376, 1, 512) if model == "small" else \
+        [(40, 4096), (24, 11008), (30, 5120), (20, 13824)]
     bw, frac = 8, 0.01
     st = cuda.QftModelState(shapes, bit_width=bw)
     st.init_from_weights(lambda i: cuda.synth(shapes[i], 1234 + i, 0.02, 0.005), frac)
