@@ -243,6 +243,9 @@ size_t rows_kernel_smem(int cols, int oldcap) {
   return (size_t)L.total();
 }
 
+#ifndef QFT_BW8
+#define QFT_BW8 1
+#endif
 // compile-time row geometry of a CCOLS-column instance (rows_kernel_nt / _oldcap)
 __host__ __device__ constexpr int geom_nt(int cols) {
   return ((((cols + 15) / 16 + rs6::V - 1) / rs6::V + 31) / 32) * 32;
@@ -255,7 +258,8 @@ __host__ __device__ constexpr int geom_oldcap(int cols, int ns) {
 // FIRST (1): every thread's first vector is inside the row (nvec >= blockDim.x).  The
 // per-vector bounds checks they cover vanish at compile time.
 // CCOLS > 0: the launch's row length is the compile-time constant CCOLS (LLaMA widths)
-template <int MAXT, int MINB, int NS, int FULL, int CCOLS>
+// and its input CSR is slotted; BWC > 0: the bit width is the constant BWC
+template <int MAXT, int MINB, int NS, int FULL, int CCOLS, int BWC>
 __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   using namespace rs6;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -268,11 +272,12 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   const int cols = CG ? CCOLS : a.cols_p;
   const int nvec = cols >> 4;
   const Smem L{NT * V, CG ? geom_oldcap(CCOLS, NS) : a.oldcap6, NW, cols, NS};
-  const int qmax = (1 << a.bit_width) - 1;
-  const uint32_t KC = (uint32_t)((1 << (a.bit_width - 1)) - 1) * 0x01010101u;
+  const int bw = BWC > 0 ? BWC : a.bit_width;
+  const int qmax = (1 << bw) - 1;
+  const uint32_t KC = (uint32_t)((1 << (bw - 1)) - 1) * 0x01010101u;
   const uint32_t QB = (uint32_t)qmax * 0x01010101u;
   const int G = gridDim.x;
-  const bool slotted = a.slotted_in != 0;
+  const bool slotted = CG || a.slotted_in != 0;
   Hyper h;
   h.lr = a.lr; h.b1 = a.b1; h.b2 = a.b2; h.wd = a.wd;
   h.c1 = __fsub_rn(1.0f, a.b1);
@@ -332,7 +337,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
       const float gv = dequant_exact(st[128 + 2 * cols + col], r.sg, r.zg);
       lion1(wv, mv, gv, h);
       const bool o = (wv < r.tmin) || (wv > r.tmax);
-      const uint32_t code = o ? zpay : quant_inlier(wv, r.sw, r.zw, a.bit_width);
+      const uint32_t code = o ? zpay : quant_inlier(wv, r.sw, r.zw, bw);
       atomicOr(&wd[col >> 4], (1u << (col & 15)) | (o ? (0x10000u << (col & 15)) : 0u));
       spval(b)[i] = wv;
       spcw(b)[i] = code | (o ? 0x100u : 0u);
@@ -558,8 +563,8 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
         // (the FMA-verified fast divide pays off where more warps wait on this chain:
         // the wide-row instances; measured same-run, slower on the 128-thread one)
         if (!(MAXT > 128 && affine_fast(lo, hi, (double)qmax, rq, smv, zmv)))
-          affine_ni(lo, hi, a.bit_width, &smv, &zmv);
-        const QuantRow qm = make_quant_row(smv, zmv, a.bit_width);
+          affine_ni(lo, hi, bw, &smv, &zmv);
+        const QuantRow qm = make_quant_row(smv, zmv, bw);
         // every m' lies in [lo, hi]: if their codes need no clip (proven with the fast
         // quantizer's own tie bound), no code of the row does
         float em = 0.0f;
@@ -770,9 +775,9 @@ __global__ void k_step_prep(const LaunchArgs a, int stable_ok) {
 }
 
 // ---------------------------------------------------------------------------- launch
-template <int MAXT, int MINB, int NS, int FULL = 0, int CCOLS = 0>
+template <int MAXT, int MINB, int NS, int FULL = 0, int CCOLS = 0, int BWC = 0>
 static cudaError_t rows_launch_t(const LaunchArgs& a, int nt, size_t smem, cudaStream_t st) {
-  auto k = rows_kernel<MAXT, MINB, NS, FULL, CCOLS>;
+  auto k = rows_kernel<MAXT, MINB, NS, FULL, CCOLS, BWC>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
@@ -817,9 +822,16 @@ cudaError_t launch_rows_step(const LaunchArgs& a0, cudaStream_t st) {
   // compile-time geometry for the LLaMA-2 widths (4096 / 11008: 7B; 5120 / 13824: 13B),
   // used only when the plan's table size is the one that geometry implies
   const int c = a.cols_p;
-  auto geom_ok = [&](int cc, int ns) { return c == cc && a.oldcap6 == geom_oldcap(cc, ns); };
-  if (nt == 128 && geom_ok(4096, 3))
+  auto geom_ok = [&](int cc, int ns) {
+    return c == cc && a.oldcap6 == geom_oldcap(cc, ns) && a.slotted_in;
+  };
+  const bool b8 = QFT_BW8 && a.bit_width == 8;  // the 7B widths also get a constant width
+  if (nt == 128 && geom_ok(4096, 3) && b8)
+    e = rows_launch_t<128, QFT_ROWS_MINB_S, 3, 2, 4096, 8>(a, nt, smem, st);
+  else if (nt == 128 && geom_ok(4096, 3))
     e = rows_launch_t<128, QFT_ROWS_MINB_S, 3, 2, 4096>(a, nt, smem, st);
+  else if (geom_ok(11008, 2) && b8)
+    e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1, 11008, 8>(a, nt, smem, st);
   else if (geom_ok(11008, 2))
     e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1, 11008>(a, nt, smem, st);
   else if (geom_ok(5120, 2))
