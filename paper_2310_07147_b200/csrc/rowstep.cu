@@ -246,6 +246,9 @@ size_t rows_kernel_smem(int cols, int oldcap) {
 #ifndef QFT_BW8
 #define QFT_BW8 1
 #endif
+#ifndef QFT_BW34
+#define QFT_BW34 1
+#endif
 // compile-time row geometry of a CCOLS-column instance (rows_kernel_nt / _oldcap)
 __host__ __device__ constexpr int geom_nt(int cols) {
   return ((((cols + 15) / 16 + rs6::V - 1) / rs6::V + 31) / 32) * 32;
@@ -832,6 +835,13 @@ cudaError_t launch_rows_step(const LaunchArgs& a0, cudaStream_t st) {
     e = rows_launch_t<128, QFT_ROWS_MINB_S, 3, 2, 4096>(a, nt, smem, st);
   else if (geom_ok(11008, 2) && b8)
     e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1, 11008, 8>(a, nt, smem, st);
+#if QFT_BW34
+  // the down-projection sweep (configs[4]) also runs 3- and 4-bit codes
+  else if (geom_ok(11008, 2) && a.bit_width == 4)
+    e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1, 11008, 4>(a, nt, smem, st);
+  else if (geom_ok(11008, 2) && a.bit_width == 3)
+    e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1, 11008, 3>(a, nt, smem, st);
+#endif
   else if (geom_ok(11008, 2))
     e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1, 11008>(a, nt, smem, st);
   else if (geom_ok(5120, 2))
