@@ -844,8 +844,12 @@ cudaError_t launch_rows_step(const LaunchArgs& a0, cudaStream_t st) {
 #endif
   else if (geom_ok(11008, 2))
     e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1, 11008>(a, nt, smem, st);
+  else if (geom_ok(5120, 2) && b8)
+    e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1, 5120, 8>(a, nt, smem, st);
   else if (geom_ok(5120, 2))
     e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1, 5120>(a, nt, smem, st);
+  else if (geom_ok(13824, 2) && b8)
+    e = rows_launch_t<512, 1, 2, 1, 13824, 8>(a, nt, smem, st);
   else if (geom_ok(13824, 2))
     e = rows_launch_t<512, 1, 2, 1, 13824>(a, nt, smem, st);
   else if (nt <= 128)
