@@ -54,6 +54,10 @@
 namespace qftk {
 using namespace qftd;
 
+#ifndef QFT_OC3
+#define QFT_OC3 64  // old-outlier table of the 3-stage class: cols / QFT_OC3 entries
+#endif
+
 namespace rs6 {
 constexpr uint32_t I_STABLE = 1u;
 constexpr int V = 2;  // 16-byte vectors per thread
@@ -230,11 +234,12 @@ int rows_kernel_nt(int cols) {
   return ((per + 31) / 32) * 32;
 }
 
-// TMA stages: 3 where the smem budget keeps 4 CTAs/SM (rows <= 4096 columns, old-outlier
-// table cols/32), else 2 (table cols/16)
+// TMA stages: 3 where the smem budget keeps 5 CTAs/SM (rows <= 4096 columns, old-outlier
+// table cols/64: 64 entries at 4096 columns; rows with more old outliers take the
+// general kernel), else 2 (table cols/16)
 static int rows_kernel_ns(int cols) { return rows_kernel_nt(cols) <= 128 ? 3 : 2; }
 int rows_kernel_oldcap(int cols) {
-  return ((rows_kernel_ns(cols) == 3 ? cols / 32 : cols / 16) + 31) & ~31;
+  return ((rows_kernel_ns(cols) == 3 ? cols / QFT_OC3 : cols / 16) + 31) & ~31;
 }
 
 size_t rows_kernel_smem(int cols, int oldcap) {
@@ -254,7 +259,7 @@ __host__ __device__ constexpr int geom_nt(int cols) {
   return ((((cols + 15) / 16 + rs6::V - 1) / rs6::V + 31) / 32) * 32;
 }
 __host__ __device__ constexpr int geom_oldcap(int cols, int ns) {
-  return ((ns >= 3 ? cols / 32 : cols / 16) + 31) & ~31;
+  return ((ns >= 3 ? cols / QFT_OC3 : cols / 16) + 31) & ~31;
 }
 
 // FULL (2): every thread owns V whole vectors of the row (cols == blockDim.x * V * 16);
@@ -806,7 +811,7 @@ bool rows_kernel_eligible(int gk, int use_bulk, int uniform_cols) {
 
 // register budget per width class (tuning: -DQFT_ROWS_MINB_S / _M)
 #ifndef QFT_ROWS_MINB_S
-#define QFT_ROWS_MINB_S 4  // rows of <= 4096 columns (<= 128 threads)
+#define QFT_ROWS_MINB_S 5  // rows of <= 4096 columns (<= 128 threads): 5 CTAs/SM
 #endif
 #ifndef QFT_ROWS_MINB_M
 #define QFT_ROWS_MINB_M 2  // rows of <= 12288 columns (<= 384 threads)
