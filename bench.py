@@ -97,8 +97,40 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU arm
+def host_cpu():
+    """(usable host threads, CPU model) of this box"""
+    try:
+        n = len(os.sched_getaffinity(0))
+    except AttributeError:
+        n = os.cpu_count() or 1
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return n, model
+
+
+def layer_row_chunks(rows_per_chunk=512):
+    """One LLaMA-2-7B decoder layer's weight matrices (4 x 4096x4096, 2 x 11008x4096,
+    4096x11008; 202.4 M params) cut into row blocks of <= rows_per_chunk rows.  The step is
+    per row (optimizer.hpp:103-118), so a row block stepped as its own layer is the same
+    work and the same bytes; the blocks let every host thread stay busy to the end."""
+    mats = [(4096, 4096)] * 4 + [(11008, 4096)] * 2 + [(4096, 11008)]
+    out = []
+    for r, c in mats:
+        for r0 in range(0, r, rows_per_chunk):
+            out.append((min(rows_per_chunk, r - r0), c))
+    return out
+
+
 def cpu_reference_run(steps, warmup, threads=None, sample=None):
-    """Time qft::lion_step_quantized (the unmodified reference) on host cores."""
+    """Time qft::lion_step_quantized (the unmodified reference, compiled from its headers)
+    on the host cores: a bounded sample of the 7B workload -- one decoder layer's matrices
+    in row blocks, several times more blocks than threads, handed out longest-first."""
     from oracle import oracle as O
     if not O.available("reference"):
         O.build()
@@ -112,10 +144,9 @@ def cpu_reference_run(steps, warmup, threads=None, sample=None):
     lib.qr_bench_params.restype = C.c_int64
     lib.qr_bench_params.argtypes = [C.c_void_p]
     lib.qr_bench_destroy.argtypes = [C.c_void_p]
-    threads = threads or os.cpu_count() or 1
-    # bounded, LLaMA-2-7B-proportioned sample of the same workload: per transformer
-    # layer the 7B mix is 4x(4096x4096) + 2x(11008x4096) + 1x(4096x11008)
-    sample = sample or [(4096, 4096)] * 4 + [(11008, 4096)] * 2 + [(4096, 11008)]
+    ncpu, model = host_cpu()
+    sample = sample or layer_row_chunks()
+    threads = min(threads or ncpu, len(sample))   # the threads that actually run
     rows = (C.c_int * len(sample))(*[r for r, _ in sample])
     cols = (C.c_int * len(sample))(*[c for _, c in sample])
     h = lib.qr_bench_create(len(sample), rows, cols, 1234, BIT_WIDTH, FRACTION, HYPER["lr"],
@@ -127,9 +158,11 @@ def cpu_reference_run(steps, warmup, threads=None, sample=None):
     lib.qr_bench_destroy(h)
     t = statistics.median(ts)
     return {"value": n / t / 1e9, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": f"{len(sample)} tensors / one LLaMA-2-7B layer's weights "
-                      f"({n / 1e6:.1f} M params), b=8 p=1%, median of {steps} steps, "
-                      f"{threads} host threads (one 1-layer model per thread)",
+            "sample": f"one LLaMA-2-7B decoder layer's 7 weight matrices ({n / 1e6:.1f} M params) "
+                      f"in {len(sample)} row blocks of <= 512 rows, b=8 p=1% u8 gradient codes, "
+                      f"median of {steps} steps; {threads} host threads (dynamic, longest "
+                      f"block first) of {ncpu} usable on '{model}'",
+            "cpu_model": model, "host_threads_usable": ncpu,
             "ms_per_step": t * 1e3, "params": n}
 
 
@@ -148,7 +181,8 @@ def run_reference_arm(args):
         "data": "synthetic",
         "config": {"workload": "llama2-7b-shaped quantized Lion step (bounded CPU sample)",
                    "bit_width": BIT_WIDTH, "outlier_fraction": FRACTION},
-        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+        "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample",
+                                            "cpu_model")},
         "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -299,7 +333,7 @@ def run_gpu_arm(args):
         try:
             cb = cpu_reference_run(steps=2, warmup=0)
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind",
-                                                       "sample")}
+                                                       "sample", "cpu_model")}
         except Exception as ex:  # reported, never fatal for the GPU number
             line["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
     if rank == 0:

@@ -184,6 +184,19 @@ int qftc_plan_step(qftc_plan* plan, int flip, qftc_lion_hyper hyper, qftc_stream
 int qftc_plan_result(qftc_plan* plan, int64_t* nnz_total, qftc_stream_t stream);
 /* number of kernel launches one qftc_plan_step enqueues (for accounting) */
 int qftc_plan_launches(const qftc_plan* plan);
+/* the main kernel instance the last qftc_plan_step launched, e.g.
+ * "rows_kernel<128,5,3,2,4096,8>" (MAXT, MINB, stages, FULL, compile-time columns, bit
+ * width) or "step_kernel<gk,aligned,wd0>"; "" before the first step */
+const char* qftc_plan_kernel_name(const qftc_plan* plan);
+/* 1 if a step of this plan has overflowed a CSR slot and qftc_plan_result has not been
+ * called since (a mapped host flag: no synchronisation, so a step still in flight may not
+ * be reflected yet).  The overflowed step's output set is incomplete: re-plan the slots
+ * and re-run it from its (intact) input set before stepping on. */
+int qftc_plan_pending_overflow(const qftc_plan* plan);
+/* rows of the last step in the stable tier (rows kernel) and the general tier (general
+ * kernel); synchronises */
+int qftc_plan_tier_rows(qftc_plan* plan, int64_t* stable_rows, int64_t* general_rows,
+                        qftc_stream_t stream);
 int qftc_plan_destroy(qftc_plan* plan);
 
 /* Single-tensor convenience: lion_step_quantized for one layer, out-of-place,

@@ -12,6 +12,7 @@
 //     on the host cores.
 // The signatures are the qo_* ones from qft_oracle.c with a qr_ prefix.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <optional>
 #include <cstdint>
@@ -354,16 +355,26 @@ void* qr_bench_create(int n_layers, const int* rows, const int* cols, uint64_t s
   return b;
 }
 
-// Runs one quantized Lion step over every layer; returns wall seconds.
+// Runs one quantized Lion step over every layer; returns wall seconds.  The layers are
+// handed out longest-first from a shared counter (dynamic scheduling), so `threads` host
+// threads stay busy until the last few layers; the sample should hold several times
+// more layers than threads.
 double qr_bench_step(void* handle, int threads) {
   auto* b = static_cast<QrBench*>(handle);
   const int L = static_cast<int>(b->models.size());
   threads = std::max(1, std::min(threads, L));
+  std::vector<int> order(L);
+  for (int l = 0; l < L; ++l) order[l] = l;
+  std::stable_sort(order.begin(), order.end(), [b](int x, int y) {
+    return b->grads[x].size() > b->grads[y].size();
+  });
+  std::atomic<int> next{0};
   const auto t0 = std::chrono::steady_clock::now();
   std::vector<std::thread> pool;
   for (int t = 0; t < threads; ++t) {
-    pool.emplace_back([b, t, threads, L] {
-      for (int l = t; l < L; l += threads) {
+    pool.emplace_back([b, &next, &order, L] {
+      for (int k = next.fetch_add(1); k < L; k = next.fetch_add(1)) {
+        const int l = order[k];
         qft::GradientStack<float> stack;
         stack.push(1, b->grads[l]);  // the stack entry the backward sink would hand over
         qft::lion_step_quantized(b->models[l], b->states[l], stack, b->h);

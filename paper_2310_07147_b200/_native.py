@@ -86,6 +86,9 @@ _SIGS = {
     "qftc_plan_step": (_i, [_vp, _i, LionHyperC, _vp]),
     "qftc_plan_result": (_i, [_vp, C.POINTER(_i64), _vp]),
     "qftc_plan_launches": (_i, [_vp]),
+    "qftc_plan_kernel_name": (C.c_char_p, [_vp]),
+    "qftc_plan_pending_overflow": (_i, [_vp]),
+    "qftc_plan_tier_rows": (_i, [_vp, C.POINTER(_i64), C.POINTER(_i64), _vp]),
     "qftc_crc32": (_i, [_vp, _vp, _i, _vp, _vp]),
     "qftc_accumulate_state": (_i, [_vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "qftc_plan_destroy": (_i, [_vp]),

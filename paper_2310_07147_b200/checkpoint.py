@@ -14,7 +14,7 @@ u8[rows*cols]; then the CRC-32 of everything before it.
 
 B200 side: the state never leaves HBM in pieces the host has to assemble.  The CRC is
 computed on the GPU over the device arrays in file order (``qftc_crc32``).  The arrays
-are streamed device -> pinned host -> file.  On load the whole file is copied to the
+are copied device -> host (pageable ``.cpu()`` copies, array by array) -> file.  On load the whole file is copied to the
 device once and verified there before the state is built.  Pass-through checkpoints
 (raw fp32 weights, ``QuantMode::passthrough``) are outside the quantized path and are
 refused.
@@ -65,8 +65,21 @@ def _dev_bytes(b: bytes, device) -> torch.Tensor:
 
 def save_checkpoint(state: QftModelState, path: str, meta: Optional[CheckpointMeta] = None):
     """save_checkpoint(model, state, path) (checkpoint.cpp:100-140) for the whole
-    device-resident state: layer l of the file is tensor l of ``state``."""
-    meta = meta or CheckpointMeta(bit_width=state.bit_width)
+    device-resident state: layer l of the file is tensor l of ``state``.
+
+    ``meta`` defaults to the config the state records: the one it was loaded with, or
+    the outlier fraction / threshold kind it was decomposed with (relu junctions, mse
+    loss -- ModelConfig's defaults).  A state that does not know its outlier fraction
+    (built by init_from_host without ``fraction``) needs an explicit ``meta``: the
+    reference writes cfg.outlier_fraction, so guessing would misreport the file."""
+    if meta is None:
+        meta = getattr(state, "checkpoint_meta", None)
+    if meta is None:
+        if getattr(state, "outlier_fraction", None) is None:
+            raise ValueError("save_checkpoint: the state does not record its outlier fraction; "
+                             "pass meta=CheckpointMeta(...)")
+        meta = CheckpointMeta(bit_width=state.bit_width, threshold_kind=state.threshold_kind,
+                              outlier_fraction=state.outlier_fraction)
     if meta.quant_mode != AFFINE:
         raise NotImplementedError("pass-through checkpoints are outside the quantized path")
     L = state.n
@@ -183,5 +196,7 @@ def load_checkpoint(path: str, device="cuda") -> Tuple[QftModelState, Checkpoint
     if r.p != r.end:
         raise RuntimeError(f"checkpoint '{path}' has trailing bytes")
     st = QftModelState(shapes, bit_width=meta.bit_width, device=device)
-    st.init_from_host(tensors)
+    st.init_from_host(tensors, fraction=meta.outlier_fraction,
+                      kind="percentile" if meta.threshold_kind == 0 else "range_fraction")
+    st.checkpoint_meta = meta
     return st, meta

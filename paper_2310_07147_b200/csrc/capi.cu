@@ -34,7 +34,6 @@ cudaError_t launch_synth(float*, int64_t, uint64_t, double, double, cudaStream_t
 cudaError_t csr_plan_slots(const int32_t*, const int32_t*, int, int, int32_t*, cudaStream_t);
 cudaError_t csr_copy_rows(int, const int32_t*, const int32_t*, const int32_t*, const float*,
                           const int32_t*, int32_t*, float*, int64_t, cudaStream_t);
-cudaError_t csr_row_ptr(const int32_t*, int, int32_t*, cudaStream_t);
 }  // namespace qftk
 
 using namespace qftk;
@@ -310,7 +309,7 @@ int qftc_decompose_dense_sparse(const float* w, int rows, int cols, const float*
   QFTC_CUDA(cudaMallocAsync((void**)&counts, (size_t)rows * 4, st), "alloc");
   cudaError_t e = decompose_codes(w, rows, cols, scale, zp, t_min, t_max, bit_width, codes,
                                   counts, st);
-  if (e == cudaSuccess) e = csr_row_ptr(counts, rows, row_ptr, st);
+  if (e == cudaSuccess) e = csr_row_ptr(counts, rows, row_ptr, st, nullptr);
   int32_t nnz = 0;
   if (e == cudaSuccess) e = cudaMemcpyAsync(&nnz, row_ptr + rows, 4, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -429,7 +428,7 @@ int qftc_csr_compact(int rows, const int32_t* row_start, const int32_t* row_coun
   if (!row_count) return fail(QFTC_EINVAL, "csr_compact: row_count is required");
   if (int rc = require_device()) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  QFTC_CUDA(csr_row_ptr(row_count, rows, row_ptr, st), "csr_row_ptr");
+  QFTC_CUDA(csr_row_ptr(row_count, rows, row_ptr, st, row_start), "csr_row_ptr");
   QFTC_CUDA(csr_copy_rows(rows, row_start, row_count, col_idx, values, row_ptr, col_out, val_out,
                           capacity, st),
             "csr_copy_rows");
@@ -459,7 +458,11 @@ struct qftc_plan {
   bool rows_path = false;     // v6 rows kernel (prep + stable rows + general rows)
   RowPrep* prep = nullptr;    // per-row records
   RowBlock* xlist = nullptr;  // general-tier rows
-  int32_t* xcount = nullptr;
+  RowsCache rc;               // resolved launches of the rows path (+ its row-list counters)
+  KLaunch gen[2];             // general path (no rows kernel): by weight decay == 0
+  const char* last_kernel = "";  // the main kernel instance of the last step
+  volatile uint32_t* oflag_host = nullptr;  // mapped pinned copy of the overflow flag
+  uint32_t* oflag_dev = nullptr;
   int slotted[2] = {0, 0};
   int32_t* col[2] = {nullptr, nullptr};
   float* val[2] = {nullptr, nullptr};
@@ -550,10 +553,22 @@ int qftc_plan_create(qftc_plan** out, const qftc_lion_tensor* ts, int n, int bit
     cudaError_t e = cudaMallocAsync((void**)&p->prep, sizeof(RowPrep) * (size_t)rows, st);
     if (e == cudaSuccess)
       e = cudaMallocAsync((void**)&p->xlist, sizeof(RowBlock) * (size_t)rows, st);
-    if (e == cudaSuccess) e = cudaMallocAsync((void**)&p->xcount, 16, st);
+    if (e == cudaSuccess) e = cudaMallocAsync((void**)&p->rc.xcount, 16, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p->rc.xcount, 0, 16, st);
     if (e != cudaSuccess) {
       qftc_plan_destroy(p);
       return fail(QFTC_ECUDA, std::string("plan_create: ") + cudaGetErrorString(e));
+    }
+  }
+  {
+    // the overflow flag, also written to mapped pinned memory so the host sees it at the
+    // next step without a synchronisation (qftc_plan_pending_overflow)
+    void* hp = nullptr;
+    if (cudaHostAlloc(&hp, 64, cudaHostAllocMapped) == cudaSuccess) {
+      p->oflag_host = reinterpret_cast<volatile uint32_t*>(hp);
+      *p->oflag_host = 0u;
+      void* dp = nullptr;
+      if (cudaHostGetDevicePointer(&dp, hp, 0) == cudaSuccess) p->oflag_dev = (uint32_t*)dp;
     }
   }
   for (int k = 0; k < 2; ++k) {
@@ -604,16 +619,20 @@ int qftc_plan_step(qftc_plan* p, int flip, qftc_lion_hyper h, qftc_stream_t stre
   a.oldcap = p->oldcap;
   a.use_bulk = p->use_bulk;
   a.slotted_in = p->slotted[flip];
+  a.oflag = p->oflag_dev;
   if (p->rows_path) {
     a.cols_p = p->uniform_cols;
     a.oldcap6 = rows_kernel_oldcap(p->uniform_cols);
     a.prep = p->prep;
     a.xlist = p->xlist;
-    a.xcount = p->xcount;
-    QFTC_CUDA(launch_rows_step(a, (cudaStream_t)stream), "lion step (rows kernel)");
+    QFTC_CUDA(launch_rows_step(a, p->rc, (cudaStream_t)stream), "lion step (rows kernel)");
+    p->last_kernel = p->rc.rows[a.slotted_in ? 1 : 0].name;
     return QFTC_OK;
   }
-  QFTC_CUDA(launch_step_kernel(p->grad_kind, a, (cudaStream_t)stream), "lion step kernel");
+  KLaunch& k = p->gen[a.wd == 0.0f ? 1 : 0];
+  if (!k.fn) QFTC_CUDA(resolve_step_kernel(p->grad_kind, a, &k), "lion step kernel (resolve)");
+  QFTC_CUDA(launch_k(k, a, (cudaStream_t)stream), "lion step kernel");
+  p->last_kernel = k.name;
   return QFTC_OK;
 }
 
@@ -626,6 +645,7 @@ int qftc_plan_result(qftc_plan* p, int64_t* nnz_total, qftc_stream_t stream) {
   // clear the sticky flags for the next check
   QFTC_CUDA(cudaMemsetAsync(&p->sc.hdr->overflow, 0, 8, st), "clear flags");
   QFTC_CUDA(cudaStreamSynchronize(st), "sync");
+  if (p->oflag_host) *p->oflag_host = 0u;
   if (h.err & ERR_MPARAMS)
     return fail(QFTC_EINVAL, "affine_params_from_bounds: min > max in momentum channel");
   if (h.err & ERR_GPARAMS)
@@ -637,12 +657,35 @@ int qftc_plan_result(qftc_plan* p, int64_t* nnz_total, qftc_stream_t stream) {
 
 int qftc_plan_launches(const qftc_plan* p) { return p ? (p->rows_path ? 3 : 1) : 0; }
 
+const char* qftc_plan_kernel_name(const qftc_plan* p) { return p ? p->last_kernel : ""; }
+
+int qftc_plan_pending_overflow(const qftc_plan* p) {
+  return (p && p->oflag_host && *p->oflag_host) ? 1 : 0;
+}
+
+int qftc_plan_tier_rows(qftc_plan* p, int64_t* stable_rows, int64_t* general_rows,
+                        qftc_stream_t stream) {
+  if (!p) return fail(QFTC_EINVAL, "plan: null");
+  int64_t gen = p->total_rows;  // without the rows kernel every row runs the general kernel
+  if (p->rows_path && p->rc.last_flip >= 0) {
+    int32_t x = 0;
+    QFTC_CUDA(cudaMemcpyAsync(&x, p->rc.xcount + p->rc.last_flip, 4, cudaMemcpyDeviceToHost,
+                              (cudaStream_t)stream), "read row list");
+    QFTC_CUDA(cudaStreamSynchronize((cudaStream_t)stream), "sync");
+    gen = x;
+  }
+  if (stable_rows) *stable_rows = p->total_rows - gen;
+  if (general_rows) *general_rows = gen;
+  return QFTC_OK;
+}
+
 int qftc_plan_destroy(qftc_plan* p) {
   if (!p) return QFTC_OK;
   cudaFree(p->sc.base);
   if (p->prep) cudaFree(p->prep);
   if (p->xlist) cudaFree(p->xlist);
-  if (p->xcount) cudaFree(p->xcount);
+  if (p->rc.xcount) cudaFree(p->rc.xcount);
+  if (p->oflag_host) cudaFreeHost(const_cast<uint32_t*>(p->oflag_host));
   delete p;
   return QFTC_OK;
 }

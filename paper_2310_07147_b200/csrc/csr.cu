@@ -26,9 +26,19 @@ __global__ void k_slot_caps(const int32_t* counts, const int32_t* row_ptr, int r
   }
 }
 
-__global__ void k_counts(const int32_t* counts, const int32_t* row_ptr, int rows, int32_t* out) {
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r <= rows; r += gridDim.x * blockDim.x)
-    out[r] = (r == rows) ? 0 : (counts ? counts[r] : row_ptr[r + 1] - row_ptr[r]);
+// per-row entry counts: from a strict row_ptr, or from slot counts clamped to their slot
+// (slot_start != nullptr: a count above its slot -- an overflowed step that was not re-run
+// -- never reaches into the next row's entries)
+__global__ void k_counts(const int32_t* counts, const int32_t* row_ptr, int rows, int32_t* out,
+                         const int32_t* slot_start) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r <= rows; r += gridDim.x * blockDim.x) {
+    int n = 0;
+    if (r < rows) {
+      n = counts ? counts[r] : row_ptr[r + 1] - row_ptr[r];
+      if (counts && slot_start) n = min(n, slot_start[r + 1] - slot_start[r]);
+    }
+    out[r] = n;
+  }
 }
 
 // copy each row's entries from src (slotted: start+count, or strict: row_ptr) to
@@ -40,7 +50,8 @@ __global__ void k_copy_rows(int rows, const int32_t* src_start, const int32_t* s
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += warps) {
     const int s = src_start[r];
-    const int n = src_count ? src_count[r] : src_start[r + 1] - s;
+    // slotted source: the used entries, never past the slot end (see k_counts)
+    const int n = src_count ? min(src_count[r], src_start[r + 1] - s) : src_start[r + 1] - s;
     const int64_t d = dst_start[r];
     for (int i = lane; i < n; i += 32) {
       if (d + i < dst_cap) {
@@ -89,12 +100,13 @@ cudaError_t csr_copy_rows(int rows, const int32_t* src_start, const int32_t* src
   return cudaGetLastError();
 }
 
-// strict row_ptr (rows+1) from slot counts
-cudaError_t csr_row_ptr(const int32_t* counts, int rows, int32_t* row_ptr, cudaStream_t st) {
+// strict row_ptr (rows+1) from counts (clamped to their slots when slot_start is given)
+cudaError_t csr_row_ptr(const int32_t* counts, int rows, int32_t* row_ptr, cudaStream_t st,
+                        const int32_t* slot_start) {
   int32_t* tmp = nullptr;
   cudaError_t e = cudaMallocAsync((void**)&tmp, sizeof(int32_t) * (rows + 1), st);
   if (e != cudaSuccess) return e;
-  k_counts<<<grid_for(rows + 1, 256), 256, 0, st>>>(counts, nullptr, rows, tmp);
+  k_counts<<<grid_for(rows + 1, 256), 256, 0, st>>>(counts, nullptr, rows, tmp, slot_start);
   e = exclusive_scan(tmp, row_ptr, rows + 1, st);
   cudaFreeAsync(tmp, st);
   return e;

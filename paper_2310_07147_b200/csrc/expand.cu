@@ -102,7 +102,9 @@ __device__ __forceinline__ RowMeta row_meta(const ExpArgs& a, long long grow) {
   m.s = T.scale[m.r];
   m.z = T.zp[m.r];
   m.b = T.rs[m.r];
-  m.n = T.cnt ? T.cnt[m.r] : (T.rs[m.r + 1] - m.b);
+  // a slotted row uses at most its slot: a count above it (an overflowed step that was
+  // not re-run) must not read the next row's entries
+  m.n = T.cnt ? min(T.cnt[m.r], T.rs[m.r + 1] - m.b) : (T.rs[m.r + 1] - m.b);
   return m;
 }
 

@@ -101,8 +101,8 @@ PYBIND11_MODULE(qft_engine, m) {
       "quantize_roundtrip",
       [](const FloatArray& x, int bit_width) {
         const auto t = to_tensor(x);
-        const auto q = qft_b200::quantize_state<QT>(t, bit_width);
-        return to_array(qft_b200::dequantize<Tensor>(q));
+        const auto q = qft_b200::generic::quantize_state<QT>(t, bit_width);
+        return to_array(qft_b200::generic::dequantize<Tensor>(q));
       },
       py::arg("x"), py::arg("bit_width") = 8,
       "Channel-wise affine quantize + dequantize; rows are channels.");
@@ -110,7 +110,7 @@ PYBIND11_MODULE(qft_engine, m) {
   m.def(
       "quantize_params",
       [](const FloatArray& x, int bit_width) {
-        const auto q = qft_b200::quantize_state<QT>(to_tensor(x), bit_width);
+        const auto q = qft_b200::generic::quantize_state<QT>(to_tensor(x), bit_width);
         py::dict d;
         d["scale"] = py::cast(q.params.scale);
         d["zero_point"] = py::cast(q.params.zero_point);
@@ -124,9 +124,9 @@ PYBIND11_MODULE(qft_engine, m) {
       [](const FloatArray& x, double outlier_fraction, int bit_width,
          const std::string& threshold_kind) {
         const auto t = to_tensor(x);
-        const auto dsw = qft_b200::decompose_weight<DSW>(t, outlier_fraction, bit_width,
+        const auto dsw = qft_b200::generic::decompose_weight<DSW>(t, outlier_fraction, bit_width,
                                                          kind_from_name(threshold_kind));
-        const auto back = qft_b200::reconstruct<Tensor>(dsw);
+        const auto back = qft_b200::generic::reconstruct<Tensor>(dsw);
         py::dict d;
         d["reconstructed"] = to_array(back);
         d["nnz"] = dsw.sparse.nnz();
@@ -147,11 +147,11 @@ PYBIND11_MODULE(qft_engine, m) {
         const int kind = kind_from_name(threshold_kind);
         py::list out;
         for (double f : fractions) {  // profiler.cpp:187-201
-          const auto dsw = qft_b200::decompose_weight<DSW>(t, f, bit_width, kind);
+          const auto dsw = qft_b200::generic::decompose_weight<DSW>(t, f, bit_width, kind);
           py::dict d;
           d["fraction"] = f;
           d["bytes"] = byte_size(dsw);
-          d["l2_error"] = l2(qft_b200::reconstruct<Tensor>(dsw), t);
+          d["l2_error"] = l2(qft_b200::generic::reconstruct<Tensor>(dsw), t);
           out.append(d);
         }
         return out;

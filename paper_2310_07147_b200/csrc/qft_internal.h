@@ -97,6 +97,8 @@ struct LaunchArgs {
   RowBlock* xlist;               // rows outside the stable tier (general kernel)
   int32_t* xcount;               // their number (device)
   const int32_t* n_blocks_dev;   // step_kernel: read the block count from the device
+  int32_t* xclear;               // prep: the OTHER flip's row-list counter, zeroed for the next step
+  uint32_t* oflag;               // mapped pinned overflow flag (host-visible without a sync)
 };
 
 // Per-row record of the rows kernel (128 B), written by k_step_prep every step and
@@ -128,12 +130,33 @@ static_assert(sizeof(RowPrep) == 128, "RowPrep is one 128-byte record");
 size_t step_kernel_smem(int gk, int cols_p, int oldcap);
 cudaError_t launch_step_kernel(int gk, const LaunchArgs& a, cudaStream_t s);
 
+// A resolved kernel launch (function, geometry, instance name), computed once per plan so
+// the per-step host path is one cudaLaunchKernel per kernel (no attribute / occupancy
+// queries, no environment reads).
+struct KLaunch {
+  const void* fn = nullptr;
+  int grid = 0, block = 0;
+  size_t smem = 0;
+  char name[96] = {0};
+};
+cudaError_t launch_k(const KLaunch& k, const LaunchArgs& a, cudaStream_t s);
+// the general step kernel's launch for grad kind gk (rows of a.n_blocks / the device list)
+cudaError_t resolve_step_kernel(int gk, const LaunchArgs& a, KLaunch* out);
+
+// per-plan launch cache of the rows path (rowstep.cu)
+struct RowsCache {
+  KLaunch rows[2];     // by slotted input (0/1)
+  KLaunch gen[2];      // general kernel over the device list, by weight decay == 0 (0/1)
+  int last_flip = -1;  // the flip of the previous step (a repeated flip re-zeroes its counter)
+  int32_t* xcount = nullptr;  // [2] row-list counters, one per flip
+};
+
 int step_kernel_max_cols();
 
 // v6 rows kernel (rowstep.cu): prep + stable rows + step_kernel over the rest
 bool rows_kernel_eligible(int gk, int use_bulk, int uniform_cols);
 int rows_kernel_oldcap(int cols);
-cudaError_t launch_rows_step(const LaunchArgs& a, cudaStream_t s);
+cudaError_t launch_rows_step(const LaunchArgs& a, RowsCache& c, cudaStream_t s);
 
 // decomposition with given thresholds (decompose.cu)
 cudaError_t decompose_codes(const float* w, int rows, int cols, const float* scale,
@@ -142,7 +165,8 @@ cudaError_t decompose_codes(const float* w, int rows, int cols, const float* sca
 cudaError_t decompose_csr(const float* w, int rows, int cols, const float* t_min,
                           const float* t_max, const int32_t* row_ptr, int32_t* col_idx,
                           float* values, cudaStream_t s);
-cudaError_t csr_row_ptr(const int32_t* counts, int rows, int32_t* row_ptr, cudaStream_t s);
+cudaError_t csr_row_ptr(const int32_t* counts, int rows, int32_t* row_ptr, cudaStream_t s,
+                        const int32_t* slot_start = nullptr);
 
 // checkpoint CRC over device segments (crc32.cu); synchronises
 cudaError_t crc32_device(const void* const* segs, const int64_t* lens, int n, uint32_t* crc_out,

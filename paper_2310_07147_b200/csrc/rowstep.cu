@@ -49,6 +49,7 @@
 #include "qft_internal.h"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 namespace qftk {
@@ -588,7 +589,10 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
         *R.m_zp_out = zmv;
         const int total = (int)(tot0 + tot1);
         *R.cnt_out = total;
-        if (total > co) atomicOr(&a.hdr->overflow, 1u);
+        if (total > co) {
+          atomicOr(&a.hdr->overflow, 1u);
+          if (a.oflag) *reinterpret_cast<volatile uint32_t*>(a.oflag) = 1u;
+        }
       }
       }
       if (NW == 1) {
@@ -681,6 +685,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
 // One thread per row of the launch: the RowPrep record and the tier decision.
 __global__ void k_step_prep(const LaunchArgs a, int stable_ok) {
   const int gr = blockIdx.x * blockDim.x + threadIdx.x;
+  if (gr == 0 && a.xclear) *a.xclear = 0;  // the next step's row-list counter
   if (gr >= a.total_rows) return;
   // tensor of the row (binary search over the row bases)
   int lo = 0, hi = a.n_tensors - 1;
@@ -783,8 +788,21 @@ __global__ void k_step_prep(const LaunchArgs a, int stable_ok) {
 }
 
 // ---------------------------------------------------------------------------- launch
+cudaError_t launch_k(const KLaunch& k, const LaunchArgs& a, cudaStream_t st) {
+  LaunchArgs aa = a;
+  void* args[] = {&aa};
+  return cudaLaunchKernel(k.fn, dim3((unsigned)k.grid), dim3((unsigned)k.block), args, k.smem, st);
+}
+
+// QFT_ROWS_GRID caps a persistent grid (read once, when a plan resolves its launches):
+// the tests use it so every CTA pipelines many rows
+static long grid_cap() {
+  const char* g = getenv("QFT_ROWS_GRID");
+  return g ? std::max(1L, atol(g)) : 0L;
+}
+
 template <int MAXT, int MINB, int NS, int FULL = 0, int CCOLS = 0, int BWC = 0>
-static cudaError_t rows_launch_t(const LaunchArgs& a, int nt, size_t smem, cudaStream_t st) {
+static cudaError_t rows_resolve_t(const LaunchArgs& a, int nt, size_t smem, KLaunch* out) {
   auto k = rows_kernel<MAXT, MINB, NS, FULL, CCOLS, BWC>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -796,11 +814,15 @@ static cudaError_t rows_launch_t(const LaunchArgs& a, int nt, size_t smem, cudaS
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   long grid = (long)sms * per_sm;
   if (grid > a.total_rows) grid = a.total_rows;
-  // QFT_ROWS_GRID caps the grid: the tests use it so every CTA pipelines many rows
-  if (const char* g = getenv("QFT_ROWS_GRID")) grid = std::min(grid, std::max(1L, atol(g)));
+  if (const long cap = grid_cap()) grid = std::min(grid, cap);
   if (grid < 1) grid = 1;
-  k<<<(unsigned)grid, nt, smem, st>>>(a);
-  return cudaGetLastError();
+  out->fn = reinterpret_cast<const void*>(k);
+  out->grid = (int)grid;
+  out->block = nt;
+  out->smem = smem;
+  snprintf(out->name, sizeof(out->name), "rows_kernel<%d,%d,%d,%d,%d,%d>", MAXT, MINB, NS, FULL,
+           CCOLS, BWC);
+  return cudaSuccess;
 }
 
 bool rows_kernel_eligible(int gk, int use_bulk, int uniform_cols) {
@@ -817,61 +839,71 @@ bool rows_kernel_eligible(int gk, int use_bulk, int uniform_cols) {
 #define QFT_ROWS_MINB_M 2  // rows of <= 12288 columns (<= 384 threads)
 #endif
 
-cudaError_t launch_rows_step(const LaunchArgs& a0, cudaStream_t st) {
-  LaunchArgs a = a0;
-  a.negzero = -0.0f;
-  cudaError_t e = cudaMemsetAsync(a.xcount, 0, sizeof(int32_t), st);
-  if (e != cudaSuccess) return e;
-  const int pt = 256;
-  k_step_prep<<<(a.total_rows + pt - 1) / pt, pt, 0, st>>>(a, 1);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+// the rows-kernel instance of a launch (compile-time geometry for the LLaMA-2 widths
+// 4096 / 11008 (7B) and 5120 / 13824 (13B), used only when the plan's table size is the
+// one that geometry implies)
+static cudaError_t rows_resolve(const LaunchArgs& a, KLaunch* out) {
   const int nt = rows_kernel_nt(a.cols_p);
   const size_t smem = rows_kernel_smem(a.cols_p, a.oldcap6);
-  // compile-time geometry for the LLaMA-2 widths (4096 / 11008: 7B; 5120 / 13824: 13B),
-  // used only when the plan's table size is the one that geometry implies
   const int c = a.cols_p;
   auto geom_ok = [&](int cc, int ns) {
     return c == cc && a.oldcap6 == geom_oldcap(cc, ns) && a.slotted_in;
   };
   const bool b8 = QFT_BW8 && a.bit_width == 8;  // the 7B widths also get a constant width
   if (nt == 128 && geom_ok(4096, 3) && b8)
-    e = rows_launch_t<128, QFT_ROWS_MINB_S, 3, 2, 4096, 8>(a, nt, smem, st);
-  else if (nt == 128 && geom_ok(4096, 3))
-    e = rows_launch_t<128, QFT_ROWS_MINB_S, 3, 2, 4096>(a, nt, smem, st);
-  else if (geom_ok(11008, 2) && b8)
-    e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1, 11008, 8>(a, nt, smem, st);
+    return rows_resolve_t<128, QFT_ROWS_MINB_S, 3, 2, 4096, 8>(a, nt, smem, out);
+  if (nt == 128 && geom_ok(4096, 3))
+    return rows_resolve_t<128, QFT_ROWS_MINB_S, 3, 2, 4096>(a, nt, smem, out);
+  if (geom_ok(11008, 2) && b8)
+    return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 11008, 8>(a, nt, smem, out);
 #if QFT_BW34
   // the down-projection sweep (configs[4]) also runs 3- and 4-bit codes
-  else if (geom_ok(11008, 2) && a.bit_width == 4)
-    e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1, 11008, 4>(a, nt, smem, st);
-  else if (geom_ok(11008, 2) && a.bit_width == 3)
-    e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1, 11008, 3>(a, nt, smem, st);
+  if (geom_ok(11008, 2) && a.bit_width == 4)
+    return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 11008, 4>(a, nt, smem, out);
+  if (geom_ok(11008, 2) && a.bit_width == 3)
+    return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 11008, 3>(a, nt, smem, out);
 #endif
-  else if (geom_ok(11008, 2))
-    e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1, 11008>(a, nt, smem, st);
-  else if (geom_ok(5120, 2) && b8)
-    e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1, 5120, 8>(a, nt, smem, st);
-  else if (geom_ok(5120, 2))
-    e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1, 5120>(a, nt, smem, st);
-  else if (geom_ok(13824, 2) && b8)
-    e = rows_launch_t<512, 1, 2, 1, 13824, 8>(a, nt, smem, st);
-  else if (geom_ok(13824, 2))
-    e = rows_launch_t<512, 1, 2, 1, 13824>(a, nt, smem, st);
-  else if (nt <= 128)
-    e = rows_launch_t<128, QFT_ROWS_MINB_S, 3>(a, nt, smem, st);
-  else if (nt <= 384 && c / 16 >= nt)
-    e = rows_launch_t<384, QFT_ROWS_MINB_M, 2, 1>(a, nt, smem, st);
-  else if (nt <= 384)
-    e = rows_launch_t<384, QFT_ROWS_MINB_M, 2>(a, nt, smem, st);
-  else
-    e = rows_launch_t<512, 1, 2>(a, nt, smem, st);
-  if (e != cudaSuccess) return e;
+  if (geom_ok(11008, 2)) return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 11008>(a, nt, smem, out);
+  if (geom_ok(5120, 2) && b8)
+    return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 5120, 8>(a, nt, smem, out);
+  if (geom_ok(5120, 2)) return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 5120>(a, nt, smem, out);
+  if (geom_ok(13824, 2) && b8) return rows_resolve_t<512, 1, 2, 1, 13824, 8>(a, nt, smem, out);
+  if (geom_ok(13824, 2)) return rows_resolve_t<512, 1, 2, 1, 13824>(a, nt, smem, out);
+  if (nt <= 128) return rows_resolve_t<128, QFT_ROWS_MINB_S, 3>(a, nt, smem, out);
+  if (nt <= 384 && c / 16 >= nt) return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1>(a, nt, smem, out);
+  if (nt <= 384) return rows_resolve_t<384, QFT_ROWS_MINB_M, 2>(a, nt, smem, out);
+  return rows_resolve_t<512, 1, 2>(a, nt, smem, out);
+}
+
+// One step of a rows-path plan: k_step_prep (records + the device list of general-tier
+// rows), the rows kernel over the stable tier, the general kernel over the list.  Every
+// launch is resolved once per plan (RowsCache); the list counter of this flip was zeroed
+// by the previous step's prep (a repeated flip -- a re-run after an overflow -- zeroes it
+// here).
+cudaError_t launch_rows_step(const LaunchArgs& a0, RowsCache& c, cudaStream_t st) {
+  LaunchArgs a = a0;
+  a.negzero = -0.0f;
+  a.xcount = c.xcount + a.flip;
+  a.xclear = c.xcount + (1 - a.flip);
+  cudaError_t e;
+  if (c.last_flip == a.flip &&
+      (e = cudaMemsetAsync(a.xcount, 0, sizeof(int32_t), st)) != cudaSuccess)
+    return e;
+  c.last_flip = a.flip;
+  const int pt = 256;
+  k_step_prep<<<(a.total_rows + pt - 1) / pt, pt, 0, st>>>(a, 1);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  KLaunch& rk = c.rows[a.slotted_in ? 1 : 0];
+  if (!rk.fn && (e = rows_resolve(a, &rk)) != cudaSuccess) return e;
+  if ((e = launch_k(rk, a, st)) != cudaSuccess) return e;
   // the general kernel over the device row list
   LaunchArgs x = a;
   x.blocks = a.xlist;
   x.n_blocks = a.total_rows;  // upper bound; the kernel reads the true count
   x.n_blocks_dev = a.xcount;
-  return launch_step_kernel(G_U8, x, st);
+  KLaunch& gk = c.gen[a.wd == 0.0f ? 1 : 0];
+  if (!gk.fn && (e = resolve_step_kernel(G_U8, x, &gk)) != cudaSuccess) return e;
+  return launch_k(gk, x, st);
 }
 
 }  // namespace qftk

@@ -40,6 +40,8 @@
 #include "qft_device.cuh"
 #include "qft_internal.h"
 
+#include <cstdio>
+
 namespace qftk {
 using namespace qftd;
 
@@ -671,7 +673,10 @@ __global__ void __launch_bounds__(ws::NW * 32, QFT_STEP_MIN_CTAS) step_kernel(co
         Tt->m_scale[out][lrow] = smv;
         Tt->m_zp[out][lrow] = zmv;
         Tt->cnt[out][lrow] = base;
-        if (base > cap_out) atomicOr(&a.hdr->overflow, 1u);
+        if (base > cap_out) {
+          atomicOr(&a.hdr->overflow, 1u);
+          if (a.oflag) *reinterpret_cast<volatile uint32_t*>(a.oflag) = 1u;
+        }
       }
       smv = __shfl_sync(FULL, smv, 0);
       zmv = __shfl_sync(FULL, zmv, 0);
@@ -740,7 +745,7 @@ __global__ void __launch_bounds__(ws::NW * 32, QFT_STEP_MIN_CTAS) step_kernel(co
 
 // ----------------------------------------------------------------------------
 template <int GK, bool AL, bool WD0>
-static cudaError_t step_launch_t(const LaunchArgs& a, size_t smem, cudaStream_t st) {
+static cudaError_t step_resolve_t(const LaunchArgs& a, size_t smem, KLaunch* out) {
   auto k = step_kernel<GK, AL, WD0>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -754,25 +759,36 @@ static cudaError_t step_launch_t(const LaunchArgs& a, size_t smem, cudaStream_t 
   const long need = ((long)a.n_blocks + ws::NW - 1) / ws::NW;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  k<<<(unsigned)grid, ws::NW * 32, smem, st>>>(a);
-  return cudaGetLastError();
+  out->fn = reinterpret_cast<const void*>(k);
+  out->grid = (int)grid;
+  out->block = ws::NW * 32;
+  out->smem = smem;
+  snprintf(out->name, sizeof(out->name), "step_kernel<%d,%d,%d>", GK, AL ? 1 : 0, WD0 ? 1 : 0);
+  return cudaSuccess;
 }
 
-cudaError_t launch_step_kernel(int gk, const LaunchArgs& a, cudaStream_t st) {
+cudaError_t resolve_step_kernel(int gk, const LaunchArgs& a, KLaunch* out) {
   const size_t smem = step_kernel_smem(gk, a.cols_p, a.oldcap);
   const bool al = a.use_bulk != 0;
   const bool wd0 = (a.wd == 0.0f);
-#define SK_L(G)                                                                   \
+#define SK_R(G)                                                                   \
   do {                                                                            \
-    if (al) return wd0 ? step_launch_t<G, true, true>(a, smem, st)                \
-                       : step_launch_t<G, true, false>(a, smem, st);              \
-    return wd0 ? step_launch_t<G, false, true>(a, smem, st)                       \
-               : step_launch_t<G, false, false>(a, smem, st);                     \
+    if (al) return wd0 ? step_resolve_t<G, true, true>(a, smem, out)              \
+                       : step_resolve_t<G, true, false>(a, smem, out);            \
+    return wd0 ? step_resolve_t<G, false, true>(a, smem, out)                     \
+               : step_resolve_t<G, false, false>(a, smem, out);                   \
   } while (0)
-  if (gk == G_U8) SK_L(G_U8);
-  if (gk == G_F32) SK_L(G_F32);
-  SK_L(G_BF16);
-#undef SK_L
+  if (gk == G_U8) SK_R(G_U8);
+  if (gk == G_F32) SK_R(G_F32);
+  SK_R(G_BF16);
+#undef SK_R
+}
+
+cudaError_t launch_step_kernel(int gk, const LaunchArgs& a, cudaStream_t st) {
+  KLaunch k;
+  cudaError_t e = resolve_step_kernel(gk, a, &k);
+  if (e != cudaSuccess) return e;
+  return launch_k(k, a, st);
 }
 
 }  // namespace qftk

@@ -66,6 +66,13 @@ class QftModelState:
         self.cur = 0
         self.steps = 0
         self.replans = 0
+        # the decomposition config the state was built with (DenseSparseWeight::
+        # outlier_fraction, quantize.hpp:70; ModelConfig::threshold_kind): recorded by
+        # init_from_weights / init_from_host(fraction=...) / load_checkpoint, written by
+        # save_checkpoint.  None: unknown (save_checkpoint then requires explicit meta).
+        self.outlier_fraction: Optional[float] = None
+        self.threshold_kind: int = 0
+        self.checkpoint_meta = None
         order = list(range(self.n))
         if group_contiguous:
             order.sort(key=lambda i: (self.shapes[i][1], i))
@@ -210,6 +217,7 @@ class QftModelState:
 
         ``weight_fn(i)`` returns the fp32 [rows, cols] CUDA tensor of tensor i."""
         k = kind_from_name(kind)
+        self.outlier_fraction, self.threshold_kind = float(fraction), int(k)
         cur = self.cur
         for g in self.groups:
             base = 0
@@ -239,11 +247,17 @@ class QftModelState:
             self._mirror_layout(g, cur)
         self._make_plans()
 
-    def init_from_host(self, tensors: Sequence[dict]):
+    def init_from_host(self, tensors: Sequence[dict], fraction: Optional[float] = None,
+                       kind="percentile"):
         """Upload reference-layout state (e.g. from the CPU oracle).  Each dict holds
         codes, scale, zero_point, t_min, t_max, row_ptr, col_idx, values (the
-        DenseSparseWeight) and optionally m_codes, m_scale, m_zero_point."""
+        DenseSparseWeight) and optionally m_codes, m_scale, m_zero_point.  `fraction` /
+        `kind`: the outlier config the thresholds were computed with (recorded for
+        save_checkpoint)."""
         cur = self.cur
+        if fraction is not None:
+            self.outlier_fraction = float(fraction)
+            self.threshold_kind = int(kind_from_name(kind))
 
         def dv(a, dt):
             return torch.as_tensor(np.ascontiguousarray(a)).to(self.device, dt)
@@ -403,21 +417,51 @@ class QftModelState:
         (the step's inputs are intact in the other set)."""
         h = N.hyper(lr, beta1, beta2, weight_decay)
         flip = self.cur
+        self._refuse_if_overflowed("step")
         for g in self.groups:
             N.check(N.lib.qftc_plan_step(g.plan, flip, h, _stream()))
         self.cur = 1 - flip
         self.steps += 1
+        self._last = (flip, h)
         if check:
             self._check(flip, h)
 
+    def _refuse_if_overflowed(self, what: str):
+        """A step enqueued with check=False that overflowed a CSR slot left its output set
+        incomplete (every consumer clamps counts to the slot, so nothing reads out of
+        bounds, but outliers are missing).  The flag is a mapped host word, visible without
+        a synchronisation once that step ran: refuse to build on the state."""
+        for g in self.groups:
+            if N.lib.qftc_plan_pending_overflow(g.plan):
+                raise N.CsrOverflow(
+                    f"{what}: a previous step(check=False) overflowed a CSR slot of the "
+                    f"{g.cols}-column group; its output is incomplete -- call recover() "
+                    "(re-plans and re-runs that step from its intact inputs) before "
+                    "feeding the next gradient")
+
+    def recover(self):
+        """Repair the last step after an unchecked overflow: re-plan the overflowed
+        groups' output slots and re-run the step from its input set (the ping-pong inputs
+        and the gradient buffers must still hold that step's inputs)."""
+        if getattr(self, "_last", None) is None:
+            return
+        self._check(*self._last)
+
     def _replan(self, g: _Group, k: int):
-        """Slots of set k re-sized from its (true) counts."""
+        """Slots of set k re-sized from its (true) counts plus, as at placement
+        (_place_strict), the dense elements at code 0 / qmax of the step's output codes:
+        only those can become new outliers in a stable-tier step, so the padding keeps the
+        no-overflow guarantee of the placement after a replan."""
         base = 0
+        qmax = (1 << self.bit_width) - 1
         for i in g.members:
             r = self.shapes[i][0]
             rs = self._rs(self.row_start[k], i)
             total = C.c_int64(0)
-            N.check(N.lib.qftc_csr_plan_slots(_p(self._rows(self.row_count[k], i)), None, r,
+            codes = self._sl(self.w_codes[k], i)
+            edge = ((codes == 0) | (codes == qmax)).sum(dim=1, dtype=torch.int32)
+            want = self._rows(self.row_count[k], i) + edge
+            N.check(N.lib.qftc_csr_plan_slots(_p(want), None, r,
                                               SLACK, _p(rs), C.byref(total), _stream()))
             rs += base
             base += int(total.value)
@@ -442,6 +486,22 @@ class QftModelState:
             if replanned:  # the dead input set takes the new layout for the next step
                 self._mirror_layout(g, out)
                 self._set_arena(g)
+
+    def kernel_names(self) -> List[str]:
+        """The main kernel instance each width class ran in the last step (per group,
+        e.g. ``rows_kernel<128,5,3,2,4096,8>``; see ``qftc_plan_kernel_name``)."""
+        return [N.lib.qftc_plan_kernel_name(g.plan).decode() for g in self.groups]
+
+    def tier_rows(self) -> Tuple[int, int]:
+        """(stable-tier rows, general-tier rows) of the last step over all groups
+        (synchronises)."""
+        st = gen = 0
+        for g in self.groups:
+            a, b = C.c_int64(0), C.c_int64(0)
+            N.check(N.lib.qftc_plan_tier_rows(g.plan, C.byref(a), C.byref(b), _stream()))
+            st += a.value
+            gen += b.value
+        return st, gen
 
     def check(self):
         """Synchronise and validate the last step (raises on overflow / bad rows)."""
@@ -541,6 +601,7 @@ class QftModelState:
         """Reconstruct every tensor (dense dequant + CSR overwrite, quantize.hpp:331-338)
         into outs (all f32 or all bf16) with one grouped launch -- the weight expansion
         for the next forward (network.hpp:208-211)."""
+        self._refuse_if_overflowed("expand")
         tab, bf16 = table if table is not None else self.expand_table(outs, rows)
         N.check(N.lib.qftc_expand(C.cast(tab, C.c_void_p), len(tab), bf16, _stream()))
         return outs
