@@ -297,7 +297,7 @@ qft::DenseSparseWeight<T> decompose_dense_sparse(const qft::Tensor<T>& w,
 template <typename T>
 qft::DenseSparseWeight<T> make_passthrough_weight(const qft::Tensor<T>& w) {
   qft::DenseSparseWeight<T> out;
-  out.dense = quantize_state(w, 8, static_cast<qft::QuantMode>(detail::kPassthrough));
+  out.dense = qft_b200::quantize_state(w, 8, static_cast<qft::QuantMode>(detail::kPassthrough));
   out.sparse.row_ptr.assign(static_cast<size_t>(w.rows()) + 1, 0);
   return out;
 }
@@ -309,7 +309,7 @@ qft::DenseSparseWeight<T> decompose_weight(const qft::Tensor<T>& w, double fract
                                            KindT kind = static_cast<KindT>(0)) {
   static_assert(std::is_same<T, float>::value, "the B200 path is fp32 (T = float)");
   if (static_cast<int>(mode) == detail::kPassthrough) {
-    auto out = make_passthrough_weight(w);
+    auto out = qft_b200::make_passthrough_weight(w);
     out.outlier_fraction = fraction;
     return out;
   }
@@ -322,11 +322,11 @@ template <typename T>
 void requantize_weight(qft::DenseSparseWeight<T>& dsw, const qft::Tensor<T>& w_fp, int bit_width) {
   if (static_cast<int>(dsw.dense.mode) == detail::kPassthrough) {
     const double fraction = dsw.outlier_fraction;
-    dsw = make_passthrough_weight(w_fp);
+    dsw = qft_b200::make_passthrough_weight(w_fp);
     dsw.outlier_fraction = fraction;
     return;
   }
-  auto next = decompose_dense_sparse(w_fp, dsw.t_min, dsw.t_max, bit_width);
+  auto next = qft_b200::decompose_dense_sparse(w_fp, dsw.t_min, dsw.t_max, bit_width);
   next.outlier_fraction = dsw.outlier_fraction;
   dsw = std::move(next);
 }
