@@ -226,12 +226,14 @@ def run_gpu_arm(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2310_07147_b200 as q
-    from paper_2310_07147_b200.shapes import count, llama2_7b, shard_rows
+    from paper_2310_07147_b200.shapes import count, llama2_7b
 
     full = llama2_7b()
-    shapes = shard_rows(full, world, rank) if world > 1 else full
+    if world > 1:
+        return run_multi_gpu(args, full, world, rank, local, q)
+    shapes = full
     t0 = time.time()
-    st = build_state(shapes, q, 1234 + 1000 * rank)
+    st = build_state(shapes, q, 1234)
     setup_s = time.time() - t0
     stream = torch.cuda.current_stream()
 
@@ -241,60 +243,36 @@ def run_gpu_arm(args):
     nnz_before = [st.group_nnz(g) for g in st.groups]
 
     # ---------------- timed region: device-resident inputs ----------------
-    if world > 1:
-        dist.barrier()
     torch.cuda.synchronize()
     clk = ClockSampler(local)
     clk.start()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    gev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-            for _ in st.groups] for _ in range(args.steps)]
-    ev0.record(stream)
-    for k in range(args.steps):
-        h = q._native.hyper(**{"lr": HYPER["lr"], "beta1": HYPER["beta1"],
-                              "beta2": HYPER["beta2"], "weight_decay": HYPER["weight_decay"]})
-        flip = st.cur
-        for gi, g in enumerate(st.groups):
-            gev[k][gi][0].record(stream)
-            q._native.check(q._native.lib.qftc_plan_step(g.plan, flip, h,
-                                                         C.c_void_p(stream.cuda_stream)))
-            gev[k][gi][1].record(stream)
-        st.cur = 1 - flip
-        st.steps += 1
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    ms = timed_region(st, args.steps, stream, HYPER)
     clocks = clk.stop()
-    ms = ev0.elapsed_time(ev1) / args.steps
     st.check()  # raises on CSR overflow / degenerate rows (never silently)
+    st_rows, gen_rows = st.tier_rows()
     nnz_after = [st.group_nnz(g) for g in st.groups]
-    per_group_ms = [statistics.mean(gev[k][gi][0].elapsed_time(gev[k][gi][1])
-                                    for k in range(args.steps)) for gi in range(len(st.groups))]
     params_local, rows_local = count(shapes)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    params_total = count(full)[0] if world > 1 else params_local
-    value = params_total / (ms * 1e-3) / 1e9
+    value = params_local / (ms * 1e-3) / 1e9
 
-    # roofline of the dominant kernel: the largest width-class launch
+    # roofline of the dominant launch: one step is ONE concurrent launch group (every
+    # width class forked onto its own stream and joined back), so the group is the step
     hbm, peak_kind = peaks()
-    gi_dom = max(range(len(st.groups)), key=lambda i: per_group_ms[i])
-    g = st.groups[gi_dom]
-    alg = algorithmic_bytes(st, g, nnz_before[gi_dom], nnz_after[gi_dom])
-    achieved = alg / (per_group_ms[gi_dom] * 1e-3) / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic_r01.json")
-    if os.path.exists(tp):
-        try:
-            traffic = json.load(open(tp)).get(f"cols{g.cols}")
-        except Exception:
-            traffic = None
     all_alg = sum(algorithmic_bytes(st, gg, nnz_before[i], nnz_after[i])
                   for i, gg in enumerate(st.groups))
+    achieved = all_alg / (ms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic_r02.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("step")
+        except Exception:
+            traffic = None
+    order, _ = st.step_plans()
+    per_class = timed_serial_classes(st, 3, stream, HYPER)
+    st.check()
+    for g in order[:-1]:  # restore the concurrent caps
+        q._native.check(q._native.lib.qftc_plan_set_ctas_per_sm(
+            g.plan, int(os.environ.get("QFT_WIDE_CTAS", "0"))))
 
     # ---------------- e2e: the reference-facing call with HOST buffers ----------------
     e2e = e2e_host(st, q, args, stream) if not args.no_e2e else None
@@ -302,51 +280,214 @@ def run_gpu_arm(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "u8",
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic (device generator, bit-identical to oracle/synth.c)",
         "config": {"workload": "llama2-7b-shaped full model-state quantized Lion step "
                                "(configs[1]): 291 tensors, 6.74 G params, b=8, p=1% percentile "
                                "outliers, u8 gradient codes",
-                   "params": params_total, "rows": rows_local, "bit_width": BIT_WIDTH,
-                   "outlier_fraction": FRACTION, "nnz": st.nnz(),
+                   "params": params_local, "rows": rows_local, "bit_width": BIT_WIDTH,
+                   "outlier_fraction": FRACTION, "nnz": st.nnz(), "lr": HYPER["lr"],
                    "l2": "inputs larger than L2 (34.8 GB moved per step vs 126 MB L2)",
-                   "parallelism": f"zero1-rows{world}" if world > 1 else "single"},
+                   "parallelism": "single"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic,
-                     "kernel": f"qftc_plan_step cols={g.cols} (k_step_prep + rows_kernel, "
-                               "stable tier + step_kernel, general tier)",
-                     "algorithmic_bytes_per_launch": alg, "launch_ms": per_group_ms[gi_dom],
+                     "kernel": "qftc_plans_step: the width classes' launch groups (k_step_prep "
+                               "+ rows_kernel, stable tier + step_kernel, general tier) forked "
+                               "onto concurrent streams -- one launch group per step",
+                     "algorithmic_bytes_per_launch": all_alg, "launch_ms": ms,
                      "peak_kind": peak_kind},
-        "step_hbm_gbs": all_alg / (ms * 1e-3) / 1e9,
-        "per_launch_ms": {f"cols{gg.cols}": per_group_ms[i] for i, gg in enumerate(st.groups)},
+        "step_hbm_gbs": achieved,
+        "step_frac": achieved / hbm,
+        "stable_rows_frac": st_rows / max(1, st_rows + gen_rows),
+        "per_class_serial_ms": {f"cols{gg.cols}": per_class[i] for i, gg in enumerate(st.groups)},
+        "per_class_serial_frac": {
+            f"cols{gg.cols}": algorithmic_bytes(st, gg, nnz_before[i], nnz_after[i]) /
+            (per_class[i] * 1e-3) / 1e9 / hbm for i, gg in enumerate(st.groups)},
+        "concurrency": {"wide_class_ctas_per_sm": int(os.environ.get("QFT_WIDE_CTAS", "0")),
+                        "order": [f"cols{g.cols}" for g in order]},
         "gpu_launches": args.steps * sum(int(q._native.lib.qftc_plan_launches(gg.plan)) for gg in st.groups),
         "clocks": clocks,
         "setup_s": setup_s,
     }
     if e2e:
         line["e2e"] = e2e
-    if world > 1 or args.zero1:
-        del st
+    if not args.no_side:
+        # the general tier: lr = 2.2e-4 puts rows on both sides of the stable-tier bound
+        try:
+            line["side_lr_2.2e-4"] = side_lr(st, args, stream, all_alg, hbm)
+        except Exception as ex:  # a side measurement never voids the headline
+            line["side_lr_2.2e-4"] = {"error": str(ex)[:300]}
+    del st
+    torch.cuda.empty_cache()
+    if not args.no_side:
+        try:
+            line["side_bf16_grad"] = side_bf16(args, full, q, stream, hbm)
+        except Exception as ex:
+            line["side_bf16_grad"] = {"error": str(ex)[:300]}
         torch.cuda.empty_cache()
+    if args.zero1:
         line["zero1_step"] = zero1_run(args, full, world, rank, q)
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if not args.no_cpu:
         try:
             cb = cpu_reference_run(steps=2, warmup=0)
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind",
                                                        "sample", "cpu_model")}
         except Exception as ex:  # reported, never fatal for the GPU number
             line["cpu_baseline"] = {"value": None, "error": str(ex)[:200]}
+    print(json.dumps(line), flush=True)
+
+
+def timed_region(st, steps, stream, hyper):
+    """`steps` fused steps over the whole model: one concurrent launch group per step (every
+    width class on its own stream, qftc_plans_step); ms per step from CUDA events on the
+    launching stream (the classes are forked from and joined back into it)."""
+    import torch
+    import paper_2310_07147_b200 as q
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    h = q._native.hyper(hyper["lr"], hyper["beta1"], hyper["beta2"], hyper["weight_decay"])
+    sh = C.c_void_p(stream.cuda_stream)
+    ev0.record(stream)
+    for _ in range(steps):
+        flip = st.cur
+        st.enqueue_step(flip, h, sh)
+        st.cur = 1 - flip
+        st.steps += 1
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    return ev0.elapsed_time(ev1) / steps
+
+
+def timed_serial_classes(st, steps, stream, hyper):
+    """Per width class: the classes stepped one after the other on one stream, uncapped
+    grids, CUDA events around each class's launch group (mean ms per class)."""
+    import torch
+    import paper_2310_07147_b200 as q
+    N = q._native
+    for g in st.groups:
+        N.check(N.lib.qftc_plan_set_ctas_per_sm(g.plan, 0))
+    st._plan_order = None
+    h = N.hyper(hyper["lr"], hyper["beta1"], hyper["beta2"], hyper["weight_decay"])
+    sh = C.c_void_p(stream.cuda_stream)
+    gev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in st.groups] for _ in range(steps)]
+    for k in range(steps):
+        flip = st.cur
+        for gi, g in enumerate(st.groups):
+            gev[k][gi][0].record(stream)
+            N.check(N.lib.qftc_plan_step(g.plan, flip, h, sh))
+            gev[k][gi][1].record(stream)
+        st.cur = 1 - flip
+        st.steps += 1
+    torch.cuda.synchronize()
+    return [statistics.mean(gev[k][gi][0].elapsed_time(gev[k][gi][1]) for k in range(steps))
+            for gi in range(len(st.groups))]
+
+
+def side_lr(st, args, stream, alg_step, hbm):
+    """The same 7B state stepped at lr = 2.2e-4 (rows whose sw is
+    below ~2*lr leave the stable tier and run the general step kernel; their codes move,
+    so CSR slots can overflow).  Every step is the checked engine step (synchronise,
+    re-plan + re-run on overflow), timed with CUDA events around it."""
+    import torch
+    hy = dict(HYPER, lr=2.2e-4)
+    for _ in range(args.warmup):
+        st.step(**hy, check=True)
+    rp0 = st.replans
+    n = min(args.steps, 5)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(n)]
+    for e0, e1 in ev:
+        e0.record(stream)
+        st.step(**hy, check=True)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev)
+    a, b = st.tier_rows()
+    return {"lr": hy["lr"], "ms_per_step": ms, "gparams_s": st.param_count / (ms * 1e-3) / 1e9,
+            "stable_rows_frac": a / max(1, a + b), "general_rows": b,
+            "replans_in_timed_steps": st.replans - rp0,
+            "step_frac_approx": alg_step / (ms * 1e-3) / 1e9 / hbm,
+            "timing": "checked engine step (host sync per step) between CUDA events"}
+
+
+def side_bf16(args, full, q, stream, hbm):
+    """The 7B step fed raw bf16 gradients (what a reduce-scatter delivers): k_grad_quant
+    (quantize_state of g into the u8 GradientStack entry) + the rows kernel, per group."""
+    import torch
+    st = q.QftModelState(full, bit_width=BIT_WIDTH, grad_kind="bf16")
+    st.init_from_weights(lambda i: q.synth(full[i], 1234 + i, 0.02, 0.005), FRACTION, "percentile")
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(7)
+    st.g_raw.normal_(0.0, 1e-3, generator=gen)
+    for _ in range(args.warmup):
+        st.step(**HYPER, check=True)
+    nnz0 = st.nnz()
+    ms = timed_region(st, min(args.steps, 5), stream, HYPER)
+    st.check()
+    a, b = st.tier_rows()
+    P, R = st.param_count, st.row_count_total
+    # 2 B bf16 read + 1 B code write + 8 B params per row (k_grad_quant), then the u8 step
+    alg = 3 * P + 8 * R + 5 * P + 8 * (nnz0 + st.nnz()) + 48 * R
+    out = {"ms_per_step": ms, "gparams_s": P / (ms * 1e-3) / 1e9, "grad": "bf16 raw",
+           "algorithmic_bytes": alg, "frac_of_hbm": alg / (ms * 1e-3) / 1e9 / hbm,
+           "stable_rows_frac": a / max(1, a + b), "kernels": st.kernel_names(),
+           "launches_per_step": sum(int(q._native.lib.qftc_plan_launches(g.plan))
+                                    for g in st.groups)}
+    del st
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_multi_gpu(args, full, world, rank, local, q):
+    """configs[2] at N > 1: the headline is the FULL ZeRO-1 step (reduce-scatter of the
+    bf16 gradient + local update + all-gather of the quantized state), device time max over
+    ranks; the update alone and the collectives are side fields."""
+    import torch
+    import torch.distributed as dist
+    from paper_2310_07147_b200.shapes import count
+    clk = ClockSampler(local)
+    clk.start()
+    z = zero1_run(args, full, world, rank, q)
+    clocks = clk.stop()
+    hbm, peak_kind = peaks()
+    params = count(full)[0]
+    ms = z["ms_per_step"]
+    d = z["dominant"]
+    achieved = d["algorithmic_bytes"] / (d["ms"] * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": params / (ms * 1e-3) / 1e9, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (device generator; bf16 gradients from torch.normal on device)",
+        "config": {"workload": "llama2-7b-shaped ZeRO-1 quantized Lion step (configs[2]): "
+                               "reduce-scatter bf16 grad + per-shard fused update + all-gather "
+                               "of W codes / CSR slots / arenas",
+                   "params": params, "bit_width": BIT_WIDTH, "outlier_fraction": FRACTION,
+                   "lr": HYPER["lr"], "parallelism": f"zero1-rows{world}",
+                   "l2": "inputs larger than L2"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": None,
+                     "kernel": "rank-local update: every width class's k_grad_quant + "
+                               "k_step_prep + rows_kernel + step_kernel, concurrent streams",
+                     "algorithmic_bytes_per_launch": d["algorithmic_bytes"],
+                     "launch_ms": d["ms"], "peak_kind": peak_kind},
+        "zero1_step": z,
+        "update_only_gparams_s": z["update_gparams_s_all_ranks"],
+        "gpu_launches": args.steps * z["gpu_launches_per_step"],
+        "clocks": clocks,
+    }
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    dist.destroy_process_group()
 
 
 def zero1_run(args, full, world, rank, q):
     """configs[2]: the full ZeRO-1 step on this rank -- reduce-scatter of the bf16
-    gradient (shard-major layout), the fused step on the rank's rows (bf16 raw-gradient
-    kind: quantize_state(g) fused in), all-gather of the updated W codes, CSR slot
-    starts/counts and arenas.  Device time, max over ranks."""
+    gradient (shard-major layout), the local update of the rank's rows (k_grad_quant:
+    quantize_state of the summed bf16 gradient into the u8 GradientStack entry, then the
+    rows kernel), all-gather of the updated W codes, CSR slot starts/counts and arenas.
+    Device time per phase (CUDA events on the launching stream), max over ranks."""
     import torch
     import torch.distributed as dist
     from paper_2310_07147_b200.zero1 import CudaShard, ShardLayout, Zero1QftLion
@@ -368,40 +509,75 @@ def zero1_run(args, full, world, rank, q):
         z = Zero1QftLion(full, local)
         gen = torch.Generator(device="cuda")
         gen.manual_seed(99 + rank)
-        z.grad_full.normal_(0.0, 1e-3, generator=gen)
+        z.grad_full.normal_(0.0, 1e-3 / world, generator=gen)
         g0 = z.grad_full.clone()
+        st = local.state
         stream = torch.cuda.current_stream()
         for _ in range(args.warmup):
             z.grad_full.copy_(g0)
             z.step(**HYPER)
-        local.state.check()
+            st.check()
         dist.barrier()
         torch.cuda.synchronize()
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-              for _ in range(args.steps)]
-        for e0, e1 in ev:
-            z.grad_full.copy_(g0)       # a fresh gradient each step (outside the event pair)
+        nnz_before = [st.group_nnz(g) for g in st.groups]
+        E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+        ev = [(E(), E(), E(), E(), E()) for _ in range(args.steps)]
+        h = _hyper_c()
+        for e0, e1, e15, e2, e3 in ev:
+            z.grad_full.copy_(g0)       # a fresh gradient each step (outside the event pairs)
             e0.record(stream)
-            z.step(**HYPER)
+            z.reduce_scatter_grads()
             e1.record(stream)
+            flip = st.cur
+            st.enqueue_step(flip, h, C.c_void_p(stream.cuda_stream))
+            e15.record(stream)
+            st.cur = 1 - flip
+            st.steps += 1
+            z.check_local()             # all-reduced overflow flag (re-plans + re-runs)
+            e2.record(stream)
+            z.all_gather_state()
+            e3.record(stream)
         torch.cuda.synchronize()
         dist.barrier()
-        local.state.check()
-        ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev)
-        t = torch.tensor([ms], device="cuda")
+        st.check()
+        nnz_after = [st.group_nnz(g) for g in st.groups]
+        mean = lambda a, b: statistics.mean(x.elapsed_time(y) for x, y in zip(a, b))  # noqa: E731
+        ms = mean([e[0] for e in ev], [e[4] for e in ev])
+        rs_ms = mean([e[0] for e in ev], [e[1] for e in ev])
+        upd_ms = mean([e[1] for e in ev], [e[3] for e in ev])
+        ag_ms = mean([e[3] for e in ev], [e[4] for e in ev])
+        kern_ms = mean([e[1] for e in ev], [e[2] for e in ev])
+        t = torch.tensor([ms, rs_ms, upd_ms, ag_ms, kern_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms, rs_ms, upd_ms, ag_ms, kern_ms = (float(x) for x in t.tolist())
         params = sum(r * c for r, c in full)
+        shard_params = st.param_count
         f = (world - 1) / world
         rs_bytes = f * 2 * layout.pad * world
         ag_bytes = f * (layout.pad + 4 * layout.rp_pad + 4 * layout.rpad +
                         8 * z.cap * len(layout.widths)) * world
+        # the update's launch group: k_grad_quant (2 B bf16 read + 1 B code write per param,
+        # 8 B params per row) + the step on the u8 entry (5 B per param,
+        # 8 B per CSR entry in and out, 48 B per row), every width class concurrently
+        alg = sum(3 * sum(st.shapes[i][0] * st.shapes[i][1] for i in g.members) + 8 * g.rows +
+                  algorithmic_bytes(st, g, nnz_before[gi], nnz_after[gi])
+                  for gi, g in enumerate(st.groups))
+        st_, gen_ = st.tier_rows()
         return {"ms_per_step": ms, "gparams_s": params / (ms * 1e-3) / 1e9,
-                "what": "reduce_scatter(bf16 grad) + fused bf16-gradient step on the row "
-                        "shard + all_gather(W codes, CSR slots, arenas)",
-                "grad_dtype": "bf16", "world": world,
+                "what": "reduce_scatter(bf16 grad) + local update of the row shard "
+                        "(k_grad_quant -> rows kernel) + all_gather(W codes, CSR slots, arenas)",
+                "grad_dtype": "bf16", "world": world, "shard_params": shard_params,
+                "rs_ms": rs_ms, "update_ms": upd_ms, "ag_ms": ag_ms,
+                "update_gparams_s_per_rank": shard_params / (upd_ms * 1e-3) / 1e9,
+                "update_gparams_s_all_ranks": params / (upd_ms * 1e-3) / 1e9,
+                "dominant": {"what": "the local update's concurrent launch group (all width "
+                                     "classes)", "ms": kern_ms, "algorithmic_bytes": alg},
+                "stable_rows_frac": st_ / max(1, st_ + gen_),
                 "rs_bytes_per_rank": rs_bytes, "ag_bytes_per_rank": ag_bytes,
-                "nvlink_gbs_per_rank": (rs_bytes + ag_bytes) / (ms * 1e-3) / 1e9}
+                "nvlink_gbs_per_rank": (rs_bytes + ag_bytes) / ((rs_ms + ag_ms) * 1e-3) / 1e9,
+                "nccl_version": ".".join(str(v) for v in torch.cuda.nccl.version()),
+                "gpu_launches_per_step": sum(int(q._native.lib.qftc_plan_launches(gg.plan))
+                                             for gg in st.groups)}
     finally:
         if own_group:
             dist.destroy_process_group()
@@ -688,9 +864,22 @@ def main():
     ap.add_argument("--mode", default="step", choices=["step", "sweep", "13b", "ckpt"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-side", action="store_true",
+                    help="skip the lr=2.2e-4 and bf16-gradient side measurements")
     ap.add_argument("--zero1", action="store_true",
                     help="also time the full ZeRO-1 step (RS + step + AG) at N=1")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torch.distributed.run
+        import socket
+        s_ = socket.socket()
+        s_.bind(("127.0.0.1", 0))
+        port_no = s_.getsockname()[1]
+        s_.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port_no}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     if args.warmup < 3 and args.impl == "own":
         args.warmup = 3
     if args.impl == "reference":

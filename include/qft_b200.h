@@ -179,6 +179,16 @@ int qftc_plan_set_arena(qftc_plan* plan, int32_t* col_idx[2], float* values[2],
  * (dequant g,m,w -> Lion -> requant m (fresh params) -> requant w (cached
  * thresholds) + ordered CSR re-extraction), reading set [flip]. */
 int qftc_plan_step(qftc_plan* plan, int flip, qftc_lion_hyper hyper, qftc_stream_t stream);
+/* One step over several plans (e.g. a model's width classes) that run CONCURRENTLY:
+ * plan i is enqueued on its own stream, forked from and joined back into `stream`
+ * (events, no host synchronisation), in the order given -- pass the wide classes first
+ * so their CTAs are resident before the dominant class fills the rest of the GPU (the
+ * rows kernel claims rows dynamically, so a class's late CTAs just take fewer rows). */
+int qftc_plans_step(qftc_plan* const* plans, int n, int flip, qftc_lion_hyper hyper,
+                    qftc_stream_t stream);
+/* Cap the resident CTAs per SM of a plan's rows kernel (0: occupancy maximum), so a
+ * concurrently stepped plan leaves room for another's CTAs. */
+int qftc_plan_set_ctas_per_sm(qftc_plan* plan, int ctas_per_sm);
 /* Synchronises; returns the new total nnz of the arena written by the last step
  * and QFTC_EOVERFLOW / QFTC_EINVAL if that step overflowed or hit a degenerate row. */
 int qftc_plan_result(qftc_plan* plan, int64_t* nnz_total, qftc_stream_t stream);

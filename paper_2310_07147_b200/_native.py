@@ -84,6 +84,8 @@ _SIGS = {
                               C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_i64), _vp]),
     "qftc_plan_set_arena": (_i, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_i64)]),
     "qftc_plan_step": (_i, [_vp, _i, LionHyperC, _vp]),
+    "qftc_plans_step": (_i, [C.POINTER(_vp), _i, _i, LionHyperC, _vp]),
+    "qftc_plan_set_ctas_per_sm": (_i, [_vp, _i]),
     "qftc_plan_result": (_i, [_vp, C.POINTER(_i64), _vp]),
     "qftc_plan_launches": (_i, [_vp]),
     "qftc_plan_kernel_name": (C.c_char_p, [_vp]),

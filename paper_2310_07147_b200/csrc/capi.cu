@@ -459,7 +459,15 @@ struct qftc_plan {
   RowPrep* prep = nullptr;    // per-row records
   RowBlock* xlist = nullptr;  // general-tier rows
   RowsCache rc;               // resolved launches of the rows path (+ its row-list counters)
+  // raw (f32/bf16) gradient on the rows path: k_grad_quant writes quantize_state(g) into
+  // this u8 scratch (the GradientStack entry) and the rows kernel steps from it
+  bool gq = false;
+  void* gq_base = nullptr;
+  KLaunch gql;
   KLaunch gen[2];             // general path (no rows kernel): by weight decay == 0
+  cudaStream_t side = nullptr;     // qftc_plans_step: this plan's stream ...
+  cudaEvent_t ev_fork = nullptr;   // ... forked from the caller's stream
+  cudaEvent_t ev_done = nullptr;   // ... and joined back
   const char* last_kernel = "";  // the main kernel instance of the last step
   volatile uint32_t* oflag_host = nullptr;  // mapped pinned copy of the overflow flag
   uint32_t* oflag_dev = nullptr;
@@ -529,9 +537,38 @@ int qftc_plan_create(qftc_plan** out, const qftc_lion_tensor* ts, int n, int bit
     if (t.cols != ucols) ucols = 0;
   }
   if (rows > 0x7fffffff) return fail(QFTC_ENOTSUP, "plan: more than 2^31 rows");
+  const char* no_rows = getenv("QFT_NO_ROWS_KERNEL");
+  const char* no_gq = getenv("QFT_NO_GRAD_QUANT");
+  const bool rows_ok = rows_kernel_eligible(QFTC_GRAD_U8, bulk ? 1 : 0, ucols) &&
+                       !(no_rows && no_rows[0] == '1');
+  // raw gradients on the rows path: quantize_state(g) into a plan-owned u8 entry first
+  const bool gq = rows_ok && grad_kind != QFTC_GRAD_U8 && !(no_gq && no_gq[0] == '1');
+  void* gq_base = nullptr;
+  if (gq) {
+    size_t code_bytes = 0;
+    for (int i = 0; i < n; ++i) code_bytes += ((size_t)ts[i].rows * ts[i].cols + 15) & ~(size_t)15;
+    const size_t row_bytes = ((size_t)rows * 4 + 255) & ~(size_t)255;
+    cudaError_t e = cudaMallocAsync(&gq_base, code_bytes + 2 * row_bytes, st);
+    if (e != cudaSuccess)
+      return fail(QFTC_ECUDA, std::string("plan_create: gradient scratch: ") + cudaGetErrorString(e));
+    uint8_t* c = reinterpret_cast<uint8_t*>(gq_base);
+    float* sc = reinterpret_cast<float*>(c + code_bytes);
+    int32_t* zp = reinterpret_cast<int32_t*>(c + code_bytes + row_bytes);
+    int64_t r0 = 0;
+    for (int i = 0; i < n; ++i) {
+      dts[(size_t)i].g_codes = c;
+      dts[(size_t)i].g_scale = sc + r0;
+      dts[(size_t)i].g_zp = zp + r0;
+      c += ((size_t)ts[i].rows * ts[i].cols + 15) & ~(size_t)15;
+      r0 += ts[i].rows;
+    }
+  }
   auto* p = new qftc_plan;
+  p->gq = gq;
+  p->gq_base = gq_base;
   int rc = scratch_alloc(p->sc, dts, 0, st);
   if (rc) {
+    if (gq_base) cudaFree(gq_base);
     delete p;
     return rc;
   }
@@ -546,15 +583,32 @@ int qftc_plan_create(qftc_plan** out, const qftc_lion_tensor* ts, int n, int bit
     p->oldcap = cfg.oldcap;
   }
   p->uniform_cols = ucols;
-  const char* no_rows = getenv("QFT_NO_ROWS_KERNEL");
-  p->rows_path = rows_kernel_eligible(grad_kind, p->use_bulk, ucols) &&
-                 !(no_rows && no_rows[0] == '1');
+  p->rows_path = rows_ok && (grad_kind == QFTC_GRAD_U8 || gq);
+  if (gq) {
+    cudaError_t e = resolve_grad_quant(grad_kind, ucols, (int)rows, &p->gql);
+    if (e != cudaSuccess) {
+      qftc_plan_destroy(p);
+      return fail(QFTC_ECUDA, std::string("plan_create: gradient quantizer: ") + cudaGetErrorString(e));
+    }
+  }
   if (p->rows_path) {
     cudaError_t e = cudaMallocAsync((void**)&p->prep, sizeof(RowPrep) * (size_t)rows, st);
     if (e == cudaSuccess)
       e = cudaMallocAsync((void**)&p->xlist, sizeof(RowBlock) * (size_t)rows, st);
     if (e == cudaSuccess) e = cudaMallocAsync((void**)&p->rc.xcount, 16, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(p->rc.xcount, 0, 16, st);
+    if (e == cudaSuccess) {
+      void* hp = nullptr;
+      if (cudaHostAlloc(&hp, 64, cudaHostAllocMapped) == cudaSuccess) {
+        p->rc.seen_host = reinterpret_cast<volatile int32_t*>(hp);
+        *p->rc.seen_host = (int32_t)rows;  // unknown: full grid
+        void* dp = nullptr;
+        if (cudaHostGetDevicePointer(&dp, hp, 0) == cudaSuccess) p->rc.seen_dev = (int32_t*)dp;
+      }
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&p->rc.sms, cudaDevAttrMultiProcessorCount, dev);
+    }
     if (e != cudaSuccess) {
       qftc_plan_destroy(p);
       return fail(QFTC_ECUDA, std::string("plan_create: ") + cudaGetErrorString(e));
@@ -625,6 +679,7 @@ int qftc_plan_step(qftc_plan* p, int flip, qftc_lion_hyper h, qftc_stream_t stre
     a.oldcap6 = rows_kernel_oldcap(p->uniform_cols);
     a.prep = p->prep;
     a.xlist = p->xlist;
+    if (p->gq) QFTC_CUDA(launch_k(p->gql, a, (cudaStream_t)stream), "gradient quantize_state");
     QFTC_CUDA(launch_rows_step(a, p->rc, (cudaStream_t)stream), "lion step (rows kernel)");
     p->last_kernel = p->rc.rows[a.slotted_in ? 1 : 0].name;
     return QFTC_OK;
@@ -633,6 +688,43 @@ int qftc_plan_step(qftc_plan* p, int flip, qftc_lion_hyper h, qftc_stream_t stre
   if (!k.fn) QFTC_CUDA(resolve_step_kernel(p->grad_kind, a, &k), "lion step kernel (resolve)");
   QFTC_CUDA(launch_k(k, a, (cudaStream_t)stream), "lion step kernel");
   p->last_kernel = k.name;
+  return QFTC_OK;
+}
+
+int qftc_plan_set_ctas_per_sm(qftc_plan* p, int ctas_per_sm) {
+  if (!p || ctas_per_sm < 0) return fail(QFTC_EINVAL, "plan_set_ctas_per_sm: bad arguments");
+  if (p->rc.cap_per_sm != ctas_per_sm) {
+    p->rc.cap_per_sm = ctas_per_sm;
+    p->rc.rows[0] = KLaunch{};  // re-resolved at the next step
+    p->rc.rows[1] = KLaunch{};
+  }
+  return QFTC_OK;
+}
+
+int qftc_plans_step(qftc_plan* const* plans, int n, int flip, qftc_lion_hyper h,
+                    qftc_stream_t stream) {
+  if (!plans || n <= 0) return fail(QFTC_EINVAL, "plans_step: no plans");
+  for (int i = 0; i < n; ++i)
+    if (!plans[i]) return fail(QFTC_EINVAL, "plans_step: null plan");
+  if (n == 1) return qftc_plan_step(plans[0], flip, h, stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int i = 0; i < n; ++i) {
+    qftc_plan* p = plans[i];
+    if (!p->side) {
+      QFTC_CUDA(cudaStreamCreateWithFlags(&p->side, cudaStreamNonBlocking), "plans_step: stream");
+      QFTC_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming), "plans_step: event");
+      QFTC_CUDA(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming), "plans_step: event");
+    }
+  }
+  QFTC_CUDA(cudaEventRecord(plans[0]->ev_fork, st), "plans_step: fork");
+  for (int i = 0; i < n; ++i) {
+    qftc_plan* p = plans[i];
+    QFTC_CUDA(cudaStreamWaitEvent(p->side, plans[0]->ev_fork, 0), "plans_step: fork wait");
+    if (int rc = qftc_plan_step(p, flip, h, (qftc_stream_t)p->side)) return rc;
+    QFTC_CUDA(cudaEventRecord(p->ev_done, p->side), "plans_step: join");
+  }
+  for (int i = 0; i < n; ++i)
+    QFTC_CUDA(cudaStreamWaitEvent(st, plans[i]->ev_done, 0), "plans_step: join wait");
   return QFTC_OK;
 }
 
@@ -655,7 +747,9 @@ int qftc_plan_result(qftc_plan* p, int64_t* nnz_total, qftc_stream_t stream) {
   return QFTC_OK;
 }
 
-int qftc_plan_launches(const qftc_plan* p) { return p ? (p->rows_path ? 3 : 1) : 0; }
+int qftc_plan_launches(const qftc_plan* p) {
+  return p ? (p->rows_path ? 3 + (p->gq ? 1 : 0) : 1) : 0;
+}
 
 const char* qftc_plan_kernel_name(const qftc_plan* p) { return p ? p->last_kernel : ""; }
 
@@ -685,6 +779,14 @@ int qftc_plan_destroy(qftc_plan* p) {
   if (p->prep) cudaFree(p->prep);
   if (p->xlist) cudaFree(p->xlist);
   if (p->rc.xcount) cudaFree(p->rc.xcount);
+  if (p->gq_base) cudaFree(p->gq_base);
+  if (p->rc.seen_host) cudaFreeHost(const_cast<int32_t*>(p->rc.seen_host));
+  if (p->side) {
+    cudaStreamSynchronize(p->side);
+    cudaStreamDestroy(p->side);
+    cudaEventDestroy(p->ev_fork);
+    cudaEventDestroy(p->ev_done);
+  }
   if (p->oflag_host) cudaFreeHost(const_cast<uint32_t*>(p->oflag_host));
   delete p;
   return QFTC_OK;

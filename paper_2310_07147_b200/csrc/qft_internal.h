@@ -99,6 +99,8 @@ struct LaunchArgs {
   const int32_t* n_blocks_dev;   // step_kernel: read the block count from the device
   int32_t* xclear;               // prep: the OTHER flip's row-list counter, zeroed for the next step
   uint32_t* oflag;               // mapped pinned overflow flag (host-visible without a sync)
+  int32_t* xseen;                // step_kernel: the row-list length it saw (mapped pinned)
+  int32_t* rclaim;               // rows kernel: row-claim counter (zeroed by k_step_prep)
 };
 
 // Per-row record of the rows kernel (128 B), written by k_step_prep every step and
@@ -148,10 +150,20 @@ struct RowsCache {
   KLaunch rows[2];     // by slotted input (0/1)
   KLaunch gen[2];      // general kernel over the device list, by weight decay == 0 (0/1)
   int last_flip = -1;  // the flip of the previous step (a repeated flip re-zeroes its counter)
-  int32_t* xcount = nullptr;  // [2] row-list counters, one per flip
+  int32_t* xcount = nullptr;  // [4]: row-list counters (one per flip), [2] row-claim counter
+  // the general-tier row count the general kernel last saw (mapped pinned, read without a
+  // sync): an empty list last time -> launch that kernel with one CTA per SM (it still
+  // covers any list length, grid-stride)
+  volatile int32_t* seen_host = nullptr;
+  int32_t* seen_dev = nullptr;
+  int sms = 0;
+  int cap_per_sm = 0;  // rows kernel: resident CTAs per SM cap (0: occupancy maximum)
 };
 
 int step_kernel_max_cols();
+
+// quantize_state of a raw (f32/bf16) gradient into the plan's u8 entry (gradquant.cu)
+cudaError_t resolve_grad_quant(int gk, int max_cols, int total_rows, KLaunch* out);
 
 // v6 rows kernel (rowstep.cu): prep + stable rows + step_kernel over the rest
 bool rows_kernel_eligible(int gk, int use_bulk, int uniform_cols);

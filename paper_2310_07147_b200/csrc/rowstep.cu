@@ -55,6 +55,15 @@
 namespace qftk {
 using namespace qftd;
 
+#ifndef QFT_STATIC_ROWS
+#define QFT_STATIC_ROWS 0  // 1: static row assignment (A/B of the dynamic row claims)
+#endif
+#ifndef QFT_CLAIM_K
+#define QFT_CLAIM_K 8  // rows per dynamic claim
+#endif
+#ifndef QFT_STATIC_NS3
+#define QFT_STATIC_NS3 0  // 1: static rows for the 3-stage (<= 4096-column) class only
+#endif
 #ifndef QFT_OC3
 #define QFT_OC3 64  // old-outlier table of the 3-stage class: cols / QFT_OC3 entries
 #endif
@@ -84,7 +93,8 @@ struct Smem {
   __device__ __host__ int o_part() const { return o_vbase() + nvec * 4; }
   __device__ __host__ int o_seg() const { return o_part() + nw * 16; }
   __device__ __host__ int o_res() const { return o_seg() + nw * 8; }
-  __device__ __host__ int total() const { return o_res() + 32; }
+  __device__ __host__ int o_rowid() const { return o_res() + 32; }  // int[4]: row of each stage
+  __device__ __host__ int total() const { return o_rowid() + 16; }
 };
 
 struct BufHdr {  // what the deferred output of a row needs after its stage is reused
@@ -169,40 +179,6 @@ __device__ __noinline__ void affine_ni(float lo, float hi, int bw, float* s, int
   affine_from_bounds(lo, hi, bw, *s, *z);
 }
 
-// affine_params_from_bounds (quantize.hpp:114-128) for lo < hi at low latency: the
-// divide by qmax via a Markstein-corrected product whose exact remainder proves the
-// correctly rounded quotient (s a power of two or a tie: refused), and the zero point
-// from an approximate reciprocal, accepted only when -lo/s is provably clear of a
-// half-integer.  Returns false (-> the exact fp64 path) whenever a proof fails.
-__device__ __forceinline__ bool affine_fast(float lo_f, float hi_f, double qmax, double rq,
-                                            float& scale, int32_t& zp) {
-  const double lo = (double)lo_f, hi = (double)hi_f;
-  if (!(lo < hi)) return false;
-  const double d = __dsub_rn(hi, lo);
-  const double q0 = __dmul_rn(d, rq);
-  const double s = __fma_rn(__fma_rn(-q0, qmax, d), rq, q0);
-  const double r1 = __fma_rn(-s, qmax, d);  // exact remainder d - s*qmax
-  const long long sb = __double_as_longlong(s);
-  const int ex = (int)((sb >> 52) & 0x7FF);
-  if (ex < 64 || ex > 2000 || (sb & 0x000FFFFFFFFFFFFFLL) == 0) return false;
-  const double half_ulp = __longlong_as_double((long long)(ex - 53) << 52);
-  if (!(fabs(r1) < qmax * half_ulp)) return false;
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(s));
-  y = __fma_rn(y, __fma_rn(-s, y, 1.0), y);
-  y = __fma_rn(y, __fma_rn(-s, y, 1.0), y);
-  const double q = __dmul_rn(-lo, y);  // within a few ulp of -lo/s
-  const double aq = fabs(q);
-  if (!(aq < 2147483000.0)) return false;
-  const double tq = trunc(aq);
-  const double fr = aq - tq;
-  if (fabs(fr - 0.5) <= aq * 0x1.0p-46 + 0x1.0p-1000) return false;
-  const double zz = copysign(fr > 0.5 ? tq + 1.0 : tq, q);
-  scale = __double2float_rn(s);
-  zp = (int32_t)zz;
-  return true;
-}
-
 // code of an INLIER weight of a stable row (its exact code lies in [0, qmax], proven
 // by code(t_min) == 0 and code(t_max) == qmax): the fast quantizer with its tie proof,
 // the reference's fp64 formula when the proof fails
@@ -285,7 +261,6 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   const int qmax = (1 << bw) - 1;
   const uint32_t KC = (uint32_t)((1 << (bw - 1)) - 1) * 0x01010101u;
   const uint32_t QB = (uint32_t)qmax * 0x01010101u;
-  const int G = gridDim.x;
   const bool slotted = CG || a.slotted_in != 0;
   Hyper h;
   h.lr = a.lr; h.b1 = a.b1; h.b2 = a.b2; h.wd = a.wd;
@@ -308,6 +283,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   float4* part = reinterpret_cast<float4*>(smem + L.o_part());
   int2* seg = reinterpret_cast<int2*>(smem + L.o_seg());
   RowRes* res = reinterpret_cast<RowRes*>(smem + L.o_res());
+  volatile int* rowid = reinterpret_cast<volatile int*>(smem + L.o_rowid());
 
   // thread 0: the row's record, codes and old CSR slot into stage s (TMA bulk copies)
   auto issue_row = [&](int grow, const RowHead& hd, int s) {
@@ -380,43 +356,78 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   };
 
   // ---------------------------------------------------------------- prologue
-  // Static row sequence: row blockIdx.x + k*G.  Rows outside the stable tier still
-  // flow through the pipeline (their record says so) but do no work here.
-  int gr = blockIdx.x;
-  if (gr >= a.total_rows) return;
+  // Rows are CLAIMED dynamically (one atomic per row on the launch's counter, zeroed by
+  // k_step_prep), so CTAs that start late -- e.g. behind a concurrently running width
+  // class -- simply take fewer rows.  The issuing thread claims two rows ahead of the one
+  // it streams (the atomic's result is not needed until the next issue, and the row's
+  // record head is loaded one issue ahead), writes the row index of every stage to
+  // rowid[] before the stage's arrive, and arrives without data (a sentinel, rowid -1)
+  // once the rows are exhausted.  Rows outside the stable tier still flow through the
+  // pipeline (their record says so) but do no work here.
+  const int TR = a.total_rows;
+  // The issuing thread streams row it+NS-1 each iteration.  With 2 stages that is
+  // thread 0 at the top of the iteration; with 3 it is the last warp's lane 0 inside
+  // the barrier window, where that warp has no other work (off the phase-1 path).
+  const int ti = (NS == 3 && NW > 1) ? NT - 32 : 0;
+  RowHead hn{};   // issuing thread: the head of the row it streams next ...
+  int nxt = TR;   // ... that row (>= TR: none)
+  int nxt2 = TR;  // the row claimed after it (atomic result, consumed one issue later)
+  // rows are claimed in chunks of QFT_CLAIM_K consecutive rows; the next chunk's atomic is
+  // issued when the current one is taken, so its result is needed only K issues later
+  int sc = blockIdx.x;  // QFT_STATIC_ROWS: the static sequence blockIdx.x + k*gridDim.x
+  int c_cur = 0, c_end = 0, c_pend = 0;
+  auto claim = [&]() -> int {
+    if (QFT_STATIC_ROWS || (QFT_STATIC_NS3 && NS == 3)) {
+      const int r = sc;
+      sc += (int)gridDim.x;
+      return r;
+    }
+    if (c_cur == c_end) {
+      if (c_end == 0) c_pend = atomicAdd(a.rclaim, QFT_CLAIM_K);  // the first chunk
+      c_cur = c_pend;
+      c_end = c_pend + QFT_CLAIM_K;
+      c_pend = atomicAdd(a.rclaim, QFT_CLAIM_K);
+    }
+    return c_cur++;
+  };
+  auto issue_or_end = [&](int s) {
+    if (nxt < TR) {
+      rowid[s] = nxt;
+      issue_row(nxt, hn, s);
+    } else {
+      rowid[s] = -1;
+      mbar_arrive(&bars[s]);  // sentinel: completes the stage's phase without data
+    }
+    nxt = nxt2;
+    if (nxt < TR) hn = load_head(a, nxt);
+    nxt2 = claim();
+  };
   if (t == 0) {
     for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
     mbar_fence_init();
   }
   clear_words(0);
   __syncthreads();
-  // The issuing thread streams row it+NS-1 each iteration.  With 2 stages that is
-  // thread 0 at the top of the iteration; with 3 it is the last warp's lane 0 inside
-  // the barrier window, where that warp has no other work (off the phase-1 path).
-  const int ti = (NS == 3 && NW > 1) ? NT - 32 : 0;
-  RowHead hn{};  // issuing thread: the head of the row it streams next
-  if (t == 0)
-    for (int i = 0; i < NS - 1; ++i)
-      if (gr + i * G < a.total_rows) issue_row(gr + i * G, load_head(a, gr + i * G), i);
-  if (t == ti && gr + (NS - 1) * G < a.total_rows) hn = load_head(a, gr + (NS - 1) * G);
+  if (t == ti) {
+    nxt = claim();
+    if (nxt < TR) hn = load_head(a, nxt);
+    nxt2 = claim();
+    for (int i = 0; i < NS - 1; ++i) issue_or_end(i);
+  }
   mbar_wait(&bars[0], 0u);
+  int gr = rowid[0];
+  if (gr < 0) return;  // no row for this CTA (its other stages hold sentinels too)
   if (rec(0)->info & I_STABLE) sparse_pass(0, 0, 0, NT);
   int on_prev = (rec(0)->info & I_STABLE) ? rec(0)->on : 0;
   __syncthreads();
 
   const int tw = NW > 1 ? 32 : 0;  // first thread of the deferred / sparse work
   int it = 0;
-  for (;; ++it, gr += G) {
+  for (;; ++it) {
     const int b = it % 3, bn = (it + 1) % 3, bp = (it + 2) % 3;
     const int s = it % NS, sn = (it + 1) % NS;
-    const int gn = gr + G;
-    const bool has_next = gn < a.total_rows;
-    const int gi = gr + (NS - 1) * G;  // the row streamed this iteration
     auto issue_ahead = [&]() {
-      if (t == ti && gi < a.total_rows) {
-        issue_row(gi, hn, (it + NS - 1) % NS);
-        if (gi + G < a.total_rows) hn = load_head(a, gi + G);
-      }
+      if (t == ti) issue_or_end((it + NS - 1) % NS);
     };
     if (NS == 2) issue_ahead();
     clear_words(bn);
@@ -537,6 +548,10 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
     const uint32_t excl = incl - cnt;
     if (lane == 31) part[wid] = make_float4(mlo, mhi, __uint_as_float(incl), 0.0f);
     __syncthreads();  // ---------------------------------------------------- A
+    // the next row's index was stored before a CTA barrier (its issue precedes barrier A
+    // of this iteration with 2 stages, barrier B of the previous one with 3)
+    const int gn = rowid[sn];
+    const bool has_next = gn >= 0;
 
     if (wid == 0) {
       if (stable) {
@@ -675,6 +690,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
     }
     on_prev = on_cur;
     if (!has_next) break;
+    gr = gn;
   }
   // the last row's old outliers
   __syncthreads();
@@ -686,6 +702,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
 __global__ void k_step_prep(const LaunchArgs a, int stable_ok) {
   const int gr = blockIdx.x * blockDim.x + threadIdx.x;
   if (gr == 0 && a.xclear) *a.xclear = 0;  // the next step's row-list counter
+  if (gr == 0 && a.rclaim) *a.rclaim = 0;  // the rows kernel's row-claim counter
   if (gr >= a.total_rows) return;
   // tensor of the row (binary search over the row bases)
   int lo = 0, hi = a.n_tensors - 1;
@@ -802,9 +819,17 @@ static long grid_cap() {
 }
 
 template <int MAXT, int MINB, int NS, int FULL = 0, int CCOLS = 0, int BWC = 0>
-static cudaError_t rows_resolve_t(const LaunchArgs& a, int nt, size_t smem, KLaunch* out) {
+static cudaError_t rows_resolve_t(const LaunchArgs& a, int nt, size_t smem, KLaunch* out,
+                                  int cap_per_sm) {
   auto k = rows_kernel<MAXT, MINB, NS, FULL, CCOLS, BWC>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // the attribute is per FUNCTION, shared by every plan that launches this instance: raise
+  // it to the device's opt-in maximum (never lower it to this plan's size, which would
+  // invalidate another plan's cached launch); occupancy follows the launch's own smem
+  int dev0 = 0, optin = 0;
+  cudaGetDevice(&dev0);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev0);
+  if ((size_t)optin < smem) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
@@ -812,6 +837,7 @@ static cudaError_t rows_resolve_t(const LaunchArgs& a, int nt, size_t smem, KLau
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, nt, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  if (cap_per_sm > 0 && per_sm > cap_per_sm) per_sm = cap_per_sm;
   long grid = (long)sms * per_sm;
   if (grid > a.total_rows) grid = a.total_rows;
   if (const long cap = grid_cap()) grid = std::min(grid, cap);
@@ -842,7 +868,7 @@ bool rows_kernel_eligible(int gk, int use_bulk, int uniform_cols) {
 // the rows-kernel instance of a launch (compile-time geometry for the LLaMA-2 widths
 // 4096 / 11008 (7B) and 5120 / 13824 (13B), used only when the plan's table size is the
 // one that geometry implies)
-static cudaError_t rows_resolve(const LaunchArgs& a, KLaunch* out) {
+static cudaError_t rows_resolve(const LaunchArgs& a, KLaunch* out, int cps) {
   const int nt = rows_kernel_nt(a.cols_p);
   const size_t smem = rows_kernel_smem(a.cols_p, a.oldcap6);
   const int c = a.cols_p;
@@ -851,28 +877,28 @@ static cudaError_t rows_resolve(const LaunchArgs& a, KLaunch* out) {
   };
   const bool b8 = QFT_BW8 && a.bit_width == 8;  // the 7B widths also get a constant width
   if (nt == 128 && geom_ok(4096, 3) && b8)
-    return rows_resolve_t<128, QFT_ROWS_MINB_S, 3, 2, 4096, 8>(a, nt, smem, out);
+    return rows_resolve_t<128, QFT_ROWS_MINB_S, 3, 2, 4096, 8>(a, nt, smem, out, cps);
   if (nt == 128 && geom_ok(4096, 3))
-    return rows_resolve_t<128, QFT_ROWS_MINB_S, 3, 2, 4096>(a, nt, smem, out);
+    return rows_resolve_t<128, QFT_ROWS_MINB_S, 3, 2, 4096>(a, nt, smem, out, cps);
   if (geom_ok(11008, 2) && b8)
-    return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 11008, 8>(a, nt, smem, out);
+    return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 11008, 8>(a, nt, smem, out, cps);
 #if QFT_BW34
   // the down-projection sweep (configs[4]) also runs 3- and 4-bit codes
   if (geom_ok(11008, 2) && a.bit_width == 4)
-    return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 11008, 4>(a, nt, smem, out);
+    return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 11008, 4>(a, nt, smem, out, cps);
   if (geom_ok(11008, 2) && a.bit_width == 3)
-    return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 11008, 3>(a, nt, smem, out);
+    return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 11008, 3>(a, nt, smem, out, cps);
 #endif
-  if (geom_ok(11008, 2)) return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 11008>(a, nt, smem, out);
+  if (geom_ok(11008, 2)) return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 11008>(a, nt, smem, out, cps);
   if (geom_ok(5120, 2) && b8)
-    return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 5120, 8>(a, nt, smem, out);
-  if (geom_ok(5120, 2)) return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 5120>(a, nt, smem, out);
-  if (geom_ok(13824, 2) && b8) return rows_resolve_t<512, 1, 2, 1, 13824, 8>(a, nt, smem, out);
-  if (geom_ok(13824, 2)) return rows_resolve_t<512, 1, 2, 1, 13824>(a, nt, smem, out);
-  if (nt <= 128) return rows_resolve_t<128, QFT_ROWS_MINB_S, 3>(a, nt, smem, out);
-  if (nt <= 384 && c / 16 >= nt) return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1>(a, nt, smem, out);
-  if (nt <= 384) return rows_resolve_t<384, QFT_ROWS_MINB_M, 2>(a, nt, smem, out);
-  return rows_resolve_t<512, 1, 2>(a, nt, smem, out);
+    return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 5120, 8>(a, nt, smem, out, cps);
+  if (geom_ok(5120, 2)) return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 5120>(a, nt, smem, out, cps);
+  if (geom_ok(13824, 2) && b8) return rows_resolve_t<512, 1, 2, 1, 13824, 8>(a, nt, smem, out, cps);
+  if (geom_ok(13824, 2)) return rows_resolve_t<512, 1, 2, 1, 13824>(a, nt, smem, out, cps);
+  if (nt <= 128) return rows_resolve_t<128, QFT_ROWS_MINB_S, 3>(a, nt, smem, out, cps);
+  if (nt <= 384 && c / 16 >= nt) return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1>(a, nt, smem, out, cps);
+  if (nt <= 384) return rows_resolve_t<384, QFT_ROWS_MINB_M, 2>(a, nt, smem, out, cps);
+  return rows_resolve_t<512, 1, 2>(a, nt, smem, out, cps);
 }
 
 // One step of a rows-path plan: k_step_prep (records + the device list of general-tier
@@ -885,6 +911,7 @@ cudaError_t launch_rows_step(const LaunchArgs& a0, RowsCache& c, cudaStream_t st
   a.negzero = -0.0f;
   a.xcount = c.xcount + a.flip;
   a.xclear = c.xcount + (1 - a.flip);
+  a.rclaim = c.xcount + 2;
   cudaError_t e;
   if (c.last_flip == a.flip &&
       (e = cudaMemsetAsync(a.xcount, 0, sizeof(int32_t), st)) != cudaSuccess)
@@ -894,7 +921,7 @@ cudaError_t launch_rows_step(const LaunchArgs& a0, RowsCache& c, cudaStream_t st
   k_step_prep<<<(a.total_rows + pt - 1) / pt, pt, 0, st>>>(a, 1);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   KLaunch& rk = c.rows[a.slotted_in ? 1 : 0];
-  if (!rk.fn && (e = rows_resolve(a, &rk)) != cudaSuccess) return e;
+  if (!rk.fn && (e = rows_resolve(a, &rk, c.cap_per_sm)) != cudaSuccess) return e;
   if ((e = launch_k(rk, a, st)) != cudaSuccess) return e;
   // the general kernel over the device row list
   LaunchArgs x = a;
@@ -903,6 +930,12 @@ cudaError_t launch_rows_step(const LaunchArgs& a0, RowsCache& c, cudaStream_t st
   x.n_blocks_dev = a.xcount;
   KLaunch& gk = c.gen[a.wd == 0.0f ? 1 : 0];
   if (!gk.fn && (e = resolve_step_kernel(G_U8, x, &gk)) != cudaSuccess) return e;
+  x.xseen = c.seen_dev;
+  if (c.seen_host && *c.seen_host == 0 && c.sms > 0 && gk.grid > c.sms) {
+    KLaunch small = gk;  // the list was empty last step: a small grid (still covers any list)
+    small.grid = c.sms;
+    return launch_k(small, x, st);
+  }
   return launch_k(gk, x, st);
 }
 

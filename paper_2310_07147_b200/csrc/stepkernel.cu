@@ -226,6 +226,7 @@ __global__ void __launch_bounds__(ws::NW * 32, QFT_STEP_MIN_CTAS) step_kernel(co
   constexpr int P0 = (GK == G_U8) ? 1 : 0;  // first pass (raw kinds: a g-range pass 0)
   // the row list of the rows kernel's general tier has a device-side length
   const int n_blocks = a.n_blocks_dev ? *a.n_blocks_dev : a.n_blocks;
+  if (a.xseen && gwarp == 0 && lane == 0) *reinterpret_cast<volatile int32_t*>(a.xseen) = n_blocks;
   if (gwarp >= n_blocks) return;  // whole warp idle (warps are independent)
 
   if (lane == 0) {
@@ -747,7 +748,14 @@ __global__ void __launch_bounds__(ws::NW * 32, QFT_STEP_MIN_CTAS) step_kernel(co
 template <int GK, bool AL, bool WD0>
 static cudaError_t step_resolve_t(const LaunchArgs& a, size_t smem, KLaunch* out) {
   auto k = step_kernel<GK, AL, WD0>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // the attribute is per FUNCTION, shared by every plan that launches this instance: raise
+  // it to the device's opt-in maximum (never lower it to this plan's size, which would
+  // invalidate another plan's cached launch); occupancy follows the launch's own smem
+  int dev0 = 0, optin = 0;
+  cudaGetDevice(&dev0);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev0);
+  if ((size_t)optin < smem) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);

@@ -25,6 +25,7 @@ The hot path is ``step()``: one launch per width class, no host synchronisation.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -116,6 +117,7 @@ class QftModelState:
             rows = sum(self.shapes[i][0] for i in mem)
             self.groups.append(_Group(c, mem, rows, [None, None], [None, None]))
         self.group_of = {i: gi for gi, g in enumerate(self.groups) for i in g.members}
+        self._plan_order = None
 
     # ------------------------------------------------------------------ views
     def _sl(self, flat, i):
@@ -374,6 +376,32 @@ class QftModelState:
             N.check(N.lib.qftc_plan_create(C.byref(plan), arr, len(g.members), self.bit_width,
                                            self.grad_kind, cols, vals, caps, _stream()))
             g.plan = plan
+        self._plan_order = None
+
+    def step_plans(self):
+        """The width classes' plans in the order one step launches them concurrently
+        (qftc_plans_step): the smaller classes first, each capped at QFT_WIDE_CTAS resident
+        CTAs per SM (default 0: no cap), so they can co-reside with the dominant class, which goes last
+        and fills the rest of the GPU.  QFT_SERIAL_GROUPS=1 steps the classes one after the
+        other on one stream instead."""
+        if self._plan_order is None:
+            dom = max(self.groups, key=lambda g: g.rows * g.cols)
+            order = [g for g in self.groups if g is not dom] + [dom]
+            cap = int(os.environ.get("QFT_WIDE_CTAS", "0"))
+            for g in order[:-1]:
+                N.check(N.lib.qftc_plan_set_ctas_per_sm(g.plan, cap))
+            arr = (C.c_void_p * len(order))(*[g.plan.value for g in order])
+            self._plan_order = (order, arr)
+        return self._plan_order
+
+    def enqueue_step(self, flip: int, h, stream_handle):
+        """Enqueue one step over every width class (no host synchronisation)."""
+        if len(self.groups) > 1 and os.environ.get("QFT_SERIAL_GROUPS", "0") != "1":
+            order, arr = self.step_plans()
+            N.check(N.lib.qftc_plans_step(arr, len(order), flip, h, stream_handle))
+        else:
+            for g in self.groups:
+                N.check(N.lib.qftc_plan_step(g.plan, flip, h, stream_handle))
 
     def __del__(self):
         for ch in getattr(self, "chunks", []):
@@ -418,8 +446,7 @@ class QftModelState:
         h = N.hyper(lr, beta1, beta2, weight_decay)
         flip = self.cur
         self._refuse_if_overflowed("step")
-        for g in self.groups:
-            N.check(N.lib.qftc_plan_step(g.plan, flip, h, _stream()))
+        self.enqueue_step(flip, h, _stream())
         self.cur = 1 - flip
         self.steps += 1
         self._last = (flip, h)

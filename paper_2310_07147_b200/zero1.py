@@ -127,9 +127,36 @@ class Zero1QftLion:
             dist.all_gather_into_tensor(self.col_full[c], col, group=self.group)
             dist.all_gather_into_tensor(self.val_full[c], val, group=self.group)
 
+    def check_local(self):
+        """Every rank learns whether ANY rank's local step overflowed a CSR slot (one
+        all-reduced flag): the overflowing ranks re-plan and re-run their step from its
+        intact ping-pong inputs, then all ranks re-agree a uniform arena capacity, so the
+        all-gather never ships a partial step or cuts off a grown arena."""
+        ov = bool(getattr(self.local, "pending_overflow", lambda: False)())
+        t = torch.tensor([1 if ov else 0], dtype=torch.int64, device=self.local.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        if int(t.item()):
+            if ov:
+                self.local.recover()
+            self._agree_capacity()
+
+    def _agree_capacity(self):
+        t = torch.tensor([self.local.arena_capacity()], dtype=torch.int64,
+                         device=self.local.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        cap = int(t.item())
+        if cap > self.cap:
+            self.cap = cap
+            self.local.ensure_arena_capacity(cap)
+            dev = self.local.device
+            for c in self.layout.widths:
+                self.col_full[c] = torch.empty(self.world * cap, dtype=torch.int32, device=dev)
+                self.val_full[c] = torch.empty(self.world * cap, dtype=torch.float32, device=dev)
+
     def step(self, lr=1e-4, beta1=0.9, beta2=0.99, weight_decay=0.0):
         self.reduce_scatter_grads()
         self.local.step(lr=lr, beta1=beta1, beta2=beta2, weight_decay=weight_decay)
+        self.check_local()
         self.all_gather_state()
 
     # ------------------------------------------------------------------ views of the gathered state
@@ -189,6 +216,15 @@ class CudaShard:
 
     def step(self, **h):
         self.state.step(**h)
+
+    def pending_overflow(self) -> bool:
+        """Synchronise and read the plans' overflow flags (mapped host words)."""
+        from . import _native as N
+        torch.cuda.current_stream(self.device).synchronize()
+        return any(N.lib.qftc_plan_pending_overflow(g.plan) for g in self.state.groups)
+
+    def recover(self):
+        self.state.recover()
 
     def codes_shard(self, pad: int) -> torch.Tensor:
         return self.state.w_codes[self.state.cur][:pad]

@@ -178,3 +178,78 @@ def test_shard_layout_partitions_rows():
             assert covered[0][0] == 0 and covered[-1][1] == r
             assert all(a[1] == b[0] for a, b in zip(covered, covered[1:]))
         assert max(L.numel) - min(L.numel) < 0.001 * L.pad  # balanced shards
+
+
+class _OverflowingShard(OracleShard):
+    """Rank 1 reports a CSR slot overflow after its first local step; its recover() grows
+    the arena (as a re-plan does), which every rank must then agree on."""
+
+    def __init__(self, *a, **k):
+        super().__init__(*a, **k)
+        self.recovered = 0
+        self.grow = 0
+
+    def pending_overflow(self):
+        return self.rank == 1 and self.recovered == 0
+
+    def recover(self):
+        self.recovered += 1
+        self.grow = 4096
+
+    def arena_capacity(self):
+        return super().arena_capacity() + self.grow
+
+
+def _overflow_worker(rank, world, port_no, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.oracle import Oracle
+        from paper_2310_07147_b200.zero1 import ShardLayout, Zero1QftLion
+        port = Oracle("port")
+        full_w = [port.decompose_weight(port.synth(s, 50 + i, 0.02, 0.01), FRAC, BW)
+                  for i, s in enumerate(SHAPES)]
+        full_m = [port.quantize_state(np.zeros(s, np.float32), BW) for s in SHAPES]
+        layout = ShardLayout(SHAPES, world)
+        local = _OverflowingShard(layout, rank, port, full_w, full_m)
+        z = Zero1QftLion(SHAPES, local)
+        cap0 = z.cap
+        ref_w, ref_m = list(full_w), list(full_m)
+        for step in range(2):
+            mine = [torch.from_numpy(_grad(s, 100 * step + i, rank)) for i, s in enumerate(SHAPES)]
+            layout.pack(mine, z.grad_full)
+            z.step(lr=1e-3, weight_decay=0.01)
+            for i, s in enumerate(SHAPES):
+                gsum = sum(_grad(s, 100 * step + i, r).astype(np.float64) for r in range(world))
+                gq = port.quantize_state(gsum.astype(np.float32), BW)
+                ref_w[i], ref_m[i], _ = port.lion_step_layer(ref_w[i], *ref_m[i], *gq, lr=1e-3,
+                                                             wd=0.01)
+                got = z.gathered_tensor(i)
+                for key in ("codes", "row_ptr", "col_idx", "values"):
+                    assert np.array_equal(got[key], getattr(ref_w[i], key)), (step, i, key)
+        # only the overflowing rank re-ran; both agreed the grown, rank-uniform capacity
+        assert local.recovered == (1 if rank == 1 else 0)
+        assert z.cap > cap0 and local.cap == z.cap
+        assert all(t.numel() == world * z.cap for t in z.col_full.values())
+        q.put((rank, "ok"))
+    except Exception:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_zero1_overflow_agreement_gloo():
+    """Zero1QftLion.check_local: one rank's CSR overflow is all-reduced; that rank
+    re-plans and re-runs (recover), all ranks re-agree the arena capacity before the
+    all-gather, and the gathered state is still the single-process reference step."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_no = _free_port()
+    procs = [ctx.Process(target=_overflow_worker, args=(r, 2, port_no, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert results == {0: "ok", 1: "ok"}, results
