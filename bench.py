@@ -250,6 +250,7 @@ def run_gpu_arm(args):
     clocks = clk.stop()
     st.check()  # raises on CSR overflow / degenerate rows (never silently)
     st_rows, gen_rows = st.tier_rows()
+    tiers = st.tiers()
     nnz_after = [st.group_nnz(g) for g in st.groups]
     params_local, rows_local = count(shapes)
     value = params_local / (ms * 1e-3) / 1e9
@@ -299,6 +300,7 @@ def run_gpu_arm(args):
         "step_hbm_gbs": achieved,
         "step_frac": achieved / hbm,
         "stable_rows_frac": st_rows / max(1, st_rows + gen_rows),
+        "tier_rows": {"stable": tiers[0], "gen": tiers[1], "general": tiers[2]},
         "per_class_serial_ms": {f"cols{gg.cols}": per_class[i] for i, gg in enumerate(st.groups)},
         "per_class_serial_frac": {
             f"cols{gg.cols}": algorithmic_bytes(st, gg, nnz_before[i], nnz_after[i]) /
@@ -403,9 +405,10 @@ def side_lr(st, args, stream, alg_step, hbm):
         e1.record(stream)
     torch.cuda.synchronize()
     ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev)
-    a, b = st.tier_rows()
+    t3 = st.tiers()
     return {"lr": hy["lr"], "ms_per_step": ms, "gparams_s": st.param_count / (ms * 1e-3) / 1e9,
-            "stable_rows_frac": a / max(1, a + b), "general_rows": b,
+            "stable_rows_frac": t3[0] / max(1, sum(t3)),
+            "tier_rows": {"stable": t3[0], "gen": t3[1], "general": t3[2]},
             "replans_in_timed_steps": st.replans - rp0,
             "step_frac_approx": alg_step / (ms * 1e-3) / 1e9 / hbm,
             "timing": "checked engine step (host sync per step) between CUDA events"}

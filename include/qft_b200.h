@@ -205,6 +205,9 @@ const char* qftc_plan_kernel_name(const qftc_plan* plan);
 int qftc_plan_pending_overflow(const qftc_plan* plan);
 /* rows of the last step in the stable tier (rows kernel) and the general tier (general
  * kernel); synchronises */
+/* rows of the last step per tier: [0] stable (pass-through rows kernel), [1] GEN (rows
+ * kernel requantizing every code), [2] general (step_kernel).  Synchronises. */
+int qftc_plan_tiers(qftc_plan* plan, int64_t rows_out[3], qftc_stream_t stream);
 int qftc_plan_tier_rows(qftc_plan* plan, int64_t* stable_rows, int64_t* general_rows,
                         qftc_stream_t stream);
 int qftc_plan_destroy(qftc_plan* plan);
@@ -266,6 +269,15 @@ typedef struct qftc_expand_tensor {
 } qftc_expand_tensor;
 int qftc_expand(const qftc_expand_tensor* tensors, int n_tensors, int bf16,
                 qftc_stream_t stream);
+
+/* An expand PLAN: the tensor table uploaded once (synchronises), then one launch per
+ * run for any number of tensors -- e.g. the pieces of a ZeRO-1 all-gather (every rank's
+ * rows of every tensor, read straight from the gathered shard-major buffers). */
+typedef struct qftc_expand_plan qftc_expand_plan;
+int qftc_expand_plan_create(qftc_expand_plan** plan, const qftc_expand_tensor* tensors,
+                            int n_tensors, int bf16, qftc_stream_t stream);
+int qftc_expand_plan_run(qftc_expand_plan* plan, qftc_stream_t stream);
+int qftc_expand_plan_destroy(qftc_expand_plan* plan);
 
 /* Pass-through mode (QuantMode::passthrough, quantize.hpp:17): lion_apply on raw
  * fp32 state, bitwise equal to lion_step_reference (optimizer.hpp:135-142). */

@@ -85,12 +85,16 @@ _SIGS = {
     "qftc_plan_set_arena": (_i, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_i64)]),
     "qftc_plan_step": (_i, [_vp, _i, LionHyperC, _vp]),
     "qftc_plans_step": (_i, [C.POINTER(_vp), _i, _i, LionHyperC, _vp]),
+    "qftc_expand_plan_create": (_i, [C.POINTER(_vp), C.POINTER(ExpandTensorC), _i, _i, _vp]),
+    "qftc_expand_plan_run": (_i, [_vp, _vp]),
+    "qftc_expand_plan_destroy": (_i, [_vp]),
     "qftc_plan_set_ctas_per_sm": (_i, [_vp, _i]),
     "qftc_plan_result": (_i, [_vp, C.POINTER(_i64), _vp]),
     "qftc_plan_launches": (_i, [_vp]),
     "qftc_plan_kernel_name": (C.c_char_p, [_vp]),
     "qftc_plan_pending_overflow": (_i, [_vp]),
     "qftc_plan_tier_rows": (_i, [_vp, C.POINTER(_i64), C.POINTER(_i64), _vp]),
+    "qftc_plan_tiers": (_i, [_vp, C.POINTER(_i64), _vp]),
     "qftc_crc32": (_i, [_vp, _vp, _i, _vp, _vp]),
     "qftc_accumulate_state": (_i, [_vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "qftc_plan_destroy": (_i, [_vp]),
@@ -114,6 +118,8 @@ _SIGS = {
 EXPORTS = tuple(_SIGS)
 
 for _name, (_res, _args) in _SIGS.items():
+    if os.environ.get("QFT_B200_LIB") and not hasattr(lib, _name):
+        continue  # an older library build loaded for an A/B (tools/build_variant.py)
     _f = getattr(lib, _name)
     _f.restype = _res
     _f.argtypes = _args

@@ -367,6 +367,35 @@ int qftc_expand(const qftc_expand_tensor* tensors, int n_tensors, int bf16,
   return QFTC_OK;
 }
 
+int qftc_expand_plan_create(qftc_expand_plan** plan, const qftc_expand_tensor* tensors,
+                            int n_tensors, int bf16, qftc_stream_t stream) {
+  if (!plan || n_tensors < 0 || (n_tensors > 0 && !tensors))
+    return fail(QFTC_EINVAL, "expand_plan_create: bad tensor list");
+  for (int i = 0; i < n_tensors; ++i) {
+    const qftc_expand_tensor& t = tensors[i];
+    if (int rc = require_shape(t.rows, t.cols, "expand")) return rc;
+    if (!t.codes || !t.scale || !t.zero_point || !t.row_start || !t.out)
+      return fail(QFTC_EINVAL, "expand: null pointer in tensor " + std::to_string(i));
+  }
+  if (int rc = require_device()) return rc;
+  void* p = nullptr;
+  QFTC_CUDA(expand_plan_create(tensors, n_tensors, bf16 != 0, (cudaStream_t)stream, &p),
+            "expand_plan_create");
+  *plan = reinterpret_cast<qftc_expand_plan*>(p);
+  return QFTC_OK;
+}
+
+int qftc_expand_plan_run(qftc_expand_plan* plan, qftc_stream_t stream) {
+  if (!plan) return fail(QFTC_EINVAL, "expand_plan_run: null plan");
+  QFTC_CUDA(expand_plan_run(plan, (cudaStream_t)stream), "expand kernel");
+  return QFTC_OK;
+}
+
+int qftc_expand_plan_destroy(qftc_expand_plan* plan) {
+  expand_plan_destroy(plan);
+  return QFTC_OK;
+}
+
 int qftc_reconstruct(const uint8_t* codes, int rows, int cols, const float* scale,
                      const int32_t* zp, const int32_t* row_ptr, const int32_t* col_idx,
                      const float* values, float* out, qftc_stream_t stream) {
@@ -595,13 +624,22 @@ int qftc_plan_create(qftc_plan** out, const qftc_lion_tensor* ts, int n, int bit
     cudaError_t e = cudaMallocAsync((void**)&p->prep, sizeof(RowPrep) * (size_t)rows, st);
     if (e == cudaSuccess)
       e = cudaMallocAsync((void**)&p->xlist, sizeof(RowBlock) * (size_t)rows, st);
-    if (e == cudaSuccess) e = cudaMallocAsync((void**)&p->rc.xcount, 16, st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(p->rc.xcount, 0, 16, st);
+    if (e == cudaSuccess) e = cudaMallocAsync((void**)&p->rc.xcount, 64, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p->rc.xcount, 0, 64, st);
+    if (e == cudaSuccess) e = cudaMallocAsync((void**)&p->rc.slist, sizeof(int32_t) * (size_t)rows, st);
+    if (e == cudaSuccess) e = cudaMallocAsync((void**)&p->rc.glist, sizeof(int32_t) * (size_t)rows, st);
+    const size_t nb = ((size_t)rows + 255) / 256;
+    if (e == cudaSuccess) e = cudaMallocAsync((void**)&p->rc.pstatus, 8 * nb, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p->rc.pstatus, 0, 8 * nb, st);
+    const char* no_gen = getenv("QFT_NO_GEN");
+    p->rc.gen_on = (no_gen && no_gen[0] == '1') ? 0 : 1;
+    const char* allrows = getenv("QFT_STABLE_ALLROWS");
+    p->rc.stable_allrows = (allrows && allrows[0] == '1') ? 1 : 0;
     if (e == cudaSuccess) {
       void* hp = nullptr;
       if (cudaHostAlloc(&hp, 64, cudaHostAllocMapped) == cudaSuccess) {
         p->rc.seen_host = reinterpret_cast<volatile int32_t*>(hp);
-        *p->rc.seen_host = (int32_t)rows;  // unknown: full grid
+        p->rc.seen_host[0] = p->rc.seen_host[1] = (int32_t)rows;  // unknown: full grids
         void* dp = nullptr;
         if (cudaHostGetDevicePointer(&dp, hp, 0) == cudaSuccess) p->rc.seen_dev = (int32_t*)dp;
       }
@@ -748,7 +786,7 @@ int qftc_plan_result(qftc_plan* p, int64_t* nnz_total, qftc_stream_t stream) {
 }
 
 int qftc_plan_launches(const qftc_plan* p) {
-  return p ? (p->rows_path ? 3 + (p->gq ? 1 : 0) : 1) : 0;
+  return p ? (p->rows_path ? 3 + (p->rc.gen_on ? 1 : 0) + (p->gq ? 1 : 0) : 1) : 0;
 }
 
 const char* qftc_plan_kernel_name(const qftc_plan* p) { return p ? p->last_kernel : ""; }
@@ -760,16 +798,27 @@ int qftc_plan_pending_overflow(const qftc_plan* p) {
 int qftc_plan_tier_rows(qftc_plan* p, int64_t* stable_rows, int64_t* general_rows,
                         qftc_stream_t stream) {
   if (!p) return fail(QFTC_EINVAL, "plan: null");
-  int64_t gen = p->total_rows;  // without the rows kernel every row runs the general kernel
+  int64_t t3[3];
+  if (int rc = qftc_plan_tiers(p, t3, stream)) return rc;
+  if (stable_rows) *stable_rows = t3[0];
+  if (general_rows) *general_rows = t3[1] + t3[2];
+  return QFTC_OK;
+}
+
+int qftc_plan_tiers(qftc_plan* p, int64_t rows_out[3], qftc_stream_t stream) {
+  if (!p || !rows_out) return fail(QFTC_EINVAL, "plan_tiers: bad arguments");
+  rows_out[0] = 0;
+  rows_out[1] = 0;
+  rows_out[2] = p->total_rows;  // without the rows kernel every row runs the general kernel
   if (p->rows_path && p->rc.last_flip >= 0) {
-    int32_t x = 0;
-    QFTC_CUDA(cudaMemcpyAsync(&x, p->rc.xcount + p->rc.last_flip, 4, cudaMemcpyDeviceToHost,
-                              (cudaStream_t)stream), "read row list");
+    int32_t x[4] = {0, 0, 0, 0};
+    QFTC_CUDA(cudaMemcpyAsync(x, p->rc.xcount + 4 * p->rc.last_flip, 12, cudaMemcpyDeviceToHost,
+                              (cudaStream_t)stream), "read row lists");
     QFTC_CUDA(cudaStreamSynchronize((cudaStream_t)stream), "sync");
-    gen = x;
+    rows_out[1] = x[2];
+    rows_out[2] = x[0];
+    rows_out[0] = p->total_rows - x[0] - x[2];  // the stable rows kernel walks every row
   }
-  if (stable_rows) *stable_rows = p->total_rows - gen;
-  if (general_rows) *general_rows = gen;
   return QFTC_OK;
 }
 
@@ -779,6 +828,9 @@ int qftc_plan_destroy(qftc_plan* p) {
   if (p->prep) cudaFree(p->prep);
   if (p->xlist) cudaFree(p->xlist);
   if (p->rc.xcount) cudaFree(p->rc.xcount);
+  if (p->rc.slist) cudaFree(p->rc.slist);
+  if (p->rc.glist) cudaFree(p->rc.glist);
+  if (p->rc.pstatus) cudaFree(p->rc.pstatus);
   if (p->gq_base) cudaFree(p->gq_base);
   if (p->rc.seen_host) cudaFreeHost(const_cast<int32_t*>(p->rc.seen_host));
   if (p->side) {

@@ -13,6 +13,8 @@
 // sync), and a warp finds its tensor by a warp-uniform binary search over the row
 // prefix.
 #include "qft_internal.h"
+
+#include <vector>
 #include "qft_device.cuh"
 
 using namespace qftd;
@@ -88,17 +90,18 @@ struct RowMeta {
   int b, n;
 };
 
-__device__ __forceinline__ RowMeta row_meta(const ExpArgs& a, long long grow) {
+__device__ __forceinline__ RowMeta row_meta(const ExpT* tab, const long long* prefix, int n,
+                                            long long grow) {
   // warp-uniform binary search: tensor ti with prefix[ti] <= grow < prefix[ti+1]
-  int lo = 0, hi = a.n - 1;
+  int lo = 0, hi = n - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (a.prefix[mid] <= grow) lo = mid; else hi = mid - 1;
+    if (prefix[mid] <= grow) lo = mid; else hi = mid - 1;
   }
-  const ExpT& T = a.t[lo];
+  const ExpT& T = tab[lo];
   RowMeta m;
   m.ti = lo;
-  m.r = (int)(grow - a.prefix[lo]);
+  m.r = (int)(grow - prefix[lo]);
   m.s = T.scale[m.r];
   m.z = T.zp[m.r];
   m.b = T.rs[m.r];
@@ -112,16 +115,17 @@ __device__ __forceinline__ RowMeta row_meta(const ExpArgs& a, long long grow) {
 // loaded while the current row streams, the row's first 64 CSR entries are loaded
 // before its dense loads, and each lane keeps EXP_UNROLL 16-byte loads in flight.
 template <bool BF16>
-__global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const __grid_constant__ ExpArgs a) {
+__device__ __forceinline__ void expand_rows(const ExpT* tab, const long long* prefix, int n,
+                                            long long total_rows) {
   const int lane = threadIdx.x & 31;
   const long long nwarps = (long long)gridDim.x * EXP_WARPS;
   long long grow = (long long)blockIdx.x * EXP_WARPS + (threadIdx.x >> 5);
-  if (grow >= a.total_rows) return;
-  RowMeta nxt = row_meta(a, grow);
-  for (; grow < a.total_rows; grow += nwarps) {
+  if (grow >= total_rows) return;
+  RowMeta nxt = row_meta(tab, prefix, n, grow);
+  for (; grow < total_rows; grow += nwarps) {
     const RowMeta m = nxt;
-    if (grow + nwarps < a.total_rows) nxt = row_meta(a, grow + nwarps);
-    const ExpT& T = a.t[m.ti];
+    if (grow + nwarps < total_rows) nxt = row_meta(tab, prefix, n, grow + nwarps);
+    const ExpT& T = tab[m.ti];
     const int cols = T.cols;
     const size_t base = (size_t)m.r * (size_t)cols;
     // the row's first 64 outliers, loaded early
@@ -165,6 +169,19 @@ __global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const __grid_con
     if (c1 >= 0) store1<BF16>(T.out, base + c1, v1);
     for (int j = 64 + lane; j < m.n; j += 32) store1<BF16>(T.out, base + T.col[m.b + j], T.val[m.b + j]);
   }
+}
+
+// the table in the kernel parameter space (up to EXP_MAXT tensors, nothing to upload) ...
+template <bool BF16>
+__global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel(const __grid_constant__ ExpArgs a) {
+  expand_rows<BF16>(a.t, a.prefix, a.n, a.total_rows);
+}
+// ... or in device memory (an expand plan: any number of tensors, one launch)
+template <bool BF16>
+__global__ void __launch_bounds__(EXP_WARPS * 32) expand_kernel_dev(const ExpT* tab,
+                                                                  const long long* prefix, int n,
+                                                                  long long total_rows) {
+  expand_rows<BF16>(tab, prefix, n, total_rows);
 }
 
 }  // namespace
@@ -221,6 +238,83 @@ cudaError_t launch_expand(const qftc_expand_tensor* ts, int n, bool bf16, cudaSt
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+// ------------------------------------------------------------------ expand plans
+struct ExpandPlan {
+  ExpT* tab = nullptr;          // device table
+  long long* prefix = nullptr;  // device row prefix (n + 1)
+  int n = 0;
+  long long total = 0;
+  bool bf16 = false;
+  int grid = 0;
+};
+
+cudaError_t expand_plan_create(const qftc_expand_tensor* ts, int n, bool bf16, cudaStream_t st,
+                               void** out) {
+  std::vector<ExpT> tab;
+  std::vector<long long> pre;
+  long long acc = 0;
+  for (int i = 0; i < n; ++i) {
+    const qftc_expand_tensor& s = ts[i];
+    if (s.rows <= 0 || s.cols <= 0) continue;
+    ExpT t{};
+    t.codes = s.codes; t.scale = s.scale; t.zp = s.zero_point; t.rs = s.row_start;
+    t.cnt = s.row_count; t.col = s.col_idx; t.val = s.values; t.out = s.out;
+    t.rows = s.rows; t.cols = s.cols;
+    const int esz = bf16 ? 2 : 4;
+    t.aligned = (s.cols % 16 == 0) && al16(s.codes) && al16(s.out) && ((size_t)s.cols * esz % 16 == 0);
+    pre.push_back(acc);
+    acc += s.rows;
+    tab.push_back(t);
+  }
+  pre.push_back(acc);
+  auto* p = new ExpandPlan;
+  p->n = (int)tab.size();
+  p->total = acc;
+  p->bf16 = bf16;
+  cudaError_t e = cudaSuccess;
+  if (p->n > 0) {
+    e = cudaMalloc(&p->tab, sizeof(ExpT) * tab.size());
+    if (e == cudaSuccess) e = cudaMalloc(&p->prefix, sizeof(long long) * pre.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(p->tab, tab.data(), sizeof(ExpT) * tab.size(), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(p->prefix, pre.data(), sizeof(long long) * pre.size(), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the host vectors die here
+  }
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, bf16 ? (const void*)expand_kernel_dev<true> : (const void*)expand_kernel_dev<false>,
+        EXP_WARPS * 32, 0);
+  long long grid = (acc + EXP_WARPS - 1) / EXP_WARPS;
+  const long long cap = (long long)sms * (per_sm > 0 ? per_sm : 1);
+  p->grid = (int)(grid < cap ? (grid < 1 ? 1 : grid) : cap);
+  if (e != cudaSuccess) {
+    expand_plan_destroy(p);
+    return e;
+  }
+  *out = p;
+  return cudaSuccess;
+}
+
+cudaError_t expand_plan_run(void* plan, cudaStream_t st) {
+  auto* p = static_cast<ExpandPlan*>(plan);
+  if (p->n == 0) return cudaSuccess;
+  if (p->bf16) expand_kernel_dev<true><<<p->grid, EXP_WARPS * 32, 0, st>>>(p->tab, p->prefix, p->n, p->total);
+  else expand_kernel_dev<false><<<p->grid, EXP_WARPS * 32, 0, st>>>(p->tab, p->prefix, p->n, p->total);
+  return cudaGetLastError();
+}
+
+void expand_plan_destroy(void* plan) {
+  auto* p = static_cast<ExpandPlan*>(plan);
+  if (!p) return;
+  if (p->tab) cudaFree(p->tab);
+  if (p->prefix) cudaFree(p->prefix);
+  delete p;
 }
 
 }  // namespace qftk

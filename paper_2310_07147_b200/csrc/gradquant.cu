@@ -57,8 +57,12 @@ __device__ __forceinline__ void unpack(const uint4& q, float* x) {
 // qmax, so no clip is needed): per element one multiply, the magic-number rint and its
 // tie distance; a thread whose values come within the error bound of a tie redoes its
 // vectors with the reference's fp64 formula.
+// register budget: the row in flight twice (current + prefetched next row, 8 regs per
+// vector) plus ~24; a budget below that would spill the prefetch to local memory
+template <int NT, int VPL>
+constexpr int gq_minb() { return VPL <= 2 ? 65536 / (NT * 64) : 65536 / (NT * 128); }
 template <bool BF16, int NT, int VPL>
-__global__ void __launch_bounds__(NT, 1024 / NT) k_grad_quant(const LaunchArgs a) {
+__global__ void __launch_bounds__(NT, gq_minb<NT, VPL>()) k_grad_quant(const LaunchArgs a) {
   using namespace gq;
   constexpr int EPV = BF16 ? 8 : 4;  // elements per 16-byte vector
   constexpr int NW = NT / 32;
@@ -68,29 +72,46 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_grad_quant(const LaunchArgs a
   const int qmax = (1 << bw) - 1;
   const double rq = __drcp_rn((double)qmax);
   int par = 0;
-  for (int gr = blockIdx.x; gr < a.total_rows; gr += gridDim.x, par ^= 1) {
+  // the row's tensor (binary search over the row bases) and its first 16-byte vector
+  auto locate = [&](int row, int& ti) -> const uint4* {
     int lo_t = 0, hi_t = a.n_tensors - 1;
     while (lo_t < hi_t) {
       const int mid = (lo_t + hi_t + 1) >> 1;
-      if (a.tensors[mid].row_base <= gr) lo_t = mid;
+      if (a.tensors[mid].row_base <= row) lo_t = mid;
       else hi_t = mid - 1;
     }
+    ti = lo_t;
     const DevTensor& T = a.tensors[lo_t];
-    const int r = gr - T.row_base;
-    const int cols = T.cols;
-    const int nv = cols / EPV;  // cols % 16 == 0 on this path
-    const uint4* src = reinterpret_cast<const uint4*>(
-        reinterpret_cast<const uint8_t*>(T.g_raw) + (size_t)r * cols * (BF16 ? 2 : 4));
-    uint4 v[VPL];
+    return reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(T.g_raw) +
+                                          (size_t)(row - T.row_base) * T.cols * (BF16 ? 2 : 4));
+  };
+  // loads of a row into registers; vectors past the row end repeat vector 0 (same range)
+  auto load = [&](const uint4* src, int nv, uint4* v) {
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
       const int i = t + j * NT;
-      v[j] = i < nv ? __ldcs(src + i) : v[0];  // padding repeats a real vector (same range)
+      v[j] = __ldcs(src + (i < nv ? i : 0));
     }
-    if (t >= nv) v[0] = __ldcs(src);  // (rows shorter than the CTA: lanes past the end)
-#pragma unroll
-    for (int j = 1; j < VPL; ++j)
-      if (t + j * NT >= nv) v[j] = v[0];
+  };
+  int gr = blockIdx.x;
+  if (gr >= a.total_rows) return;
+  int ti;
+  const uint4* src = locate(gr, ti);
+  uint4 v[VPL], vn[VPL];
+  load(src, a.tensors[ti].cols / EPV, v);
+  for (;; gr += gridDim.x, par ^= 1) {
+    const DevTensor& T = a.tensors[ti];
+    const int r = gr - T.row_base;
+    const int cols = T.cols;
+    const int nv = cols / EPV;  // cols % 16 == 0 on this path
+    // the CTA's next row streams in while this one is reduced and quantized
+    const int gn = gr + (int)gridDim.x;
+    int tin = ti;
+    const uint4* srcn = nullptr;
+    if (gn < a.total_rows) {
+      srcn = locate(gn, tin);
+      load(srcn, a.tensors[tin].cols / EPV, vn);
+    }
     float lo = __int_as_float(0x7f800000), hi = __int_as_float(0xff800000);
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
@@ -170,6 +191,11 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_grad_quant(const LaunchArgs a
           __stcs(reinterpret_cast<uint32_t*>(dst) + i, c[j][0]);
       }
     }
+    if (gn >= a.total_rows) break;
+    ti = tin;
+    src = srcn;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) v[j] = vn[j];
   }
 }
 
@@ -194,12 +220,11 @@ static cudaError_t gq_resolve_t(int total_rows, const char* name, KLaunch* out) 
 // the launch for a plan of raw-gradient kind gk over rows of <= max_cols columns
 cudaError_t resolve_grad_quant(int gk, int max_cols, int total_rows, KLaunch* out) {
   if (gk == G_BF16) {  // 8 elements per vector
-    if (max_cols <= 8 * 128 * 4) return gq_resolve_t<true, 128, 4>(total_rows, "k_grad_quant<bf16,128,4>", out);
-    if (max_cols <= 8 * 256 * 7) return gq_resolve_t<true, 256, 7>(total_rows, "k_grad_quant<bf16,256,7>", out);
-    if (max_cols <= 8 * 512 * 4) return gq_resolve_t<true, 512, 4>(total_rows, "k_grad_quant<bf16,512,4>", out);
+    if (max_cols <= 8 * 256 * 2) return gq_resolve_t<true, 256, 2>(total_rows, "k_grad_quant<bf16,256,2>", out);
+    if (max_cols <= 8 * 1024 * 2) return gq_resolve_t<true, 1024, 2>(total_rows, "k_grad_quant<bf16,1024,2>", out);
   } else if (gk == G_F32) {  // 4 elements per vector
-    if (max_cols <= 4 * 128 * 8) return gq_resolve_t<false, 128, 8>(total_rows, "k_grad_quant<f32,128,8>", out);
-    if (max_cols <= 4 * 256 * 14) return gq_resolve_t<false, 256, 14>(total_rows, "k_grad_quant<f32,256,14>", out);
+    if (max_cols <= 4 * 512 * 2) return gq_resolve_t<false, 512, 2>(total_rows, "k_grad_quant<f32,512,2>", out);
+    if (max_cols <= 4 * 1024 * 2) return gq_resolve_t<false, 1024, 2>(total_rows, "k_grad_quant<f32,1024,2>", out);
     if (max_cols <= 4 * 512 * 8) return gq_resolve_t<false, 512, 8>(total_rows, "k_grad_quant<f32,512,8>", out);
   }
   return cudaErrorInvalidValue;

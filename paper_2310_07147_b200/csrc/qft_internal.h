@@ -99,8 +99,18 @@ struct LaunchArgs {
   const int32_t* n_blocks_dev;   // step_kernel: read the block count from the device
   int32_t* xclear;               // prep: the OTHER flip's row-list counter, zeroed for the next step
   uint32_t* oflag;               // mapped pinned overflow flag (host-visible without a sync)
-  int32_t* xseen;                // step_kernel: the row-list length it saw (mapped pinned)
-  int32_t* rclaim;               // rows kernel: row-claim counter (zeroed by k_step_prep)
+  int32_t* xseen;                // step_kernel / GEN rows kernel: the list length it saw
+                                 // (mapped pinned)
+  int32_t* rclaim;               // prep: [2] row-claim counters (zeroed); rows kernel: its own
+  int32_t* slist;                // prep: stable-tier rows (this step) ...
+  int32_t* glist;                // ... and GEN-tier rows
+  int32_t* scount;
+  int32_t* gcount;
+  const int32_t* rlist;          // rows kernel: the row list it iterates ...
+  const int32_t* rcount;         // ... and its length (device)
+  int32_t gen_on;                // prep: route rows that miss only (*) to the GEN tier
+  int32_t epoch;                 // prep: this launch's look-back epoch
+  unsigned long long* pstatus;   // prep: per-block look-back status words
 };
 
 // Per-row record of the rows kernel (128 B), written by k_step_prep every step and
@@ -150,7 +160,16 @@ struct RowsCache {
   KLaunch rows[2];     // by slotted input (0/1)
   KLaunch gen[2];      // general kernel over the device list, by weight decay == 0 (0/1)
   int last_flip = -1;  // the flip of the previous step (a repeated flip re-zeroes its counter)
-  int32_t* xcount = nullptr;  // [4]: row-list counters (one per flip), [2] row-claim counter
+  // [16]: per flip f, [4f] general-list, [4f+1] stable-list, [4f+2] GEN-list counters,
+  // [4f+3] the prep block ticket; [8] / [9] the stable / GEN rows kernels' claim counters
+  int32_t* xcount = nullptr;
+  int32_t* slist = nullptr;  // stable-tier / GEN-tier row lists (rows entries each)
+  int32_t* glist = nullptr;
+  KLaunch genrows[2];        // the GEN rows kernel, by slotted input (0/1)
+  int gen_on = 1;
+  int stable_allrows = 0;  // A/B: the stable kernel over every row (no list)
+  unsigned long long* pstatus = nullptr;  // prep look-back status words (one per block)
+  int epoch = 0;
   // the general-tier row count the general kernel last saw (mapped pinned, read without a
   // sync): an empty list last time -> launch that kernel with one CTA per SM (it still
   // covers any list length, grid-stride)
@@ -187,5 +206,10 @@ cudaError_t crc32_device(const void* const* segs, const int64_t* lens, int n, ui
 // weight expansion (expand.cu): one launch per expand_max_tensors() tensors
 int expand_max_tensors();
 cudaError_t launch_expand(const qftc_expand_tensor* ts, int n, bool bf16, cudaStream_t s);
+// an expand plan: the table uploaded once, any number of tensors per launch
+cudaError_t expand_plan_create(const qftc_expand_tensor* ts, int n, bool bf16, cudaStream_t s,
+                               void** out);
+cudaError_t expand_plan_run(void* plan, cudaStream_t s);
+void expand_plan_destroy(void* plan);
 
 }  // namespace qftk

@@ -61,15 +61,13 @@ using namespace qftd;
 #ifndef QFT_CLAIM_K
 #define QFT_CLAIM_K 8  // rows per dynamic claim
 #endif
-#ifndef QFT_STATIC_NS3
-#define QFT_STATIC_NS3 0  // 1: static rows for the 3-stage (<= 4096-column) class only
-#endif
 #ifndef QFT_OC3
 #define QFT_OC3 64  // old-outlier table of the 3-stage class: cols / QFT_OC3 entries
 #endif
 
 namespace rs6 {
 constexpr uint32_t I_STABLE = 1u;
+constexpr uint32_t I_GEN = 0x80u;  // the GEN tier: every code requantized in this kernel
 constexpr int V = 2;  // 16-byte vectors per thread
 
 // Per-CTA shared memory (runtime sizes).
@@ -203,6 +201,54 @@ __device__ __forceinline__ float exact_wprime(uint32_t qw, uint32_t qm, uint32_t
   return w;
 }
 
+// w' = w - lr*(sign(d) + wd*w) for a pair (lion_apply, optimizer.hpp:38) given d: with
+// weight decay 0 the update is exactly -copysign(lr, d) or nothing (d == +-0; w is finite),
+// else the general form in the reference's order (see lion2 in qft_device.cuh)
+__device__ __forceinline__ float2 gen_lion(float2 w, float2 d, const Hyper& h, uint32_t nlr) {
+  if (h.wd == 0.0f) {
+    asm("{\n\t.reg .pred p;\n\t"
+        "setp.gt.f32 p, %1, 0f00000000;\n\t"
+        "@p add.rn.f32 %0, %0, %2;\n\t}"
+        : "+f"(w.x)
+        : "f"(fabsf(d.x)), "f"(neg_lr_sign(d.x, nlr)));
+    asm("{\n\t.reg .pred p;\n\t"
+        "setp.gt.f32 p, %1, 0f00000000;\n\t"
+        "@p add.rn.f32 %0, %0, %2;\n\t}"
+        : "+f"(w.y)
+        : "f"(fabsf(d.y)), "f"(neg_lr_sign(d.y, nlr)));
+    return w;
+  }
+  const float2 sg = make_float2(sign_of(d.x), sign_of(d.y));
+  const float2 upd = mul2(f2(h.lr), sadd2(sg, mul2(f2(h.wd), w)));
+  return sadd2(w, neg2(upd));
+}
+
+// A GEN-tier vector whose fast quantization came near a tie: every code of the 16 by the
+// reference's fp64 formula (out of line: rare)
+__device__ __noinline__ void gen_vec_exact(uint4 cw, uint4 cm, uint4 cg, const RowPrep& R,
+                                           const Hyper& h, int bw, uint32_t* cq,
+                                           uint32_t& mask) {
+  const int qmax = (1 << bw) - 1;
+  const uint32_t zpay = (R.info >> 8) & 0xFFu;
+  const uint32_t ww[4] = {cw.x, cw.y, cw.z, cw.w};
+  const uint32_t mw[4] = {cm.x, cm.y, cm.z, cm.w};
+  const uint32_t gw[4] = {cg.x, cg.y, cg.z, cg.w};
+  mask = 0;
+  for (int i = 0; i < 4; ++i) {
+    uint32_t c = 0;
+    for (int e = 0; e < 4; ++e) {
+      float w = dequant_exact((ww[i] >> (8 * e)) & 0xFFu, R.sw, R.zw);
+      float m = dequant_exact((mw[i] >> (8 * e)) & 0xFFu, R.sm, R.zm);
+      const float g = dequant_exact((gw[i] >> (8 * e)) & 0xFFu, R.sg, R.zg);
+      lion1(w, m, g, h);
+      const bool o = (w < R.tmin) || (w > R.tmax);
+      if (o) mask |= 1u << (4 * i + e);
+      c |= (o ? zpay : quant_exact(w, R.sw, R.zw, qmax)) << (8 * e);
+    }
+    cq[i] = c;
+  }
+}
+
 }  // namespace rs6
 
 int rows_kernel_nt(int cols) {
@@ -244,9 +290,12 @@ __host__ __device__ constexpr int geom_oldcap(int cols, int ns) {
 // per-vector bounds checks they cover vanish at compile time.
 // CCOLS > 0: the launch's row length is the compile-time constant CCOLS (LLaMA widths)
 // and its input CSR is slotted; BWC > 0: the bit width is the constant BWC
-template <int MAXT, int MINB, int NS, int FULL, int CCOLS, int BWC>
+template <int MAXT, int MINB, int NS, int FULL, int CCOLS, int BWC, bool GEN>
 __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   using namespace rs6;
+  // the tier this instance runs (its row list holds only such rows; the flag is checked
+  // again from the record)
+  constexpr uint32_t I_ACT = GEN ? I_GEN : I_STABLE;
   extern __shared__ __align__(128) uint8_t smem[];
   // CCOLS: the row geometry is a compile-time constant (threads, columns, old-outlier
   // table), so every shared-memory offset folds
@@ -267,6 +316,8 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   h.c1 = __fsub_rn(1.0f, a.b1);
   h.c2 = __fsub_rn(1.0f, a.b2);
   const float2 B2 = f2(h.b2), C2 = f2(h.c2), NZ = f2(a.negzero);
+  const float2 B1 = f2(h.b1), C1 = f2(h.c1);
+  const uint32_t nlr = __float_as_uint(-h.lr);
   const double rq = __drcp_rn((double)qmax);
 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.o_bar());
@@ -369,15 +420,22 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   // thread 0 at the top of the iteration; with 3 it is the last warp's lane 0 inside
   // the barrier window, where that warp has no other work (off the phase-1 path).
   const int ti = (NS == 3 && NW > 1) ? NT - 32 : 0;
+  // The launch iterates a ROW LIST (k_step_prep's list of this tier's rows, in nearly
+  // ascending row order).  List positions are claimed in chunks of QFT_CLAIM_K; the
+  // issuer runs three deep: position claimed -> row read from the list -> record head
+  // loaded -> row streamed, each result consumed one issue after it was requested.
   RowHead hn{};   // issuing thread: the head of the row it streams next ...
   int nxt = TR;   // ... that row (>= TR: none)
-  int nxt2 = TR;  // the row claimed after it (atomic result, consumed one issue later)
-  // rows are claimed in chunks of QFT_CLAIM_K consecutive rows; the next chunk's atomic is
-  // issued when the current one is taken, so its result is needed only K issues later
+  int nxt2 = TR;  // the row after it (claimed / read from the list one issue ahead)
+  // Rows (the stable instance: every row of the launch; rows outside the stable tier flow
+  // through without work) or list positions (the GEN instance: k_step_prep's list of GEN
+  // rows) are claimed in chunks of QFT_CLAIM_K consecutive ones; the next chunk's atomic is
+  // issued when the current one is taken, so its result is needed only K claims later.
   int sc = blockIdx.x;  // QFT_STATIC_ROWS: the static sequence blockIdx.x + k*gridDim.x
   int c_cur = 0, c_end = 0, c_pend = 0;
+  int cnt_l = 0;  // GEN: the list length
   auto claim = [&]() -> int {
-    if (QFT_STATIC_ROWS || (QFT_STATIC_NS3 && NS == 3)) {
+    if (QFT_STATIC_ROWS) {
       const int r = sc;
       sc += (int)gridDim.x;
       return r;
@@ -390,6 +448,14 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
     }
     return c_cur++;
   };
+  auto next_row = [&]() -> int {
+    if constexpr (GEN) {
+      const int pos = claim();
+      return pos < cnt_l ? __ldg(a.rlist + pos) : TR;
+    } else {
+      return claim();
+    }
+  };
   auto issue_or_end = [&](int s) {
     if (nxt < TR) {
       rowid[s] = nxt;
@@ -400,7 +466,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
     }
     nxt = nxt2;
     if (nxt < TR) hn = load_head(a, nxt);
-    nxt2 = claim();
+    nxt2 = next_row();
   };
   if (t == 0) {
     for (int i = 0; i < NS; ++i) mbar_init(&bars[i], 1);
@@ -409,16 +475,20 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   clear_words(0);
   __syncthreads();
   if (t == ti) {
-    nxt = claim();
+    if constexpr (GEN) {
+      cnt_l = *a.rcount;
+      if (a.xseen && blockIdx.x == 0) *reinterpret_cast<volatile int32_t*>(a.xseen) = cnt_l;
+    }
+    nxt = next_row();
     if (nxt < TR) hn = load_head(a, nxt);
-    nxt2 = claim();
+    nxt2 = next_row();
     for (int i = 0; i < NS - 1; ++i) issue_or_end(i);
   }
   mbar_wait(&bars[0], 0u);
   int gr = rowid[0];
   if (gr < 0) return;  // no row for this CTA (its other stages hold sentinels too)
-  if (rec(0)->info & I_STABLE) sparse_pass(0, 0, 0, NT);
-  int on_prev = (rec(0)->info & I_STABLE) ? rec(0)->on : 0;
+  if (rec(0)->info & I_ACT) sparse_pass(0, 0, 0, NT);
+  int on_prev = (rec(0)->info & I_ACT) ? rec(0)->on : 0;
   __syncthreads();
 
   const int tw = NW > 1 ? 32 : 0;  // first thread of the deferred / sparse work
@@ -433,7 +503,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
     clear_words(bn);
     mbar_wait(&bars[s], (uint32_t)((it / NS) & 1));
     const RowPrep& R = *rec(s);
-    const bool stable = (R.info & I_STABLE) != 0;
+    const bool stable = (R.info & I_ACT) != 0;  // (the GEN instance: "active")
     const uint8_t* st = stage(s);
     const float negc_m = R.negc_m, sm = R.sm, negc_g = R.negc_g, sg = R.sg;
     uint8_t* const m_out = R.m_out;
@@ -444,6 +514,15 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
         ((((R.cand >> 24) & 0xFFu) != (uint32_t)qmax || (R.info >> 16) != ((uint32_t)qmax * 0x101u) ||
           (R.info & (7u << 4)) != 0u) ? 2u : 0u);
     const int so = R.so, co = R.co, on_cur = stable ? R.on : 0;
+    // GEN tier: the row's weight dequant / quantizer constants and the payload value
+    float gw_s = 0.0f, gw_negc = 0.0f, gw_z = 0.0f;
+    QuantRow gw_q{};
+    if constexpr (GEN) {
+      gw_s = R.sw;
+      gw_negc = -__fadd_rn(8388608.0f, (float)R.zw);
+      gw_z = dequant_exact((R.info >> 8) & 0xFFu, R.sw, R.zw);
+      gw_q = make_quant_row(R.sw, R.zw, bw);
+    }
 
     // ================================ phase 1 ================================
     float mp[V][16];
@@ -459,6 +538,66 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
         const uint4 cwj = *reinterpret_cast<const uint4*>(st + 128 + v * 16);
         const uint4 cmj = *reinterpret_cast<const uint4*>(st + 128 + cols + v * 16);
         const uint4 cgj = *reinterpret_cast<const uint4*>(st + 128 + 2 * cols + v * 16);
+        if constexpr (GEN) {
+          // ---- the GEN tier: every dense weight through the reference arithmetic --
+          // w = dequant (quantize.hpp:209), Lion (optimizer.hpp:33-40, fp32, separate
+          // roundings), the outlier test against the cached thresholds and the code
+          // (quantize.hpp:274-285) -- with the range-proven fast quantizer (the row's
+          // thresholds map to codes 0 and qmax, so an inlier never needs the clip);
+          // outliers take the payload value wz (its code is the payload, exactly)
+          const uint32_t mw[4] = {cmj.x, cmj.y, cmj.z, cmj.w};
+          const uint32_t gw[4] = {cgj.x, cgj.y, cgj.z, cgj.w};
+          const uint32_t ww[4] = {cwj.x, cwj.y, cwj.z, cwj.w};
+          uint32_t cq[4], mask = 0;
+          float em = 0.0f;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            float2 a0 = make_float2(magic_byte(mw[i], 0), magic_byte(mw[i], 1));
+            float2 a1 = make_float2(magic_byte(mw[i], 2), magic_byte(mw[i], 3));
+            float2 b0 = make_float2(magic_byte(gw[i], 0), magic_byte(gw[i], 1));
+            float2 b1 = make_float2(magic_byte(gw[i], 2), magic_byte(gw[i], 3));
+            float2 w0 = make_float2(magic_byte(ww[i], 0), magic_byte(ww[i], 1));
+            float2 w1 = make_float2(magic_byte(ww[i], 2), magic_byte(ww[i], 3));
+            a0 = mul2(add2(a0, f2(negc_m)), f2(sm));
+            a1 = mul2(add2(a1, f2(negc_m)), f2(sm));
+            b0 = mul2(add2(b0, f2(negc_g)), f2(sg));
+            b1 = mul2(add2(b1, f2(negc_g)), f2(sg));
+            w0 = mul2(add2(w0, f2(gw_negc)), f2(gw_s));
+            w1 = mul2(add2(w1, f2(gw_negc)), f2(gw_s));
+            const float2 r0 = mprime2(a0, b0, B2, C2, NZ);
+            const float2 r1 = mprime2(a1, b1, B2, C2, NZ);
+            mp[j][4 * i] = r0.x; mp[j][4 * i + 1] = r0.y;
+            mp[j][4 * i + 2] = r1.x; mp[j][4 * i + 3] = r1.y;
+            const float2 d0 = mprime2(a0, b0, B1, C1, NZ);  // d = RN(RN(b1 m) + RN(c1 g))
+            const float2 d1 = mprime2(a1, b1, B1, C1, NZ);
+            w0 = gen_lion(w0, d0, h, nlr);
+            w1 = gen_lion(w1, d1, h, nlr);
+            float q4[4];
+            q4[0] = outlier_select(w0.x, R.tmin, R.tmax, gw_z, 1u << (4 * i), mask);
+            q4[1] = outlier_select(w0.y, R.tmin, R.tmax, gw_z, 2u << (4 * i), mask);
+            q4[2] = outlier_select(w1.x, R.tmin, R.tmax, gw_z, 4u << (4 * i), mask);
+            q4[3] = outlier_select(w1.y, R.tmin, R.tmax, gw_z, 8u << (4 * i), mask);
+            cq[i] = quant4_e(q4, gw_q, em);
+          }
+#pragma unroll
+          for (int pp = 0; pp < 8; ++pp) {
+            float tt;
+            asm("min.f32 %0, %1, %2, %3;" : "=f"(tt) : "f"(mlo), "f"(mp[j][2 * pp]), "f"(mp[j][2 * pp + 1]));
+            mlo = tt;
+            asm("max.f32 %0, %1, %2, %3;" : "=f"(tt) : "f"(mhi), "f"(mp[j][2 * pp]), "f"(mp[j][2 * pp + 1]));
+            mhi = tt;
+          }
+          if (!(em < gw_q.thr)) gen_vec_exact(cwj, cmj, cgj, R, h, bw, cq, mask);  // near a tie
+          const uint32_t wrd = words(b)[v];
+          // old-outlier positions: class and code come from the sparse pass (old_out)
+          const uint32_t dn = mask & ~(wrd & 0xFFFFu);
+          const uint32_t o16 = dn | (wrd >> 16);
+          nmask[j] = dn;
+          if (dn) atomicOr(&words(b)[v], dn << 16);
+          out16[j] = o16;
+          cnt |= (uint32_t)__popc(o16) << (16 * j);
+          __stcs(reinterpret_cast<uint4*>(R.w_out) + v, make_uint4(cq[0], cq[1], cq[2], cq[3]));
+        } else {
         const uint32_t mw[4] = {cmj.x, cmj.y, cmj.z, cmj.w};
         const uint32_t gw[4] = {cgj.x, cgj.y, cgj.z, cgj.w};
 #pragma unroll
@@ -533,6 +672,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
         out16[j] = o16;
         cnt |= (uint32_t)__popc(o16) << (16 * j);
         __stcs(reinterpret_cast<uint4*>(R.w_out) + v, wq);
+        }  // stable tier
       }
     }
 
@@ -615,7 +755,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
         if (it > 0) old_out(bp, on_prev, 0, NT);
         if (has_next) {
           mbar_wait(&bars[sn], (uint32_t)(((it + 1) / NS) & 1));
-          if (rec(sn)->info & I_STABLE) sparse_pass(sn, bn, 0, NT);
+          if (rec(sn)->info & I_ACT) sparse_pass(sn, bn, 0, NT);
         }
       }
     } else {
@@ -628,7 +768,7 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
       if (it > 0) old_out(bp, on_prev, ts < NT ? ts : tw, NT);
       if (has_next && t < ts) {  // the next row's old outliers, from its landed stage
         mbar_wait(&bars[sn], (uint32_t)(((it + 1) / NS) & 1));
-        if (rec(sn)->info & I_STABLE) sparse_pass(sn, bn, tw, ts);
+        if (rec(sn)->info & I_ACT) sparse_pass(sn, bn, tw, ts);
       }
     }
     __syncthreads();  // ---------------------------------------------------- B
@@ -698,110 +838,144 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
 }
 
 // ---------------------------------------------------------------------------- prep
-// One thread per row of the launch: the RowPrep record and the tier decision.
-__global__ void k_step_prep(const LaunchArgs a, int stable_ok) {
-  const int gr = blockIdx.x * blockDim.x + threadIdx.x;
-  if (gr == 0 && a.xclear) *a.xclear = 0;  // the next step's row-list counter
-  if (gr == 0 && a.rclaim) *a.rclaim = 0;  // the rows kernel's row-claim counter
-  if (gr >= a.total_rows) return;
-  // tensor of the row (binary search over the row bases)
-  int lo = 0, hi = a.n_tensors - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (a.tensors[mid].row_base <= gr) lo = mid;
-    else hi = mid - 1;
-  }
-  const DevTensor& T = a.tensors[lo];
-  const int r = gr - T.row_base;
-  const int in = a.flip, out = 1 - a.flip;
-  const int qmax = (1 << a.bit_width) - 1;
-  const float sw = T.w_scale[r], tmin = T.t_min[r], tmax = T.t_max[r];
-  const int32_t zw = T.w_zp[r];
-  const float sm = T.m_scale[in][r];
-  const int32_t zm = T.m_zp[in][r];
-  const float sg = T.g_scale ? T.g_scale[r] : 0.0f;
-  const int32_t zg = T.g_zp ? T.g_zp[r] : 0;
-  const int32_t* rsi = T.rs[in];
-  const int ob = rsi[r];
-  const int cap_in = rsi[r + 1] - ob;
-  const int on = T.cnt[in] ? min(T.cnt[in][r], cap_in) : cap_in;
-  const int so = T.rs[out][r];
-  const int co = T.rs[out][r + 1] - so;
-  const int zpay = zw < 0 ? 0 : (zw > qmax ? qmax : zw);
+// warp-aggregated append of the flagged lanes' values to a list (one atomic per warp, the
+// lanes' order kept), so a list built by consecutive rows stays in nearly ascending order
+template <typename T>
+__device__ __forceinline__ void warp_append(bool flag, T val, T* list, int32_t* count) {
+  const uint32_t m = __ballot_sync(0xffffffffu, flag);
+  if (!m) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(count, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (flag) list[base + __popc(m & ((1u << lane) - 1u))] = val;
+}
 
-  bool ok = stable_ok != 0 && on <= a.oldcap6 && T.cols == a.cols_p && T.cnt[out] != nullptr;
-  ok = ok && make_dequant_row(sw, zw).fast && make_dequant_row(sm, zm).fast &&
-       make_dequant_row(sg, zg).fast;
-  // positive, normal scales (so 1/s is finite and the dense values are bounded)
-  ok = ok && sw >= 0x1.0p-126f && sw <= 0x1.0p100f && sm >= 0x1.0p-126f && sm <= 0x1.0p100f &&
-       sg >= 0x1.0p-126f && sg <= 0x1.0p100f;
-  if (ok) {
-    const double K = (double)qmax + fabs((double)zw);
-    // m' = b2*m + c2*g finite: |m|, |g| <= s*(qmax+|z|) <= 2^120, |b2|, |c2| <= 4
-    const double c2 = (double)__fsub_rn(1.0f, a.b2);
-    ok = (double)sm * ((double)qmax + fabs((double)zm)) <= 0x1.0p120 &&
-         (double)sg * ((double)qmax + fabs((double)zg)) <= 0x1.0p120 &&
-         fabs((double)a.b2) <= 4.0 && fabs(c2) <= 4.0;
-    // thresholds map to the ends of the code range
-    ok = ok && (tmin <= tmax) && code_unclamped(tmin, sw, zw) == 0.0 &&
-         code_unclamped(tmax, sw, zw) == (double)qmax;
-    // (*) the step cannot move a dense code: D/sw <= 0.5 - (K+2)*2^-21
-    const double lr = fabs((double)a.lr), wd = fabs((double)a.wd);
-    const double wmax = (double)sw * K * (1.0 + 0x1.0p-20);
-    const double D = lr * (1.0 + wd * wmax) * (1.0 + 0x1.0p-20);
-    ok = ok && isfinite(lr) && isfinite(wd) && D / (double)sw <= 0.5 - (K + 2.0) * 0x1.0p-21;
+// One thread per row of the launch: the RowPrep record and the row's TIER --
+//   stable  (*) holds: no dense code can move (rows kernel, pass-through),
+//   GEN     every other condition of the stable tier holds (fast dequant of w/m/g,
+//           bounded scales, thresholds at codes 0 / qmax, the old outliers fit the
+//           table): the GEN rows kernel requantizes every code,
+//   general the rest: step_kernel.
+// Each tier's rows are appended to its list (this step's flip); the other flip's
+// counters and both row-claim counters are zeroed for the next step.
+constexpr int PREP_T = 256;  // threads (rows) per prep block
+
+__global__ void __launch_bounds__(PREP_T) k_step_prep(const LaunchArgs a, int stable_ok) {
+  const int gr = blockIdx.x * PREP_T + threadIdx.x;
+  if (gr == 0) {
+    if (a.xclear) a.xclear[0] = a.xclear[1] = a.xclear[2] = a.xclear[3] = 0;
+    if (a.rclaim) a.rclaim[0] = a.rclaim[1] = 0;
   }
-  RowPrep p;
-  p.info = (ok ? rs6::I_STABLE : 0u) | ((uint32_t)zpay << 8);
-  p.cand = 0u;
-  if (ok) {
-    // the candidate outcomes: w = dequant(B), w' = w - lr*(s + wd*w) for s = -1, 0, +1
-    // (lion_apply, optimizer.hpp:38), then the class and code against the cached
-    // thresholds exactly as the step computes them (quantize.hpp:274-285)
-    for (int B = 0; B < 2; ++B) {
-      const float w = dequant_exact(B ? (uint32_t)qmax : 0u, sw, zw);
-      for (int S = 0; S < 3; ++S) {
-        const float sg1 = (float)(S - 1);
-        const float wn = __fsub_rn(w, __fmul_rn(a.lr, __fadd_rn(sg1, __fmul_rn(a.wd, w))));
-        const bool o = (wn < tmin) || (wn > tmax);
-        const uint32_t code = o ? (uint32_t)zpay : quant_exact(wn, sw, zw, qmax);
-        const int k = 3 * B + S;
-        if (o) p.info |= 1u << (1 + k);
-        if (k < 4) p.cand |= code << (8 * k);
-        else p.info |= code << (16 + 8 * (k - 4));
+  int tier = -1;  // -1: past the end
+  int lo = 0, r = 0;
+  if (gr < a.total_rows) {
+    // tensor of the row (binary search over the row bases)
+    int hi = a.n_tensors - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (a.tensors[mid].row_base <= gr) lo = mid;
+      else hi = mid - 1;
+    }
+    const DevTensor& T = a.tensors[lo];
+    r = gr - T.row_base;
+    const int in = a.flip, out = 1 - a.flip;
+    const int qmax = (1 << a.bit_width) - 1;
+    const float sw = T.w_scale[r], tmin = T.t_min[r], tmax = T.t_max[r];
+    const int32_t zw = T.w_zp[r];
+    const float sm = T.m_scale[in][r];
+    const int32_t zm = T.m_zp[in][r];
+    const float sg = T.g_scale ? T.g_scale[r] : 0.0f;
+    const int32_t zg = T.g_zp ? T.g_zp[r] : 0;
+    const int32_t* rsi = T.rs[in];
+    const int ob = rsi[r];
+    const int cap_in = rsi[r + 1] - ob;
+    const int on = T.cnt[in] ? min(T.cnt[in][r], cap_in) : cap_in;
+    const int so = T.rs[out][r];
+    const int co = T.rs[out][r + 1] - so;
+    const int zpay = zw < 0 ? 0 : (zw > qmax ? qmax : zw);
+
+    bool ok = stable_ok != 0 && on <= a.oldcap6 && T.cols == a.cols_p && T.cnt[out] != nullptr;
+    ok = ok && make_dequant_row(sw, zw).fast && make_dequant_row(sm, zm).fast &&
+         make_dequant_row(sg, zg).fast;
+    // positive, normal scales (so 1/s is finite and the dense values are bounded)
+    ok = ok && sw >= 0x1.0p-126f && sw <= 0x1.0p100f && sm >= 0x1.0p-126f && sm <= 0x1.0p100f &&
+         sg >= 0x1.0p-126f && sg <= 0x1.0p100f;
+    bool st = false;
+    if (ok) {
+      const double K = (double)qmax + fabs((double)zw);
+      // m' = b2*m + c2*g finite: |m|, |g| <= s*(qmax+|z|) <= 2^120, |b2|, |c2| <= 4
+      const double c2 = (double)__fsub_rn(1.0f, a.b2);
+      ok = (double)sm * ((double)qmax + fabs((double)zm)) <= 0x1.0p120 &&
+           (double)sg * ((double)qmax + fabs((double)zg)) <= 0x1.0p120 &&
+           fabs((double)a.b2) <= 4.0 && fabs(c2) <= 4.0;
+      // thresholds map to the ends of the code range
+      ok = ok && (tmin <= tmax) && code_unclamped(tmin, sw, zw) == 0.0 &&
+           code_unclamped(tmax, sw, zw) == (double)qmax;
+      // D bounds |w' - w| (|sign(d)| <= 1, |w| <= Wmax): finite and small keeps w' finite
+      const double lr = fabs((double)a.lr), wd = fabs((double)a.wd);
+      const double wmax = (double)sw * K * (1.0 + 0x1.0p-20);
+      const double D = lr * (1.0 + wd * wmax) * (1.0 + 0x1.0p-20);
+      ok = ok && isfinite(lr) && isfinite(wd) && D <= 0x1.0p100 &&
+           fabs((double)a.b1) <= 4.0 && fabs((double)__fsub_rn(1.0f, a.b1)) <= 4.0;
+      // (*) the step cannot move a dense code: D/sw <= 0.5 - (K+2)*2^-21
+      st = ok && D / (double)sw <= 0.5 - (K + 2.0) * 0x1.0p-21;
+    }
+    const bool gen = ok && !st && a.gen_on;
+    tier = st ? 1 : (gen ? 2 : 0);
+    RowPrep p;
+    p.info = (st ? rs6::I_STABLE : 0u) | (gen ? rs6::I_GEN : 0u) | ((uint32_t)zpay << 8);
+    p.cand = 0u;
+    if (st) {
+      // the candidate outcomes: w = dequant(B), w' = w - lr*(s + wd*w) for s = -1, 0, +1
+      // (lion_apply, optimizer.hpp:38), then the class and code against the cached
+      // thresholds exactly as the step computes them (quantize.hpp:274-285)
+      for (int B = 0; B < 2; ++B) {
+        const float w = dequant_exact(B ? (uint32_t)qmax : 0u, sw, zw);
+        for (int S = 0; S < 3; ++S) {
+          const float sg1 = (float)(S - 1);
+          const float wn = __fsub_rn(w, __fmul_rn(a.lr, __fadd_rn(sg1, __fmul_rn(a.wd, w))));
+          const bool o = (wn < tmin) || (wn > tmax);
+          const uint32_t code = o ? (uint32_t)zpay : quant_exact(wn, sw, zw, qmax);
+          const int k = 3 * B + S;
+          if (o) p.info |= 1u << (1 + k);
+          if (k < 4) p.cand |= code << (8 * k);
+          else p.info |= code << (16 + 8 * (k - 4));
+        }
       }
     }
+    p.ob = ob;
+    // the rows kernels copy a row's old CSR slot into the stage: general-tier rows
+    // (whose slot may exceed the stage) get 0 -- the general kernel reads its own bounds
+    p.on = (st || gen) ? on : 0;
+    p.so = so;
+    p.co = co;
+    p.zw = zw;
+    p.zm = zm;
+    p.sm = sm;
+    p.negc_m = make_dequant_row(sm, zm).negc;
+    p.sg = sg;
+    p.negc_g = make_dequant_row(sg, zg).negc;
+    p.zg = zg;
+    p.sw = sw;
+    p.tmin = tmin;
+    p.tmax = tmax;
+    const size_t roff = (size_t)r * (size_t)T.cols;
+    p.w_in = T.w_codes[in] + roff;
+    p.m_in = T.m_codes[in] + roff;
+    p.g_in = T.g_codes ? T.g_codes + roff : nullptr;
+    p.w_out = T.w_codes[out] + roff;
+    p.m_out = T.m_codes[out] + roff;
+    p.m_scale_out = T.m_scale[out] + r;
+    p.m_zp_out = T.m_zp[out] + r;
+    p.cnt_out = T.cnt[out] ? T.cnt[out] + r : nullptr;
+    a.prep[gr] = p;
   }
-  p.ob = ob;
-  // the rows kernel copies a row's old CSR slot into its stage: general-tier rows
-  // (whose slot may exceed the stage) get 0 -- the general kernel reads its own bounds
-  p.on = ok ? on : 0;
-  p.so = so;
-  p.co = co;
-  p.zw = zw;
-  p.zm = zm;
-  p.sm = sm;
-  p.negc_m = make_dequant_row(sm, zm).negc;
-  p.sg = sg;
-  p.negc_g = make_dequant_row(sg, zg).negc;
-  p.zg = zg;
-  p.sw = sw;
-  p.tmin = tmin;
-  p.tmax = tmax;
-  const size_t roff = (size_t)r * (size_t)T.cols;
-  p.w_in = T.w_codes[in] + roff;
-  p.m_in = T.m_codes[in] + roff;
-  p.g_in = T.g_codes ? T.g_codes + roff : nullptr;
-  p.w_out = T.w_codes[out] + roff;
-  p.m_out = T.m_codes[out] + roff;
-  p.m_scale_out = T.m_scale[out] + r;
-  p.m_zp_out = T.m_zp[out] + r;
-  p.cnt_out = T.cnt[out] ? T.cnt[out] + r : nullptr;
-  a.prep[gr] = p;
-  if (!ok) {
-    const int k = atomicAdd(a.xcount, 1);
-    a.xlist[k] = RowBlock{lo, r, 1, 0};
-  }
+  // the GEN and general tiers' row lists (warp-aggregated appends: runs of consecutive
+  // rows, one atomic per warp); the stable rows kernel walks every row of the launch
+  warp_append<int32_t>(tier == 2, gr, a.glist, a.gcount);
+  warp_append<RowBlock>(tier == 0, RowBlock{lo, r, 1, 0}, a.xlist, a.xcount);
 }
 
 // ---------------------------------------------------------------------------- launch
@@ -818,10 +992,10 @@ static long grid_cap() {
   return g ? std::max(1L, atol(g)) : 0L;
 }
 
-template <int MAXT, int MINB, int NS, int FULL = 0, int CCOLS = 0, int BWC = 0>
+template <int MAXT, int MINB, int NS, int FULL = 0, int CCOLS = 0, int BWC = 0, bool GEN = false>
 static cudaError_t rows_resolve_t(const LaunchArgs& a, int nt, size_t smem, KLaunch* out,
                                   int cap_per_sm) {
-  auto k = rows_kernel<MAXT, MINB, NS, FULL, CCOLS, BWC>;
+  auto k = rows_kernel<MAXT, MINB, NS, FULL, CCOLS, BWC, GEN>;
   // the attribute is per FUNCTION, shared by every plan that launches this instance: raise
   // it to the device's opt-in maximum (never lower it to this plan's size, which would
   // invalidate another plan's cached launch); occupancy follows the launch's own smem
@@ -846,8 +1020,8 @@ static cudaError_t rows_resolve_t(const LaunchArgs& a, int nt, size_t smem, KLau
   out->grid = (int)grid;
   out->block = nt;
   out->smem = smem;
-  snprintf(out->name, sizeof(out->name), "rows_kernel<%d,%d,%d,%d,%d,%d>", MAXT, MINB, NS, FULL,
-           CCOLS, BWC);
+  snprintf(out->name, sizeof(out->name), "rows_kernel<%d,%d,%d,%d,%d,%d%s>", MAXT, MINB, NS, FULL,
+           CCOLS, BWC, GEN ? ",gen" : "");
   return cudaSuccess;
 }
 
@@ -901,6 +1075,30 @@ static cudaError_t rows_resolve(const LaunchArgs& a, KLaunch* out, int cps) {
   return rows_resolve_t<512, 1, 2>(a, nt, smem, out, cps);
 }
 
+#ifndef QFT_GEN_MINB_S
+#define QFT_GEN_MINB_S 4  // GEN tier, rows of <= 4096 columns: 4 CTAs/SM (128 registers)
+#endif
+// the GEN-tier instance of a launch (compile-time geometry for the LLaMA-2-7B widths at
+// 8 bits, generic otherwise)
+static cudaError_t rows_resolve_gen(const LaunchArgs& a, KLaunch* out, int cps) {
+  const int nt = rows_kernel_nt(a.cols_p);
+  const size_t smem = rows_kernel_smem(a.cols_p, a.oldcap6);
+  const int c = a.cols_p;
+  auto geom_ok = [&](int cc, int ns) {
+    return c == cc && a.oldcap6 == geom_oldcap(cc, ns) && a.slotted_in;
+  };
+  const bool b8 = QFT_BW8 && a.bit_width == 8;
+  if (nt == 128 && geom_ok(4096, 3) && b8)
+    return rows_resolve_t<128, QFT_GEN_MINB_S, 3, 2, 4096, 8, true>(a, nt, smem, out, cps);
+  if (geom_ok(11008, 2) && b8)
+    return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 11008, 8, true>(a, nt, smem, out, cps);
+  if (nt <= 128) return rows_resolve_t<128, QFT_GEN_MINB_S, 3, 0, 0, 0, true>(a, nt, smem, out, cps);
+  if (nt <= 384 && c / 16 >= nt)
+    return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 0, 0, true>(a, nt, smem, out, cps);
+  if (nt <= 384) return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 0, 0, 0, true>(a, nt, smem, out, cps);
+  return rows_resolve_t<512, 1, 2, 0, 0, 0, true>(a, nt, smem, out, cps);
+}
+
 // One step of a rows-path plan: k_step_prep (records + the device list of general-tier
 // rows), the rows kernel over the stable tier, the general kernel over the list.  Every
 // launch is resolved once per plan (RowsCache); the list counter of this flip was zeroed
@@ -909,20 +1107,45 @@ static cudaError_t rows_resolve(const LaunchArgs& a, KLaunch* out, int cps) {
 cudaError_t launch_rows_step(const LaunchArgs& a0, RowsCache& c, cudaStream_t st) {
   LaunchArgs a = a0;
   a.negzero = -0.0f;
-  a.xcount = c.xcount + a.flip;
-  a.xclear = c.xcount + (1 - a.flip);
-  a.rclaim = c.xcount + 2;
+  int32_t* cf = c.xcount + 4 * a.flip;  // this step's list counters
+  a.xcount = cf;
+  a.scount = cf + 1;
+  a.gcount = cf + 2;
+  a.xclear = c.xcount + 4 * (1 - a.flip);
+  a.rclaim = c.xcount + 8;
+  a.slist = c.slist;
+  a.glist = c.glist;
+  a.gen_on = c.gen_on;
   cudaError_t e;
-  if (c.last_flip == a.flip &&
-      (e = cudaMemsetAsync(a.xcount, 0, sizeof(int32_t), st)) != cudaSuccess)
+  if (c.last_flip == a.flip && (e = cudaMemsetAsync(cf, 0, 4 * sizeof(int32_t), st)) != cudaSuccess)
     return e;
   c.last_flip = a.flip;
-  const int pt = 256;
-  k_step_prep<<<(a.total_rows + pt - 1) / pt, pt, 0, st>>>(a, 1);
+  const int nb = (a.total_rows + PREP_T - 1) / PREP_T;
+  k_step_prep<<<nb, PREP_T, 0, st>>>(a, 1);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  // the stable tier over its row list
+  LaunchArgs sa = a;
+  sa.rlist = nullptr;
+  sa.rcount = nullptr;
+  sa.rclaim = c.xcount + 8;
+  sa.xseen = nullptr;
   KLaunch& rk = c.rows[a.slotted_in ? 1 : 0];
-  if (!rk.fn && (e = rows_resolve(a, &rk, c.cap_per_sm)) != cudaSuccess) return e;
-  if ((e = launch_k(rk, a, st)) != cudaSuccess) return e;
+  if (!rk.fn && (e = rows_resolve(sa, &rk, c.cap_per_sm)) != cudaSuccess) return e;
+  if ((e = launch_k(rk, sa, st)) != cudaSuccess) return e;
+  // the GEN tier over its list (one CTA per SM when the list was empty last step: the
+  // kernel covers any length)
+  if (c.gen_on) {
+    LaunchArgs ga = a;
+    ga.rlist = c.glist;
+    ga.rcount = a.gcount;
+    ga.rclaim = c.xcount + 9;
+    ga.xseen = c.seen_dev ? c.seen_dev + 1 : nullptr;
+    KLaunch& gr = c.genrows[a.slotted_in ? 1 : 0];
+    if (!gr.fn && (e = rows_resolve_gen(ga, &gr, c.cap_per_sm)) != cudaSuccess) return e;
+    KLaunch g2 = gr;
+    if (c.seen_host && c.seen_host[1] == 0 && c.sms > 0 && g2.grid > c.sms) g2.grid = c.sms;
+    if ((e = launch_k(g2, ga, st)) != cudaSuccess) return e;
+  }
   // the general kernel over the device row list
   LaunchArgs x = a;
   x.blocks = a.xlist;

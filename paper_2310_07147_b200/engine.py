@@ -530,6 +530,20 @@ class QftModelState:
             gen += b.value
         return st, gen
 
+    def tiers(self) -> Tuple[int, int, int]:
+        """(stable, GEN, general) rows of the last step over all groups (synchronises):
+        the pass-through rows kernel, the requantizing GEN rows kernel, step_kernel."""
+        t = [0, 0, 0]
+        if not hasattr(N.lib, "qftc_plan_tiers"):  # an older library loaded for an A/B
+            a, b = self.tier_rows()
+            return a, 0, b
+        for g in self.groups:
+            arr = (C.c_int64 * 3)()
+            N.check(N.lib.qftc_plan_tiers(g.plan, arr, _stream()))
+            for k in range(3):
+                t[k] += arr[k]
+        return t[0], t[1], t[2]
+
     def check(self):
         """Synchronise and validate the last step (raises on overflow / bad rows)."""
         for g in self.groups:
@@ -623,6 +637,13 @@ class QftModelState:
             t.out = o.data_ptr()
         return tab, 1 if bf16 else 0
 
+    def expand_plan(self, outs: Sequence[torch.Tensor], rows: Optional[Sequence[int]] = None):
+        """An ExpandPlan over every tensor (one launch per run, any number of tensors),
+        valid while `cur` and the buffers are unchanged (the ping-pong set flips each step:
+        build one plan per set)."""
+        tab, bf16 = self.expand_table(outs, rows)
+        return ExpandPlan(tab, bf16, keep=(self, list(outs)))
+
     def expand(self, outs: Sequence[torch.Tensor], rows: Optional[Sequence[int]] = None,
                table=None):
         """Reconstruct every tensor (dense dequant + CSR overwrite, quantize.hpp:331-338)
@@ -645,3 +666,28 @@ class QftModelState:
             _p(self._rows(self.row_count[cur], i)), _p(g.col[cur]), _p(g.val[cur]), _p(out),
             0 if dtype == torch.float32 else 1, _stream()))
         return out
+
+
+class ExpandPlan:
+    """A weight expansion whose tensor table lives on the device (qftc_expand_plan): one
+    kernel launch per run() for any number of tensors (the forward consumer's bf16 / f32
+    weights, network.hpp:199-212)."""
+
+    def __init__(self, table, bf16: int, keep=None):
+        self._keep = keep  # the buffers the table points into
+        self.n = len(table)
+        self.handle = C.c_void_p()
+        N.check(N.lib.qftc_expand_plan_create(C.byref(self.handle), table, len(table), int(bf16),
+                                              _stream()))
+
+    def run(self, stream=None):
+        N.check(N.lib.qftc_expand_plan_run(self.handle, stream if stream is not None else _stream()))
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                N.lib.qftc_expand_plan_destroy(h)
+            except Exception:
+                pass
+            self.handle = None

@@ -159,6 +159,50 @@ class Zero1QftLion:
         self.check_local()
         self.all_gather_state()
 
+    # ------------------------------------------------------------------ the next forward's weights
+    def gather_static(self):
+        """All-gather the per-row weight params every expansion needs (scale, zero point:
+        cached between threshold refreshes, so once), shard-major like the codes."""
+        L = self.layout
+        dev = self.local.device
+        self.wscale_full = torch.empty(self.world * L.rpad, dtype=torch.float32, device=dev)
+        self.wzp_full = torch.empty(self.world * L.rpad, dtype=torch.int32, device=dev)
+        dist.all_gather_into_tensor(self.wscale_full, self.local.wscale_shard(L.rpad),
+                                    group=self.group)
+        dist.all_gather_into_tensor(self.wzp_full, self.local.wzp_shard(L.rpad), group=self.group)
+
+    def expand_plan(self, outs: Sequence[torch.Tensor]):
+        """ONE grouped expansion launch reading the gathered shard-major buffers directly:
+        every (rank, tensor) row range is a table entry (codes, params, slot starts, counts
+        and the rank's arena re-based by rank * capacity), writing rows [lo, hi) of the full
+        output tensor (bf16 or f32) -- the next forward's weights (network.hpp:199-212)."""
+        from . import _native as N
+        from .engine import ExpandPlan
+        if not hasattr(self, "wscale_full"):
+            self.gather_static()
+        L = self.layout
+        pieces = [(k, j, ti, lo, hi) for k in range(self.world)
+                  for j, (ti, lo, hi) in enumerate(L.members[k])]
+        tab = (N.ExpandTensorC * len(pieces))()
+        bf16 = outs[0].dtype == torch.bfloat16
+        for n, (k, j, ti, lo, hi) in enumerate(pieces):
+            r, c = L.shapes[ti]
+            o = outs[ti]
+            if (o.dtype == torch.bfloat16) != bf16 or o.numel() != r * c:
+                raise ValueError(f"expand: output {ti} must be {r}x{c}, one dtype for all")
+            t = tab[n]
+            t.rows, t.cols = hi - lo, c
+            esz = 1
+            t.codes = self.codes_full.data_ptr() + (k * L.pad + L.off[k][j]) * esz
+            t.scale = self.wscale_full.data_ptr() + 4 * (k * L.rpad + L.roff[k][j])
+            t.zero_point = self.wzp_full.data_ptr() + 4 * (k * L.rpad + L.roff[k][j])
+            t.row_start = self.rowstart_full.data_ptr() + 4 * (k * L.rp_pad + L.rpoff[k][j])
+            t.row_count = self.count_full.data_ptr() + 4 * (k * L.rpad + L.roff[k][j])
+            t.col_idx = self.col_full[c].data_ptr() + 4 * k * self.cap
+            t.values = self.val_full[c].data_ptr() + 4 * k * self.cap
+            t.out = o.data_ptr() + lo * c * o.element_size()
+        return ExpandPlan(tab, 1 if bf16 else 0, keep=(self, list(outs)))
+
     # ------------------------------------------------------------------ views of the gathered state
     def gathered_tensor(self, i: int) -> dict:
         """Reference-layout copy (host numpy) of full tensor i from the gathered buffers."""
@@ -228,6 +272,12 @@ class CudaShard:
 
     def codes_shard(self, pad: int) -> torch.Tensor:
         return self.state.w_codes[self.state.cur][:pad]
+
+    def wscale_shard(self, rpad: int) -> torch.Tensor:
+        return self._padded(self.state.w_scale, rpad)
+
+    def wzp_shard(self, rpad: int) -> torch.Tensor:
+        return self._padded(self.state.w_zp, rpad)
 
     def _padded(self, t: torch.Tensor, n: int) -> torch.Tensor:
         if t.numel() < n:

@@ -47,7 +47,8 @@ def test_rows_path_raw_gradient_matches_oracle(cuda, port, gkind, cols, bw, lr, 
     eng, ora = _build(cuda, port, shapes, bw, gkind)
     N = cuda._native
     for g in eng.groups:
-        assert N.lib.qftc_plan_launches(g.plan) == 4, "raw gradient did not take the rows path"
+        # k_grad_quant + prep + stable rows + GEN rows (when on) + general
+        assert N.lib.qftc_plan_launches(g.plan) >= 4, "raw gradient did not take the rows path"
     for step in range(4):
         for i, sh in enumerate(shapes):
             g = _grad(port, sh, 900 + 10 * step + i, step)
@@ -83,7 +84,7 @@ def test_rows_path_raw_gradient_equals_general_kernel(cuda, port, monkeypatch):
         if off == "1":
             assert all(cuda._native.lib.qftc_plan_launches(g.plan) == 1 for g in eng.groups)
         else:
-            assert all(cuda._native.lib.qftc_plan_launches(g.plan) == want for g in eng.groups)
+            assert all(cuda._native.lib.qftc_plan_launches(g.plan) >= want for g in eng.groups)
         for step in range(3):
             for i, sh in enumerate(shapes):
                 eng.grad_views(i).copy_(torch.from_numpy(_grad(port, sh, 77 + step + 5 * i, step))
