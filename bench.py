@@ -739,54 +739,89 @@ def run_sweep(args):
 
 
 def run_13b_dequant(args):
-    """configs[3] per rank on one GPU: rank 0's row shard (1/8) of LLaMA-2-13B stepped,
-    then the on-the-fly bf16 expansion of ALL 13B weights (what every rank does after the
-    all-gather, for its next forward) in one grouped launch (qftc_expand)."""
+    """configs[3] per rank, on one GPU: rank 0 of 8's row shard of LLaMA-2-13B stepped with
+    the bf16 gradient a reduce-scatter delivers (k_grad_quant -> rows kernels, width classes
+    concurrent), then the next forward's bf16 weights of the WHOLE model expanded in ONE
+    launch straight from the all-gathered, shard-major buffers (Zero1QftLion.expand_plan).
+    The 8 ranks' gathered content is rank 0's shard for ranks 0-6 and rank 7's (which also
+    holds the 1-row norms) -- the same layout and byte counts as a real all-gather; the
+    collectives themselves need 8 GPUs."""
     import torch
     import paper_2310_07147_b200 as q
-    from paper_2310_07147_b200.shapes import llama2_13b, shard_rows
+    from paper_2310_07147_b200.shapes import llama2_13b
+    from paper_2310_07147_b200.zero1 import CudaShard, ShardLayout, Zero1QftLion
     hbm, _ = peaks()
     full = llama2_13b()
-    shard = shard_rows(full, 8, 0)
+    world = 8
+    L = ShardLayout(full, world)
     stream = torch.cuda.current_stream()
-    st = build_state(shard, q, 1313)
+    shards = {}
+    for k in (0, world - 1):
+        sh = CudaShard(L, k, bit_width=BIT_WIDTH, grad_dtype=torch.bfloat16)
+        ss = L.shard_shapes(k)
+        sh.state.init_from_weights(lambda i, ss=ss, k=k: q.synth(ss[i], 1313 + 1000 * k + i, 0.02, 0.005),
+                                   FRACTION, "percentile")
+        gen = torch.Generator(device="cuda")
+        gen.manual_seed(5 + k)
+        sh.state.g_raw.normal_(0.0, 1e-3, generator=gen)
+        shards[k] = sh
+    st = shards[0].state
     for _ in range(args.warmup):
         st.step(**HYPER, check=True)
-    per = timed_steps(st, args.steps, stream)
-    step_ms = sum(per)
-    shard_params = st.param_count
-    del st
-    torch.cuda.empty_cache()
-    # the gathered full-model state: every 13B tensor's codes + params + CSR
-    fst = build_state(full, q, 2626)
+    nnz0 = st.nnz()
+    step_ms = timed_region(st, args.steps, stream, HYPER)
+    st.check()
+    P, R = st.param_count, st.row_count_total
+    step_alg = 3 * P + 8 * R + 5 * P + 8 * (nnz0 + st.nnz()) + 48 * R
+    # the all-gathered buffers (all_gather_into_tensor layout: rank-major, uniform sizes)
+    cap = max(s.arena_capacity() for s in shards.values())
+    for s in shards.values():
+        s.ensure_arena_capacity(cap)
+    src = [shards[0]] * (world - 1) + [shards[world - 1]]
+    z = Zero1QftLion.__new__(Zero1QftLion)
+    z.layout, z.world, z.cap, z.local = L, world, cap, shards[0]
+    z.codes_full = torch.cat([s.codes_shard(L.pad) for s in src])
+    z.rowstart_full = torch.cat([s.rowstart_shard(L.rp_pad) for s in src])
+    z.count_full = torch.cat([s.count_shard(L.rpad) for s in src])
+    z.wscale_full = torch.cat([s.wscale_shard(L.rpad) for s in src])
+    z.wzp_full = torch.cat([s.wzp_shard(L.rpad) for s in src])
+    z.col_full, z.val_full = {}, {}
+    for c in L.widths:
+        cols, vals = zip(*[s.arena(c, cap) for s in src])
+        z.col_full[c], z.val_full[c] = torch.cat(cols), torch.cat(vals)
     outs = [torch.empty((r, c), dtype=torch.bfloat16, device="cuda") for r, c in full]
-    table = fst.expand_table(outs)
+    plan = z.expand_plan(outs)
     for _ in range(2):
-        fst.expand(outs, table=table)
+        plan.run()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     torch.cuda.synchronize()
     for e0, e1 in ev:
         e0.record(stream)
-        fst.expand(outs, table=table)
+        plan.run()
         e1.record(stream)
     torch.cuda.synchronize()
     dq_ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in ev)
-    n_el = fst.param_count
-    nnz = fst.nnz()
-    # algorithmic bytes: 1 B code read + 2 B bf16 written per param, 8 B per CSR entry
-    # read (+2 B scattered bf16 write), 16 B per row (scale, zp, row_start, row_count)
-    dq_bytes = 3 * n_el + 10 * nnz + 16 * fst.row_count_total
-    launches = (len(full) + 223) // 224
-    print(json.dumps({"config": "llama2-13b per-rank (dp8 row shard) step + full bf16 expansion",
-                      "shard_params": shard_params, "step_ms": step_ms,
-                      "step_gparams_s": shard_params / (step_ms * 1e-3) / 1e9,
-                      "dequant_params": n_el, "dequant_nnz": nnz, "dequant_ms": dq_ms,
-                      "dequant_launches": launches,
-                      "dequant_gparams_s": n_el / (dq_ms * 1e-3) / 1e9,
-                      "dequant_gbs": dq_bytes / (dq_ms * 1e-3) / 1e9,
-                      "dequant_frac_of_hbm": dq_bytes / (dq_ms * 1e-3) / 1e9 / hbm,
-                      "peak_gbs": hbm}), flush=True)
+    n_el = sum(r * c for r, c in full)
+    cnt = z.count_full.view(world, L.rpad)
+    nnz = int(sum(int(cnt[k, :L.rows[k]].sum().item()) for k in range(world)))
+    rows_all = sum(r for r, _ in full)
+    # 1 B code read + 2 B bf16 written per param, 8 B per CSR entry read (+2 B scattered
+    # bf16 write), 16 B per row (scale, zp, slot start, count)
+    dq_bytes = 3 * n_el + 10 * nnz + 16 * rows_all
+    print(json.dumps({
+        "config": "llama2-13b per rank of 8 (configs[3]): row-shard step fed bf16 reduce-scatter "
+                  "gradients + the whole model's bf16 weights expanded from the all-gathered "
+                  "shard-major buffers", "shard_params": P,
+        "step_ms": step_ms, "step_gparams_s": P / (step_ms * 1e-3) / 1e9,
+        "step_frac_of_hbm": step_alg / (step_ms * 1e-3) / 1e9 / hbm,
+        "step_kernels": st.kernel_names(),
+        "dequant_params": n_el, "dequant_nnz": nnz, "dequant_ms": dq_ms,
+        "dequant_launches": 1, "dequant_table_entries": plan.n,
+        "dequant_gparams_s": n_el / (dq_ms * 1e-3) / 1e9,
+        "dequant_gbs": dq_bytes / (dq_ms * 1e-3) / 1e9,
+        "dequant_frac_of_hbm": dq_bytes / (dq_ms * 1e-3) / 1e9 / hbm,
+        "per_rank_compute_ms": step_ms + dq_ms, "peak_gbs": hbm}), flush=True)
 
 
 def run_ckpt(args):

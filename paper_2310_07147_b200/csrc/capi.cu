@@ -717,7 +717,7 @@ int qftc_plan_step(qftc_plan* p, int flip, qftc_lion_hyper h, qftc_stream_t stre
     a.oldcap6 = rows_kernel_oldcap(p->uniform_cols);
     a.prep = p->prep;
     a.xlist = p->xlist;
-    if (p->gq) QFTC_CUDA(launch_k(p->gql, a, (cudaStream_t)stream), "gradient quantize_state");
+    if (p->gq) QFTC_CUDA(launch_k2(p->gql, a, (cudaStream_t)stream), "gradient quantize_state");
     QFTC_CUDA(launch_rows_step(a, p->rc, (cudaStream_t)stream), "lion step (rows kernel)");
     p->last_kernel = p->rc.rows[a.slotted_in ? 1 : 0].name;
     return QFTC_OK;

@@ -48,171 +48,196 @@ __device__ __forceinline__ void unpack(const uint4& q, float* x) {
 }
 }  // namespace gq
 
-// One CTA of NT threads per row (persistent, static row stride); every thread holds VPL
-// 16-byte vectors of the row in registers, so a row is read from HBM once and the CTA's
-// loads are all in flight together.  The min/max partials of the warps go through shared
-// memory (double-buffered by row parity, so ONE barrier per row suffices) and every thread
-// derives the row's affine params itself (FMA-proven fast divide, exact fp64 fallback).
-// Quantization is range-proven (every value lies in [lo, hi], whose codes are 0 and
-// qmax, so no clip is needed): per element one multiply, the magic-number rint and its
-// tie distance; a thread whose values come within the error bound of a tie redoes its
-// vectors with the reference's fp64 formula.
-// register budget: the row in flight twice (current + prefetched next row, 8 regs per
-// vector) plus ~24; a budget below that would spill the prefetch to local memory
-template <int NT, int VPL>
-constexpr int gq_minb() { return VPL <= 2 ? 65536 / (NT * 64) : 65536 / (NT * 128); }
+// One CTA of NT threads per row (persistent, static row stride).  Rows stream into a
+// 4-stage shared-memory ring by TMA bulk copies (thread 0, two rows ahead, one mbarrier
+// per stage), and the rows are SOFTWARE-PIPELINED: while row r's min/max is reduced
+// (every thread its VPL 16-byte vectors, from the stage), row r-1 -- whose quantizer
+// thread 0 derived during the previous iteration -- is quantized from its stage and
+// stored.  The row's serial part (thread 0: the fp64 affine params, FMA-proven fast divide
+// or the reference formula) overlaps the other threads' quantization; a row costs ONE
+// barrier, and the row is read from HBM once.
+// Quantization: the clamped fast quantizer with its tie proof per group of 4 elements, the
+// reference's fp64 formula for a group near a tie (quantize.hpp:160-166).
+constexpr int GQ_NS = 4;  // ring stages
+
 template <bool BF16, int NT, int VPL>
-__global__ void __launch_bounds__(NT, gq_minb<NT, VPL>()) k_grad_quant(const LaunchArgs a) {
+__global__ void __launch_bounds__(NT + 32) k_grad_quant(const LaunchArgs a, int stage_bytes) {
   using namespace gq;
   constexpr int EPV = BF16 ? 8 : 4;  // elements per 16-byte vector
-  constexpr int NW = NT / 32;
+  constexpr int NW = NT / 32;        // worker warps; warp NW is the control warp
+  extern __shared__ __align__(128) uint8_t gsm[];
   __shared__ float red[2][2][NW];
+  __shared__ float prm[2][4];  // per row parity: s, z, RN(1/s), fast
+  __shared__ __align__(8) uint64_t bars[GQ_NS];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const bool ctrl = wid == NW;  // the control warp: TMA issue + the row's quantizer
+  const int tc = NT;            // its lane 0
   const int bw = a.bit_width;
   const int qmax = (1 << bw) - 1;
   const double rq = __drcp_rn((double)qmax);
-  int par = 0;
-  // the row's tensor (binary search over the row bases) and its first 16-byte vector
-  auto locate = [&](int row, int& ti) -> const uint4* {
-    int lo_t = 0, hi_t = a.n_tensors - 1;
-    while (lo_t < hi_t) {
-      const int mid = (lo_t + hi_t + 1) >> 1;
-      if (a.tensors[mid].row_base <= row) lo_t = mid;
-      else hi_t = mid - 1;
-    }
-    ti = lo_t;
-    const DevTensor& T = a.tensors[lo_t];
-    return reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(T.g_raw) +
-                                          (size_t)(row - T.row_base) * T.cols * (BF16 ? 2 : 4));
+  const int G = (int)gridDim.x;
+  const int TR = a.total_rows;
+  // rows come in increasing order per CTA: the tensor index only moves forward
+  int ti_issue = 0, ti_cur = 0;
+  auto tensor_of = [&](int row, int& ti) -> const DevTensor& {
+    while (ti + 1 < a.n_tensors && a.tensors[ti + 1].row_base <= row) ++ti;
+    return a.tensors[ti];
   };
-  // loads of a row into registers; vectors past the row end repeat vector 0 (same range)
-  auto load = [&](const uint4* src, int nv, uint4* v) {
-#pragma unroll
-    for (int j = 0; j < VPL; ++j) {
-      const int i = t + j * NT;
-      v[j] = __ldcs(src + (i < nv ? i : 0));
-    }
+  // thread 0: row `row` into stage st (one bulk copy of the row)
+  auto issue = [&](int row, int st) {
+    const DevTensor& T = tensor_of(row, ti_issue);
+    const uint32_t nb = (uint32_t)T.cols * (BF16 ? 2u : 4u);
+    mbar_arrive_expect_tx(&bars[st], nb);
+    bulk_g2s(gsm + (size_t)st * stage_bytes,
+             reinterpret_cast<const uint8_t*>(T.g_raw) + (size_t)(row - T.row_base) * nb, nb,
+             &bars[st]);
   };
-  int gr = blockIdx.x;
-  if (gr >= a.total_rows) return;
-  int ti;
-  const uint4* src = locate(gr, ti);
-  uint4 v[VPL], vn[VPL];
-  load(src, a.tensors[ti].cols / EPV, v);
-  for (;; gr += gridDim.x, par ^= 1) {
-    const DevTensor& T = a.tensors[ti];
-    const int r = gr - T.row_base;
-    const int cols = T.cols;
-    const int nv = cols / EPV;  // cols % 16 == 0 on this path
-    // the CTA's next row streams in while this one is reduced and quantized
-    const int gn = gr + (int)gridDim.x;
-    int tin = ti;
-    const uint4* srcn = nullptr;
-    if (gn < a.total_rows) {
-      srcn = locate(gn, tin);
-      load(srcn, a.tensors[tin].cols / EPV, vn);
-    }
-    float lo = __int_as_float(0x7f800000), hi = __int_as_float(0xff800000);
-#pragma unroll
-    for (int j = 0; j < VPL; ++j) {
-      float x[EPV];
-      unpack<BF16>(v[j], x);
-#pragma unroll
-      for (int e = 0; e < EPV; e += 2) minmax2(lo, hi, x[e], x[e + 1]);
-    }
-    asm("redux.sync.min.f32 %0, %1, 0xffffffff;" : "=f"(lo) : "f"(lo));
-    asm("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(hi) : "f"(hi));
-    if (lane == 0) {
-      red[par][0][wid] = lo;
-      red[par][1][wid] = hi;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      lo = fminf(lo, red[par][0][w]);
-      hi = fmaxf(hi, red[par][1][w]);
-    }
-    // column 0: a NaN there is the initial bound and sticks (tensor.hpp:133-148)
-    if (t == 0) {
-      const float c0 = BF16 ? __uint_as_float(v[0].x << 16) : __uint_as_float(v[0].x);
-      if (c0 != c0) atomicOr(&a.hdr->err, ERR_GPARAMS);
-    }
-    const float c0 = BF16 ? __uint_as_float(__ldg(reinterpret_cast<const uint32_t*>(src)) << 16)
-                          : __ldg(reinterpret_cast<const float*>(src));
-    if (c0 != c0) lo = hi = c0;
-    float s;
-    int32_t z;
-    bool ok = affine_fast(lo, hi, (double)qmax, rq, s, z);
-    if (!ok) {
-      ok = affine_from_bounds(lo, hi, bw, s, z);
-      if (!ok) {
-        s = 1.0f;
-        z = 0;
-      }
-    }
-    if (t == 0) {
-      if (!ok) atomicOr(&a.hdr->err, ERR_GPARAMS);
-      const_cast<float*>(T.g_scale)[r] = s;
-      const_cast<int32_t*>(T.g_zp)[r] = z;
-    }
-    const QuantRow q = make_quant_row(s, z, bw);
-    // range proof: lo and hi quantize (fast form, unclamped) to codes inside [0, qmax]
-    float el = 0.0f;
-    const float lh[4] = {lo, hi, lo, hi};
-    (void)quant4_e(lh, q, el);
-    const float ylo = __fmul_rn(lo, q.inv_s), yhi = __fmul_rn(hi, q.inv_s);
-    const bool fast = ok && q.fast && el < q.thr && ylo > q.ylo - 0.5f && yhi < q.yhi + 0.5f;
-    uint32_t c[VPL][EPV / 4];
-    float em = 0.0f;
-#pragma unroll
-    for (int j = 0; j < VPL; ++j) {
-      float x[EPV];
-      unpack<BF16>(v[j], x);
-#pragma unroll
-      for (int k = 0; k < EPV / 4; ++k) c[j][k] = quant4_e(x + 4 * k, q, em);
-    }
-    if (!(fast && em < q.thr)) {  // near a tie (or no range proof): the reference formula
-#pragma unroll
-      for (int j = 0; j < VPL; ++j) {
-        float x[EPV];
-        unpack<BF16>(v[j], x);
-#pragma unroll
-        for (int k = 0; k < EPV / 4; ++k) c[j][k] = quant4_exact(x + 4 * k, q);
-      }
-    }
-    uint8_t* dst = const_cast<uint8_t*>(T.g_codes) + (size_t)r * cols;
+  auto vec = [&](int st, int i) {
+    return reinterpret_cast<const uint4*>(gsm + (size_t)st * stage_bytes)[i];
+  };
+  // quantize row `row` (stage st, quantizer of parity p) and store its codes
+  int ti_q = 0;
+  auto quantize_store = [&](int row, int st, int p) {
+    if (ctrl) return;
+    const DevTensor& T = tensor_of(row, ti_q);
+    const int nv = T.cols / EPV;
+    uint8_t* dst = const_cast<uint8_t*>(T.g_codes) + (size_t)(row - T.row_base) * T.cols;
+    QuantRow q;
+    q.s = prm[p][0];
+    q.z = __float_as_int(prm[p][1]);
+    q.inv_s = prm[p][2];
+    q.qmax = qmax;
+    q.ylo = (float)(-q.z);
+    q.yhi = (float)(qmax - q.z);
+    q.magic = __fadd_rn(kMagicRound, (float)q.z);
+    q.thr = 0.5f - (float)((q.z < 0 ? -(int64_t)q.z : (int64_t)q.z) + qmax + 2) * 0x1.0p-21f;
+    q.fast = prm[p][3] != 0.0f;
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
       const int i = t + j * NT;
       if (i < nv) {
+        float x[EPV];
+        unpack<BF16>(vec(st, i), x);
+        uint32_t c[EPV / 4];
+#pragma unroll
+        for (int k = 0; k < EPV / 4; ++k) {
+          float em = 0.0f;
+          c[k] = q.fast ? quant4_fast(x + 4 * k, q, em) : 0u;
+          if (!q.fast || !(em < q.thr)) c[k] = quant4_exact(x + 4 * k, q);
+        }
         if constexpr (BF16)
-          __stcs(reinterpret_cast<uint2*>(dst) + i, make_uint2(c[j][0], c[j][1]));
+          __stcs(reinterpret_cast<uint2*>(dst) + i, make_uint2(c[0], c[1]));
         else
-          __stcs(reinterpret_cast<uint32_t*>(dst) + i, c[j][0]);
+          __stcs(reinterpret_cast<uint32_t*>(dst) + i, c[0]);
       }
     }
-    if (gn >= a.total_rows) break;
-    ti = tin;
-    src = srcn;
-#pragma unroll
-    for (int j = 0; j < VPL; ++j) v[j] = vn[j];
+  };
+
+  int gr = blockIdx.x;
+  if (gr >= TR) return;
+  if (t == tc) {
+    for (int i = 0; i < GQ_NS; ++i) mbar_init(&bars[i], 1);
+    mbar_fence_init();
   }
+  __syncthreads();
+  if (t == tc) {  // this CTA's first two rows in flight
+    for (int k = 0; k < GQ_NS - 2; ++k)
+      if (gr + k * G < TR) issue(gr + k * G, k);
+  }
+  int it = 0, par = 0;
+  for (;; ++it, par ^= 1) {
+    const int st = it % GQ_NS;
+    const DevTensor& T = tensor_of(gr, ti_cur);
+    float lo = __int_as_float(0x7f800000), hi = __int_as_float(0xff800000);
+    if (!ctrl) {
+      mbar_wait(&bars[st], (uint32_t)((it / GQ_NS) & 1));
+      const int nv = T.cols / EPV;
+      // row gr: min/max partials (vectors past the row end repeat vector 0: same range)
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+        const int i = t + j * NT;
+        float x[EPV];
+        unpack<BF16>(vec(st, i < nv ? i : 0), x);
+#pragma unroll
+        for (int e = 0; e < EPV; e += 2) minmax2(lo, hi, x[e], x[e + 1]);
+      }
+      asm("redux.sync.min.f32 %0, %1, 0xffffffff;" : "=f"(lo) : "f"(lo));
+      asm("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(hi) : "f"(hi));
+      if (lane == 0) {
+        red[par][0][wid] = lo;
+        red[par][1][wid] = hi;
+      }
+    }
+    __syncthreads();  // red[par] complete; the previous row's quantizer published; the
+                      // stage of row gr - 2G is free (its quantization ended before this)
+    if (t == tc) {
+      // two rows ahead: row gr + 2G into the stage row gr - 2G vacated (the stages hold
+      // gr - G (quantized now), gr, gr + G and this one)
+      const int gi = gr + (GQ_NS - 2) * G;
+      if (gi < TR) issue(gi, (it + GQ_NS - 2) % GQ_NS);
+      // row gr's quantizer (quantize_state: channel_minmax -> affine_params_from_bounds)
+#pragma unroll
+      for (int w = 0; w < NW; ++w) {
+        lo = fminf(lo, red[par][0][w]);
+        hi = fmaxf(hi, red[par][1][w]);
+      }
+      // column 0: a NaN there is the initial bound and sticks (tensor.hpp:133-148)
+      float x0[EPV];
+      mbar_wait(&bars[st], (uint32_t)((it / GQ_NS) & 1));  // (complete: the workers saw it)
+      unpack<BF16>(vec(st, 0), x0);
+      if (x0[0] != x0[0]) lo = hi = x0[0];
+      float s;
+      int32_t z;
+      bool ok = affine_fast(lo, hi, (double)qmax, rq, s, z);
+      if (!ok) {
+        ok = affine_from_bounds(lo, hi, bw, s, z);
+        if (!ok) {
+          atomicOr(&a.hdr->err, ERR_GPARAMS);
+          s = 1.0f;
+          z = 0;
+        }
+      }
+      const_cast<float*>(T.g_scale)[gr - T.row_base] = s;
+      const_cast<int32_t*>(T.g_zp)[gr - T.row_base] = z;
+      const QuantRow q0 = make_quant_row(s, z, bw);
+      prm[par][0] = s;
+      prm[par][1] = __int_as_float(z);
+      prm[par][2] = q0.inv_s;
+      prm[par][3] = q0.fast ? 1.0f : 0.0f;
+    }
+    if (it > 0) quantize_store(gr - G, (it + GQ_NS - 1) % GQ_NS, par ^ 1);
+    if (gr + G >= TR) break;
+    gr += G;
+  }
+  __syncthreads();  // the last row's quantizer
+  quantize_store(gr, it % GQ_NS, par);
 }
 
 template <bool BF16, int NT, int VPL>
-static cudaError_t gq_resolve_t(int total_rows, const char* name, KLaunch* out) {
+static cudaError_t gq_resolve_t(int total_rows, int max_cols, const char* name, KLaunch* out) {
   const void* fn = reinterpret_cast<const void*>(k_grad_quant<BF16, NT, VPL>);
-  int dev = 0, sms = 0, per_sm = 0;
+  const int stage = ((max_cols * (BF16 ? 2 : 4)) + 127) & ~127;
+  const size_t smem = (size_t)GQ_NS * stage;
+  int dev = 0, sms = 0, per_sm = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NT, 0);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa{};
+  cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+  if (e != cudaSuccess) return e;
+  const int maxdyn = optin - (int)fa.sharedSizeBytes;  // the static part counts against it
+  if ((size_t)maxdyn < smem) return cudaErrorInvalidValue;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, maxdyn);
+  if (e != cudaSuccess) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NT + 32, smem);
   if (e != cudaSuccess) return e;
   long grid = (long)sms * (per_sm > 0 ? per_sm : 1);
   if (grid > total_rows) grid = total_rows;
   out->fn = fn;
   out->grid = (int)(grid < 1 ? 1 : grid);
-  out->block = NT;
-  out->smem = 0;
+  out->block = NT + 32;
+  out->smem = smem;
+  out->arg1 = stage;
   snprintf(out->name, sizeof(out->name), "%s", name);
   return cudaSuccess;
 }
@@ -220,12 +245,11 @@ static cudaError_t gq_resolve_t(int total_rows, const char* name, KLaunch* out) 
 // the launch for a plan of raw-gradient kind gk over rows of <= max_cols columns
 cudaError_t resolve_grad_quant(int gk, int max_cols, int total_rows, KLaunch* out) {
   if (gk == G_BF16) {  // 8 elements per vector
-    if (max_cols <= 8 * 256 * 2) return gq_resolve_t<true, 256, 2>(total_rows, "k_grad_quant<bf16,256,2>", out);
-    if (max_cols <= 8 * 1024 * 2) return gq_resolve_t<true, 1024, 2>(total_rows, "k_grad_quant<bf16,1024,2>", out);
+    if (max_cols <= 8 * 128 * 4) return gq_resolve_t<true, 128, 4>(total_rows, max_cols, "k_grad_quant<bf16,128,4>", out);
+    if (max_cols <= 8 * 256 * 8) return gq_resolve_t<true, 256, 8>(total_rows, max_cols, "k_grad_quant<bf16,256,8>", out);
   } else if (gk == G_F32) {  // 4 elements per vector
-    if (max_cols <= 4 * 512 * 2) return gq_resolve_t<false, 512, 2>(total_rows, "k_grad_quant<f32,512,2>", out);
-    if (max_cols <= 4 * 1024 * 2) return gq_resolve_t<false, 1024, 2>(total_rows, "k_grad_quant<f32,1024,2>", out);
-    if (max_cols <= 4 * 512 * 8) return gq_resolve_t<false, 512, 8>(total_rows, "k_grad_quant<f32,512,8>", out);
+    if (max_cols <= 4 * 128 * 8) return gq_resolve_t<false, 128, 8>(total_rows, max_cols, "k_grad_quant<f32,128,8>", out);
+    if (max_cols <= 4 * 256 * 16) return gq_resolve_t<false, 256, 16>(total_rows, max_cols, "k_grad_quant<f32,256,16>", out);
   }
   return cudaErrorInvalidValue;
 }

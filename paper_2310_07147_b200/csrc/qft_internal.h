@@ -149,9 +149,11 @@ struct KLaunch {
   const void* fn = nullptr;
   int grid = 0, block = 0;
   size_t smem = 0;
+  int arg1 = 0;  // the kernel's second argument, for kernels taking (LaunchArgs, int)
   char name[96] = {0};
 };
 cudaError_t launch_k(const KLaunch& k, const LaunchArgs& a, cudaStream_t s);
+cudaError_t launch_k2(const KLaunch& k, const LaunchArgs& a, cudaStream_t s);  // (a, k.arg1)
 // the general step kernel's launch for grad kind gk (rows of a.n_blocks / the device list)
 cudaError_t resolve_step_kernel(int gk, const LaunchArgs& a, KLaunch* out);
 

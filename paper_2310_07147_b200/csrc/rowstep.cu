@@ -984,6 +984,12 @@ cudaError_t launch_k(const KLaunch& k, const LaunchArgs& a, cudaStream_t st) {
   void* args[] = {&aa};
   return cudaLaunchKernel(k.fn, dim3((unsigned)k.grid), dim3((unsigned)k.block), args, k.smem, st);
 }
+cudaError_t launch_k2(const KLaunch& k, const LaunchArgs& a, cudaStream_t st) {
+  LaunchArgs aa = a;
+  int a1 = k.arg1;
+  void* args[] = {&aa, &a1};
+  return cudaLaunchKernel(k.fn, dim3((unsigned)k.grid), dim3((unsigned)k.block), args, k.smem, st);
+}
 
 // QFT_ROWS_GRID caps a persistent grid (read once, when a plan resolves its launches):
 // the tests use it so every CTA pipelines many rows
