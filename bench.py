@@ -824,6 +824,59 @@ def run_13b_dequant(args):
         "per_rank_compute_ms": step_ms + dq_ms, "peak_gbs": hbm}), flush=True)
 
 
+def run_gemm(args):
+    """the forward GEMM of a LLaMA-2-7B layer's projections with the
+    weight dequantization fused into its operand producer (QftModelState.linear ->
+    qftc_dequant_gemm, tcgen05 + TMA), against the materialised path (bf16 expansion of the
+    weight, qftc_expand, + cuBLAS torch.matmul) and cuBLAS alone on pre-expanded weights."""
+    import torch
+    import paper_2310_07147_b200 as q
+    pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak_tf = float(pk.get("bf16_tflops", 2250.0))
+    tokens = 4096  # a micro-batch of 8 x 512 tokens
+    stream = torch.cuda.current_stream()
+    out = []
+    for name, (r, c) in (("q/k/v/o", (4096, 4096)), ("gate/up", (11008, 4096)),
+                         ("down", (4096, 11008))):
+        st = q.QftModelState([(r, c)], bit_width=BIT_WIDTH)
+        st.init_from_weights(lambda i: q.synth((r, c), 4242, 0.02, 0.005), FRACTION, "percentile")
+        x = (torch.randn(tokens, c, device="cuda") * 0.5).to(torch.bfloat16)
+        wb = torch.empty((r, c), dtype=torch.bfloat16, device="cuda")
+        y = torch.empty((tokens, r), dtype=torch.bfloat16, device="cuda")
+        plan = st.expand_plan([wb])
+
+        def timeit(fn, n=max(args.steps, 10)):
+            for _ in range(3):
+                fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(n):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / n
+
+        fused = timeit(lambda: st.linear(0, x, out=y))
+        mat = timeit(lambda: (plan.run(), torch.matmul(x, wb.t(), out=y)))
+        plan.run()
+        cublas = timeit(lambda: torch.matmul(x, wb.t(), out=y))
+        flops = 2.0 * tokens * r * c
+        out.append({"proj": name, "M": tokens, "N": r, "K": c,
+                    "fused_ms": fused, "fused_tflops": flops / fused / 1e9,
+                    "fused_frac_of_bf16_peak": flops / fused / 1e9 / peak_tf,
+                    "expand_plus_cublas_ms": mat, "cublas_only_ms": cublas,
+                    "cublas_tflops": flops / cublas / 1e9,
+                    "weight_bytes_read_fused": r * c + 10 * st.nnz() + 16 * r,
+                    "weight_bytes_materialised": 3 * r * c + 2 * r * c})
+        del st, x, wb, y, plan
+        torch.cuda.empty_cache()
+    print(json.dumps({"gemm": "y = x . W^T, W dense-and-sparse (b=8, p=1%), x/y bf16, "
+                              "fused dequant (tcgen05) vs expand + cuBLAS",
+                      "bf16_peak_tflops": peak_tf, "rows": out}), flush=True)
+
+
 def run_ckpt(args):
     """QFTC v1 checkpoint of the 7B state: the GPU CRC-32
     over every array of the file in file order (HBM-resident, ~13.8 GB), zlib.crc32 on
@@ -899,7 +952,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
-    ap.add_argument("--mode", default="step", choices=["step", "sweep", "13b", "ckpt"])
+    ap.add_argument("--mode", default="step", choices=["step", "sweep", "13b", "ckpt", "gemm"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-side", action="store_true",
@@ -928,6 +981,8 @@ def main():
         run_13b_dequant(args)
     elif args.mode == "ckpt":
         run_ckpt(args)
+    elif args.mode == "gemm":
+        run_gemm(args)
     else:
         run_gpu_arm(args)
 

@@ -270,6 +270,17 @@ typedef struct qftc_expand_tensor {
 int qftc_expand(const qftc_expand_tensor* tensors, int n_tensors, int bf16,
                 qftc_stream_t stream);
 
+/* The forward consumer's GEMM with the dequantization fused into its operand producer
+ * (network.hpp:113-129 forward_core: matmul(cur, transpose(w))):
+ * y[m,n] = x[m,k] . W^T for a dense-and-sparse weight W [n,k] (codes, per-row params,
+ * CSR -- slotted with row_count, or strict with row_count = NULL), x and y bf16 row-major.
+ * The tensor cores read bf16 RNE(reconstruct(W)) built in shared memory from the u8
+ * codes; W never exists in HBM.  k % 64 == 0; x, codes, y 16-byte aligned. */
+int qftc_dequant_gemm(const void* x_bf16, int m, int k, const uint8_t* codes, int n,
+                      const float* scale, const int32_t* zero_point, const int32_t* row_start,
+                      const int32_t* row_count, const int32_t* col_idx, const float* values,
+                      void* y_bf16, qftc_stream_t stream);
+
 /* An expand PLAN: the tensor table uploaded once (synchronises), then one launch per
  * run for any number of tensors -- e.g. the pieces of a ZeRO-1 all-gather (every rank's
  * rows of every tensor, read straight from the gathered shard-major buffers). */

@@ -1,0 +1,352 @@
+// dqgemm.cu -- the forward consumer's GEMM with the weight dequantization fused into its
+// operand producer: Y[M,N] = X[M,K] . W^T, where W is a QFT
+// dense-and-sparse weight -- u8 codes [N,K] (rows = output channels, tensor.hpp:13-16),
+// per-row (scale, zero point) and the CSR outliers -- and X, Y are bf16.  The reference
+// consumer reconstructs W (quantize.hpp:331-338: dequantize every code, then overwrite the
+// CSR positions with their fp32 values) and multiplies (network.hpp:113-129,
+// forward_core: matmul(cur, transpose(weight_at(l)))); here the bf16 operand the tensor
+// cores read is exactly RNE(reconstruct(W)) -- the bytes qftc_expand(bf16) would write --
+// but it never exists in HBM: W streams as 1 byte per element instead of 2.
+//
+// sm_100a, one 128 x BN output tile per CTA, K in blocks of 64:
+//   warp 0 (lane 0)  TMA: the X tile (128 x 64 bf16, SWIZZLE_128B) and the W code tile
+//                    (BN x 64 u8) of a K block into a stage of the smem ring (mbarrier tx)
+//   warps 4-7        the dequant producers: thread j owns W row n0 + j: its 64 codes of
+//                    the stage -> s*(q-z) (fp32, one rounding, quantize.hpp:209) -> its
+//                    CSR outliers in [k0, k0+64) overwrite their positions -> bf16 (RNE)
+//                    -> the K-major SWIZZLE_128B layout tcgen05 reads; fence.proxy.async;
+//                    one arrive per warp.  Each keeps a cursor into its row's CSR slot
+//                    (columns ascending), so the outliers cost O(nnz) per row in total.
+//   warp 1 (lane 0)  tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16 x 4 per block,
+//                    accumulating in TMEM (fp32); tcgen05.commit frees the stage
+//   warps 4-7        the epilogue after the last block: tcgen05.ld 32x32b -> bf16 -> HBM
+//   warp 2           TMEM allocation (BN columns) and release
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
+#include <cstdio>
+
+#include "qft_device.cuh"
+#include "qft_internal.h"
+
+namespace qftk {
+using namespace qftd;
+
+namespace dq {
+constexpr int BM = 128;     // output rows (X rows) per CTA
+constexpr int BN = 128;     // output columns (W rows) per CTA
+constexpr int BK = 64;      // K per block: 128 bytes of bf16 = one SWIZZLE_128B row
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+constexpr int B_BYTES = BN * BK * 2;  // 16 KB
+constexpr int C_BYTES = BN * BK;      // 8 KB of codes
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES + C_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;  // + 1024-byte alignment slack
+
+// K-major SWIZZLE_128B smem descriptor (tcgen05 matrix descriptor): start >> 4,
+// leading byte offset 1 (unused for swizzled K-major), stride byte offset 1024 B between
+// 8-row groups, version 1, layout type 2 (SWIZZLE_128B)
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1u << 46) | ((uint64_t)2u << 61);
+}
+// instruction descriptor: D f32, A/B bf16, both K-major, N = BN, M = 128
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
+      "{%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_after_sync() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_before_sync() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
+}  // namespace dq
+
+struct DqArgs {
+  const float* scale;        // [N]
+  const int32_t* zp;         // [N]
+  const int32_t* row_start;  // [N] CSR slot starts (arena offsets)
+  const int32_t* row_count;  // [N] used entries (null: strict CSR, count = rs[n+1]-rs[n])
+  const int32_t* col;        // arena
+  const float* val;
+  __nv_bfloat16* y;          // [M, N]
+  int M, N, K;
+};
+
+__global__ void __launch_bounds__(256, 1)
+    k_dq_gemm(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
+              const DqArgs a) {
+  using namespace dq;
+  extern __shared__ uint8_t dsm_raw[];
+  uint8_t* dsm = reinterpret_cast<uint8_t*>(((uintptr_t)dsm_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full_tma[STAGES], full_b[STAGES], empty[STAGES], acc_full;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int nkb = a.K / BK;
+  auto a_tile = [&](int s) { return dsm + s * STAGE_BYTES; };
+  auto b_tile = [&](int s) { return dsm + s * STAGE_BYTES + A_BYTES; };
+  auto c_tile = [&](int s) { return dsm + s * STAGE_BYTES + A_BYTES + B_BYTES; };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_tma[s], 1);
+      mbar_init(&full_b[s], 4);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&acc_full, 1);
+    mbar_fence_init();
+  }
+  if (warp == 2) {  // TMEM: BN fp32 columns x 128 lanes
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base)),
+                 "n"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  const uint32_t tmem_d = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGES;
+        mbar_wait(&empty[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
+        mbar_arrive_expect_tx(&full_tma[s], (uint32_t)(A_BYTES + C_BYTES));
+        tma_load_2d(a_tile(s), &tm_x, kb * BK, m0, &full_tma[s]);
+        tma_load_2d(c_tile(s), &tm_w, kb * BK, n0, &full_tma[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (uint32_t)((kb / STAGES) & 1);
+        mbar_wait(&full_tma[s], ph);
+        mbar_wait(&full_b[s], ph);
+        tc_after_sync();
+        const uint32_t sa = smem_u32(a_tile(s)), sb = smem_u32(b_tile(s));
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk)
+          mma_bf16(tmem_d, sw128_desc(sa + 32 * kk), sw128_desc(sb + 32 * kk), IDESC,
+                   (kb > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&empty[s]);  // the stage is free once these MMAs have read it
+      }
+      mma_commit(&acc_full);
+    }
+  } else if (warp >= 4) {
+    // ---------------- dequant producers (then the epilogue)
+    const int j = threadIdx.x - 128;  // W row n0 + j of the tile
+    const int n = n0 + j;
+    const bool live = n < a.N;
+    float s_n = 0.0f, negc = 0.0f;
+    int32_t z_n = 0;
+    int cur = 0, end = 0;
+    if (live) {
+      s_n = a.scale[n];
+      z_n = a.zp[n];
+      negc = make_dequant_row(s_n, z_n).negc;
+      cur = a.row_start[n];
+      end = cur + (a.row_count ? min(a.row_count[n], a.row_start[n + 1] - cur)
+                               : a.row_start[n + 1] - cur);
+    }
+    const bool fast = make_dequant_row(s_n, z_n).fast;
+    // a 4-entry register window over the row's CSR slot (columns ascending): the per-block
+    // test is a register compare, and an entry's load is issued 4 outliers before it is used
+    constexpr int NONE = 0x7fffffff;
+    int oc0 = NONE, oc1 = NONE, oc2 = NONE, oc3 = NONE;
+    float ov0 = 0.0f, ov1 = 0.0f, ov2 = 0.0f, ov3 = 0.0f;
+    int nxt = cur;  // next CSR entry to load into the window
+    auto fetch = [&](int& c, float& v) {
+      if (nxt < end) {
+        c = __ldg(a.col + nxt);
+        v = __ldg(a.val + nxt);
+        ++nxt;
+      } else {
+        c = NONE;
+      }
+    };
+    fetch(oc0, ov0);
+    fetch(oc1, ov1);
+    fetch(oc2, ov2);
+    fetch(oc3, ov3);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (uint32_t)((kb / STAGES) & 1);
+      mbar_wait(&full_tma[s], ph);  // the codes landed (and the stage's B slot is free:
+                                    // full_tma follows empty in the TMA thread)
+      uint8_t* bt = b_tile(s) + j * 128;
+      const uint4* cr = reinterpret_cast<const uint4*>(c_tile(s) + j * BK);
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {  // 16 codes -> 2 swizzled 16-byte chunks
+        const uint4 q = live ? cr[c4] : make_uint4(0, 0, 0, 0);
+        const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+        uint32_t pk[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float f[4];
+          if (fast) {
+            float2 u = make_float2(magic_byte(w4[i], 0), magic_byte(w4[i], 1));
+            float2 v = make_float2(magic_byte(w4[i], 2), magic_byte(w4[i], 3));
+            u = mul2(add2(u, f2(negc)), f2(s_n));
+            v = mul2(add2(v, f2(negc)), f2(s_n));
+            f[0] = u.x; f[1] = u.y; f[2] = v.x; f[3] = v.y;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) f[e] = dequant_exact((w4[i] >> (8 * e)) & 0xFFu, s_n, z_n);
+          }
+          if (!live) f[0] = f[1] = f[2] = f[3] = 0.0f;
+          pk[2 * i] = pack_bf16(f[0], f[1]);
+          pk[2 * i + 1] = pack_bf16(f[2], f[3]);
+        }
+        const int c0 = 2 * c4, c1 = 2 * c4 + 1;  // 8 bf16 per 16-byte chunk
+        *reinterpret_cast<uint4*>(bt + ((c0 ^ (j & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4*>(bt + ((c1 ^ (j & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+      // the row's outliers in this K block overwrite their positions with their exact
+      // fp32 values (RNE to bf16)
+      const int k0 = kb * BK;
+      while (oc0 < k0 + BK) {
+        const int k = oc0 - k0;
+        const uint32_t h = pack_bf16(ov0, 0.0f) & 0xFFFFu;
+        *reinterpret_cast<uint16_t*>(bt + ((((k >> 3) ^ (j & 7)) << 4) | ((k & 7) << 1))) = (uint16_t)h;
+        oc0 = oc1; ov0 = ov1;
+        oc1 = oc2; ov1 = ov2;
+        oc2 = oc3; ov2 = ov3;
+        fetch(oc3, ov3);
+      }
+      fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor cores
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full_b[s]);
+    }
+    // ---------------- epilogue: TMEM lanes 32*(warp-4) .. +32 -> rows of Y
+    mbar_wait(&acc_full, 0u);
+    tc_after_sync();
+    const int row = m0 + 32 * (warp - 4) + lane;
+    const uint32_t lane_base = (uint32_t)(32 * (warp - 4)) << 16;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      uint32_t r[32];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+          "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+          "%28, %29, %30, %31}, [%32];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+            "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+            "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+            "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+            "=r"(r[31])
+          : "r"(tmem_d + lane_base + (uint32_t)c0));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < a.M) {
+        __nv_bfloat16* yr = a.y + (size_t)row * a.N + n0 + c0;
+        if (n0 + c0 + 32 <= a.N && (a.N % 8) == 0) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 o;
+            o.x = pack_bf16(__uint_as_float(r[8 * q]), __uint_as_float(r[8 * q + 1]));
+            o.y = pack_bf16(__uint_as_float(r[8 * q + 2]), __uint_as_float(r[8 * q + 3]));
+            o.z = pack_bf16(__uint_as_float(r[8 * q + 4]), __uint_as_float(r[8 * q + 5]));
+            o.w = pack_bf16(__uint_as_float(r[8 * q + 6]), __uint_as_float(r[8 * q + 7]));
+            reinterpret_cast<uint4*>(yr)[q] = o;
+          }
+        } else {
+          for (int e = 0; e < 32 && n0 + c0 + e < a.N; ++e)
+            yr[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
+        }
+      }
+    }
+  }
+  tc_before_sync();
+  __syncthreads();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "n"(BN));
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+cudaError_t launch_dq_gemm(const void* x, int M, int K, const uint8_t* codes, int N,
+                           const float* scale, const int32_t* zp, const int32_t* row_start,
+                           const int32_t* row_count, const int32_t* col, const float* val,
+                           void* y, cudaStream_t st) {
+  using namespace dq;
+  auto enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  CUtensorMap tx{}, tw{};
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
+    const cuuint64_t strides[1] = {(cuuint64_t)K * 2};
+    const cuuint32_t box[2] = {BK, BM};
+    const cuuint32_t es[2] = {1, 1};
+    if (enc(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)N};
+    const cuuint64_t strides[1] = {(cuuint64_t)K};
+    const cuuint32_t box[2] = {BK, BN};
+    const cuuint32_t es[2] = {1, 1};
+    if (enc(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(codes), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_dq_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  DqArgs a{scale, zp, row_start, row_count, col, val, reinterpret_cast<__nv_bfloat16*>(y), M, N, K};
+  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
+  k_dq_gemm<<<grid, 256, SMEM_BYTES, st>>>(tx, tw, a);
+  return cudaGetLastError();
+}
+
+}  // namespace qftk

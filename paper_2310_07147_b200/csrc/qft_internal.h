@@ -208,6 +208,12 @@ cudaError_t crc32_device(const void* const* segs, const int64_t* lens, int n, ui
 // weight expansion (expand.cu): one launch per expand_max_tensors() tensors
 int expand_max_tensors();
 cudaError_t launch_expand(const qftc_expand_tensor* ts, int n, bool bf16, cudaStream_t s);
+// the consumer GEMM with the weight dequantization fused into its operand producer
+// (dqgemm.cu): y[M,N] = x[M,K] . W^T, x / y bf16, W a dense-and-sparse QFT weight
+cudaError_t launch_dq_gemm(const void* x, int M, int K, const uint8_t* codes, int N,
+                           const float* scale, const int32_t* zp, const int32_t* row_start,
+                           const int32_t* row_count, const int32_t* col, const float* val,
+                           void* y, cudaStream_t s);
 // an expand plan: the table uploaded once, any number of tensors per launch
 cudaError_t expand_plan_create(const qftc_expand_tensor* ts, int n, bool bf16, cudaStream_t s,
                                void** out);

@@ -607,6 +607,25 @@ class QftModelState:
             0 if out.dtype == torch.float32 else 1, _stream()))
         return out
 
+    def linear(self, i: int, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """The forward consumer of tensor i: y = x . W_i^T (network.hpp:113-129), x bf16
+        [M, cols] -> y bf16 [M, rows], with W_i dequantized inside the GEMM's operand producer
+        (qftc_dequant_gemm: tcgen05 tensor cores read RNE(reconstruct(W_i)) built in shared
+        memory from the u8 codes and the CSR outliers; W_i never exists in HBM as bf16)."""
+        cur = self.cur
+        g = self.groups[self.group_of[i]]
+        r, c = self.shapes[i]
+        if x.dtype != torch.bfloat16 or x.dim() != 2 or x.shape[1] != c or not x.is_contiguous():
+            raise ValueError(f"linear: x must be a contiguous bf16 [M, {c}] tensor")
+        y = out if out is not None else torch.empty((x.shape[0], r), dtype=torch.bfloat16,
+                                                    device=x.device)
+        N.check(N.lib.qftc_dequant_gemm(
+            _p(x), x.shape[0], c, _p(self._sl(self.w_codes[cur], i)), r,
+            _p(self._rows(self.w_scale, i)), _p(self._rows(self.w_zp, i)),
+            _p(self._rs(self.row_start[cur], i)), _p(self._rows(self.row_count[cur], i)),
+            _p(g.col[cur]), _p(g.val[cur]), _p(y), _stream()))
+        return y
+
     def expand_table(self, outs: Sequence[torch.Tensor], rows: Optional[Sequence[int]] = None):
         """ctypes table (qftc_expand_tensor[n]) expanding tensor i's first rows[i] rows into
         outs[i] from the CURRENT state; reusable while `cur` and the buffers are unchanged."""
