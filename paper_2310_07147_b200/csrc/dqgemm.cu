@@ -8,19 +8,20 @@
 // cores read is exactly RNE(reconstruct(W)) -- the bytes qftc_expand(bf16) would write --
 // but it never exists in HBM: W streams as 1 byte per element instead of 2.
 //
-// sm_100a, one 128 x BN output tile per CTA, K in blocks of 64:
-//   warp 0 (lane 0)  TMA: the X tile (128 x 64 bf16, SWIZZLE_128B) and the W code tile
-//                    (BN x 64 u8) of a K block into a stage of the smem ring (mbarrier tx)
-//   warps 4-7        the dequant producers: thread j owns W row n0 + j: its 64 codes of
+// sm_100a, one 128 x 256 output tile per CTA, K in blocks of 64:
+//   warp 0 (lane 0)  TMA: the X tile (128 x 64 bf16, SWIZZLE_128B) of a K block into a
+//                    stage of the X / W-operand ring (3 stages, mbarrier tx)
+//   warp 3 (lane 0)  TMA: the W code tile (256 x 64 u8) into its own 4-stage ring
+//   warps 4-11       the dequant producers: thread j owns W row n0 + j: its 64 codes of
 //                    the stage -> s*(q-z) (fp32, one rounding, quantize.hpp:209) -> its
 //                    CSR outliers in [k0, k0+64) overwrite their positions -> bf16 (RNE)
 //                    -> the K-major SWIZZLE_128B layout tcgen05 reads; fence.proxy.async;
 //                    one arrive per warp.  Each keeps a cursor into its row's CSR slot
 //                    (columns ascending), so the outliers cost O(nnz) per row in total.
-//   warp 1 (lane 0)  tcgen05.mma.cta_group::1.kind::f16, M=128, N=BN, K=16 x 4 per block,
+//   warp 1 (lane 0)  tcgen05.mma.cta_group::1.kind::f16, M=128, N=256, K=16 x 4 per block,
 //                    accumulating in TMEM (fp32); tcgen05.commit frees the stage
-//   warps 4-7        the epilogue after the last block: tcgen05.ld 32x32b -> bf16 -> HBM
-//   warp 2           TMEM allocation (BN columns) and release
+//   warps 4-11       the epilogue after the last block: tcgen05.ld 32x32b -> bf16 -> HBM
+//   warp 2           TMEM allocation (256 columns) and release
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -35,14 +36,16 @@ using namespace qftd;
 
 namespace dq {
 constexpr int BM = 128;     // output rows (X rows) per CTA
-constexpr int BN = 128;     // output columns (W rows) per CTA
+constexpr int BN = 256;     // output columns (W rows) per CTA: UMMA N = 256
 constexpr int BK = 64;      // K per block: 128 bytes of bf16 = one SWIZZLE_128B row
-constexpr int STAGES = 4;
+constexpr int STAGES = 3;   // X / W-operand ring
+constexpr int CSTAGES = 4;  // W-code ring (runs one block further ahead)
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
-constexpr int B_BYTES = BN * BK * 2;  // 16 KB
-constexpr int C_BYTES = BN * BK;      // 8 KB of codes
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES + C_BYTES;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;  // + 1024-byte alignment slack
+constexpr int B_BYTES = BN * BK * 2;  // 32 KB
+constexpr int C_BYTES = BN * BK;      // 16 KB of codes
+constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + CSTAGES * C_BYTES + 1024;
+constexpr int NPW = BN / 32;          // producer warps (one thread per W row)
+constexpr int NT = 128 + BN;          // TMA (X), MMA, TMEM, TMA (codes) warps + producers
 
 // K-major SWIZZLE_128B smem descriptor (tcgen05 matrix descriptor): start >> 4,
 // leading byte offset 1 (unused for swizzled K-major), stride byte offset 1024 B between
@@ -103,26 +106,31 @@ struct DqArgs {
   int M, N, K;
 };
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(dq::NT, 1)
     k_dq_gemm(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
               const DqArgs a) {
   using namespace dq;
   extern __shared__ uint8_t dsm_raw[];
   uint8_t* dsm = reinterpret_cast<uint8_t*>(((uintptr_t)dsm_raw + 1023) & ~(uintptr_t)1023);
-  __shared__ __align__(8) uint64_t full_tma[STAGES], full_b[STAGES], empty[STAGES], acc_full;
+  __shared__ __align__(8) uint64_t full_a[STAGES], full_b[STAGES], empty_ab[STAGES];
+  __shared__ __align__(8) uint64_t full_c[CSTAGES], empty_c[CSTAGES], acc_full;
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int nkb = a.K / BK;
-  auto a_tile = [&](int s) { return dsm + s * STAGE_BYTES; };
-  auto b_tile = [&](int s) { return dsm + s * STAGE_BYTES + A_BYTES; };
-  auto c_tile = [&](int s) { return dsm + s * STAGE_BYTES + A_BYTES + B_BYTES; };
+  auto a_tile = [&](int s) { return dsm + s * (A_BYTES + B_BYTES); };
+  auto b_tile = [&](int s) { return dsm + s * (A_BYTES + B_BYTES) + A_BYTES; };
+  auto c_tile = [&](int c) { return dsm + STAGES * (A_BYTES + B_BYTES) + c * C_BYTES; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full_tma[s], 1);
-      mbar_init(&full_b[s], 4);
-      mbar_init(&empty[s], 1);
+      mbar_init(&full_a[s], 1);
+      mbar_init(&full_b[s], NPW);
+      mbar_init(&empty_ab[s], 1);
+    }
+    for (int c = 0; c < CSTAGES; ++c) {
+      mbar_init(&full_c[c], 1);
+      mbar_init(&empty_c[c], NPW);
     }
     mbar_init(&acc_full, 1);
     mbar_fence_init();
@@ -139,13 +147,21 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem_d = tmem_base;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
+    if (lane == 0) {  // ---------------- TMA: X tiles
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % STAGES;
-        mbar_wait(&empty[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
-        mbar_arrive_expect_tx(&full_tma[s], (uint32_t)(A_BYTES + C_BYTES));
-        tma_load_2d(a_tile(s), &tm_x, kb * BK, m0, &full_tma[s]);
-        tma_load_2d(c_tile(s), &tm_w, kb * BK, n0, &full_tma[s]);
+        mbar_wait(&empty_ab[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
+        mbar_arrive_expect_tx(&full_a[s], (uint32_t)A_BYTES);
+        tma_load_2d(a_tile(s), &tm_x, kb * BK, m0, &full_a[s]);
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {  // ---------------- TMA: W code tiles (their own, deeper ring)
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int c = kb % CSTAGES;
+        mbar_wait(&empty_c[c], (uint32_t)(((kb / CSTAGES) & 1) ^ 1));
+        mbar_arrive_expect_tx(&full_c[c], (uint32_t)C_BYTES);
+        tma_load_2d(c_tile(c), &tm_w, kb * BK, n0, &full_c[c]);
       }
     }
   } else if (warp == 1) {
@@ -153,7 +169,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % STAGES;
         const uint32_t ph = (uint32_t)((kb / STAGES) & 1);
-        mbar_wait(&full_tma[s], ph);
+        mbar_wait(&full_a[s], ph);
         mbar_wait(&full_b[s], ph);
         tc_after_sync();
         const uint32_t sa = smem_u32(a_tile(s)), sb = smem_u32(b_tile(s));
@@ -161,7 +177,7 @@ __global__ void __launch_bounds__(256, 1)
         for (int kk = 0; kk < BK / 16; ++kk)
           mma_bf16(tmem_d, sw128_desc(sa + 32 * kk), sw128_desc(sb + 32 * kk), IDESC,
                    (kb > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&empty[s]);  // the stage is free once these MMAs have read it
+        mma_commit(&empty_ab[s]);  // the X / W-operand stage is free once these MMAs read it
       }
       mma_commit(&acc_full);
     }
@@ -202,16 +218,20 @@ __global__ void __launch_bounds__(256, 1)
     fetch(oc2, ov2);
     fetch(oc3, ov3);
     for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (uint32_t)((kb / STAGES) & 1);
-      mbar_wait(&full_tma[s], ph);  // the codes landed (and the stage's B slot is free:
-                                    // full_tma follows empty in the TMA thread)
+      const int s = kb % STAGES, c = kb % CSTAGES;
+      mbar_wait(&full_c[c], (uint32_t)((kb / CSTAGES) & 1));
+      const uint4* cr = reinterpret_cast<const uint4*>(c_tile(c) + j * BK);
+      uint4 q4[4];
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) q4[c4] = live ? cr[c4] : make_uint4(0, 0, 0, 0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_c[c]);  // the code slot is consumed
+      // the W-operand slot of stage s is free once the MMAs of its previous use completed
+      mbar_wait(&empty_ab[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
       uint8_t* bt = b_tile(s) + j * 128;
-      const uint4* cr = reinterpret_cast<const uint4*>(c_tile(s) + j * BK);
 #pragma unroll
       for (int c4 = 0; c4 < 4; ++c4) {  // 16 codes -> 2 swizzled 16-byte chunks
-        const uint4 q = live ? cr[c4] : make_uint4(0, 0, 0, 0);
-        const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+        const uint32_t w4[4] = {q4[c4].x, q4[c4].y, q4[c4].z, q4[c4].w};
         uint32_t pk[8];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -226,7 +246,6 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
             for (int e = 0; e < 4; ++e) f[e] = dequant_exact((w4[i] >> (8 * e)) & 0xFFu, s_n, z_n);
           }
-          if (!live) f[0] = f[1] = f[2] = f[3] = 0.0f;
           pk[2 * i] = pack_bf16(f[0], f[1]);
           pk[2 * i + 1] = pack_bf16(f[2], f[3]);
         }
@@ -250,13 +269,15 @@ __global__ void __launch_bounds__(256, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&full_b[s]);
     }
-    // ---------------- epilogue: TMEM lanes 32*(warp-4) .. +32 -> rows of Y
+    // ---------------- epilogue: TMEM lanes 32*((warp-4)%4) .. +32 -> rows of Y, columns
+    // half (warp-4)/4 of the tile
     mbar_wait(&acc_full, 0u);
     tc_after_sync();
-    const int row = m0 + 32 * (warp - 4) + lane;
-    const uint32_t lane_base = (uint32_t)(32 * (warp - 4)) << 16;
+    const int wq = (warp - 4) & 3, half = (warp - 4) >> 2;
+    const int row = m0 + 32 * wq + lane;
+    const uint32_t lane_base = (uint32_t)(32 * wq) << 16;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
+    for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
       uint32_t r[32];
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
@@ -345,7 +366,7 @@ cudaError_t launch_dq_gemm(const void* x, int M, int K, const uint8_t* codes, in
   }
   DqArgs a{scale, zp, row_start, row_count, col, val, reinterpret_cast<__nv_bfloat16*>(y), M, N, K};
   dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
-  k_dq_gemm<<<grid, 256, SMEM_BYTES, st>>>(tx, tw, a);
+  k_dq_gemm<<<grid, NT, SMEM_BYTES, st>>>(tx, tw, a);
   return cudaGetLastError();
 }
 
