@@ -8,20 +8,23 @@
 // cores read is exactly RNE(reconstruct(W)) -- the bytes qftc_expand(bf16) would write --
 // but it never exists in HBM: W streams as 1 byte per element instead of 2.
 //
-// sm_100a, one 128 x 256 output tile per CTA, K in blocks of 64:
-//   warp 0 (lane 0)  TMA: the X tile (128 x 64 bf16, SWIZZLE_128B) of a K block into a
+// sm_100a, one 256 x 256 output tile per CTA, K in blocks of 64:
+//   warp 0 (lane 0)  TMA: the X tile (256 x 64 bf16, SWIZZLE_128B) of a K block into a
 //                    stage of the X / W-operand ring (3 stages, mbarrier tx)
-//   warp 3 (lane 0)  TMA: the W code tile (256 x 64 u8) into its own 4-stage ring
-//   warps 4-11       the dequant producers: thread j owns W row n0 + j: its 64 codes of
+//   warp 3 (lane 0)  TMA: the W code tile (256 x 64 u8) into its own 2-stage ring
+//   warps 4-19       the dequant producers: a thread pair owns W row n0 + j, each thread
+//                    32 columns of a block: its codes of
 //                    the stage -> s*(q-z) (fp32, one rounding, quantize.hpp:209) -> its
 //                    CSR outliers in [k0, k0+64) overwrite their positions -> bf16 (RNE)
 //                    -> the K-major SWIZZLE_128B layout tcgen05 reads; fence.proxy.async;
 //                    one arrive per warp.  Each keeps a cursor into its row's CSR slot
 //                    (columns ascending), so the outliers cost O(nnz) per row in total.
-//   warp 1 (lane 0)  tcgen05.mma.cta_group::1.kind::f16, M=128, N=256, K=16 x 4 per block,
-//                    accumulating in TMEM (fp32); tcgen05.commit frees the stage
-//   warps 4-11       the epilogue after the last block: tcgen05.ld 32x32b -> bf16 -> HBM
-//   warp 2           TMEM allocation (256 columns) and release
+//   warp 1 (lane 0)  tcgen05.mma.cta_group::1.kind::f16, M=128, N=256, K=16 x 4 per block
+//                    for each of the two 128-row halves (both read the same dequantized W
+//                    operand: each dequantized element feeds 2 x 128 rows of MMA), into
+//                    two TMEM accumulators (fp32); tcgen05.commit frees the stage
+//   warps 4-19       the epilogue after the last block: tcgen05.ld 32x32b -> bf16 -> HBM
+//   warp 2           TMEM allocation (512 columns: both accumulators) and release
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -34,18 +37,31 @@
 namespace qftk {
 using namespace qftd;
 
+#ifndef DQ_NOPROD
+#define DQ_NOPROD 0
+#endif
+#ifndef DQ_NOFENCE
+#define DQ_NOFENCE 0
+#endif
 namespace dq {
-constexpr int BM = 128;     // output rows (X rows) per CTA
+constexpr int BM = 256;     // output rows (X rows) per CTA: two M=128 accumulators
 constexpr int BN = 256;     // output columns (W rows) per CTA: UMMA N = 256
 constexpr int BK = 64;      // K per block: 128 bytes of bf16 = one SWIZZLE_128B row
-constexpr int STAGES = 3;   // X / W-operand ring
-constexpr int CSTAGES = 4;  // W-code ring (runs one block further ahead)
-constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+#ifndef DQ_STAGES
+#define DQ_STAGES 2
+#endif
+#ifndef DQ_CSTAGES
+#define DQ_CSTAGES 4
+#endif
+constexpr int STAGES = DQ_STAGES;    // X / W-operand ring
+constexpr int CSTAGES = DQ_CSTAGES;  // W-code ring
+constexpr int A_BYTES = BM * BK * 2;  // 32 KB (two 128-row halves)
 constexpr int B_BYTES = BN * BK * 2;  // 32 KB
 constexpr int C_BYTES = BN * BK;      // 16 KB of codes
 constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + CSTAGES * C_BYTES + 1024;
-constexpr int NPW = BN / 32;          // producer warps (one thread per W row)
-constexpr int NT = 128 + BN;          // TMA (X), MMA, TMEM, TMA (codes) warps + producers
+constexpr int HALVES = 2;             // producer threads per W row (32 columns each)
+constexpr int NPW = BN * HALVES / 32; // producer warps
+constexpr int NT = 128 + BN * HALVES; // TMA (X), MMA, TMEM, TMA (codes) warps + producers
 
 // K-major SWIZZLE_128B smem descriptor (tcgen05 matrix descriptor): start >> 4,
 // leading byte offset 1 (unused for swizzled K-major), stride byte offset 1024 B between
@@ -54,9 +70,10 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1u << 46) | ((uint64_t)2u << 61);
 }
-// instruction descriptor: D f32, A/B bf16, both K-major, N = BN, M = 128
+// instruction descriptor: D f32, A/B bf16, both K-major, N = BN, M = 128 (per accumulator)
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
+                           ((uint32_t)(128 >> 4) << 24);
+constexpr int TMEM_COLS = 2 * BN;  // two fp32 accumulators of BN columns
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
                                             uint64_t* bar) {
@@ -111,7 +128,9 @@ __global__ void __launch_bounds__(dq::NT, 1)
               const DqArgs a) {
   using namespace dq;
   extern __shared__ uint8_t dsm_raw[];
-  uint8_t* dsm = reinterpret_cast<uint8_t*>(((uintptr_t)dsm_raw + 1023) & ~(uintptr_t)1023);
+  // 1024-byte aligned (SWIZZLE_128B atoms); pointer arithmetic on the shared array keeps
+  // the address space visible to the compiler (LDS/STS, not generic loads and stores)
+  uint8_t* dsm = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
   __shared__ __align__(8) uint64_t full_a[STAGES], full_b[STAGES], empty_ab[STAGES];
   __shared__ __align__(8) uint64_t full_c[CSTAGES], empty_c[CSTAGES], acc_full;
   __shared__ uint32_t tmem_base;
@@ -135,10 +154,10 @@ __global__ void __launch_bounds__(dq::NT, 1)
     mbar_init(&acc_full, 1);
     mbar_fence_init();
   }
-  if (warp == 2) {  // TMEM: BN fp32 columns x 128 lanes
+  if (warp == 2) {  // TMEM: two accumulators of BN fp32 columns x 128 lanes
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_base)),
-                 "n"(BN));
+                 "n"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_before_sync();
@@ -174,16 +193,21 @@ __global__ void __launch_bounds__(dq::NT, 1)
         tc_after_sync();
         const uint32_t sa = smem_u32(a_tile(s)), sb = smem_u32(b_tile(s));
 #pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk)
-          mma_bf16(tmem_d, sw128_desc(sa + 32 * kk), sw128_desc(sb + 32 * kk), IDESC,
-                   (kb > 0 || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < BK / 16; ++kk) {  // both 128-row halves share the W operand
+          const uint64_t bd = sw128_desc(sb + 32 * kk);
+          const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+          mma_bf16(tmem_d, sw128_desc(sa + 32 * kk), bd, IDESC, acc);
+          mma_bf16(tmem_d + BN, sw128_desc(sa + 128 * 128 + 32 * kk), bd, IDESC, acc);
+        }
         mma_commit(&empty_ab[s]);  // the X / W-operand stage is free once these MMAs read it
       }
       mma_commit(&acc_full);
     }
   } else if (warp >= 4) {
     // ---------------- dequant producers (then the epilogue)
-    const int j = threadIdx.x - 128;  // W row n0 + j of the tile
+    const int pt = threadIdx.x - 128;
+    const int j = pt % BN;            // W row n0 + j of the tile ...
+    const int hf = pt / BN;           // ... columns [32 hf, 32 hf + 32) of each block
     const int n = n0 + j;
     const bool live = n < a.N;
     float s_n = 0.0f, negc = 0.0f;
@@ -220,44 +244,76 @@ __global__ void __launch_bounds__(dq::NT, 1)
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % STAGES, c = kb % CSTAGES;
       mbar_wait(&full_c[c], (uint32_t)((kb / CSTAGES) & 1));
-      const uint4* cr = reinterpret_cast<const uint4*>(c_tile(c) + j * BK);
-      uint4 q4[4];
+#if DQ_NOPROD  // A/B: the pipeline without the dequantization work (wrong results)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_c[c]);
+      mbar_wait(&empty_ab[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full_b[s]);
+      continue;
+#endif
+      const uint4* cr = reinterpret_cast<const uint4*>(c_tile(c) + j * BK + 32 * hf);
+      uint4 q4[2];
 #pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) q4[c4] = live ? cr[c4] : make_uint4(0, 0, 0, 0);
+      for (int c4 = 0; c4 < 2; ++c4) q4[c4] = live ? cr[c4] : make_uint4(0, 0, 0, 0);
+      // generic-proxy reads of the slot, then the TMA (async proxy) refills it: order them
+      fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_c[c]);  // the code slot is consumed
       // the W-operand slot of stage s is free once the MMAs of its previous use completed
       mbar_wait(&empty_ab[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
       uint8_t* bt = b_tile(s) + j * 128;
+      // 32 codes -> 4 swizzled 16-byte chunks of bf16: the row's branch (fast magic-number
+      // dequant, or the exact form for |z| >= 2^22) is taken once per block
+      uint32_t pk[2][8];
+      if (fast) {
 #pragma unroll
-      for (int c4 = 0; c4 < 4; ++c4) {  // 16 codes -> 2 swizzled 16-byte chunks
-        const uint32_t w4[4] = {q4[c4].x, q4[c4].y, q4[c4].z, q4[c4].w};
-        uint32_t pk[8];
+        for (int c4 = 0; c4 < 2; ++c4) {
+          const uint32_t w4[4] = {q4[c4].x, q4[c4].y, q4[c4].z, q4[c4].w};
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          float f[4];
-          if (fast) {
+          for (int i = 0; i < 4; ++i) {
             float2 u = make_float2(magic_byte(w4[i], 0), magic_byte(w4[i], 1));
             float2 v = make_float2(magic_byte(w4[i], 2), magic_byte(w4[i], 3));
             u = mul2(add2(u, f2(negc)), f2(s_n));
             v = mul2(add2(v, f2(negc)), f2(s_n));
-            f[0] = u.x; f[1] = u.y; f[2] = v.x; f[3] = v.y;
-          } else {
+            pk[c4][2 * i] = pack_bf16(u.x, u.y);
+            pk[c4][2 * i + 1] = pack_bf16(v.x, v.y);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int c4 = 0; c4 < 2; ++c4) {
+          const uint32_t w4[4] = {q4[c4].x, q4[c4].y, q4[c4].z, q4[c4].w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            float f[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) f[e] = dequant_exact((w4[i] >> (8 * e)) & 0xFFu, s_n, z_n);
+            pk[c4][2 * i] = pack_bf16(f[0], f[1]);
+            pk[c4][2 * i + 1] = pack_bf16(f[2], f[3]);
           }
-          pk[2 * i] = pack_bf16(f[0], f[1]);
-          pk[2 * i + 1] = pack_bf16(f[2], f[3]);
         }
-        const int c0 = 2 * c4, c1 = 2 * c4 + 1;  // 8 bf16 per 16-byte chunk
-        *reinterpret_cast<uint4*>(bt + ((c0 ^ (j & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        *reinterpret_cast<uint4*>(bt + ((c1 ^ (j & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+      }
+#pragma unroll
+      for (int c4 = 0; c4 < 2; ++c4) {
+        const int c0 = 4 * hf + 2 * c4, c1 = c0 + 1;  // 8 bf16 per 16-byte chunk
+        *reinterpret_cast<uint4*>(bt + ((c0 ^ (j & 7)) << 4)) =
+            make_uint4(pk[c4][0], pk[c4][1], pk[c4][2], pk[c4][3]);
+        *reinterpret_cast<uint4*>(bt + ((c1 ^ (j & 7)) << 4)) =
+            make_uint4(pk[c4][4], pk[c4][5], pk[c4][6], pk[c4][7]);
       }
       // the row's outliers in this K block overwrite their positions with their exact
       // fp32 values (RNE to bf16)
-      const int k0 = kb * BK;
-      while (oc0 < k0 + BK) {
-        const int k = oc0 - k0;
+      const int k0 = kb * BK + 32 * hf;  // this thread's half of the block
+      // (the other half's entries below it are skipped: they belong to the other thread)
+      while (oc0 < k0) {
+        oc0 = oc1; ov0 = ov1;
+        oc1 = oc2; ov1 = ov2;
+        oc2 = oc3; ov2 = ov3;
+        fetch(oc3, ov3);
+      }
+      while (oc0 < k0 + 32) {
+        const int k = oc0 - kb * BK;
         const uint32_t h = pack_bf16(ov0, 0.0f) & 0xFFFFu;
         *reinterpret_cast<uint16_t*>(bt + ((((k >> 3) ^ (j & 7)) << 4) | ((k & 7) << 1))) = (uint16_t)h;
         oc0 = oc1; ov0 = ov1;
@@ -265,7 +321,9 @@ __global__ void __launch_bounds__(dq::NT, 1)
         oc2 = oc3; ov2 = ov3;
         fetch(oc3, ov3);
       }
+#if !DQ_NOFENCE
       fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor cores
+#endif
       __syncwarp();
       if (lane == 0) mbar_arrive(&full_b[s]);
     }
@@ -273,11 +331,14 @@ __global__ void __launch_bounds__(dq::NT, 1)
     // half (warp-4)/4 of the tile
     mbar_wait(&acc_full, 0u);
     tc_after_sync();
-    const int wq = (warp - 4) & 3, half = (warp - 4) >> 2;
-    const int row = m0 + 32 * wq + lane;
+    // warp (4 + 4g + q) drains TMEM lanes 32q.. of group g: accumulator g >> 1 (rows
+    // m0 + 128 (g >> 1) ..), columns half g & 1
+    const int wq = (warp - 4) & 3, grp = (warp - 4) >> 2;
+    const int accn = grp >> 1, chalf = grp & 1;
+    const int row = m0 + 128 * accn + 32 * wq + lane;
     const uint32_t lane_base = (uint32_t)(32 * wq) << 16;
 #pragma unroll 1
-    for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
+    for (int c0 = chalf * (BN / 2); c0 < (chalf + 1) * (BN / 2); c0 += 32) {
       uint32_t r[32];
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
@@ -289,7 +350,7 @@ __global__ void __launch_bounds__(dq::NT, 1)
             "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
             "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
             "=r"(r[31])
-          : "r"(tmem_d + lane_base + (uint32_t)c0));
+          : "r"(tmem_d + lane_base + (uint32_t)(accn * BN + c0)));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       if (row < a.M) {
         __nv_bfloat16* yr = a.y + (size_t)row * a.N + n0 + c0;
@@ -313,7 +374,8 @@ __global__ void __launch_bounds__(dq::NT, 1)
   tc_before_sync();
   __syncthreads();
   if (warp == 2)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "n"(BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d),
+                 "n"(TMEM_COLS));
 }
 
 // ------------------------------------------------------------------ host side
