@@ -281,6 +281,24 @@ int qftc_dequant_gemm(const void* x_bf16, int m, int k, const uint8_t* codes, in
                       const int32_t* row_count, const int32_t* col_idx, const float* values,
                       void* y_bf16, qftc_stream_t stream);
 
+/* Opt-in QFTC format extensions (checkpoint.cpp:100-140 is the v1
+ * layout they extend; the files carry version 0x8001, which the reference rejects):
+ * b-bit codes (b in [2, 8]) bit-packed LSB-first per row, each row padded to a byte
+ * (lossless), and the momentum re-quantized with one affine (scale, zero point) per
+ * block of `block` elements of a row -- and back to the per-row form of quantize_state
+ * (lossy).  The momentum conversions synchronise (they report min > max). */
+int qftc_pack_codes(const uint8_t* codes, int rows, int cols, int bits, uint8_t* packed,
+                    qftc_stream_t stream);
+int qftc_unpack_codes(const uint8_t* packed, int rows, int cols, int bits, uint8_t* codes,
+                      qftc_stream_t stream);
+int qftc_momentum_to_blocks(const uint8_t* codes, const float* scale, const int32_t* zero_point,
+                            int rows, int cols, int bit_width, int block, uint8_t* block_codes,
+                            float* block_scale, int32_t* block_zero_point, qftc_stream_t stream);
+int qftc_momentum_from_blocks(const uint8_t* block_codes, const float* block_scale,
+                              const int32_t* block_zero_point, int rows, int cols, int bit_width,
+                              int block, uint8_t* codes, float* scale, int32_t* zero_point,
+                              qftc_stream_t stream);
+
 /* An expand PLAN: the tensor table uploaded once (synchronises), then one launch per
  * run for any number of tensors -- e.g. the pieces of a ZeRO-1 all-gather (every rank's
  * rows of every tensor, read straight from the gathered shard-major buffers). */

@@ -85,6 +85,10 @@ _SIGS = {
     "qftc_plan_set_arena": (_i, [_vp, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_i64)]),
     "qftc_plan_step": (_i, [_vp, _i, LionHyperC, _vp]),
     "qftc_plans_step": (_i, [C.POINTER(_vp), _i, _i, LionHyperC, _vp]),
+    "qftc_pack_codes": (_i, [_vp, _i, _i, _i, _vp, _vp]),
+    "qftc_unpack_codes": (_i, [_vp, _i, _i, _i, _vp, _vp]),
+    "qftc_momentum_to_blocks": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp]),
+    "qftc_momentum_from_blocks": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "qftc_dequant_gemm": (_i, [_vp, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "qftc_expand_plan_create": (_i, [C.POINTER(_vp), C.POINTER(ExpandTensorC), _i, _i, _vp]),
     "qftc_expand_plan_run": (_i, [_vp, _vp]),

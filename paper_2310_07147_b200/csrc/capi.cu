@@ -413,6 +413,67 @@ int qftc_dequant_gemm(const void* x_bf16, int m, int k, const uint8_t* codes, in
   return QFTC_OK;
 }
 
+static int pack_impl(const uint8_t* src, int rows, int cols, int bits, uint8_t* dst,
+                     bool unpack, qftc_stream_t stream) {
+  if (int rc = require_shape(rows, cols, unpack ? "unpack_codes" : "pack_codes")) return rc;
+  if (bits < 2 || bits > 8) return fail(QFTC_EINVAL, "pack_codes: bits must be in [2, 8]");
+  if (!src || !dst) return fail(QFTC_EINVAL, "pack_codes: null pointer");
+  if (int rc = require_device()) return rc;
+  QFTC_CUDA(launch_pack_codes(src, rows, cols, bits, dst, unpack, (cudaStream_t)stream),
+            "pack_codes kernel");
+  return QFTC_OK;
+}
+
+int qftc_pack_codes(const uint8_t* codes, int rows, int cols, int bits, uint8_t* packed,
+                    qftc_stream_t stream) {
+  return pack_impl(codes, rows, cols, bits, packed, false, stream);
+}
+
+int qftc_unpack_codes(const uint8_t* packed, int rows, int cols, int bits, uint8_t* codes,
+                      qftc_stream_t stream) {
+  return pack_impl(packed, rows, cols, bits, codes, true, stream);
+}
+
+static int mom_impl(const uint8_t* codes, const float* scale, const int32_t* zp, int rows,
+                    int cols, int bits, int block, uint8_t* out, float* oscale, int32_t* ozp,
+                    bool from_blocks, qftc_stream_t stream) {
+  if (int rc = require_shape(rows, cols, "momentum_blocks")) return rc;
+  if (int rc = require_bit_width(bits)) return rc;
+  if (block <= 0) return fail(QFTC_EINVAL, "momentum_blocks: block must be positive");
+  if (!codes || !scale || !zp || !out || !oscale || !ozp)
+    return fail(QFTC_EINVAL, "momentum_blocks: null pointer");
+  if (int rc = require_device()) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* err = nullptr;
+  QFTC_CUDA(cudaMallocAsync((void**)&err, 4, st), "momentum_blocks: alloc");
+  QFTC_CUDA(cudaMemsetAsync(err, 0, 4, st), "momentum_blocks: memset");
+  cudaError_t e = launch_mom_blocks(codes, scale, zp, rows, cols, bits, block, out, oscale, ozp,
+                                    from_blocks, err, st);
+  uint32_t h = 0;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&h, err, 4, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(err, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  QFTC_CUDA(e, "momentum_blocks kernel");
+  if (h) return fail(QFTC_EINVAL, "affine_params_from_bounds: min > max in momentum channel");
+  return QFTC_OK;
+}
+
+int qftc_momentum_to_blocks(const uint8_t* codes, const float* scale, const int32_t* zero_point,
+                            int rows, int cols, int bit_width, int block, uint8_t* block_codes,
+                            float* block_scale, int32_t* block_zero_point,
+                            qftc_stream_t stream) {
+  return mom_impl(codes, scale, zero_point, rows, cols, bit_width, block, block_codes,
+                  block_scale, block_zero_point, false, stream);
+}
+
+int qftc_momentum_from_blocks(const uint8_t* block_codes, const float* block_scale,
+                              const int32_t* block_zero_point, int rows, int cols, int bit_width,
+                              int block, uint8_t* codes, float* scale, int32_t* zero_point,
+                              qftc_stream_t stream) {
+  return mom_impl(block_codes, block_scale, block_zero_point, rows, cols, bit_width, block, codes,
+                  scale, zero_point, true, stream);
+}
+
 int qftc_reconstruct(const uint8_t* codes, int rows, int cols, const float* scale,
                      const int32_t* zp, const int32_t* row_ptr, const int32_t* col_idx,
                      const float* values, float* out, qftc_stream_t stream) {

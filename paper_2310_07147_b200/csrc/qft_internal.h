@@ -214,6 +214,13 @@ cudaError_t launch_dq_gemm(const void* x, int M, int K, const uint8_t* codes, in
                            const float* scale, const int32_t* zp, const int32_t* row_start,
                            const int32_t* row_count, const int32_t* col, const float* val,
                            void* y, cudaStream_t s);
+// opt-in checkpoint format extensions (ckptext.cu)
+cudaError_t launch_pack_codes(const uint8_t* src, int rows, int cols, int bits, uint8_t* dst,
+                              bool unpack, cudaStream_t s);
+cudaError_t launch_mom_blocks(const uint8_t* codes, const float* scale, const int32_t* zp,
+                              int rows, int cols, int bits, int block, uint8_t* out,
+                              float* oscale, int32_t* ozp, bool from_blocks, uint32_t* err,
+                              cudaStream_t s);
 // an expand plan: the table uploaded once, any number of tensors per launch
 cudaError_t expand_plan_create(const qftc_expand_tensor* ts, int n, bool bf16, cudaStream_t s,
                                void** out);
