@@ -186,6 +186,18 @@ int qftc_plan_step(qftc_plan* plan, int flip, qftc_lion_hyper hyper, qftc_stream
  * rows kernel claims rows dynamically, so a class's late CTAs just take fewer rows). */
 int qftc_plans_step(qftc_plan* const* plans, int n, int flip, qftc_lion_hyper hyper,
                     qftc_stream_t stream);
+/* The fused ZeRO-1 reduce-scatter: a bf16 raw-gradient plan reads
+ * its rows of the summed gradient straight from npeer peer buffers over NVLink peer memory
+ * (peer p's copy of a row lives at the plan's own gradient address + byte_deltas[p]), sums
+ * them in fp32 in peer order and quantizes them (quantize_state) in the same pass; npeer 0
+ * restores the local gradient.  CUDA IPC helpers map the peers' buffers: a handle of the
+ * allocation holding ptr (+ ptr's offset in it), its mapping in this process, the unmap. */
+int qftc_plan_set_peer_gradients(qftc_plan* plan, const int64_t* byte_deltas, int npeer);
+int qftc_ipc_handle(const void* ptr, unsigned char handle[64], int64_t* offset);
+int qftc_ipc_open(const unsigned char handle[64], void** base);
+int qftc_ipc_close(void* base);
+/* device -> device copy between (IPC-mapped) peer and local buffers (cudaMemcpyDefault) */
+int qftc_copy_peer(void* dst, const void* src, size_t bytes, qftc_stream_t stream);
 /* Cap the resident CTAs per SM of a plan's rows kernel (0: occupancy maximum), so a
  * concurrently stepped plan leaves room for another's CTAs. */
 int qftc_plan_set_ctas_per_sm(qftc_plan* plan, int ctas_per_sm);

@@ -94,6 +94,11 @@ _SIGS = {
     "qftc_expand_plan_run": (_i, [_vp, _vp]),
     "qftc_expand_plan_destroy": (_i, [_vp]),
     "qftc_plan_set_ctas_per_sm": (_i, [_vp, _i]),
+    "qftc_plan_set_peer_gradients": (_i, [_vp, C.POINTER(_i64), _i]),
+    "qftc_ipc_handle": (_i, [_vp, C.c_char_p, C.POINTER(_i64)]),
+    "qftc_ipc_open": (_i, [C.c_char_p, C.POINTER(_vp)]),
+    "qftc_ipc_close": (_i, [_vp]),
+    "qftc_copy_peer": (_i, [_vp, _vp, C.c_size_t, _vp]),
     "qftc_plan_result": (_i, [_vp, C.POINTER(_i64), _vp]),
     "qftc_plan_launches": (_i, [_vp]),
     "qftc_plan_kernel_name": (C.c_char_p, [_vp]),

@@ -12,6 +12,9 @@
 #include <vector>
 
 #include "qft_b200.h"
+#include <cuda.h>
+#include <cstring>
+
 #include "qft_internal.h"
 
 namespace qftk {
@@ -571,6 +574,10 @@ struct qftc_plan {
   bool gq = false;
   void* gq_base = nullptr;
   KLaunch gql;
+  // the fused ZeRO-1 reduce-scatter: the raw gradient summed from npeer peer buffers
+  int npeer = 0;
+  int64_t* peer_deltas = nullptr;  // device [16]
+  KLaunch rsl;
   KLaunch gen[2];             // general path (no rows kernel): by weight decay == 0
   cudaStream_t side = nullptr;     // qftc_plans_step: this plan's stream ...
   cudaEvent_t ev_fork = nullptr;   // ... forked from the caller's stream
@@ -795,7 +802,11 @@ int qftc_plan_step(qftc_plan* p, int flip, qftc_lion_hyper h, qftc_stream_t stre
     a.oldcap6 = rows_kernel_oldcap(p->uniform_cols);
     a.prep = p->prep;
     a.xlist = p->xlist;
-    if (p->gq) QFTC_CUDA(launch_k2(p->gql, a, (cudaStream_t)stream), "gradient quantize_state");
+    if (p->gq && p->npeer > 0)
+      QFTC_CUDA(launch_rs_grad_quant(p->rsl, a, p->peer_deltas, p->npeer, (cudaStream_t)stream),
+                "fused reduce-scatter + quantize_state");
+    else if (p->gq)
+      QFTC_CUDA(launch_k2(p->gql, a, (cudaStream_t)stream), "gradient quantize_state");
     QFTC_CUDA(launch_rows_step(a, p->rc, (cudaStream_t)stream), "lion step (rows kernel)");
     p->last_kernel = p->rc.rows[a.slotted_in ? 1 : 0].name;
     return QFTC_OK;
@@ -804,6 +815,62 @@ int qftc_plan_step(qftc_plan* p, int flip, qftc_lion_hyper h, qftc_stream_t stre
   if (!k.fn) QFTC_CUDA(resolve_step_kernel(p->grad_kind, a, &k), "lion step kernel (resolve)");
   QFTC_CUDA(launch_k(k, a, (cudaStream_t)stream), "lion step kernel");
   p->last_kernel = k.name;
+  return QFTC_OK;
+}
+
+int qftc_plan_set_peer_gradients(qftc_plan* p, const int64_t* byte_deltas, int npeer) {
+  if (!p || npeer < 0 || npeer > 16 || (npeer > 0 && !byte_deltas))
+    return fail(QFTC_EINVAL, "plan_set_peer_gradients: bad arguments");
+  if (npeer > 0 && !(p->gq && p->grad_kind == QFTC_GRAD_BF16))
+    return fail(QFTC_ENOTSUP, "plan_set_peer_gradients: needs a bf16 raw-gradient rows-path plan");
+  if (!p->peer_deltas)
+    QFTC_CUDA(cudaMalloc((void**)&p->peer_deltas, 16 * sizeof(int64_t)), "peer deltas");
+  if (npeer > 0) {
+    QFTC_CUDA(cudaMemcpy(p->peer_deltas, byte_deltas, (size_t)npeer * sizeof(int64_t),
+                         cudaMemcpyHostToDevice), "peer deltas");
+    if (!p->rsl.fn) QFTC_CUDA(resolve_rs_grad_quant(p->uniform_cols, p->total_rows, &p->rsl),
+                              "fused reduce-scatter kernel (resolve)");
+  }
+  p->npeer = npeer;
+  return QFTC_OK;
+}
+
+int qftc_ipc_handle(const void* ptr, unsigned char handle[64], int64_t* offset) {
+  if (!ptr || !handle || !offset) return fail(QFTC_EINVAL, "ipc_handle: null argument");
+  if (int rc = require_device()) return rc;
+  using PFN_range = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static PFN_range range = nullptr;
+  if (!range) {
+    void* fp = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(QFTC_ENOTSUP, "ipc_handle: cuMemGetAddressRange unavailable");
+    range = reinterpret_cast<PFN_range>(fp);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (CUdeviceptr)(uintptr_t)ptr) != CUDA_SUCCESS)
+    return fail(QFTC_EINVAL, "ipc_handle: not a device allocation");
+  cudaIpcMemHandle_t h;
+  QFTC_CUDA(cudaIpcGetMemHandle(&h, (void*)(uintptr_t)base), "cudaIpcGetMemHandle");
+  memcpy(handle, &h, 64);
+  *offset = (int64_t)((uintptr_t)ptr - (uintptr_t)base);
+  return QFTC_OK;
+}
+
+int qftc_ipc_open(const unsigned char handle[64], void** base) {
+  if (!handle || !base) return fail(QFTC_EINVAL, "ipc_open: null argument");
+  if (int rc = require_device()) return rc;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, 64);
+  QFTC_CUDA(cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+  return QFTC_OK;
+}
+
+int qftc_ipc_close(void* base) {
+  if (!base) return QFTC_OK;
+  QFTC_CUDA(cudaIpcCloseMemHandle(base), "cudaIpcCloseMemHandle");
   return QFTC_OK;
 }
 
@@ -910,6 +977,7 @@ int qftc_plan_destroy(qftc_plan* p) {
   if (p->rc.glist) cudaFree(p->rc.glist);
   if (p->rc.pstatus) cudaFree(p->rc.pstatus);
   if (p->gq_base) cudaFree(p->gq_base);
+  if (p->peer_deltas) cudaFree(p->peer_deltas);
   if (p->rc.seen_host) cudaFreeHost(const_cast<int32_t*>(p->rc.seen_host));
   if (p->side) {
     cudaStreamSynchronize(p->side);
@@ -1039,6 +1107,13 @@ int qftc_copy_to_device(void* dst, const void* src, size_t bytes, qftc_stream_t 
   if (!bytes) return QFTC_OK;
   QFTC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, (cudaStream_t)stream),
             "copy_to_device");
+  return QFTC_OK;
+}
+
+int qftc_copy_peer(void* dst, const void* src, size_t bytes, qftc_stream_t stream) {
+  if (!bytes) return QFTC_OK;
+  QFTC_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream),
+            "copy_peer");
   return QFTC_OK;
 }
 

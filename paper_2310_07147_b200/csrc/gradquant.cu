@@ -255,3 +255,144 @@ cudaError_t resolve_grad_quant(int gk, int max_cols, int total_rows, KLaunch* ou
 }
 
 }  // namespace qftk
+
+// ---------------------------------------------------------------------------------------
+// The ZeRO-1 reduce-scatter fused with the sink's quantize_state:
+// rank k's shard rows of the summed gradient are read straight from every peer's full
+// (shard-major) bf16 gradient buffer over NVLink peer memory -- the source of a row for
+// peer j is its local address + deltas[j] bytes -- summed in fp32 in rank order
+// (deterministic), reduced for the row's min/max and quantized into the plan's u8 entry.
+// No reduced gradient is ever written: the collective and the quantization are one pass.
+// One CTA per row; every thread keeps its VPL vectors' fp32 sums in registers.
+namespace qftk {
+using namespace qftd;
+
+template <int NT, int VPL>
+__global__ void __launch_bounds__(NT) k_rs_grad_quant(const LaunchArgs a, const int64_t* deltas,
+                                                       int npeer) {
+  using namespace gq;
+  constexpr int NW = NT / 32;
+  __shared__ float red[2][NW];
+  __shared__ float prm[4];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int bw = a.bit_width;
+  const int qmax = (1 << bw) - 1;
+  const double rq = __drcp_rn((double)qmax);
+  int ti = 0;
+  for (int gr = blockIdx.x; gr < a.total_rows; gr += gridDim.x) {
+    while (ti + 1 < a.n_tensors && a.tensors[ti + 1].row_base <= gr) ++ti;
+    const DevTensor& T = a.tensors[ti];
+    const int r = gr - T.row_base;
+    const int nv = T.cols / 8;  // bf16 vectors
+    const uint8_t* local = reinterpret_cast<const uint8_t*>(T.g_raw) + (size_t)r * T.cols * 2;
+    float sum[VPL][8];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) sum[j][e] = 0.0f;
+    for (int p = 0; p < npeer; ++p) {
+      const uint4* src = reinterpret_cast<const uint4*>(local + deltas[p]);
+      uint4 v[VPL];
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+        const int i = t + j * NT;
+        v[j] = __ldcv(src + (i < nv ? i : 0));  // peers' buffers: never cached stale
+      }
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+        float x[8];
+        unpack<true>(v[j], x);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) sum[j][e] = p == 0 ? x[e] : __fadd_rn(sum[j][e], x[e]);
+      }
+    }
+    float lo = __int_as_float(0x7f800000), hi = __int_as_float(0xff800000);
+#pragma unroll
+    for (int j = 0; j < VPL; ++j)
+#pragma unroll
+      for (int e = 0; e < 8; e += 2) minmax2(lo, hi, sum[j][e], sum[j][e + 1]);
+    asm("redux.sync.min.f32 %0, %1, 0xffffffff;" : "=f"(lo) : "f"(lo));
+    asm("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(hi) : "f"(hi));
+    if (lane == 0) {
+      red[0][wid] = lo;
+      red[1][wid] = hi;
+    }
+    __syncthreads();
+    if (t == 0) {
+#pragma unroll
+      for (int w = 1; w < NW; ++w) {
+        lo = fminf(lo, red[0][w]);
+        hi = fmaxf(hi, red[1][w]);
+      }
+      if (sum[0][0] != sum[0][0]) lo = hi = sum[0][0];  // column 0's NaN sticks
+      float s;
+      int32_t z;
+      bool ok = affine_fast(lo, hi, (double)qmax, rq, s, z);
+      if (!ok) {
+        ok = affine_from_bounds(lo, hi, bw, s, z);
+        if (!ok) {
+          atomicOr(&a.hdr->err, ERR_GPARAMS);
+          s = 1.0f;
+          z = 0;
+        }
+      }
+      const_cast<float*>(T.g_scale)[r] = s;
+      const_cast<int32_t*>(T.g_zp)[r] = z;
+      prm[0] = s;
+      prm[1] = __int_as_float(z);
+    }
+    __syncthreads();
+    const QuantRow q = make_quant_row(prm[0], __float_as_int(prm[1]), bw);
+    uint8_t* dst = const_cast<uint8_t*>(T.g_codes) + (size_t)r * T.cols;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int i = t + j * NT;
+      if (i < nv) {
+        uint32_t c[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          float em = 0.0f;
+          c[k] = q.fast ? quant4_fast(sum[j] + 4 * k, q, em) : 0u;
+          if (!q.fast || !(em < q.thr)) c[k] = quant4_exact(sum[j] + 4 * k, q);
+        }
+        __stcs(reinterpret_cast<uint2*>(dst) + i, make_uint2(c[0], c[1]));
+      }
+    }
+    __syncthreads();  // red / prm are rewritten by the next row
+  }
+}
+
+template <int NT, int VPL>
+static cudaError_t rs_resolve_t(int total_rows, const char* name, KLaunch* out) {
+  const void* fn = reinterpret_cast<const void*>(k_rs_grad_quant<NT, VPL>);
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, NT, 0);
+  if (e != cudaSuccess) return e;
+  long grid = (long)sms * (per_sm > 0 ? per_sm : 1);
+  if (grid > total_rows) grid = total_rows;
+  out->fn = fn;
+  out->grid = (int)(grid < 1 ? 1 : grid);
+  out->block = NT;
+  out->smem = 0;
+  snprintf(out->name, sizeof(out->name), "%s", name);
+  return cudaSuccess;
+}
+
+cudaError_t resolve_rs_grad_quant(int max_cols, int total_rows, KLaunch* out) {
+  if (max_cols <= 8 * 256 * 2) return rs_resolve_t<256, 2>(total_rows, "k_rs_grad_quant<256,2>", out);
+  if (max_cols <= 8 * 512 * 4) return rs_resolve_t<512, 4>(total_rows, "k_rs_grad_quant<512,4>", out);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_rs_grad_quant(const KLaunch& k, const LaunchArgs& a, const int64_t* deltas,
+                                 int npeer, cudaStream_t st) {
+  LaunchArgs aa = a;
+  const int64_t* d = deltas;
+  int np = npeer;
+  void* args[] = {&aa, &d, &np};
+  return cudaLaunchKernel(k.fn, dim3((unsigned)k.grid), dim3((unsigned)k.block), args, k.smem, st);
+}
+
+}  // namespace qftk

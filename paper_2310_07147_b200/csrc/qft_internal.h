@@ -185,6 +185,10 @@ int step_kernel_max_cols();
 
 // quantize_state of a raw (f32/bf16) gradient into the plan's u8 entry (gradquant.cu)
 cudaError_t resolve_grad_quant(int gk, int max_cols, int total_rows, KLaunch* out);
+// ... and the ZeRO-1 reduce-scatter fused with it: bf16 rows summed from npeer peer buffers
+cudaError_t resolve_rs_grad_quant(int max_cols, int total_rows, KLaunch* out);
+cudaError_t launch_rs_grad_quant(const KLaunch& k, const LaunchArgs& a, const int64_t* deltas,
+                                 int npeer, cudaStream_t s);
 
 // v6 rows kernel (rowstep.cu): prep + stable rows + step_kernel over the rest
 bool rows_kernel_eligible(int gk, int use_bulk, int uniform_cols);

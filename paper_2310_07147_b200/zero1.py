@@ -24,6 +24,7 @@ collective choreography with gloo.
 """
 from __future__ import annotations
 
+import ctypes as C
 from typing import Dict, List, Sequence, Tuple
 
 import numpy as np
@@ -108,6 +109,8 @@ class Zero1QftLion:
         self.val_full = {c: torch.empty(self.world * self.cap, dtype=torch.float32, device=dev)
                          for c in L.widths}
         self.launches = 0
+        self.fused = False
+        self._mapped = []
 
     # ------------------------------------------------------------------ the step
     def reduce_scatter_grads(self):
@@ -126,6 +129,100 @@ class Zero1QftLion:
             col, val = self.local.arena(c, self.cap)
             dist.all_gather_into_tensor(self.col_full[c], col, group=self.group)
             dist.all_gather_into_tensor(self.val_full[c], val, group=self.group)
+
+    # ------------------------------------------------------------------ the fused path
+    def enable_peer_memory(self):
+        """the step over NVLink peer memory instead of NCCL.  Every
+        rank maps (CUDA IPC) every peer's full bf16 gradient buffer and gathered buffers.
+        The reduce-scatter is fused into the local update: the plans read their rows of
+        the summed gradient straight from the peers' buffers and quantize them in one pass
+        (``qftc_plan_set_peer_gradients`` -> ``k_rs_grad_quant``); the all-gather is a push
+        of the rank's updated shard into every peer's gathered buffers (copy engines over
+        the mapped pointers).  Host barriers order the ranks (the gradients are complete
+        before anyone reads them; every push lands before anyone reuses a buffer)."""
+        from . import _native as N
+        names = ["grad", "codes", "rowstart", "count"] + \
+                [f"col{c}" for c in self.layout.widths] + [f"val{c}" for c in self.layout.widths]
+
+        def buf(name):
+            if name == "grad":
+                return self.grad_full
+            if name == "codes":
+                return self.codes_full
+            if name == "rowstart":
+                return self.rowstart_full
+            if name == "count":
+                return self.count_full
+            return (self.col_full if name.startswith("col") else self.val_full)[int(name[3:])]
+
+        mine = {}
+        for n in names:
+            h = C.create_string_buffer(64)
+            off = C.c_int64(0)
+            N.check(N.lib.qftc_ipc_handle(C.c_void_p(buf(n).data_ptr()), h, C.byref(off)))
+            mine[n] = (h.raw, int(off.value))
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=self.group)
+        self._close_peers()
+        self.peer = []  # per rank: name -> device address
+        for k in range(self.world):
+            if k == self.rank:
+                self.peer.append({n: buf(n).data_ptr() for n in names})
+                continue
+            d = {}
+            for n in names:
+                hb, off = allh[k][n]
+                base = C.c_void_p()
+                N.check(N.lib.qftc_ipc_open(hb, C.byref(base)))
+                self._mapped.append(base)
+                d[n] = base.value + off
+            self.peer.append(d)
+        # the local plans read their gradient rows from every rank's grad_full
+        st = self.local.state
+        esz = self.grad_full.element_size()
+        deltas = (C.c_int64 * self.world)(*[
+            self.peer[j]["grad"] + self.rank * self.layout.pad * esz - st.g_raw.data_ptr()
+            for j in range(self.world)])
+        for g in st.groups:
+            N.check(N.lib.qftc_plan_set_peer_gradients(g.plan, deltas, self.world))
+        self.fused = True
+
+    def _close_peers(self):
+        from . import _native as N
+        for b in getattr(self, "_mapped", []):
+            N.lib.qftc_ipc_close(b)
+        self._mapped = []
+
+    def push_state(self):
+        """The all-gather as a push: this rank's updated shard into slot `rank` of every
+        rank's gathered buffers (mapped peer memory)."""
+        from . import _native as N
+        L, k = self.layout, self.rank
+        stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        parts = [("codes", self.local.codes_shard(L.pad), L.pad),
+                 ("rowstart", self.local.rowstart_shard(L.rp_pad), L.rp_pad),
+                 ("count", self.local.count_shard(L.rpad), L.rpad)]
+        for c in L.widths:
+            col, val = self.local.arena(c, self.cap)
+            parts += [(f"col{c}", col, self.cap), (f"val{c}", val, self.cap)]
+        for j in range(self.world):
+            for name, src, n in parts:
+                esz = src.element_size()
+                N.check(N.lib.qftc_copy_peer(C.c_void_p(self.peer[j][name] + k * n * esz),
+                                             C.c_void_p(src.data_ptr()), n * esz, stream))
+
+    def step_fused(self, lr=1e-4, beta1=0.9, beta2=0.99, weight_decay=0.0):
+        """reduce-scatter fused into the update, then the push all-gather (enable first)."""
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group)          # every rank's gradient is complete
+        self.local.step(lr=lr, beta1=beta1, beta2=beta2, weight_decay=weight_decay)
+        cap0 = self.cap
+        self.check_local()                      # synchronises; all-reduced overflow flag
+        if self.cap != cap0:                    # gathered arenas were reallocated: re-map
+            self.enable_peer_memory()
+        self.push_state()
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group)          # every push has landed
 
     def check_local(self):
         """Every rank learns whether ANY rank's local step overflowed a CSR slot (one
