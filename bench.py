@@ -329,6 +329,11 @@ def run_gpu_arm(args):
         torch.cuda.empty_cache()
     if args.zero1:
         line["zero1_step"] = zero1_run(args, full, world, rank, q)
+        torch.cuda.empty_cache()
+        try:
+            line["zero1_fused_step"] = zero1_fused_run(args, full, world, rank, q)
+        except Exception as ex:  # a side measurement never voids the headline
+            line["zero1_fused_step"] = {"error": str(ex)[:300]}
     if not args.no_cpu:
         try:
             cb = cpu_reference_run(steps=2, warmup=0)
@@ -453,6 +458,11 @@ def run_multi_gpu(args, full, world, rank, local, q):
     clk.start()
     z = zero1_run(args, full, world, rank, q)
     clocks = clk.stop()
+    torch.cuda.empty_cache()
+    try:
+        zf = zero1_fused_run(args, full, world, rank, q)
+    except Exception as ex:  # a side measurement never voids the headline
+        zf = {"error": str(ex)[:300]}
     hbm, peak_kind = peaks()
     params = count(full)[0]
     ms = z["ms_per_step"]
@@ -476,6 +486,7 @@ def run_multi_gpu(args, full, world, rank, local, q):
                      "algorithmic_bytes_per_launch": d["algorithmic_bytes"],
                      "launch_ms": d["ms"], "peak_kind": peak_kind},
         "zero1_step": z,
+        "zero1_fused_step": zf,
         "update_only_gparams_s": z["update_gparams_s_all_ranks"],
         "gpu_launches": args.steps * z["gpu_launches_per_step"],
         "clocks": clocks,
@@ -483,6 +494,60 @@ def run_multi_gpu(args, full, world, rank, local, q):
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
+
+
+def zero1_fused_run(args, full, world, rank, q):
+    """§8(f) row 3: the ZeRO-1 step over peer memory (CUDA IPC mappings instead of NCCL):
+    the reduce-scatter fused into the update's gradient quantizer (k_rs_grad_quant reads
+    every rank's bf16 rows and quantizes their fp32 sum in one pass), then the push
+    all-gather.  Device time between CUDA events around the whole step (its host barriers
+    included), max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2310_07147_b200.zero1 import CudaShard, ShardLayout, Zero1QftLion
+    own_group = not dist.is_initialized()
+    if own_group:
+        import socket
+        s_ = socket.socket()
+        s_.bind(("127.0.0.1", 0))
+        port_no = s_.getsockname()[1]
+        s_.close()
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port_no}", rank=0,
+                                world_size=1)
+    try:
+        layout = ShardLayout(full, world)
+        local = CudaShard(layout, rank, bit_width=BIT_WIDTH, grad_dtype=torch.bfloat16)
+        shard = layout.shard_shapes(rank)
+        local.state.init_from_weights(
+            lambda i: q.synth(shard[i], 4321 + 1000 * rank + i, 0.02, 0.005), FRACTION, "percentile")
+        z = Zero1QftLion(full, local)
+        z.enable_peer_memory()
+        gen = torch.Generator(device="cuda")
+        gen.manual_seed(99 + rank)
+        z.grad_full.normal_(0.0, 1e-3 / world, generator=gen)
+        stream = torch.cuda.current_stream()
+        for _ in range(args.warmup):
+            z.step_fused(**HYPER)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        for e0, e1 in ev:
+            e0.record(stream)
+            z.step_fused(**HYPER)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        ms = statistics.mean(e0.elapsed_time(e1) for e0, e1 in ev)
+        t = torch.tensor([ms])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        params = sum(r * c for r, c in full)
+        z._close_peers()
+        return {"ms_per_step": ms, "gparams_s": params / (ms * 1e-3) / 1e9, "world": world,
+                "what": "fused reduce-scatter + quantize_state over peer memory (k_rs_grad_quant), "
+                        "rows kernels, push all-gather; host barriers included",
+                "kernels": local.state.kernel_names()}
+    finally:
+        if own_group:
+            dist.destroy_process_group()
 
 
 def zero1_run(args, full, world, rank, q):
