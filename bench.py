@@ -622,8 +622,7 @@ def zero1_run(args, full, world, rank, q):
         shard_params = st.param_count
         f = (world - 1) / world
         rs_bytes = f * 2 * layout.pad * world
-        ag_bytes = f * (layout.pad + 4 * layout.rp_pad + 4 * layout.rpad +
-                        8 * z.cap * len(layout.widths)) * world
+        ag_bytes = f * z.gather_bytes_per_rank() * world   # packed: only used CSR entries
         # the update's launch group: k_grad_quant (2 B bf16 read + 1 B code write per param,
         # 8 B params per row) + the step on the u8 entry (5 B per param,
         # 8 B per CSR entry in and out, 48 B per row), every width class concurrently

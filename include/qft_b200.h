@@ -204,7 +204,9 @@ int qftc_plan_set_ctas_per_sm(qftc_plan* plan, int ctas_per_sm);
 /* Synchronises; returns the new total nnz of the arena written by the last step
  * and QFTC_EOVERFLOW / QFTC_EINVAL if that step overflowed or hit a degenerate row. */
 int qftc_plan_result(qftc_plan* plan, int64_t* nnz_total, qftc_stream_t stream);
-/* number of kernel launches one qftc_plan_step enqueues (for accounting) */
+/* number of kernel launches one qftc_plan_step enqueues (for accounting; a step that
+ * routes its few stable rows into the GEN list -- fewer than 1/16 of the rows were stable
+ * the step before -- skips the stable launch and enqueues one fewer) */
 int qftc_plan_launches(const qftc_plan* plan);
 /* the main kernel instance the last qftc_plan_step launched, e.g.
  * "rows_kernel<128,5,3,2,4096,8>" (MAXT, MINB, stages, FULL, compile-time columns, bit
@@ -218,7 +220,8 @@ int qftc_plan_pending_overflow(const qftc_plan* plan);
 /* rows of the last step in the stable tier (rows kernel) and the general tier (general
  * kernel); synchronises */
 /* rows of the last step per tier: [0] stable (pass-through rows kernel), [1] GEN (rows
- * kernel requantizing every code), [2] general (step_kernel).  Synchronises. */
+ * kernel requantizing every code; includes stable rows routed into the GEN list), [2]
+ * general (step_kernel).  Synchronises. */
 int qftc_plan_tiers(qftc_plan* plan, int64_t rows_out[3], qftc_stream_t stream);
 int qftc_plan_tier_rows(qftc_plan* plan, int64_t* stable_rows, int64_t* general_rows,
                         qftc_stream_t stream);
@@ -249,6 +252,29 @@ int qftc_csr_copy_rows(int rows, const int32_t* src_start, const int32_t* src_co
                        const int32_t* src_col, const float* src_val, const int32_t* dst_start,
                        int32_t* dst_col, float* dst_val, int64_t dst_capacity,
                        qftc_stream_t stream);
+/* ZeRO-1 all-gather of only the USED CSR entries.  A pack PLAN
+ * describes nseg slotted segments (one per tensor row range): rows, width class (< nwidth
+ * <= 8), the offset of its rows+1 slot starts in row_start and of its rows counts in
+ * row_count (counts are clamped to their slots).  A run packs each class's used entries
+ * densely -- classes independent, segments in table order -- from col_in[w] / val_in[w]
+ * (the class's slotted arena) into col_out[w] / val_out[w] (capacity: the class's nnz)
+ * and writes row_start_out (row_start's layout): the packed starts plus base[w], the
+ * rank's offset inside the gathered arena, so receivers index the gathered entries
+ * directly.  create uploads the chunk table and synchronises; run is asynchronous (three
+ * launches for any number of segments); col_in..base are host arrays of nwidth entries. */
+typedef struct qftc_pack_segment {
+  int32_t rows, width;
+  int64_t rs_off, cnt_off;
+} qftc_pack_segment;
+typedef struct qftc_csr_pack_plan qftc_csr_pack_plan;
+int qftc_csr_pack_plan_create(qftc_csr_pack_plan** plan, const qftc_pack_segment* segments,
+                              int nseg, int nwidth, qftc_stream_t stream);
+int qftc_csr_pack_run(qftc_csr_pack_plan* plan, const int32_t* row_start,
+                      const int32_t* row_count, const int32_t* const* col_in,
+                      const float* const* val_in, int32_t* const* col_out,
+                      float* const* val_out, const int64_t* base, int32_t* row_start_out,
+                      qftc_stream_t stream);
+int qftc_csr_pack_plan_destroy(qftc_csr_pack_plan* plan);
 /* slotted -> strict reference CSR (SparseOutliers, quantize.hpp:48-57): row_ptr =
  * exclusive scan of the counts, entries gathered.  Synchronises for *nnz_host;
  * QFTC_EOVERFLOW if nnz > capacity. */

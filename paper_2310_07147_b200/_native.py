@@ -53,6 +53,12 @@ class ExpandTensorC(C.Structure):
     ]
 
 
+class PackSegmentC(C.Structure):
+    """``qftc_pack_segment``: one slotted segment of a ZeRO-1 packed CSR gather."""
+    _fields_ = [("rows", C.c_int32), ("width", C.c_int32), ("rs_off", C.c_int64),
+                ("cnt_off", C.c_int64)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -115,6 +121,9 @@ _SIGS = {
     "qftc_csr_copy_rows": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp]),
     "qftc_csr_compact": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, C.POINTER(_i64),
                               _vp]),
+    "qftc_csr_pack_plan_create": (_i, [C.POINTER(_vp), C.POINTER(PackSegmentC), _i, _i, _vp]),
+    "qftc_csr_pack_run": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(_i64), _vp, _vp]),
+    "qftc_csr_pack_plan_destroy": (_i, [_vp]),
     "qftc_reconstruct_slots": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp]),
     "qftc_expand": (_i, [_vp, _i, _i, _vp]),
     "qftc_device_alloc": (_i, [C.POINTER(_vp), C.c_size_t]),

@@ -552,6 +552,50 @@ int qftc_csr_compact(int rows, const int32_t* row_start, const int32_t* row_coun
   return QFTC_OK;
 }
 
+int qftc_csr_pack_plan_create(qftc_csr_pack_plan** plan, const qftc_pack_segment* segs,
+                              int nseg, int nwidth, qftc_stream_t stream) {
+  if (!plan || nseg < 0 || (nseg > 0 && !segs) || nwidth <= 0 || nwidth > QFT_PACK_MAXW)
+    return fail(QFTC_EINVAL, "csr_pack_plan_create: need a segment table and 1..8 classes");
+  for (int i = 0; i < nseg; ++i)
+    if (segs[i].rows < 0 || segs[i].width < 0 || segs[i].width >= nwidth || segs[i].rs_off < 0 ||
+        segs[i].cnt_off < 0 || segs[i].rs_off + segs[i].rows >= (int64_t)INT32_MAX ||
+        segs[i].cnt_off + segs[i].rows > (int64_t)INT32_MAX)
+      return fail(QFTC_EINVAL, "csr_pack_plan_create: bad segment " + std::to_string(i));
+  if (int rc = require_device()) return rc;
+  void* p = nullptr;
+  QFTC_CUDA(csr_pack_plan_create(segs, nseg, nwidth, (cudaStream_t)stream, &p),
+            "csr_pack_plan_create");
+  *plan = reinterpret_cast<qftc_csr_pack_plan*>(p);
+  return QFTC_OK;
+}
+
+int qftc_csr_pack_run(qftc_csr_pack_plan* plan, const int32_t* row_start,
+                      const int32_t* row_count, const int32_t* const* col_in,
+                      const float* const* val_in, int32_t* const* col_out,
+                      float* const* val_out, const int64_t* base, int32_t* row_start_out,
+                      qftc_stream_t stream) {
+  if (!plan || !row_start || !row_count || !row_start_out || !col_in || !val_in || !col_out ||
+      !val_out || !base)
+    return fail(QFTC_EINVAL, "csr_pack_run: null argument");
+  PackWidths P{};
+  const int nwidth = csr_pack_nwidth(plan);
+  for (int w = 0; w < nwidth; ++w) {
+    P.col_in[w] = col_in[w];
+    P.val_in[w] = val_in[w];
+    P.col_out[w] = col_out[w];
+    P.val_out[w] = val_out[w];
+    P.base[w] = base[w];
+  }
+  QFTC_CUDA(csr_pack_run(plan, row_start, row_count, P, row_start_out, (cudaStream_t)stream),
+            "csr_pack");
+  return QFTC_OK;
+}
+
+int qftc_csr_pack_plan_destroy(qftc_csr_pack_plan* plan) {
+  csr_pack_plan_destroy(plan);
+  return QFTC_OK;
+}
+
 }  // extern "C"
 
 // ------------------------------------------------------------------ plans
@@ -720,11 +764,14 @@ int qftc_plan_create(qftc_plan** out, const qftc_lion_tensor* ts, int n, int bit
     p->rc.gen_on = (no_gen && no_gen[0] == '1') ? 0 : 1;
     const char* allrows = getenv("QFT_STABLE_ALLROWS");
     p->rc.stable_allrows = (allrows && allrows[0] == '1') ? 1 : 0;
+    const char* no_route = getenv("QFT_NO_ROUTE");
+    p->rc.route_on = (no_route && no_route[0] == '1') ? 0 : 1;
     if (e == cudaSuccess) {
       void* hp = nullptr;
       if (cudaHostAlloc(&hp, 64, cudaHostAllocMapped) == cudaSuccess) {
         p->rc.seen_host = reinterpret_cast<volatile int32_t*>(hp);
         p->rc.seen_host[0] = p->rc.seen_host[1] = (int32_t)rows;  // unknown: full grids
+        p->rc.seen_host[2] = (int32_t)rows;                         // ... and no routing
         void* dp = nullptr;
         if (cudaHostGetDevicePointer(&dp, hp, 0) == cudaSuccess) p->rc.seen_dev = (int32_t*)dp;
       }
@@ -808,7 +855,7 @@ int qftc_plan_step(qftc_plan* p, int flip, qftc_lion_hyper h, qftc_stream_t stre
     else if (p->gq)
       QFTC_CUDA(launch_k2(p->gql, a, (cudaStream_t)stream), "gradient quantize_state");
     QFTC_CUDA(launch_rows_step(a, p->rc, (cudaStream_t)stream), "lion step (rows kernel)");
-    p->last_kernel = p->rc.rows[a.slotted_in ? 1 : 0].name;
+    p->last_kernel = (p->rc.routed ? p->rc.genrows : p->rc.rows)[a.slotted_in ? 1 : 0].name;
     return QFTC_OK;
   }
   KLaunch& k = p->gen[a.wd == 0.0f ? 1 : 0];

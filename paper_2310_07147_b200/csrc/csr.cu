@@ -7,8 +7,14 @@
 //   * plan slots from counts (capacity = count + count/4 + slack, rounded to 4),
 //   * copy rows between a strict reference CSR (row_ptr) and a slotted arena,
 //   * compact a slotted arena into the strict reference CSR (row_ptr = exclusive
-//     scan of the counts; what the reference's SparseOutliers holds).
+//     scan of the counts; what the reference's SparseOutliers holds),
+//   * pack the used entries of many slotted segments per width class for the ZeRO-1
+//     all-gather (only used entries travel; the row starts are re-based to the rank's
+//     offset inside the gathered arena).
 #include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <vector>
 
 #include "qft_internal.h"
 
@@ -110,6 +116,167 @@ cudaError_t csr_row_ptr(const int32_t* counts, int rows, int32_t* row_ptr, cudaS
   e = exclusive_scan(tmp, row_ptr, rows + 1, st);
   cudaFreeAsync(tmp, st);
   return e;
+}
+
+// ------------------------------------------------------------------ ZeRO-1 packed gather
+// The rows of every segment (one tensor's row range: rows+1 slot starts at rs_off, rows
+// counts at cnt_off) are cut into chunks of <= PACK_T rows, ordered by width class, then
+// segment.  Per run: the used entries of every chunk (one CTA per chunk), an exclusive scan
+// of the chunk totals (cub), and the pack (one CTA per chunk: a block scan of its rows'
+// used counts -> row starts + base, the entries copied one warp per row).
+constexpr int PACK_T = 256;
+
+struct PackChunk {
+  int32_t rs_off;   // first row's slot start (the segment's rs_off + r0)
+  int32_t cnt_off;  // first row's count
+  int32_t rows;     // rows in the chunk (0: an empty segment's terminator only)
+  int32_t flags;    // width class | 0x100: last chunk of its segment
+};
+
+__device__ __forceinline__ int used_entries(const int32_t* rs, const int32_t* cnt, int r) {
+  const int s = rs[r];
+  return max(0, min(cnt[r], rs[r + 1] - s));  // clamped to the slot (an unrepaired overflow)
+}
+
+__global__ void __launch_bounds__(PACK_T) k_chunk_totals(const PackChunk* __restrict__ ch,
+                                                          const int32_t* __restrict__ rs,
+                                                          const int32_t* __restrict__ cnt,
+                                                          int32_t* __restrict__ tot) {
+  __shared__ int red[PACK_T / 32];
+  const PackChunk c = ch[blockIdx.x];
+  int n = threadIdx.x < c.rows ? used_entries(rs + c.rs_off, cnt + c.cnt_off, threadIdx.x) : 0;
+  for (int o = 16; o > 0; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = n;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < PACK_T / 32; ++w) n += red[w];
+    tot[blockIdx.x] = n;
+  }
+}
+
+__global__ void __launch_bounds__(PACK_T) k_pack_chunks(const PackChunk* __restrict__ ch,
+                                                         const int32_t* __restrict__ scan,
+                                                         const int32_t* __restrict__ rs_all,
+                                                         const int32_t* __restrict__ cnt_all,
+                                                         PackWidths P,
+                                                         int32_t* __restrict__ rs_out_all) {
+  __shared__ int wsum[PACK_T / 32];
+  __shared__ int r_src[PACK_T], r_dst[PACK_T], r_n[PACK_T];
+  const PackChunk c = ch[blockIdx.x];
+  const int w = c.flags & 0xFF;
+  const int32_t* rs = rs_all + c.rs_off;
+  const int32_t* cnt = cnt_all + c.cnt_off;
+  int32_t* rs_out = rs_out_all + c.rs_off;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int off = scan[blockIdx.x] - scan[P.first_chunk[w]];  // within the class
+  const int64_t base = P.base[w];
+  int n = 0, src = 0;
+  if (tid < c.rows) {
+    src = rs[tid];
+    n = used_entries(rs, cnt, tid);
+  }
+  int x = n;  // inclusive warp scan
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  int before = 0;
+  for (int k = 0; k < wid; ++k) before += wsum[k];
+  const int excl = off + before + x - n;
+  if (tid < c.rows) rs_out[tid] = (int32_t)(base + excl);
+  if ((c.flags & 0x100) && tid == PACK_T - 1) rs_out[c.rows] = (int32_t)(base + excl + n);
+  r_src[tid] = src;
+  r_dst[tid] = excl;
+  r_n[tid] = n;
+  __syncthreads();
+  const int32_t* col_in = P.col_in[w];
+  const float* val_in = P.val_in[w];
+  int32_t* col_out = P.col_out[w];
+  float* val_out = P.val_out[w];
+  for (int i = wid; i < c.rows; i += PACK_T / 32) {
+    const int s0 = r_src[i], d0 = r_dst[i], m = r_n[i];
+    for (int e = lane; e < m; e += 32) {
+      col_out[d0 + e] = __ldcs(col_in + s0 + e);
+      val_out[d0 + e] = __ldcs(val_in + s0 + e);
+    }
+  }
+}
+
+struct PackPlan {
+  PackChunk* chunks = nullptr;
+  int32_t* tot = nullptr;
+  int32_t* scan = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  int nchunks = 0, nwidth = 0;
+  int first_chunk[QFT_PACK_MAXW] = {};
+};
+
+cudaError_t csr_pack_plan_create(const qftc_pack_segment* segs, int nseg, int nwidth,
+                                 cudaStream_t st, void** out) {
+  std::vector<PackChunk> v;
+  PackPlan* p = new PackPlan;
+  p->nwidth = nwidth;
+  for (int w = 0; w < nwidth; ++w) {
+    p->first_chunk[w] = (int)v.size();
+    for (int i = 0; i < nseg; ++i) {
+      const qftc_pack_segment& s = segs[i];
+      if (s.width != w) continue;
+      for (int r0 = 0; r0 < s.rows || (r0 == 0 && s.rows == 0); r0 += PACK_T) {
+        const int n = std::min(PACK_T, s.rows - r0);
+        const bool last = r0 + PACK_T >= s.rows;
+        v.push_back(PackChunk{(int32_t)(s.rs_off + r0), (int32_t)(s.cnt_off + r0), n,
+                              w | (last ? 0x100 : 0)});
+      }
+    }
+  }
+  p->nchunks = (int)v.size();
+  const int nc = std::max(1, p->nchunks);
+  cudaError_t e = cudaMalloc((void**)&p->chunks, sizeof(PackChunk) * nc);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&p->tot, sizeof(int32_t) * nc);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&p->scan, sizeof(int32_t) * nc);
+  if (e == cudaSuccess && p->nchunks)
+    e = cudaMemcpyAsync(p->chunks, v.data(), sizeof(PackChunk) * v.size(),
+                        cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = cub::DeviceScan::ExclusiveSum(nullptr, p->tmp_bytes, p->tot, p->scan, nc, st);
+  if (e == cudaSuccess) e = cudaMalloc(&p->tmp, p->tmp_bytes ? p->tmp_bytes : 1);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    csr_pack_plan_destroy(p);
+    return e;
+  }
+  *out = p;
+  return cudaSuccess;
+}
+
+cudaError_t csr_pack_run(void* plan, const int32_t* row_start, const int32_t* row_count,
+                         PackWidths P, int32_t* row_start_out, cudaStream_t st) {
+  PackPlan* p = static_cast<PackPlan*>(plan);
+  if (!p->nchunks) return cudaSuccess;
+  for (int w = 0; w < p->nwidth; ++w) P.first_chunk[w] = std::min(p->first_chunk[w], p->nchunks - 1);
+  k_chunk_totals<<<p->nchunks, PACK_T, 0, st>>>(p->chunks, row_start, row_count, p->tot);
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(p->tmp, p->tmp_bytes, p->tot, p->scan,
+                                                p->nchunks, st);
+  if (e != cudaSuccess) return e;
+  k_pack_chunks<<<p->nchunks, PACK_T, 0, st>>>(p->chunks, p->scan, row_start, row_count, P,
+                                               row_start_out);
+  return cudaGetLastError();
+}
+
+int csr_pack_nwidth(const void* plan) { return static_cast<const PackPlan*>(plan)->nwidth; }
+
+void csr_pack_plan_destroy(void* plan) {
+  PackPlan* p = static_cast<PackPlan*>(plan);
+  if (!p) return;
+  cudaFree(p->chunks);
+  cudaFree(p->tot);
+  cudaFree(p->scan);
+  cudaFree(p->tmp);
+  delete p;
 }
 
 }  // namespace qftk

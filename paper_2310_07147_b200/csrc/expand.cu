@@ -22,9 +22,15 @@ using namespace qftk;
 
 namespace {
 
+#ifndef QFT_EXP_WARPS
+#define QFT_EXP_WARPS 2
+#endif
+#ifndef QFT_EXP_UNROLL
+#define QFT_EXP_UNROLL 10
+#endif
 constexpr int EXP_MAXT = 224;      // tensors per launch (param space: <= 32 KB)
-constexpr int EXP_WARPS = 8;       // warps per CTA
-constexpr int EXP_UNROLL = 8;      // 16-code vectors in flight per lane
+constexpr int EXP_WARPS = QFT_EXP_WARPS;    // warps per CTA
+constexpr int EXP_UNROLL = QFT_EXP_UNROLL;  // 16-code vectors in flight per lane
 
 struct ExpT {
   const uint8_t* codes;

@@ -170,6 +170,8 @@ struct RowsCache {
   KLaunch genrows[2];        // the GEN rows kernel, by slotted input (0/1)
   int gen_on = 1;
   int stable_allrows = 0;  // A/B: the stable kernel over every row (no list)
+  int route_on = 1;        // QFT_NO_ROUTE=1 disables routing stable rows into the GEN list
+  bool routed = false;     // the last step routed its stable rows (no stable launch)
   unsigned long long* pstatus = nullptr;  // prep look-back status words (one per block)
   int epoch = 0;
   // the general-tier row count the general kernel last saw (mapped pinned, read without a
@@ -204,6 +206,22 @@ cudaError_t decompose_csr(const float* w, int rows, int cols, const float* t_min
                           float* values, cudaStream_t s);
 cudaError_t csr_row_ptr(const int32_t* counts, int rows, int32_t* row_ptr, cudaStream_t s,
                         const int32_t* slot_start = nullptr);
+// ZeRO-1 packed all-gather of slotted segments (csr.cu)
+constexpr int QFT_PACK_MAXW = 8;
+struct PackWidths {
+  const int32_t* col_in[QFT_PACK_MAXW];
+  const float* val_in[QFT_PACK_MAXW];
+  int32_t* col_out[QFT_PACK_MAXW];
+  float* val_out[QFT_PACK_MAXW];
+  int64_t base[QFT_PACK_MAXW];
+  int32_t first_chunk[QFT_PACK_MAXW];
+};
+cudaError_t csr_pack_plan_create(const qftc_pack_segment* segs, int nseg, int nwidth,
+                                 cudaStream_t s, void** plan);
+cudaError_t csr_pack_run(void* plan, const int32_t* row_start, const int32_t* row_count,
+                         PackWidths P, int32_t* row_start_out, cudaStream_t s);
+void csr_pack_plan_destroy(void* plan);
+int csr_pack_nwidth(const void* plan);
 
 // checkpoint CRC over device segments (crc32.cu); synchronises
 cudaError_t crc32_device(const void* const* segs, const int64_t* lens, int n, uint32_t* crc_out,

@@ -477,7 +477,11 @@ __global__ void __launch_bounds__(MAXT, MINB) rows_kernel(const LaunchArgs a) {
   if (t == ti) {
     if constexpr (GEN) {
       cnt_l = *a.rcount;
-      if (a.xseen && blockIdx.x == 0) *reinterpret_cast<volatile int32_t*>(a.xseen) = cnt_l;
+      if (a.xseen && blockIdx.x == 0) {
+        *reinterpret_cast<volatile int32_t*>(a.xseen) = cnt_l;
+        // the stable rows k_step_prep counted (routed or not): next step's routing decision
+        if (a.scount) reinterpret_cast<volatile int32_t*>(a.xseen)[1] = *a.scount;
+      }
     }
     nxt = next_row();
     if (nxt < TR) hn = load_head(a, nxt);
@@ -922,6 +926,16 @@ __global__ void __launch_bounds__(PREP_T) k_step_prep(const LaunchArgs a, int st
       // (*) the step cannot move a dense code: D/sw <= 0.5 - (K+2)*2^-21
       st = ok && D / (double)sw <= 0.5 - (K + 2.0) * 0x1.0p-21;
     }
+    // stable_ok bit 1: few rows were stable last step, so this step runs no stable launch
+    // and its stable rows join the GEN list (the GEN kernel requantizes every code: the
+    // same bytes, the reference's arithmetic); they are still counted as stable
+    if (st && a.scount) {
+      const unsigned m = __activemask();
+      const int leader = __ffs(m) - 1;
+      if ((int)(threadIdx.x & 31) == leader) atomicAdd(a.scount, __popc(m));
+    }
+    const bool route = st && (stable_ok & 2) && a.gen_on;
+    if (route) st = false;
     const bool gen = ok && !st && a.gen_on;
     tier = st ? 1 : (gen ? 2 : 0);
     RowPrep p;
@@ -1126,10 +1140,16 @@ cudaError_t launch_rows_step(const LaunchArgs& a0, RowsCache& c, cudaStream_t st
   if (c.last_flip == a.flip && (e = cudaMemsetAsync(cf, 0, 4 * sizeof(int32_t), st)) != cudaSuccess)
     return e;
   c.last_flip = a.flip;
+  // stable rows below 1/16 of the launch last step (seen_host[2], published by the GEN
+  // kernel): route them into the GEN list and skip the stable launch, whose walk over
+  // every row would cost a full read of the row records for a handful of rows
+  const bool route = c.gen_on && c.route_on && c.seen_host &&
+                     (long long)c.seen_host[2] * 16 < (long long)a.total_rows;
   const int nb = (a.total_rows + PREP_T - 1) / PREP_T;
-  k_step_prep<<<nb, PREP_T, 0, st>>>(a, 1);
+  k_step_prep<<<nb, PREP_T, 0, st>>>(a, route ? 3 : 1);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  // the stable tier over its row list
+  c.routed = route;
+  // the stable tier: the rows kernel walks every row of the launch
   LaunchArgs sa = a;
   sa.rlist = nullptr;
   sa.rcount = nullptr;
@@ -1137,7 +1157,7 @@ cudaError_t launch_rows_step(const LaunchArgs& a0, RowsCache& c, cudaStream_t st
   sa.xseen = nullptr;
   KLaunch& rk = c.rows[a.slotted_in ? 1 : 0];
   if (!rk.fn && (e = rows_resolve(sa, &rk, c.cap_per_sm)) != cudaSuccess) return e;
-  if ((e = launch_k(rk, sa, st)) != cudaSuccess) return e;
+  if (!route && (e = launch_k(rk, sa, st)) != cudaSuccess) return e;
   // the GEN tier over its list (one CTA per SM when the list was empty last step: the
   // kernel covers any length)
   if (c.gen_on) {

@@ -12,11 +12,15 @@ the update.  The exchange steps are the data-parallel ones:
    shard rows of the summed gradient equals quantizing the full summed gradient.
 2. the fused local step on the shard (grad kind f32/bf16: quantize_state(g) ->
    dequantize fused into the kernel); momentum stays sharded (ZeRO-1);
-3. ``all_gather_into_tensor`` of the updated W codes, of the slotted-CSR row
-   starts and counts and of the CSR arenas (fixed, rank-uniform capacity, so no
-   host round trip is needed to size the gather); slot offsets are
-   arena-absolute, so rank k's segment is re-based by ``k * arena_capacity`` when
-   read from the gathered buffer.
+3. ``all_gather_into_tensor`` of the updated W codes, of the CSR row starts and
+   counts and of the CSR entries.  By default only the USED entries travel
+   (``packed_csr``): every rank packs its slotted arenas densely per width class
+   (``qftc_csr_pack``), the ranks agree the largest packed size per class in the same
+   all-reduce that carries the overflow flag (no extra host round trip), and each rank
+   re-bases its packed row starts by ``rank * packed_size`` so receivers index the
+   gathered entries directly.  ``packed_csr=False`` ships the whole slotted arenas
+   (fixed rank-uniform capacity; rank k's slot offsets re-based by
+   ``k * arena_capacity`` when read).
 
 The local update is pluggable: on GPUs it is :class:`CudaShard` (the fused
 sm_100a kernel through the C-ABI); the CPU tests plug the oracle in to check the
@@ -25,7 +29,8 @@ collective choreography with gloo.
 from __future__ import annotations
 
 import ctypes as C
-from typing import Dict, List, Sequence, Tuple
+import os
+from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 import torch
@@ -87,8 +92,12 @@ class ShardLayout:
 class Zero1QftLion:
     """Row-sharded quantized Lion step for one rank of a process group."""
 
-    def __init__(self, shapes: Sequence[Shape], local, group=None, arena_capacity: int = 0):
+    def __init__(self, shapes: Sequence[Shape], local, group=None, arena_capacity: int = 0,
+                 packed_csr: Optional[bool] = None):
         self.group = group
+        if packed_csr is None:   # default on; QFT_ZERO1_PACKED=0 ships whole arenas (A/B)
+            packed_csr = os.environ.get("QFT_ZERO1_PACKED", "1") != "0"
+        self.packed = bool(packed_csr) and hasattr(local, "pack_csr")
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.layout = ShardLayout(shapes, self.world)
@@ -108,6 +117,8 @@ class Zero1QftLion:
                          for c in L.widths}
         self.val_full = {c: torch.empty(self.world * self.cap, dtype=torch.float32, device=dev)
                          for c in L.widths}
+        self.pcap = {c: 0 for c in L.widths}   # packed entries per rank and class, this step
+        self.generation = 0                    # bumps when gathered buffers are reallocated
         self.launches = 0
         self.fused = False
         self._mapped = []
@@ -117,18 +128,51 @@ class Zero1QftLion:
         dist.reduce_scatter_tensor(self.local.grad_shard(self.layout.pad), self.grad_full,
                                    op=dist.ReduceOp.SUM, group=self.group)
 
-    def all_gather_state(self):
+    def _state_parts(self):
+        """(name, this rank's source tensor, entries per rank) of everything the all-gather
+        ships; with packed_csr the row starts and entries are the packed ones."""
         L = self.layout
-        dist.all_gather_into_tensor(self.codes_full, self.local.codes_shard(L.pad),
-                                    group=self.group)
-        dist.all_gather_into_tensor(self.rowstart_full, self.local.rowstart_shard(L.rp_pad),
-                                    group=self.group)
-        dist.all_gather_into_tensor(self.count_full, self.local.count_shard(L.rpad),
-                                    group=self.group)
+        if self.packed:
+            rs, ents = self.local.pack_csr(self.pcap, {c: self.rank * self.pcap[c]
+                                                       for c in L.widths}, L.rp_pad)
+        else:
+            rs = self.local.rowstart_shard(L.rp_pad)
+            ents = {c: self.local.arena(c, self.cap) for c in L.widths}
+        parts = [("codes", self.local.codes_shard(L.pad), L.pad),
+                 ("rowstart", rs, L.rp_pad),
+                 ("count", self.local.count_shard(L.rpad), L.rpad)]
         for c in L.widths:
-            col, val = self.local.arena(c, self.cap)
-            dist.all_gather_into_tensor(self.col_full[c], col, group=self.group)
-            dist.all_gather_into_tensor(self.val_full[c], val, group=self.group)
+            n = self.pcap[c] if self.packed else self.cap
+            col, val = ents[c]
+            parts += [(f"col{c}", col[:n], n), (f"val{c}", val[:n], n)]
+        return parts
+
+    def _full(self, name):
+        if name == "grad":
+            return self.grad_full
+        if name == "codes":
+            return self.codes_full
+        if name == "rowstart":
+            return self.rowstart_full
+        if name == "count":
+            return self.count_full
+        return (self.col_full if name.startswith("col") else self.val_full)[int(name[3:])]
+
+    def all_gather_state(self):
+        for name, src, n in self._state_parts():
+            if n:
+                dist.all_gather_into_tensor(self._full(name)[:self.world * n], src,
+                                            group=self.group)
+
+    def gather_bytes_per_rank(self) -> int:
+        """Bytes one rank contributes to the state all-gather of the last step."""
+        L = self.layout
+        n = sum(self.pcap.values()) if self.packed else self.cap * len(L.widths)
+        return L.pad + 4 * L.rp_pad + 4 * L.rpad + 8 * n
+
+    def _arena_base(self, k: int) -> int:
+        """Offset of rank k's entries in the gathered arena that its row starts omit."""
+        return 0 if getattr(self, "packed", False) else k * self.cap
 
     # ------------------------------------------------------------------ the fused path
     def enable_peer_memory(self):
@@ -143,18 +187,7 @@ class Zero1QftLion:
         from . import _native as N
         names = ["grad", "codes", "rowstart", "count"] + \
                 [f"col{c}" for c in self.layout.widths] + [f"val{c}" for c in self.layout.widths]
-
-        def buf(name):
-            if name == "grad":
-                return self.grad_full
-            if name == "codes":
-                return self.codes_full
-            if name == "rowstart":
-                return self.rowstart_full
-            if name == "count":
-                return self.count_full
-            return (self.col_full if name.startswith("col") else self.val_full)[int(name[3:])]
-
+        buf = self._full
         mine = {}
         for n in names:
             h = C.create_string_buffer(64)
@@ -186,6 +219,7 @@ class Zero1QftLion:
         for g in st.groups:
             N.check(N.lib.qftc_plan_set_peer_gradients(g.plan, deltas, self.world))
         self.fused = True
+        self._mapped_generation = self.generation
 
     def _close_peers(self):
         from . import _native as N
@@ -197,16 +231,13 @@ class Zero1QftLion:
         """The all-gather as a push: this rank's updated shard into slot `rank` of every
         rank's gathered buffers (mapped peer memory)."""
         from . import _native as N
-        L, k = self.layout, self.rank
+        k = self.rank
         stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-        parts = [("codes", self.local.codes_shard(L.pad), L.pad),
-                 ("rowstart", self.local.rowstart_shard(L.rp_pad), L.rp_pad),
-                 ("count", self.local.count_shard(L.rpad), L.rpad)]
-        for c in L.widths:
-            col, val = self.local.arena(c, self.cap)
-            parts += [(f"col{c}", col, self.cap), (f"val{c}", val, self.cap)]
+        parts = self._state_parts()
         for j in range(self.world):
             for name, src, n in parts:
+                if not n:
+                    continue
                 esz = src.element_size()
                 N.check(N.lib.qftc_copy_peer(C.c_void_p(self.peer[j][name] + k * n * esz),
                                              C.c_void_p(src.data_ptr()), n * esz, stream))
@@ -216,9 +247,8 @@ class Zero1QftLion:
         torch.cuda.current_stream().synchronize()
         dist.barrier(group=self.group)          # every rank's gradient is complete
         self.local.step(lr=lr, beta1=beta1, beta2=beta2, weight_decay=weight_decay)
-        cap0 = self.cap
         self.check_local()                      # synchronises; all-reduced overflow flag
-        if self.cap != cap0:                    # gathered arenas were reallocated: re-map
+        if self.generation != self._mapped_generation:  # gathered buffers reallocated
             self.enable_peer_memory()
         self.push_state()
         torch.cuda.current_stream().synchronize()
@@ -230,12 +260,42 @@ class Zero1QftLion:
         intact ping-pong inputs, then all ranks re-agree a uniform arena capacity, so the
         all-gather never ships a partial step or cuts off a grown arena."""
         ov = bool(getattr(self.local, "pending_overflow", lambda: False)())
-        t = torch.tensor([1 if ov else 0], dtype=torch.int64, device=self.local.device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
-        if int(t.item()):
+        t = self._flag_and_sizes(ov)
+        if t[0]:
             if ov:
                 self.local.recover()
             self._agree_capacity()
+            if self.packed:
+                t = self._flag_and_sizes(False)
+        if self.packed:
+            self._agree_packed(t[1:])
+
+    def _flag_and_sizes(self, ov: bool) -> List[int]:
+        """ONE all-reduce(MAX) of [overflow flag, used entries per width class]."""
+        vals = [1 if ov else 0]
+        if self.packed:
+            nnz = self.local.csr_nnz()
+            vals += [int(nnz.get(c, 0)) for c in self.layout.widths]
+        t = torch.tensor(vals, dtype=torch.int64, device=self.local.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return [int(x) for x in t.tolist()]
+
+    def _agree_packed(self, maxnnz: Sequence[int]):
+        """Per class: the rank-uniform packed size (max used entries, rounded to 32 so every
+        rank's segment stays 128-byte aligned); grow the gathered buffers when it no
+        longer fits (x1.25 headroom) -- row starts are int32, so world * size < 2^31."""
+        dev = self.local.device
+        for c, n in zip(self.layout.widths, maxnnz):
+            n = (int(n) + 31) & ~31
+            if self.world * n >= 2 ** 31:
+                raise OverflowError(f"packed CSR all-gather: {self.world} x {n} entries of "
+                                    f"width {c} exceed int32 row starts")
+            self.pcap[c] = n
+            if self.col_full[c].numel() < self.world * n:
+                m = min(2 ** 31 - 1, self.world * (n + n // 4 + 32))
+                self.col_full[c] = torch.empty(m, dtype=torch.int32, device=dev)
+                self.val_full[c] = torch.empty(m, dtype=torch.float32, device=dev)
+                self.generation += 1
 
     def _agree_capacity(self):
         t = torch.tensor([self.local.arena_capacity()], dtype=torch.int64,
@@ -245,10 +305,13 @@ class Zero1QftLion:
         if cap > self.cap:
             self.cap = cap
             self.local.ensure_arena_capacity(cap)
+            if self.packed:
+                return                          # gathered buffers follow the packed sizes
             dev = self.local.device
             for c in self.layout.widths:
                 self.col_full[c] = torch.empty(self.world * cap, dtype=torch.int32, device=dev)
                 self.val_full[c] = torch.empty(self.world * cap, dtype=torch.float32, device=dev)
+            self.generation += 1
 
     def step(self, lr=1e-4, beta1=0.9, beta2=0.99, weight_decay=0.0):
         self.reduce_scatter_grads()
@@ -270,9 +333,10 @@ class Zero1QftLion:
 
     def expand_plan(self, outs: Sequence[torch.Tensor]):
         """ONE grouped expansion launch reading the gathered shard-major buffers directly:
-        every (rank, tensor) row range is a table entry (codes, params, slot starts, counts
-        and the rank's arena re-based by rank * capacity), writing rows [lo, hi) of the full
-        output tensor (bf16 or f32) -- the next forward's weights (network.hpp:199-212)."""
+        every (rank, tensor) row range is a table entry (codes, params, row starts, counts
+        and the gathered entries -- rank k's arena re-based by k * capacity unless packed),
+        writing rows [lo, hi) of the full output tensor (bf16 or f32) -- the next forward's
+        weights (network.hpp:199-212).  Valid while ``generation`` is unchanged."""
         from . import _native as N
         from .engine import ExpandPlan
         if not hasattr(self, "wscale_full"):
@@ -295,8 +359,8 @@ class Zero1QftLion:
             t.zero_point = self.wzp_full.data_ptr() + 4 * (k * L.rpad + L.roff[k][j])
             t.row_start = self.rowstart_full.data_ptr() + 4 * (k * L.rp_pad + L.rpoff[k][j])
             t.row_count = self.count_full.data_ptr() + 4 * (k * L.rpad + L.roff[k][j])
-            t.col_idx = self.col_full[c].data_ptr() + 4 * k * self.cap
-            t.values = self.val_full[c].data_ptr() + 4 * k * self.cap
+            t.col_idx = self.col_full[c].data_ptr() + 4 * self._arena_base(k)
+            t.values = self.val_full[c].data_ptr() + 4 * self._arena_base(k)
             t.out = o.data_ptr() + lo * c * o.element_size()
         return ExpandPlan(tab, 1 if bf16 else 0, keep=(self, list(outs)))
 
@@ -319,8 +383,8 @@ class Zero1QftLion:
                                         k * L.rp_pad + L.rpoff[k][j + 1]].cpu().numpy()
                 cnt = self.count_full[k * L.rpad + L.roff[k][j]:
                                       k * L.rpad + L.roff[k][j + 1]].cpu().numpy()
-                ca = self.col_full[c][k * self.cap:(k + 1) * self.cap].cpu().numpy()
-                va = self.val_full[c][k * self.cap:(k + 1) * self.cap].cpu().numpy()
+                ca = self.col_full[c][self._arena_base(k):].cpu().numpy()
+                va = self.val_full[c][self._arena_base(k):].cpu().numpy()
                 for rr in range(hi - lo):
                     a0, n = int(rs[rr]), int(cnt[rr])
                     cols.append(ca[a0:a0 + n])
@@ -388,6 +452,70 @@ class CudaShard:
 
     def count_shard(self, rpad: int) -> torch.Tensor:
         return self._padded(self.state.row_count[self.state.cur], rpad)
+
+    def csr_nnz(self) -> Dict[int, int]:
+        """Used CSR entries per width class: one device reduction, one synchronisation."""
+        st, widths = self.state, self.layout.widths
+        if not hasattr(self, "_wrow"):
+            w = np.concatenate([np.full(st.shapes[i][0], widths.index(st.shapes[i][1]), np.int64)
+                                for i in st.order])
+            self._wrow = torch.from_numpy(w).to(self.device)
+        cnt = st.row_count[st.cur][:self._wrow.numel()].to(torch.float64)
+        tot = torch.bincount(self._wrow, weights=cnt, minlength=len(widths)).tolist()
+        return {c: int(tot[j]) for j, c in enumerate(widths)}
+
+    def pack_csr(self, pcap: Dict[int, int], base: Dict[int, int], rp_pad: int):
+        """The used entries of every width class packed densely (a qftc_csr_pack plan: three
+        launches for all classes) and the packed row starts + base[class], in the row-start
+        layout of rowstart_shard.  Returns (row starts [rp_pad], {class: (col, val)})."""
+        from . import _native as N
+        st, widths = self.state, self.layout.widths
+        nw = len(widths)
+        if getattr(self, "_pack_plan", None) is None:
+            segs = (N.PackSegmentC * max(1, st.n))()
+            for p, i in enumerate(st.order):          # flat positions of the row arrays
+                r, c = st.shapes[i]
+                segs[p].rows, segs[p].width = r, widths.index(c)
+                segs[p].rs_off, segs[p].cnt_off = int(st.rpoff[p]), int(st.roff[p])
+            plan = C.c_void_p()
+            N.check(N.lib.qftc_csr_pack_plan_create(C.byref(plan), segs, st.n, nw, None))
+            self._pack_plan = plan
+            self._rs_out = torch.zeros(max(rp_pad, st.row_start[0].numel()), dtype=torch.int32,
+                                       device=self.device)
+            self._pk = {}
+        out = {}
+        for c in widths:
+            n = max(32, int(pcap.get(c, 0)))
+            if c not in self._pk or self._pk[c][0].numel() < n:
+                m = n + n // 4
+                self._pk[c] = (torch.empty(m, dtype=torch.int32, device=self.device),
+                               torch.empty(m, dtype=torch.float32, device=self.device))
+            out[c] = self._pk[c]
+        k = st.cur
+        grp = {g.cols: g for g in st.groups}
+        P = C.c_void_p * nw
+        col_in = P(*[(grp[c].col[k] if c in grp else out[c][0]).data_ptr() for c in widths])
+        val_in = P(*[(grp[c].val[k] if c in grp else out[c][1]).data_ptr() for c in widths])
+        col_out = P(*[out[c][0].data_ptr() for c in widths])
+        val_out = P(*[out[c][1].data_ptr() for c in widths])
+        bases = (C.c_int64 * nw)(*[int(base.get(c, 0)) for c in widths])
+        stream = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        N.check(N.lib.qftc_csr_pack_run(self._pack_plan, C.c_void_p(st.row_start[k].data_ptr()),
+                                        C.c_void_p(st.row_count[k].data_ptr()),
+                                        C.cast(col_in, C.c_void_p), C.cast(val_in, C.c_void_p),
+                                        C.cast(col_out, C.c_void_p),
+                                        C.cast(val_out, C.c_void_p), bases,
+                                        C.c_void_p(self._rs_out.data_ptr()), stream))
+        return self._rs_out[:rp_pad], out
+
+    def __del__(self):
+        plan = getattr(self, "_pack_plan", None)
+        if plan is not None:
+            try:
+                from . import _native as N
+                N.lib.qftc_csr_pack_plan_destroy(plan)
+            except Exception:
+                pass
 
     def arena(self, width: int, cap: int):
         g = next((g for g in self.state.groups if g.cols == width), None)

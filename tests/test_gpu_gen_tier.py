@@ -86,3 +86,47 @@ def test_gen_tier_equals_general_kernel(cuda, port, monkeypatch):
     for i in range(len(shapes)):
         for k in KEYS:
             _eq(res[0][i][k], res[1][i][k], f"tensor {i} {k}: GEN tier vs step_kernel")
+
+
+@pytest.mark.parametrize("route", ["1", "0"])
+def test_few_stable_rows_route_into_gen_list(cuda, port, monkeypatch, route):
+    """At a large lr most rows leave the stable tier; when fewer than 1/16 of the rows were
+    stable the step before, the step skips the stable launch and its stable rows run in the
+    GEN kernel (QFT_NO_ROUTE=1 keeps them in the stable kernel).  Bytes equal the oracle
+    either way."""
+    monkeypatch.setenv("QFT_NO_ROUTE", "0" if route == "1" else "1")
+    shapes = [(40, 4096), (13, 4096)]
+    bw, lr, wd = 8, 2.2e-4, 0.01
+    eng = cuda.QftModelState(shapes, bit_width=bw)
+    host, ora = [], []
+    for i, sh in enumerate(shapes):
+        w = port.synth(sh, 70 + i, 0.02, 0.005)
+        if i == 0:
+            w[:2] *= 20.0              # two rows with a coarse scale: stable at this lr
+        d = port.decompose_weight(w, 0.01, bw)
+        host.append(dict(codes=d.codes, scale=d.scale, zero_point=d.zero_point, t_min=d.t_min,
+                         t_max=d.t_max, row_ptr=d.row_ptr, col_idx=d.col_idx, values=d.values))
+        ora.append([d, port.quantize_state(np.zeros(sh, np.float32), bw)])
+    eng.init_from_host(host)
+    tiers = []
+    for step in range(4):
+        for i, sh in enumerate(shapes):
+            gq = port.quantize_state(port.synth(sh, 500 + 10 * step + i, 1e-3, 0.01), bw)
+            c, s_, z = eng.grad_views(i)
+            c.copy_(torch.from_numpy(gq[0]))
+            s_.copy_(torch.from_numpy(gq[1]))
+            z.copy_(torch.from_numpy(gq[2]))
+            d, m = ora[i]
+            ora[i] = list(port.lion_step_layer(d, *m, *gq, lr=lr, wd=wd)[:2])
+        eng.step(lr=lr, weight_decay=wd, check=True)
+        tiers.append(eng.tiers())
+        for i in range(len(shapes)):
+            got = eng.export_tensor(i)
+            d, m = ora[i]
+            for k, ref in zip(KEYS, (d.codes, d.row_ptr, d.col_idx, d.values, m[0], m[1], m[2])):
+                _eq(got[k], ref, f"route {route} step {step} tensor {i} {k}")
+    assert 0 < tiers[0][0] * 16 < sum(shapes[i][0] for i in range(2)), tiers
+    if route == "1":   # the first step had no history; later steps routed
+        assert all(t[0] == 0 for t in tiers[1:]), tiers
+    else:
+        assert all(t[0] > 0 for t in tiers), tiers

@@ -104,6 +104,17 @@ class OracleShard:
     def count_shard(self, rpad):
         return self.counts[:rpad]
 
+    def csr_nnz(self):
+        return dict(self.nnz)
+
+    def pack_csr(self, pcap, base, rp_pad):
+        """A strict CSR is already packed: the row starts only move by base[class]."""
+        L, k = self.layout, self.rank
+        rs = self.rowstart.clone()
+        for j, (i, lo, hi) in enumerate(self.mem):
+            rs[L.rpoff[k][j]:L.rpoff[k][j + 1]] += int(base[L.shapes[i][1]])
+        return rs[:rp_pad], {c: self.arena(c, max(pcap[c], 1)) for c in L.widths}
+
     def arena(self, width, cap):
         col, val = self.arenas[width]
         oc = torch.zeros(cap, dtype=torch.int32)
@@ -118,7 +129,7 @@ def _grad(shape, seed, rank):
     return (rng.integers(-2**18, 2**18, size=shape).astype(np.float64) * 2.0**-24).astype(np.float32)
 
 
-def _worker(rank, world, port_no, q):
+def _worker(rank, world, port_no, q, packed=True):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port_no))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -129,7 +140,9 @@ def _worker(rank, world, port_no, q):
                   for i, s in enumerate(SHAPES)]
         full_m = [port.quantize_state(np.zeros(s, np.float32), BW) for s in SHAPES]
         layout = ShardLayout(SHAPES, world)
-        z = Zero1QftLion(SHAPES, OracleShard(layout, rank, port, full_w, full_m))
+        z = Zero1QftLion(SHAPES, OracleShard(layout, rank, port, full_w, full_m),
+                         packed_csr=packed)
+        assert z.packed == packed
         ref_w, ref_m = list(full_w), list(full_m)
         for step in range(3):
             mine = [torch.from_numpy(_grad(s, 100 * step + i, rank)) for i, s in enumerate(SHAPES)]
@@ -144,6 +157,12 @@ def _worker(rank, world, port_no, q):
                 for key in ("codes", "row_ptr", "col_idx", "values"):
                     a, b = got[key], getattr(ref_w[i], key)
                     assert a.shape == b.shape and np.array_equal(a, b), (step, i, key)
+            if packed:   # only used entries travel: the largest rank's nnz, 32-aligned
+                mine_nnz = z.local.csr_nnz()
+                for c in layout.widths:
+                    assert z.pcap[c] % 32 == 0 and mine_nnz[c] <= z.pcap[c]
+                assert z.gather_bytes_per_rank() < layout.pad + 4 * (layout.rp_pad + layout.rpad) \
+                    + 8 * z.cap * len(layout.widths)
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover - reported to the parent
         import traceback
@@ -152,11 +171,14 @@ def _worker(rank, world, port_no, q):
         dist.destroy_process_group()
 
 
-def test_zero1_two_ranks_gloo():
+@pytest.mark.parametrize("packed", [True, False])
+def test_zero1_two_ranks_gloo(packed):
+    """packed: only the used CSR entries are all-gathered (row starts re-based per rank);
+    not packed: the whole slotted arenas at a rank-uniform capacity."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port_no = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port_no, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port_no, q, packed)) for r in range(2)]
     for p in procs:
         p.start()
     results = dict(q.get(timeout=300) for _ in procs)
@@ -212,7 +234,7 @@ def _overflow_worker(rank, world, port_no, q):
         full_m = [port.quantize_state(np.zeros(s, np.float32), BW) for s in SHAPES]
         layout = ShardLayout(SHAPES, world)
         local = _OverflowingShard(layout, rank, port, full_w, full_m)
-        z = Zero1QftLion(SHAPES, local)
+        z = Zero1QftLion(SHAPES, local, packed_csr=False)
         cap0 = z.cap
         ref_w, ref_m = list(full_w), list(full_m)
         for step in range(2):
