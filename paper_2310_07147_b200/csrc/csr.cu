@@ -123,7 +123,8 @@ cudaError_t csr_row_ptr(const int32_t* counts, int rows, int32_t* row_ptr, cudaS
 // counts at cnt_off) are cut into chunks of <= PACK_T rows, ordered by width class, then
 // segment.  Per run: the used entries of every chunk (one CTA per chunk), an exclusive scan
 // of the chunk totals (cub), and the pack (one CTA per chunk: a block scan of its rows'
-// used counts -> row starts + base, the entries copied one warp per row).
+// used counts -> row starts + base; the chunk's entries are one contiguous output range,
+// copied with consecutive threads on consecutive entries).
 constexpr int PACK_T = 256;
 
 struct PackChunk {
@@ -161,7 +162,7 @@ __global__ void __launch_bounds__(PACK_T) k_pack_chunks(const PackChunk* __restr
                                                          PackWidths P,
                                                          int32_t* __restrict__ rs_out_all) {
   __shared__ int wsum[PACK_T / 32];
-  __shared__ int r_src[PACK_T], r_dst[PACK_T], r_n[PACK_T];
+  __shared__ int r_src[PACK_T], r_dst[PACK_T], s_total;
   const PackChunk c = ch[blockIdx.x];
   const int w = c.flags & 0xFF;
   const int32_t* rs = rs_all + c.rs_off;
@@ -189,19 +190,22 @@ __global__ void __launch_bounds__(PACK_T) k_pack_chunks(const PackChunk* __restr
   if (tid < c.rows) rs_out[tid] = (int32_t)(base + excl);
   if ((c.flags & 0x100) && tid == PACK_T - 1) rs_out[c.rows] = (int32_t)(base + excl + n);
   r_src[tid] = src;
-  r_dst[tid] = excl;
-  r_n[tid] = n;
+  r_dst[tid] = excl - off;  // the row's first entry within the chunk's output range
+  if (tid == PACK_T - 1) s_total = excl + n - off;
   __syncthreads();
   const int32_t* col_in = P.col_in[w];
   const float* val_in = P.val_in[w];
-  int32_t* col_out = P.col_out[w];
-  float* val_out = P.val_out[w];
-  for (int i = wid; i < c.rows; i += PACK_T / 32) {
-    const int s0 = r_src[i], d0 = r_dst[i], m = r_n[i];
-    for (int e = lane; e < m; e += 32) {
-      col_out[d0 + e] = __ldcs(col_in + s0 + e);
-      val_out[d0 + e] = __ldcs(val_in + s0 + e);
-    }
+  int32_t* col_out = P.col_out[w] + off;
+  float* val_out = P.val_out[w] + off;
+  // the chunk's output is one contiguous range: thread tid writes entries tid, tid+256, ...
+  // (coalesced), finding each entry's row with a cursor that only moves forward
+  const int total = s_total;
+  int row = 0;
+  for (int e = tid; e < total; e += PACK_T) {
+    while (row + 1 < c.rows && r_dst[row + 1] <= e) ++row;
+    const int src_e = r_src[row] + (e - r_dst[row]);
+    col_out[e] = __ldcs(col_in + src_e);
+    val_out[e] = __ldcs(val_in + src_e);
   }
 }
 

@@ -8,23 +8,24 @@
 // cores read is exactly RNE(reconstruct(W)) -- the bytes qftc_expand(bf16) would write --
 // but it never exists in HBM: W streams as 1 byte per element instead of 2.
 //
-// sm_100a, one 256 x 256 output tile per CTA, K in blocks of 64:
-//   warp 0 (lane 0)  TMA: the X tile (256 x 64 bf16, SWIZZLE_128B) of a K block into a
-//                    stage of the X / W-operand ring (3 stages, mbarrier tx)
-//   warp 3 (lane 0)  TMA: the W code tile (256 x 64 u8) into its own 2-stage ring
-//   warps 4-19       the dequant producers: a thread pair owns W row n0 + j, each thread
+// sm_100a, one 512 x 128 output tile per CTA (DQ_BN=128: 4 accumulators; DQ_BN=256 gives
+// 256 x 256 with 2), K in blocks of 64:
+//   warp 0 (lane 0)  TMA: the X tile (512 x 64 bf16, two 256-row boxes, SWIZZLE_128B) of a
+//                    K block into a stage of the X / W-operand ring (2 stages, mbarrier tx)
+//   warp 3 (lane 0)  TMA: the W code tile (128 x 64 u8) into its own 4-stage ring
+//   warps 4-11       the dequant producers: a thread pair owns W row n0 + j, each thread
 //                    32 columns of a block: its codes of
 //                    the stage -> s*(q-z) (fp32, one rounding, quantize.hpp:209) -> its
 //                    CSR outliers in [k0, k0+64) overwrite their positions -> bf16 (RNE)
 //                    -> the K-major SWIZZLE_128B layout tcgen05 reads; fence.proxy.async;
 //                    one arrive per warp.  Each keeps a cursor into its row's CSR slot
 //                    (columns ascending), so the outliers cost O(nnz) per row in total.
-//   warp 1 (lane 0)  tcgen05.mma.cta_group::1.kind::f16, M=128, N=256, K=16 x 4 per block
-//                    for each of the two 128-row halves (both read the same dequantized W
-//                    operand: each dequantized element feeds 2 x 128 rows of MMA), into
-//                    two TMEM accumulators (fp32); tcgen05.commit frees the stage
-//   warps 4-19       the epilogue after the last block: tcgen05.ld 32x32b -> bf16 -> HBM
-//   warp 2           TMEM allocation (512 columns: both accumulators) and release
+//   warp 1 (lane 0)  tcgen05.mma.cta_group::1.kind::f16, M=128, N=128, K=16 x 4 per block
+//                    for each of the four 128-row blocks of X (all read the same
+//                    dequantized W operand: each dequantized element feeds 4 x 128 rows of
+//                    MMA), into four TMEM accumulators (fp32); tcgen05.commit frees the stage
+//   warps 4-11       the epilogue after the last block: tcgen05.ld 32x32b -> bf16 -> HBM
+//   warp 2           TMEM allocation (512 columns: the accumulators) and release
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -44,8 +45,12 @@ using namespace qftd;
 #define DQ_NOFENCE 0
 #endif
 namespace dq {
-constexpr int BM = 256;     // output rows (X rows) per CTA: two M=128 accumulators
-constexpr int BN = 256;     // output columns (W rows) per CTA: UMMA N = 256
+#ifndef DQ_BN
+#define DQ_BN 128
+#endif
+constexpr int BN = DQ_BN;          // output columns (W rows) per CTA: UMMA N
+constexpr int NACC = 512 / BN;     // M=128 accumulators: all 512 TMEM columns
+constexpr int BM = 128 * NACC;     // output rows (X rows) per CTA
 constexpr int BK = 64;      // K per block: 128 bytes of bf16 = one SWIZZLE_128B row
 #ifndef DQ_STAGES
 #define DQ_STAGES 2
@@ -55,11 +60,16 @@ constexpr int BK = 64;      // K per block: 128 bytes of bf16 = one SWIZZLE_128B
 #endif
 constexpr int STAGES = DQ_STAGES;    // X / W-operand ring
 constexpr int CSTAGES = DQ_CSTAGES;  // W-code ring
-constexpr int A_BYTES = BM * BK * 2;  // 32 KB (two 128-row halves)
-constexpr int B_BYTES = BN * BK * 2;  // 32 KB
-constexpr int C_BYTES = BN * BK;      // 16 KB of codes
+constexpr int A_BYTES = BM * BK * 2;  // NACC 128-row blocks of 16 KB
+constexpr int B_BYTES = BN * BK * 2;
+constexpr int C_BYTES = BN * BK;      // codes
 constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + CSTAGES * C_BYTES + 1024;
-constexpr int HALVES = 2;             // producer threads per W row (32 columns each)
+#ifndef DQ_HALVES
+#define DQ_HALVES 2
+#endif
+constexpr int HALVES = DQ_HALVES;     // producer threads per W row
+constexpr int CPT = BK / HALVES;      // columns of a K block per producer thread
+constexpr int NQ = CPT / 16;          // 16-code vectors per producer thread and block
 constexpr int NPW = BN * HALVES / 32; // producer warps
 constexpr int NT = 128 + BN * HALVES; // TMA (X), MMA, TMEM, TMA (codes) warps + producers
 
@@ -73,7 +83,8 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
 // instruction descriptor: D f32, A/B bf16, both K-major, N = BN, M = 128 (per accumulator)
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                            ((uint32_t)(128 >> 4) << 24);
-constexpr int TMEM_COLS = 2 * BN;  // two fp32 accumulators of BN columns
+constexpr int TMEM_COLS = NACC * BN;  // NACC fp32 accumulators of BN columns (512)
+constexpr int XBOX = BM < 256 ? BM : 256;  // TMA box rows (<= 256): BM / XBOX loads per X tile
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
                                             uint64_t* bar) {
@@ -171,7 +182,9 @@ __global__ void __launch_bounds__(dq::NT, 1)
         const int s = kb % STAGES;
         mbar_wait(&empty_ab[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
         mbar_arrive_expect_tx(&full_a[s], (uint32_t)A_BYTES);
-        tma_load_2d(a_tile(s), &tm_x, kb * BK, m0, &full_a[s]);
+#pragma unroll
+        for (int xb = 0; xb < BM / XBOX; ++xb)
+          tma_load_2d(a_tile(s) + xb * XBOX * 128, &tm_x, kb * BK, m0 + xb * XBOX, &full_a[s]);
       }
     }
   } else if (warp == 3) {
@@ -193,11 +206,12 @@ __global__ void __launch_bounds__(dq::NT, 1)
         tc_after_sync();
         const uint32_t sa = smem_u32(a_tile(s)), sb = smem_u32(b_tile(s));
 #pragma unroll
-        for (int kk = 0; kk < BK / 16; ++kk) {  // both 128-row halves share the W operand
+        for (int kk = 0; kk < BK / 16; ++kk) {  // every 128-row block shares the W operand
           const uint64_t bd = sw128_desc(sb + 32 * kk);
           const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
-          mma_bf16(tmem_d, sw128_desc(sa + 32 * kk), bd, IDESC, acc);
-          mma_bf16(tmem_d + BN, sw128_desc(sa + 128 * 128 + 32 * kk), bd, IDESC, acc);
+#pragma unroll
+          for (int ab = 0; ab < NACC; ++ab)
+            mma_bf16(tmem_d + ab * BN, sw128_desc(sa + ab * 128 * 128 + 32 * kk), bd, IDESC, acc);
         }
         mma_commit(&empty_ab[s]);  // the X / W-operand stage is free once these MMAs read it
       }
@@ -252,10 +266,10 @@ __global__ void __launch_bounds__(dq::NT, 1)
       if (lane == 0) mbar_arrive(&full_b[s]);
       continue;
 #endif
-      const uint4* cr = reinterpret_cast<const uint4*>(c_tile(c) + j * BK + 32 * hf);
-      uint4 q4[2];
+      const uint4* cr = reinterpret_cast<const uint4*>(c_tile(c) + j * BK + CPT * hf);
+      uint4 q4[NQ];
 #pragma unroll
-      for (int c4 = 0; c4 < 2; ++c4) q4[c4] = live ? cr[c4] : make_uint4(0, 0, 0, 0);
+      for (int c4 = 0; c4 < NQ; ++c4) q4[c4] = live ? cr[c4] : make_uint4(0, 0, 0, 0);
       // generic-proxy reads of the slot, then the TMA (async proxy) refills it: order them
       fence_proxy_async();
       __syncwarp();
@@ -265,10 +279,10 @@ __global__ void __launch_bounds__(dq::NT, 1)
       uint8_t* bt = b_tile(s) + j * 128;
       // 32 codes -> 4 swizzled 16-byte chunks of bf16: the row's branch (fast magic-number
       // dequant, or the exact form for |z| >= 2^22) is taken once per block
-      uint32_t pk[2][8];
+      uint32_t pk[NQ][8];
       if (fast) {
 #pragma unroll
-        for (int c4 = 0; c4 < 2; ++c4) {
+        for (int c4 = 0; c4 < NQ; ++c4) {
           const uint32_t w4[4] = {q4[c4].x, q4[c4].y, q4[c4].z, q4[c4].w};
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
@@ -282,7 +296,7 @@ __global__ void __launch_bounds__(dq::NT, 1)
         }
       } else {
 #pragma unroll
-        for (int c4 = 0; c4 < 2; ++c4) {
+        for (int c4 = 0; c4 < NQ; ++c4) {
           const uint32_t w4[4] = {q4[c4].x, q4[c4].y, q4[c4].z, q4[c4].w};
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
@@ -295,8 +309,8 @@ __global__ void __launch_bounds__(dq::NT, 1)
         }
       }
 #pragma unroll
-      for (int c4 = 0; c4 < 2; ++c4) {
-        const int c0 = 4 * hf + 2 * c4, c1 = c0 + 1;  // 8 bf16 per 16-byte chunk
+      for (int c4 = 0; c4 < NQ; ++c4) {
+        const int c0 = (CPT / 8) * hf + 2 * c4, c1 = c0 + 1;  // 8 bf16 per 16-byte chunk
         *reinterpret_cast<uint4*>(bt + ((c0 ^ (j & 7)) << 4)) =
             make_uint4(pk[c4][0], pk[c4][1], pk[c4][2], pk[c4][3]);
         *reinterpret_cast<uint4*>(bt + ((c1 ^ (j & 7)) << 4)) =
@@ -304,7 +318,7 @@ __global__ void __launch_bounds__(dq::NT, 1)
       }
       // the row's outliers in this K block overwrite their positions with their exact
       // fp32 values (RNE to bf16)
-      const int k0 = kb * BK + 32 * hf;  // this thread's half of the block
+      const int k0 = kb * BK + CPT * hf;  // this thread's part of the block
       // (the other half's entries below it are skipped: they belong to the other thread)
       while (oc0 < k0) {
         oc0 = oc1; ov0 = ov1;
@@ -312,7 +326,7 @@ __global__ void __launch_bounds__(dq::NT, 1)
         oc2 = oc3; ov2 = ov3;
         fetch(oc3, ov3);
       }
-      while (oc0 < k0 + 32) {
+      while (oc0 < k0 + CPT) {
         const int k = oc0 - kb * BK;
         const uint32_t h = pack_bf16(ov0, 0.0f) & 0xFFFFu;
         *reinterpret_cast<uint16_t*>(bt + ((((k >> 3) ^ (j & 7)) << 4) | ((k & 7) << 1))) = (uint16_t)h;
@@ -331,14 +345,15 @@ __global__ void __launch_bounds__(dq::NT, 1)
     // half (warp-4)/4 of the tile
     mbar_wait(&acc_full, 0u);
     tc_after_sync();
-    // warp (4 + 4g + q) drains TMEM lanes 32q.. of group g: accumulator g >> 1 (rows
-    // m0 + 128 (g >> 1) ..), columns half g & 1
+    // warp (4 + 4g + q) drains TMEM lanes 32q.. for warp group g: the (accumulator,
+    // 32-column chunk) units g, g + NPW/4, ... (accumulator a: rows m0 + 128a ..)
     const int wq = (warp - 4) & 3, grp = (warp - 4) >> 2;
-    const int accn = grp >> 1, chalf = grp & 1;
-    const int row = m0 + 128 * accn + 32 * wq + lane;
     const uint32_t lane_base = (uint32_t)(32 * wq) << 16;
+    constexpr int CH = BN / 32, GROUPS = NPW / 4;
 #pragma unroll 1
-    for (int c0 = chalf * (BN / 2); c0 < (chalf + 1) * (BN / 2); c0 += 32) {
+    for (int u = grp; u < NACC * CH; u += GROUPS) {
+      const int accn = u / CH, c0 = (u % CH) * 32;
+      const int row = m0 + 128 * accn + 32 * wq + lane;
       uint32_t r[32];
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
@@ -402,7 +417,7 @@ cudaError_t launch_dq_gemm(const void* x, int M, int K, const uint8_t* codes, in
   {
     const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
     const cuuint64_t strides[1] = {(cuuint64_t)K * 2};
-    const cuuint32_t box[2] = {BK, BM};
+    const cuuint32_t box[2] = {BK, XBOX};
     const cuuint32_t es[2] = {1, 1};
     if (enc(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

@@ -56,9 +56,29 @@ __device__ __forceinline__ void unpack(const uint4& q, float* x) {
 // stored.  The row's serial part (thread 0: the fp64 affine params, FMA-proven fast divide
 // or the reference formula) overlaps the other threads' quantization; a row costs ONE
 // barrier, and the row is read from HBM once.
-// Quantization: the clamped fast quantizer with its tie proof per group of 4 elements, the
-// reference's fp64 formula for a group near a tie (quantize.hpp:160-166).
+// Quantization: the fast quantizer (range-proven, no clamp: gq_quant4) with its tie proof
+// per group of 4 elements, the reference's fp64 formula for a group near a tie
+// (quantize.hpp:160-166).
 constexpr int GQ_NS = 4;  // ring stages
+#ifndef QFT_GQ_NOCLAMP
+#define QFT_GQ_NOCLAMP 1
+#endif
+
+// The fast quantizer of a value of the row's own [lo, hi] range.  The clamp to the code
+// range is provably unnecessary (QFT_GQ_NOCLAMP): with s = the fp32 scale and z the zero
+// point of affine_params_from_bounds(lo, hi), every x in [lo, hi] has x/s in
+// [-z - 0.5 - d, qmax - z + 0.5 + d], d <= (qmax + |z| + 1) * 2^-23.9 (the fp32 rounding of
+// s and the +-0.5 of z's rounding), so a value whose nearest integer lies outside the code
+// range sits within d + (the product's error) of a half-integer: its tie check
+// (|y - rint(y)| < 0.5 - (qmax + |z| + 2) * 2^-21) fails and it takes the exact formula,
+// which clips.  NaN propagates into the check (max.NaN) and takes the exact path too.
+__device__ __forceinline__ uint32_t gq_quant4(const float* x, const QuantRow& q, float& em) {
+#if QFT_GQ_NOCLAMP
+  return quant4_e(x, q, em);
+#else
+  return quant4_fast(x, q, em);
+#endif
+}
 
 template <bool BF16, int NT, int VPL>
 __global__ void __launch_bounds__(NT + 32) k_grad_quant(const LaunchArgs a, int stage_bytes) {
@@ -122,8 +142,8 @@ __global__ void __launch_bounds__(NT + 32) k_grad_quant(const LaunchArgs a, int 
 #pragma unroll
         for (int k = 0; k < EPV / 4; ++k) {
           float em = 0.0f;
-          c[k] = q.fast ? quant4_fast(x + 4 * k, q, em) : 0u;
-          if (!q.fast || !(em < q.thr)) c[k] = quant4_exact(x + 4 * k, q);
+          c[k] = q.fast ? gq_quant4(x + 4 * k, q, em) : 0u;
+          if (!q.fast || !(em < q.thr)) c[k] = quant4_exact_fast(x + 4 * k, q);
         }
         if constexpr (BF16)
           __stcs(reinterpret_cast<uint2*>(dst) + i, make_uint2(c[0], c[1]));
@@ -352,8 +372,8 @@ __global__ void __launch_bounds__(NT) k_rs_grad_quant(const LaunchArgs a, const 
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
           float em = 0.0f;
-          c[k] = q.fast ? quant4_fast(sum[j] + 4 * k, q, em) : 0u;
-          if (!q.fast || !(em < q.thr)) c[k] = quant4_exact(sum[j] + 4 * k, q);
+          c[k] = q.fast ? gq_quant4(sum[j] + 4 * k, q, em) : 0u;
+          if (!q.fast || !(em < q.thr)) c[k] = quant4_exact_fast(sum[j] + 4 * k, q);
         }
         __stcs(reinterpret_cast<uint2*>(dst) + i, make_uint2(c[0], c[1]));
       }

@@ -223,13 +223,16 @@ __device__ __forceinline__ float2 gen_lion(float2 w, float2 d, const Hyper& h, u
   return sadd2(w, neg2(upd));
 }
 
-// A GEN-tier vector whose fast quantization came near a tie: every code of the 16 by the
-// reference's fp64 formula (out of line: rare)
+// A GEN-tier vector whose fast quantization came near a tie: every code of the 16 exactly
+// (quant_exact32: the fp32 tie decision; out of line: rare)
 __device__ __noinline__ void gen_vec_exact(uint4 cw, uint4 cm, uint4 cg, const RowPrep& R,
                                            const Hyper& h, int bw, uint32_t* cq,
                                            uint32_t& mask) {
   const int qmax = (1 << bw) - 1;
   const uint32_t zpay = (R.info >> 8) & 0xFFu;
+  const float inv = __frcp_rn(R.sw);
+  const float lim = fmaxf(fabsf((float)R.zw), fabsf((float)(qmax - R.zw))) + 2.0f;
+  const bool x32 = R.sw >= 0x1.0p-100f && R.sw <= 0x1.0p125f && lim < 1048576.0f;
   const uint32_t ww[4] = {cw.x, cw.y, cw.z, cw.w};
   const uint32_t mw[4] = {cm.x, cm.y, cm.z, cm.w};
   const uint32_t gw[4] = {cg.x, cg.y, cg.z, cg.w};
@@ -243,7 +246,12 @@ __device__ __noinline__ void gen_vec_exact(uint4 cw, uint4 cm, uint4 cg, const R
       lion1(w, m, g, h);
       const bool o = (w < R.tmin) || (w > R.tmax);
       if (o) mask |= 1u << (4 * i + e);
+#if QFT_EXACT32
+      c |= (o ? zpay : (x32 ? quant_exact32(w, R.sw, inv, R.zw, qmax)
+                            : quant_exact(w, R.sw, R.zw, qmax))) << (8 * e);
+#else
       c |= (o ? zpay : quant_exact(w, R.sw, R.zw, qmax)) << (8 * e);
+#endif
     }
     cq[i] = c;
   }

@@ -47,6 +47,8 @@ class _Group:
     col: List[Optional[torch.Tensor]]
     val: List[Optional[torch.Tensor]]
     plan: Optional[C.c_void_p] = None
+    replans: int = 0          # slot re-plans so far: each widens the headroom (_replan)
+    layout_idx: Optional[tuple] = None   # cached (rs positions, scan index, contiguous)
 
 
 class QftModelState:
@@ -478,22 +480,57 @@ class QftModelState:
         """Slots of set k re-sized from its (true) counts plus, as at placement
         (_place_strict), the dense elements at code 0 / qmax of the step's output codes:
         only those can become new outliers in a stable-tier step, so the padding keeps the
-        no-overflow guarantee of the placement after a replan."""
-        base = 0
+        no-overflow guarantee of the placement after a replan.  Rows that overflow are
+        drifting (a large lr moves codes every step), so a re-planned slot also holds 8
+        steps of the row's last growth (its count minus the step's input count), and
+        every re-plan of the group widens the headroom -- count/4 more per level, the
+        slack 8 -> 32 -> 64 entries -- instead of re-planning again the next step.  Batched over the group: one
+        row-count pass, one scan, one scatter into the slot starts, one synchronisation."""
         qmax = (1 << self.bit_width) - 1
-        for i in g.members:
-            r = self.shapes[i][0]
-            rs = self._rs(self.row_start[k], i)
-            total = C.c_int64(0)
-            codes = self._sl(self.w_codes[k], i)
-            edge = ((codes == 0) | (codes == qmax)).sum(dim=1, dtype=torch.int32)
-            want = self._rows(self.row_count[k], i) + edge
-            N.check(N.lib.qftc_csr_plan_slots(_p(want), None, r,
-                                              SLACK, _p(rs), C.byref(total), _stream()))
-            rs += base
-            base += int(total.value)
-        if g.col[k].numel() < base:
-            g.col[k], g.val[k] = self._alloc(base)
+        dev = self.device
+        if g.layout_idx is None:
+            pos, idx, rb = [], [], 0
+            for i in g.members:
+                r = self.shapes[i][0]
+                p0 = int(self.rpoff[self.pos[i]])
+                pos.append(torch.arange(p0, p0 + r + 1, dtype=torch.int64))
+                idx.append(torch.arange(rb, rb + r + 1, dtype=torch.int64))
+                rb += r
+            ps = [self.pos[i] for i in g.members]
+            contiguous = ps == list(range(ps[0], ps[0] + len(ps)))
+            g.layout_idx = (torch.cat(pos).to(dev), torch.cat(idx).to(dev), contiguous)
+        rs_pos, scan_idx, contiguous = g.layout_idx
+        if contiguous:   # the group's codes / counts are one [rows, cols] block
+            p0, p1 = self.pos[g.members[0]], self.pos[g.members[-1]] + 1
+            codes = self.w_codes[k][self.off[p0]:self.off[p1]].view(-1, g.cols)
+            want = self.row_count[k][self.roff[p0]:self.roff[p1]].to(torch.int64)
+            grow = (want - self.row_count[1 - k][self.roff[p0]:self.roff[p1]]).clamp_(min=0)
+            step = max(1, (1 << 28) // g.cols)     # bounded temporaries (~256 MB per pass)
+            for r0 in range(0, codes.shape[0], step):
+                c = codes[r0:r0 + step]
+                want[r0:r0 + step] += ((c == 0) | (c == qmax)).sum(dim=1, dtype=torch.int64)
+        else:
+            parts, gparts = [], []
+            for i in g.members:
+                codes = self._sl(self.w_codes[k], i)
+                edge = ((codes == 0) | (codes == qmax)).sum(dim=1, dtype=torch.int64)
+                cnt = self._rows(self.row_count[k], i).to(torch.int64)
+                gparts.append((cnt - self._rows(self.row_count[1 - k], i)).clamp_(min=0))
+                parts.append(cnt + edge)
+            want = torch.cat(parts)
+            grow = torch.cat(gparts)
+        lvl = min(g.replans, 3)
+        caps = want + want // 4 + 8 * grow + (want * lvl) // 4 + min(SLACK << (2 * lvl), 64)
+        caps = (caps + 3) & ~3                       # 16-byte aligned slots (TMA)
+        cum = torch.zeros(caps.numel() + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(caps, 0, out=cum[1:])
+        total = int(cum[-1].item())
+        if total >= 2 ** 31:
+            raise OverflowError(f"CSR arena of the {g.cols}-column group: {total} entries")
+        self.row_start[k].index_copy_(0, rs_pos, cum.index_select(0, scan_idx).to(torch.int32))
+        g.replans += 1
+        if g.col[k].numel() < total:
+            g.col[k], g.val[k] = self._alloc(total)
 
     def _check(self, flip, h):
         out = 1 - flip

@@ -103,7 +103,12 @@ def test_engine_every_rows_kernel_instance(cuda, port, monkeypatch, cols, bw, lr
             d, m = ora[i]
             ora[i] = list(port.lion_step_layer(d, *m, *gq, lr=lr)[:2])
         st.step(lr=lr, check=True)
-        assert st.kernel_names() == [INSTANCES[(cols, bw)]], st.kernel_names()
+        # at the large lr the 8-bit rows leave the stable tier: from the second step the
+        # few stable rows are routed into the GEN kernel of the same geometry
+        names = st.kernel_names()
+        assert names == [INSTANCES[(cols, bw)]] or (
+            step > 0 and len(names) == 1 and names[0].startswith("rows_kernel<") and
+            names[0].endswith(",gen>")), names
         stable_seen += st.tier_rows()[0]
         _compare(st, ora, f"{cols}x b{bw} lr {lr} step {step}")
     if lr < 1e-4:  # at 2.2e-4 the 8-bit rows fail the proof (lr > sw/2): general tier only

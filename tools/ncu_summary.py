@@ -1,44 +1,56 @@
-"""Summarise an ncu report of the step kernel: key metrics, opcode mix, hot blocks, stalls."""
-import csv, subprocess, sys
+"""Summarise an ncu --set full report: headline metrics, top stall reasons, and the
+executed-instruction mix by opcode (from the SASS source page)."""
+import csv
+import io
+import subprocess
+import sys
 from collections import Counter
+
 rep = sys.argv[1]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout.splitlines()
-rows = list(csv.reader(raw)); hdr = rows[0]; units = rows[1]; idx = {h: i for i, h in enumerate(hdr)}
-want = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
-        'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed', 'sm__throughput.avg.pct_of_peak_sustained_elapsed',
-        'smsp__issue_active.avg.pct_of_peak_sustained_active', 'sm__warps_active.avg.pct_of_peak_sustained_active',
-        'smsp__inst_executed.sum', 'launch__grid_size', 'launch__shared_mem_per_block_dynamic',
-        'launch__occupancy_limit_shared_mem', 'launch__registers_per_thread']
-stall_keys = [h for h in hdr if h.startswith('smsp__average_warp_latency_issue_stalled_') or
-              h.startswith('smsp__pcsamp_warps_issue_stalled_')]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                     text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+h = rows[0]
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+        "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+        "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+        "launch__shared_mem_per_block_dynamic", "launch__occupancy_limit_shared_mem",
+        "launch__occupancy_limit_registers"]
 for r in rows[2:]:
-    print("kernel", r[idx['Kernel Name']][:60])
-    for w in want:
-        if w in idx: print(f"  {w:60s} {r[idx[w]]} {units[idx[w]]}")
-    st = sorted(((float(r[idx[k]] or 0), k) for k in stall_keys if 'pcsamp' in k and not k.endswith('_not_issued')), reverse=True)[:8]
-    for v, k in st: print(f"  stall {k.replace('smsp__pcsamp_warps_issue_stalled_','')}: {v:.0f}")
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True, text=True).stdout.splitlines()
-rows = list(csv.reader(src)); hdr = rows[1]; idx = {h: i for i, h in enumerate(hdr)}
-data = []
-for r in rows[2:]:
-    if len(r) < len(hdr) or r[0].startswith('Kernel'): break
-    data.append(r)
-tot = sum(float(r[idx['Instructions Executed']] or 0) for r in data)
-cnt = Counter()
-for r in data:
-    t = r[idx['Source']].split()
-    if not t: continue
-    op = t[1] if t[0].startswith('@') else t[0]
-    cnt[op.split('.')[0]] += float(r[idx['Instructions Executed']] or 0)
-print("total warp-instr (first kernel)", tot)
-print("  ".join(f"{op}:{c/tot*100:.1f}%" for op, c in cnt.most_common(24)))
-ex = [float(r[idx['Instructions Executed']] or 0) for r in data]
-blocks = []; cur = None
-for i, e in enumerate(ex):
-    if cur and abs(e - cur[2]) <= 0.02 * max(e, 1): cur[1] = i; cur[3] += e
-    else:
-        if cur: blocks.append(cur)
-        cur = [i, i, e, e]
-blocks.append(cur); blocks.sort(key=lambda b: -b[3])
-for b in blocks[:int(sys.argv[2]) if len(sys.argv) > 2 else 12]:
-    print(f"  lines {b[0]}-{b[1]} ({b[1]-b[0]+1}) exec {b[2]:.3g} share {b[3]/tot*100:.1f}%  {data[b[0]][idx['Source']][:50]}")
+    d = dict(zip(h, r))
+    print("kernel", d.get("Kernel Name", "")[:120])
+    for k in KEYS:
+        print(f"  {k:60s} {d.get(k)}")
+    st = [(float(v.replace(",", "")) if v else 0.0, k) for k, v in d.items()
+          if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")]
+    for v, k in sorted(st, reverse=True)[:10]:
+        print(f"  stall {k.replace('smsp__pcsamp_warps_issue_stalled_', ''):40s} {v:.0f}")
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                     capture_output=True, text=True).stdout
+lines = list(csv.reader(io.StringIO(src)))
+hdr = None
+mix = Counter()
+tot = 0
+for ln in lines:
+    if "Source" in ln and "Instructions Executed" in ln:
+        hdr = ln
+        continue
+    if hdr is None or len(ln) != len(hdr):
+        continue
+    d = dict(zip(hdr, ln))
+    try:
+        n = float(d["Instructions Executed"].replace(",", ""))
+    except ValueError:
+        continue
+    op = d["Source"].strip().split()
+    if not op:
+        continue
+    o = op[0] if not op[0].startswith("@") else (op[1] if len(op) > 1 else op[0])
+    mix[o.split(".")[0]] += n
+    tot += n
+if tot:
+    print(f"  executed warp-instructions (source page) {tot:.4g}")
+    print("  " + "  ".join(f"{k}:{100 * v / tot:.1f}%" for k, v in mix.most_common(24)))
