@@ -941,6 +941,71 @@ def run_gemm(args):
                       "bf16_peak_tflops": peak_tf, "rows": out}), flush=True)
 
 
+def run_wgrad(args):
+    """the backward's weight gradient G = dy^T . x of a LLaMA-2-7B
+    layer's projections with the sink's quantize_state fused into the GEMM epilogue
+    (QftModelState.sink_wgrad -> qftc_wgrad_quant, tcgen05 + TMA, MN-major operands; the
+    fp32 gradient never reaches HBM), against the materialised path: cuBLAS bf16 GEMM with
+    fp32 output (torch.mm out_dtype=float32) + the quantize_state row kernel, and cuBLAS
+    alone.  Both the push (first micro-batch) and the accumulate form are timed."""
+    import torch
+    import paper_2310_07147_b200 as q
+    pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    peak_tf = float(pk.get("bf16_tflops", 2250.0))
+    tokens = 4096  # a micro-batch of 8 x 512 tokens
+    stream = torch.cuda.current_stream()
+    out = []
+    for name, (r, c) in (("q/k/v/o", (4096, 4096)), ("gate/up", (11008, 4096)),
+                         ("down", (4096, 11008))):
+        st = q.QftModelState([(r, c)], bit_width=BIT_WIDTH)
+        st.init_from_weights(lambda i: q.synth((r, c), 4242, 0.02, 0.005), FRACTION, "percentile")
+        dy = (torch.randn(tokens, r, device="cuda") * 1e-2).to(torch.bfloat16)
+        x = torch.randn(tokens, c, device="cuda").to(torch.bfloat16)
+        g = torch.empty((r, c), dtype=torch.float32, device="cuda")
+        codes, s, z = st.grad_views(0)
+
+        def timeit(fn, n=max(args.steps, 10)):
+            for _ in range(3):
+                fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(n):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1) / n
+
+        fused = timeit(lambda: st.sink_wgrad(0, dy, x))
+        fused_acc = timeit(lambda: st.sink_wgrad(0, dy, x, accumulate=True))
+
+        from paper_2310_07147_b200 import _native as NN
+        from paper_2310_07147_b200.quantize import _p, _stream
+
+        def materialised():  # no host synchronisation (check = 0), like the fused call
+            torch.mm(dy.t(), x, out_dtype=torch.float32, out=g)
+            NN.check(NN.lib.qftc_quantize_state(_p(g), r, c, BIT_WIDTH, _p(codes), _p(s), _p(z),
+                                                0, _stream()))
+
+        mat = timeit(materialised)
+        cublas = timeit(lambda: torch.mm(dy.t(), x, out_dtype=torch.float32, out=g))
+        flops = 2.0 * tokens * r * c
+        out.append({"proj": name, "out": r, "in": c, "tokens": tokens,
+                    "fused_ms": fused, "fused_tflops": flops / fused / 1e9,
+                    "fused_frac_of_bf16_peak": flops / fused / 1e9 / peak_tf,
+                    "fused_accumulate_ms": fused_acc,
+                    "cublas_f32_plus_quantize_state_ms": mat,
+                    "cublas_f32_only_ms": cublas, "cublas_tflops": flops / cublas / 1e9,
+                    "gradient_bytes_written_fused": r * c + 8 * r,
+                    "gradient_bytes_materialised": 4 * r * c + 4 * r * c + r * c + 8 * r})
+        del st, dy, x, g
+        torch.cuda.empty_cache()
+    print(json.dumps({"wgrad": "G = dy^T . x, quantize_state(G) (b=8) in the GEMM epilogue "
+                               "(tcgen05) vs cuBLAS f32-output GEMM + quantize_state kernel",
+                      "bf16_peak_tflops": peak_tf, "rows": out}), flush=True)
+
+
 def run_ckpt(args):
     """QFTC v1 checkpoint of the 7B state: the GPU CRC-32
     over every array of the file in file order (HBM-resident, ~13.8 GB), zlib.crc32 on
@@ -1016,7 +1081,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
-    ap.add_argument("--mode", default="step", choices=["step", "sweep", "13b", "ckpt", "gemm"])
+    ap.add_argument("--mode", default="step", choices=["step", "sweep", "13b", "ckpt", "gemm", "wgrad"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-side", action="store_true",
@@ -1047,6 +1112,8 @@ def main():
         run_ckpt(args)
     elif args.mode == "gemm":
         run_gemm(args)
+    elif args.mode == "wgrad":
+        run_wgrad(args)
     else:
         run_gpu_arm(args)
 

@@ -308,6 +308,25 @@ typedef struct qftc_expand_tensor {
 int qftc_expand(const qftc_expand_tensor* tensors, int n_tensors, int bf16,
                 qftc_stream_t stream);
 
+/* The backward's weight gradient with the sink fused into the GEMM epilogue (SURVEY.md
+ * §8(f) row 2; network.hpp:131-155 backward_core: wgrad = matmul(transpose(out_grad), in),
+ * then the sink gradflow.hpp:70-84).  G[out,in] = dy[tokens,out]^T . x[tokens,in] (bf16
+ * row-major activations, fp32 accumulation in TMEM) goes straight into the GradientStack
+ * entry (codes [out,in] u8, scale [out], zero_point [out]):
+ *   accumulate == 0: quantize_state(G, bit_width)                       (gradflow.hpp:77)
+ *   accumulate == 1: quantize_state(dequantize(entry) + G), in place    (accumulate, :52-58)
+ * The fp32 gradient never reaches HBM.  Optional: g_out [out,in] f32 receives the values
+ * that were quantized (G, or the sum), norm_sq (device double) += sum(G^2) (backward_core's
+ * norm, network.hpp:140).  workspace: qftc_wgrad_workspace_bytes(out) device bytes.
+ * in % 64 == 0, out % 8 == 0; dy, x, codes, g_out 16-byte aligned; a row may span at most
+ * one tile of 256 columns per SM (QFTC_ENOTSUP otherwise).  check != 0 synchronises and
+ * reports a NaN in column 0 as QFTC_EINVAL (the reference's min > max). */
+int64_t qftc_wgrad_workspace_bytes(int out_features);
+int qftc_wgrad_quant(const void* dy_bf16, const void* x_bf16, int tokens, int out_features,
+                     int in_features, int bit_width, int accumulate, uint8_t* codes, float* scale,
+                     int32_t* zero_point, float* g_out, double* norm_sq, void* workspace,
+                     int check, qftc_stream_t stream);
+
 /* The forward consumer's GEMM with the dequantization fused into its operand producer
  * (network.hpp:113-129 forward_core: matmul(cur, transpose(w))):
  * y[m,n] = x[m,k] . W^T for a dense-and-sparse weight W [n,k] (codes, per-row params,

@@ -416,6 +416,44 @@ int qftc_dequant_gemm(const void* x_bf16, int m, int k, const uint8_t* codes, in
   return QFTC_OK;
 }
 
+int64_t qftc_wgrad_workspace_bytes(int out_features) {
+  return out_features > 0 ? (int64_t)wgrad_workspace_bytes(out_features) : 0;
+}
+
+int qftc_wgrad_quant(const void* dy_bf16, const void* x_bf16, int tokens, int out_features,
+                     int in_features, int bit_width, int accumulate, uint8_t* codes, float* scale,
+                     int32_t* zero_point, float* g_out, double* norm_sq, void* workspace,
+                     int check, qftc_stream_t stream) {
+  if (tokens <= 0 || out_features <= 0 || in_features <= 0)
+    return fail(QFTC_EINVAL, "wgrad_quant: empty shape");
+  if (int rc = require_bit_width(bit_width)) return rc;
+  if (in_features % 64 != 0 || out_features % 8 != 0)
+    return fail(QFTC_ENOTSUP, "wgrad_quant: in_features % 64 and out_features % 8 must be 0");
+  if (!dy_bf16 || !x_bf16 || !codes || !scale || !zero_point || !workspace)
+    return fail(QFTC_EINVAL, "wgrad_quant: null pointer");
+  if (!al16(dy_bf16) || !al16(x_bf16) || !al16(codes) || (g_out && !al16(g_out)))
+    return fail(QFTC_EINVAL, "wgrad_quant: dy, x, codes and g_out must be 16-byte aligned");
+  if (int rc = require_device()) return rc;
+  static const uint32_t lbo = (uint32_t)(getenv("QFT_WG_LBO") ? atoi(getenv("QFT_WG_LBO")) : 0);
+  static const uint32_t sbo = (uint32_t)(getenv("QFT_WG_SBO") ? atoi(getenv("QFT_WG_SBO")) : 0);
+  cudaStream_t st = (cudaStream_t)stream;
+  const cudaError_t e = launch_wgrad_quant(dy_bf16, x_bf16, tokens, out_features, in_features,
+                                           bit_width, accumulate, codes, scale, zero_point, g_out,
+                                           norm_sq, workspace, lbo, sbo, st);
+  if (e == cudaErrorInvalidConfiguration)
+    return fail(QFTC_ENOTSUP, "wgrad_quant: a gradient row spans more tiles than SMs");
+  QFTC_CUDA(e, "wgrad_quant kernel");
+  if (check) {
+    const int64_t wb = (int64_t)wgrad_workspace_bytes(out_features);
+    uint32_t h = 0;
+    QFTC_CUDA(cudaMemcpyAsync(&h, reinterpret_cast<char*>(workspace) + wb - 4, 4,
+                              cudaMemcpyDeviceToHost, st), "copy");
+    QFTC_CUDA(cudaStreamSynchronize(st), "sync");
+    if (h) return fail(QFTC_EINVAL, "affine_params_from_bounds: min > max in a channel");
+  }
+  return QFTC_OK;
+}
+
 static int pack_impl(const uint8_t* src, int rows, int cols, int bits, uint8_t* dst,
                      bool unpack, qftc_stream_t stream) {
   if (int rc = require_shape(rows, cols, unpack ? "unpack_codes" : "pack_codes")) return rc;

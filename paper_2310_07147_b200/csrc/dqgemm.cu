@@ -34,6 +34,7 @@
 
 #include "qft_device.cuh"
 #include "qft_internal.h"
+#include "umma.cuh"
 
 namespace qftk {
 using namespace qftd;
@@ -45,6 +46,7 @@ using namespace qftd;
 #define DQ_NOFENCE 0
 #endif
 namespace dq {
+using namespace um;
 #ifndef DQ_BN
 #define DQ_BN 128
 #endif
@@ -73,54 +75,12 @@ constexpr int NQ = CPT / 16;          // 16-code vectors per producer thread and
 constexpr int NPW = BN * HALVES / 32; // producer warps
 constexpr int NT = 128 + BN * HALVES; // TMA (X), MMA, TMEM, TMA (codes) warps + producers
 
-// K-major SWIZZLE_128B smem descriptor (tcgen05 matrix descriptor): start >> 4,
-// leading byte offset 1 (unused for swizzled K-major), stride byte offset 1024 B between
-// 8-row groups, version 1, layout type 2 (SWIZZLE_128B)
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) | ((uint64_t)(1024 >> 4) << 32) |
-         ((uint64_t)1u << 46) | ((uint64_t)2u << 61);
-}
 // instruction descriptor: D f32, A/B bf16, both K-major, N = BN, M = 128 (per accumulator)
 constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
                            ((uint32_t)(128 >> 4) << 24);
 constexpr int TMEM_COLS = NACC * BN;  // NACC fp32 accumulators of BN columns (512)
 constexpr int XBOX = BM < 256 ? BM : 256;  // TMA box rows (<= 256): BM / XBOX loads per X tile
 
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, "
-      "{%2, %3}], [%4];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tc_after_sync() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_before_sync() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                         uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
-  uint32_t r;
-  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
-  return r;
-}
 }  // namespace dq
 
 struct DqArgs {
@@ -394,24 +354,12 @@ __global__ void __launch_bounds__(dq::NT, 1)
 }
 
 // ------------------------------------------------------------------ host side
-static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q{};
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
 cudaError_t launch_dq_gemm(const void* x, int M, int K, const uint8_t* codes, int N,
                            const float* scale, const int32_t* zp, const int32_t* row_start,
                            const int32_t* row_count, const int32_t* col, const float* val,
                            void* y, cudaStream_t st) {
   using namespace dq;
-  auto enc = encode_fn();
+  auto enc = um::encode_fn();
   if (!enc) return cudaErrorNotSupported;
   CUtensorMap tx{}, tw{};
   {

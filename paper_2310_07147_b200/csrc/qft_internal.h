@@ -236,6 +236,14 @@ cudaError_t launch_dq_gemm(const void* x, int M, int K, const uint8_t* codes, in
                            const float* scale, const int32_t* zp, const int32_t* row_start,
                            const int32_t* row_count, const int32_t* col, const float* val,
                            void* y, cudaStream_t s);
+// the backward weight gradient with the sink's quantization in the GEMM epilogue (wgrad.cu):
+// codes/scale/zp = quantize_state(dY^T . X [+ dequantize(entry)]); workspace: rows bounds,
+// counters and the error word (its last uint32)
+size_t wgrad_workspace_bytes(int O);
+cudaError_t launch_wgrad_quant(const void* dy, const void* x, int T, int O, int I, int bw,
+                               int accumulate, uint8_t* codes, float* scale, int32_t* zp,
+                               float* g_out, double* norm_sq, void* workspace, uint32_t lbo,
+                               uint32_t sbo, cudaStream_t st);
 // opt-in checkpoint format extensions (ckptext.cu)
 cudaError_t launch_pack_codes(const uint8_t* src, int rows, int cols, int bits, uint8_t* dst,
                               bool unpack, cudaStream_t s);

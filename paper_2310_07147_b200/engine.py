@@ -161,6 +161,33 @@ class QftModelState:
             N.check(N.lib.qftc_quantize_state(_p(g), r, c, self.bit_width, _p(codes), _p(s),
                                               _p(z), 1, _stream()))
 
+    def sink_wgrad(self, i: int, dy: torch.Tensor, x: torch.Tensor, accumulate: bool = False,
+                   norm_sq: Optional[torch.Tensor] = None, g_out: Optional[torch.Tensor] = None,
+                   check: bool = False):
+        """The backward's weight gradient of tensor i with the sink fused into the GEMM
+        epilogue (qftc_wgrad_quant; backward_core network.hpp:139 wgrad =
+        matmul(transpose(out_grad), in) -> gradflow.hpp:70-84): dy bf16 [T, rows], x bf16
+        [T, cols]; the stack entry receives quantize_state(dy^T x) (or, accumulating, the
+        integer-form sum) without an fp32 gradient in HBM.  norm_sq: a float64 device
+        scalar += sum of squares (backward_core's norm); g_out: the f32 values quantized."""
+        if self.grad_kind != N.GRAD_U8:
+            raise ValueError("sink_wgrad: the engine keeps raw gradients (grad kind f32/bf16)")
+        r, c = self.shapes[i]
+        for name, t, w in (("dy", dy, r), ("x", x, c)):
+            if t.dtype != torch.bfloat16 or t.dim() != 2 or t.shape[1] != w or not t.is_contiguous():
+                raise ValueError(f"sink_wgrad: {name} must be a contiguous bf16 [T, {w}] tensor")
+        if dy.shape[0] != x.shape[0]:
+            raise ValueError("sink_wgrad: dy and x must have the same number of rows (tokens)")
+        ws = getattr(self, "_wg_ws", None)
+        need = int(N.lib.qftc_wgrad_workspace_bytes(r))
+        if ws is None or ws.numel() < need:
+            ws = self._wg_ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        codes, s, z = self.grad_views(i)
+        N.check(N.lib.qftc_wgrad_quant(
+            _p(dy), _p(x), dy.shape[0], r, c, self.bit_width, int(bool(accumulate)), _p(codes),
+            _p(s), _p(z), _p(g_out) if g_out is not None else None,
+            _p(norm_sq) if norm_sq is not None else None, _p(ws), int(bool(check)), _stream()))
+
     # ------------------------------------------------------------------ arenas / slots
     def _alloc(self, cap: int):
         return (torch.empty(max(cap, 4), dtype=torch.int32, device=self.device),
