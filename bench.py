@@ -923,18 +923,27 @@ def run_gemm(args):
             return e0.elapsed_time(e1) / n
 
         fused = timeit(lambda: st.linear(0, x, out=y))
+        dy = (torch.randn(tokens, r, device="cuda") * 0.5).to(torch.bfloat16)
+        dx = torch.empty((tokens, c), dtype=torch.bfloat16, device="cuda")
+        fused_t = timeit(lambda: st.linear_backward(0, dy, out=dx))
         mat = timeit(lambda: (plan.run(), torch.matmul(x, wb.t(), out=y)))
         plan.run()
         cublas = timeit(lambda: torch.matmul(x, wb.t(), out=y))
+        mat_t = timeit(lambda: (plan.run(), torch.matmul(dy, wb, out=dx)))
+        cublas_t = timeit(lambda: torch.matmul(dy, wb, out=dx))
         flops = 2.0 * tokens * r * c
         out.append({"proj": name, "M": tokens, "N": r, "K": c,
                     "fused_ms": fused, "fused_tflops": flops / fused / 1e9,
                     "fused_frac_of_bf16_peak": flops / fused / 1e9 / peak_tf,
                     "expand_plus_cublas_ms": mat, "cublas_only_ms": cublas,
                     "cublas_tflops": flops / cublas / 1e9,
+                    "backward_dx_fused_ms": fused_t,
+                    "backward_dx_fused_tflops": flops / fused_t / 1e9,
+                    "backward_dx_expand_plus_cublas_ms": mat_t,
+                    "backward_dx_cublas_only_ms": cublas_t,
                     "weight_bytes_read_fused": r * c + 10 * st.nnz() + 16 * r,
                     "weight_bytes_materialised": 3 * r * c + 2 * r * c})
-        del st, x, wb, y, plan
+        del st, x, wb, y, plan, dy, dx
         torch.cuda.empty_cache()
     print(json.dumps({"gemm": "y = x . W^T, W dense-and-sparse (b=8, p=1%), x/y bf16, "
                               "fused dequant (tcgen05) vs expand + cuBLAS",

@@ -308,6 +308,22 @@ typedef struct qftc_expand_tensor {
 int qftc_expand(const qftc_expand_tensor* tensors, int n_tensors, int bf16,
                 qftc_stream_t stream);
 
+/* The backward's input gradient with the dequantization fused into the operand producer
+ * (backward weight operand; network.hpp:145 backward_core:
+ * in_grad = matmul(out_grad, w), w = reconstruct(W), gradflow.hpp:78): dx[tokens,in] =
+ * dy[tokens,out] . W for the dense-and-sparse W [out,in] (codes, per-row params, slotted CSR
+ * with row_count or strict with row_count = NULL), dy / dx bf16 row-major.  The tensor cores
+ * read bf16 RNE(reconstruct(W)) as an MN-major operand built in shared memory from the u8
+ * codes.  workspace: qftc_dequant_gemm_t_workspace_bytes(out, in) device bytes (a per-row,
+ * per-column-tile CSR index rebuilt by the call).  out % 64 == 0, in % 64 == 0; dy, codes, dx
+ * 16-byte aligned. */
+int64_t qftc_dequant_gemm_t_workspace_bytes(int out_features, int in_features);
+int qftc_dequant_gemm_t(const void* dy_bf16, int tokens, int out_features, const uint8_t* codes,
+                        int in_features, const float* scale, const int32_t* zero_point,
+                        const int32_t* row_start, const int32_t* row_count,
+                        const int32_t* col_idx, const float* values, void* dx_bf16,
+                        void* workspace, qftc_stream_t stream);
+
 /* The backward's weight gradient with the sink fused into the GEMM epilogue (SURVEY.md
  * §8(f) row 2; network.hpp:131-155 backward_core: wgrad = matmul(transpose(out_grad), in),
  * then the sink gradflow.hpp:70-84).  G[out,in] = dy[tokens,out]^T . x[tokens,in] (bf16

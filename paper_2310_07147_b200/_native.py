@@ -97,6 +97,8 @@ _SIGS = {
     "qftc_momentum_from_blocks": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "qftc_dequant_gemm": (_i, [_vp, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "qftc_wgrad_workspace_bytes": (_i64, [_i]),
+    "qftc_dequant_gemm_t_workspace_bytes": (_i64, [_i, _i]),
+    "qftc_dequant_gemm_t": (_i, [_vp, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "qftc_wgrad_quant": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp]),
     "qftc_expand_plan_create": (_i, [C.POINTER(_vp), C.POINTER(ExpandTensorC), _i, _i, _vp]),
     "qftc_expand_plan_run": (_i, [_vp, _vp]),

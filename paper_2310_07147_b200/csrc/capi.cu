@@ -416,6 +416,34 @@ int qftc_dequant_gemm(const void* x_bf16, int m, int k, const uint8_t* codes, in
   return QFTC_OK;
 }
 
+int64_t qftc_dequant_gemm_t_workspace_bytes(int out_features, int in_features) {
+  return out_features > 0 && in_features > 0
+             ? (int64_t)dq_gemm_t_workspace_bytes(out_features, in_features)
+             : 0;
+}
+
+int qftc_dequant_gemm_t(const void* dy_bf16, int tokens, int out_features, const uint8_t* codes,
+                        int in_features, const float* scale, const int32_t* zero_point,
+                        const int32_t* row_start, const int32_t* row_count,
+                        const int32_t* col_idx, const float* values, void* dx_bf16,
+                        void* workspace, qftc_stream_t stream) {
+  if (tokens <= 0 || out_features <= 0 || in_features <= 0)
+    return fail(QFTC_EINVAL, "dequant_gemm_t: empty shape");
+  if (out_features % 64 != 0 || in_features % 64 != 0)
+    return fail(QFTC_ENOTSUP, "dequant_gemm_t: out_features and in_features must be multiples of 64");
+  if (!dy_bf16 || !codes || !scale || !zero_point || !row_start || !col_idx || !values ||
+      !dx_bf16 || !workspace)
+    return fail(QFTC_EINVAL, "dequant_gemm_t: null pointer");
+  if (!al16(dy_bf16) || !al16(codes) || !al16(dx_bf16))
+    return fail(QFTC_EINVAL, "dequant_gemm_t: dy, codes and dx must be 16-byte aligned");
+  if (int rc = require_device()) return rc;
+  QFTC_CUDA(launch_dq_gemm_t(dy_bf16, tokens, out_features, codes, in_features, scale, zero_point,
+                             row_start, row_count, col_idx, values, dx_bf16, workspace,
+                             (cudaStream_t)stream),
+            "dequant_gemm_t kernel");
+  return QFTC_OK;
+}
+
 int64_t qftc_wgrad_workspace_bytes(int out_features) {
   return out_features > 0 ? (int64_t)wgrad_workspace_bytes(out_features) : 0;
 }

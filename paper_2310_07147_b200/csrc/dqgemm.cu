@@ -301,50 +301,10 @@ __global__ void __launch_bounds__(dq::NT, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&full_b[s]);
     }
-    // ---------------- epilogue: TMEM lanes 32*((warp-4)%4) .. +32 -> rows of Y, columns
-    // half (warp-4)/4 of the tile
+    // ---------------- epilogue: TMEM -> bf16 -> HBM
     mbar_wait(&acc_full, 0u);
     tc_after_sync();
-    // warp (4 + 4g + q) drains TMEM lanes 32q.. for warp group g: the (accumulator,
-    // 32-column chunk) units g, g + NPW/4, ... (accumulator a: rows m0 + 128a ..)
-    const int wq = (warp - 4) & 3, grp = (warp - 4) >> 2;
-    const uint32_t lane_base = (uint32_t)(32 * wq) << 16;
-    constexpr int CH = BN / 32, GROUPS = NPW / 4;
-#pragma unroll 1
-    for (int u = grp; u < NACC * CH; u += GROUPS) {
-      const int accn = u / CH, c0 = (u % CH) * 32;
-      const int row = m0 + 128 * accn + 32 * wq + lane;
-      uint32_t r[32];
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-          "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
-          "%28, %29, %30, %31}, [%32];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-            "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
-            "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-            "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
-            "=r"(r[31])
-          : "r"(tmem_d + lane_base + (uint32_t)(accn * BN + c0)));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (row < a.M) {
-        __nv_bfloat16* yr = a.y + (size_t)row * a.N + n0 + c0;
-        if (n0 + c0 + 32 <= a.N && (a.N % 8) == 0) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 o;
-            o.x = pack_bf16(__uint_as_float(r[8 * q]), __uint_as_float(r[8 * q + 1]));
-            o.y = pack_bf16(__uint_as_float(r[8 * q + 2]), __uint_as_float(r[8 * q + 3]));
-            o.z = pack_bf16(__uint_as_float(r[8 * q + 4]), __uint_as_float(r[8 * q + 5]));
-            o.w = pack_bf16(__uint_as_float(r[8 * q + 6]), __uint_as_float(r[8 * q + 7]));
-            reinterpret_cast<uint4*>(yr)[q] = o;
-          }
-        } else {
-          for (int e = 0; e < 32 && n0 + c0 + e < a.N; ++e)
-            yr[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
-        }
-      }
-    }
+    epilogue_bf16<BN, NACC, NPW>(tmem_d, warp, lane, m0, n0, a.M, a.N, a.y);
   }
   tc_before_sync();
   __syncthreads();

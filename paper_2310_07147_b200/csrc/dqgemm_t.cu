@@ -1,0 +1,324 @@
+// dqgemm_t.cu -- the backward's input gradient with the weight dequantization fused into
+// the GEMM's operand producer (the backward weight operand):
+// dX[T,I] = dY[T,O] . W, W a QFT dense-and-sparse weight [O,I] (u8 codes, per-row params,
+// CSR outliers).  The reference reconstructs W for the backward too (gradflow.hpp:78,
+// weight_at = reconstruct, quantize.hpp:331-338) and multiplies (network.hpp:145,
+// backward_core: in_grad = matmul(out_grad, w)); here the tensor cores read
+// RNE(reconstruct(W)) -- the bytes qftc_expand(bf16) writes -- built in shared memory from the
+// codes: W streams as 1 byte per element and never exists in HBM as bf16.
+//
+// The forward kernel (dqgemm.cu) reads W K-major (rows of W = output channels = N); here W's
+// rows are the REDUCTION dimension, so the operand is MN-major: a K block is 64 rows of W,
+// each contributing BN contiguous columns -- one 128-byte SWIZZLE_128B row per 64 columns.
+// A W row's CSR outliers inside the CTA's BN columns are located through a per-(row, column
+// tile) index built by a small pre-pass (k_csr_tile_index: the first slot entry at or past
+// each tile's first column), so a producer scans only the ~1-2 entries of its own window.
+//
+// sm_100a, one 512 x 128 output tile per CTA (four M=128 TMEM accumulators share each
+// dequantized W operand block), K in blocks of 64 W rows:
+//   warp 0 (lane 0)  TMA: the dY tile (512 x 64 bf16, K-major, SWIZZLE_128B) -> X/W ring
+//   warp 3 (lane 0)  TMA: the W code tile (64 rows x 128 columns u8) -> its own 4-stage ring
+//   warps 4-11       producers: thread (r, j, h) dequantizes W row k0 + r, columns
+//                    [64j + 32h, +32) of the tile -> 4 swizzled 16-byte chunks of row r of
+//                    the operand's MN chunk j; then its outliers; fence.proxy.async; arrive
+//   warp 1 (lane 0)  tcgen05.mma kind::f16, A K-major, B MN-major, M=128 x4, N=128, K=16 x4
+//   warps 4-11       the bf16 epilogue (umma.cuh)
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
+#include <cstdio>
+
+#include "qft_device.cuh"
+#include "qft_internal.h"
+#include "umma.cuh"
+
+namespace qftk {
+using namespace qftd;
+
+namespace dqt {
+using namespace um;
+constexpr int BN = 128;          // output columns (W columns) per CTA: UMMA N
+constexpr int NACC = 512 / BN;   // 4 accumulators of M = 128 (all 512 TMEM columns)
+constexpr int BM = 128 * NACC;   // output rows (tokens) per CTA
+constexpr int BK = 64;           // W rows per K block
+constexpr int STAGES = 2;        // dY / W-operand ring
+constexpr int CSTAGES = 4;       // W-code ring
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int B_BYTES = BN * BK * 2;  // BN/64 MN chunks of 64 x 64 bf16 (8 KB each)
+constexpr int C_BYTES = BN * BK;
+constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + CSTAGES * C_BYTES + 1024;
+constexpr int NPW = 8;                // producer warps
+constexpr int NT = 128 + 32 * NPW;
+constexpr int XBOX = 256;
+// D f32, A/B bf16, A K-major, B MN-major (bit 16), N = BN, M = 128
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
+                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+constexpr int TMEM_COLS = NACC * BN;
+constexpr uint32_t B_LBO = 64 * BK * 2;  // bytes between the operand's 64-column MN chunks
+}  // namespace dqt
+
+struct DqtArgs {
+  const float* scale;     // [O]
+  const int32_t* zp;      // [O]
+  const int32_t* tix;     // [O, tiles_n + 1] arena positions: first entry of each column tile
+  const int32_t* col;     // arena
+  const float* val;
+  __nv_bfloat16* y;       // [M, N] = dX [T, I]
+  int M, N, K;            // T, I, O
+  int tiles_n;
+};
+
+// tix[o][t] = the first entry of row o's slot whose column is >= t * BN (t < tiles_n), and
+// tix[o][tiles_n] = the slot's used end; slot entries are column-ascending.
+__global__ void k_csr_tile_index(const int32_t* row_start, const int32_t* row_count,
+                                 const int32_t* col, int O, int tiles_n, int tile_cols,
+                                 int32_t* tix) {
+  const int64_t n = (int64_t)O * (tiles_n + 1);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int o = (int)(i / (tiles_n + 1)), t = (int)(i % (tiles_n + 1));
+    const int b = row_start[o];
+    const int e = b + (row_count ? min(row_count[o], row_start[o + 1] - b) : row_start[o + 1] - b);
+    int lo = b, hi = e;
+    if (t < tiles_n) {
+      const int c0 = t * tile_cols;
+      while (lo < hi) {  // lower_bound(col[b..e), c0)
+        const int mid = (lo + hi) >> 1;
+        if (col[mid] < c0) lo = mid + 1; else hi = mid;
+      }
+    } else {
+      lo = e;
+    }
+    tix[i] = lo;
+  }
+}
+
+__global__ void __launch_bounds__(dqt::NT, 1)
+    k_dq_gemm_t(const __grid_constant__ CUtensorMap tm_dy, const __grid_constant__ CUtensorMap tm_w,
+                const DqtArgs a) {
+  using namespace dqt;
+  extern __shared__ uint8_t dsm_raw[];
+  uint8_t* dsm = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
+  __shared__ __align__(8) uint64_t full_a[STAGES], full_b[STAGES], empty_ab[STAGES];
+  __shared__ __align__(8) uint64_t full_c[CSTAGES], empty_c[CSTAGES], acc_full;
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int nkb = a.K / BK;
+  auto a_tile = [&](int s) { return dsm + s * (A_BYTES + B_BYTES); };
+  auto b_tile = [&](int s) { return dsm + s * (A_BYTES + B_BYTES) + A_BYTES; };
+  auto c_tile = [&](int c) { return dsm + STAGES * (A_BYTES + B_BYTES) + c * C_BYTES; };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_a[s], 1);
+      mbar_init(&full_b[s], NPW);
+      mbar_init(&empty_ab[s], 1);
+    }
+    for (int c = 0; c < CSTAGES; ++c) {
+      mbar_init(&full_c[c], 1);
+      mbar_init(&empty_c[c], NPW);
+    }
+    mbar_init(&acc_full, 1);
+    mbar_fence_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_before_sync();
+  __syncthreads();
+  tc_after_sync();
+  const uint32_t tmem_d = tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA: dY tiles
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGES;
+        mbar_wait(&empty_ab[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
+        mbar_arrive_expect_tx(&full_a[s], (uint32_t)A_BYTES);
+#pragma unroll
+        for (int xb = 0; xb < BM / XBOX; ++xb)
+          tma_load_2d(a_tile(s) + xb * XBOX * 128, &tm_dy, kb * BK, m0 + xb * XBOX, &full_a[s]);
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {  // ---------------- TMA: W code tiles (64 W rows x BN columns)
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int c = kb % CSTAGES;
+        mbar_wait(&empty_c[c], (uint32_t)(((kb / CSTAGES) & 1) ^ 1));
+        mbar_arrive_expect_tx(&full_c[c], (uint32_t)C_BYTES);
+        tma_load_2d(c_tile(c), &tm_w, n0, kb * BK, &full_c[c]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGES;
+        const uint32_t ph = (uint32_t)((kb / STAGES) & 1);
+        mbar_wait(&full_a[s], ph);
+        mbar_wait(&full_b[s], ph);
+        tc_after_sync();
+        const uint32_t sa = smem_u32(a_tile(s)), sb = smem_u32(b_tile(s));
+#pragma unroll
+        for (int kk = 0; kk < BK / 16; ++kk) {
+          // B MN-major: 16 K rows = two 8-row swizzle atoms (2048 B) per K=16 step
+          const uint64_t bd = sw128_desc_mn(sb + 2048 * kk, B_LBO, 1024u);
+          const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+#pragma unroll
+          for (int ab = 0; ab < NACC; ++ab)
+            mma_bf16(tmem_d + ab * BN, sw128_desc(sa + ab * 128 * 128 + 32 * kk), bd, IDESC, acc);
+        }
+        mma_commit(&empty_ab[s]);
+      }
+      mma_commit(&acc_full);
+    }
+  } else if (warp >= 4) {
+    // ---------------- dequant producers: thread (r, j, h) of the 64 x 2 x 2 units
+    const int pt = threadIdx.x - 128;
+    const int r = pt >> 2, j = (pt >> 1) & 1, h = pt & 1;
+    const int tn = blockIdx.x;
+    const int cbeg = n0 + 64 * j + 32 * h;  // this thread's 32 columns of the W rows
+    // the block's row parameters, loaded one block ahead
+    auto load_row = [&](int kb, float& s, int32_t& z, int& eb, int& ee) {
+      const int o = kb * BK + r;
+      s = __ldg(a.scale + o);
+      z = __ldg(a.zp + o);
+      const int32_t* t = a.tix + (size_t)o * (a.tiles_n + 1) + tn;
+      eb = __ldg(t);
+      ee = __ldg(t + 1);
+    };
+    float s_n, s_nx = 0.0f;
+    int32_t z_n, z_nx = 0;
+    int eb, ee, eb_nx = 0, ee_nx = 0;
+    load_row(0, s_n, z_n, eb, ee);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % STAGES, c = kb % CSTAGES;
+      if (kb + 1 < nkb) load_row(kb + 1, s_nx, z_nx, eb_nx, ee_nx);
+      mbar_wait(&full_c[c], (uint32_t)((kb / CSTAGES) & 1));
+      const uint4* cr = reinterpret_cast<const uint4*>(c_tile(c) + r * BN + 64 * j + 32 * h);
+      const uint4 q0 = cr[0], q1 = cr[1];
+      fence_proxy_async();  // generic reads of the slot before the TMA refills it
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_c[c]);
+      mbar_wait(&empty_ab[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
+      // row r of MN chunk j: 64 bf16 = 128 bytes, 16-byte chunk k at (k ^ (r & 7)) << 4
+      uint8_t* bt = b_tile(s) + j * B_LBO + r * 128;
+      const DequantRow d = make_dequant_row(s_n, z_n);
+      const uint32_t w8[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+      uint32_t pk[16];
+      if (d.fast) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float2 u = make_float2(magic_byte(w8[i], 0), magic_byte(w8[i], 1));
+          float2 v = make_float2(magic_byte(w8[i], 2), magic_byte(w8[i], 3));
+          u = mul2(add2(u, f2(d.negc)), f2(s_n));
+          v = mul2(add2(v, f2(d.negc)), f2(s_n));
+          pk[2 * i] = pack_bf16(u.x, u.y);
+          pk[2 * i + 1] = pack_bf16(v.x, v.y);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float f[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) f[e] = dequant_exact((w8[i] >> (8 * e)) & 0xFFu, s_n, z_n);
+          pk[2 * i] = pack_bf16(f[0], f[1]);
+          pk[2 * i + 1] = pack_bf16(f[2], f[3]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int ch = 4 * h + k;  // 16-byte chunk of the 128-byte row (8 bf16)
+        *reinterpret_cast<uint4*>(bt + ((ch ^ (r & 7)) << 4)) =
+            make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
+      }
+      // the row's outliers in [cbeg, cbeg + 32): exact fp32 values, RNE to bf16
+      for (int e = eb; e < ee; ++e) {
+        const int cc = __ldg(a.col + e);
+        if (cc >= cbeg + 32) break;
+        if (cc >= cbeg) {
+          const int k = cc - n0 - 64 * j;  // 0..63 within the MN chunk row
+          const uint32_t hv = pack_bf16(__ldg(a.val + e), 0.0f) & 0xFFFFu;
+          *reinterpret_cast<uint16_t*>(bt + ((((k >> 3) ^ (r & 7)) << 4) | ((k & 7) << 1))) =
+              (uint16_t)hv;
+        }
+      }
+      fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor cores
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full_b[s]);
+      s_n = s_nx;
+      z_n = z_nx;
+      eb = eb_nx;
+      ee = ee_nx;
+    }
+    mbar_wait(&acc_full, 0u);
+    tc_after_sync();
+    epilogue_bf16<BN, NACC, NPW>(tmem_d, warp, lane, m0, n0, a.M, a.N, a.y);
+  }
+  tc_before_sync();
+  __syncthreads();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d),
+                 "n"(TMEM_COLS));
+}
+
+// ------------------------------------------------------------------ host side
+size_t dq_gemm_t_workspace_bytes(int O, int I) {
+  return (size_t)O * ((I + dqt::BN - 1) / dqt::BN + 1) * sizeof(int32_t);
+}
+
+cudaError_t launch_dq_gemm_t(const void* dy, int T, int O, const uint8_t* codes, int I,
+                             const float* scale, const int32_t* zp, const int32_t* row_start,
+                             const int32_t* row_count, const int32_t* col, const float* val,
+                             void* dx, void* workspace, cudaStream_t st) {
+  using namespace dqt;
+  auto enc = um::encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  CUtensorMap tdy{}, tw{};
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)O, (cuuint64_t)T};
+    const cuuint64_t strides[1] = {(cuuint64_t)O * 2};
+    const cuuint32_t box[2] = {BK, XBOX};
+    const cuuint32_t es[2] = {1, 1};
+    if (enc(&tdy, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(dy), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)I, (cuuint64_t)O};
+    const cuuint64_t strides[1] = {(cuuint64_t)I};
+    const cuuint32_t box[2] = {BN, BK};
+    const cuuint32_t es[2] = {1, 1};
+    if (enc(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(codes), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_dq_gemm_t, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int tiles_n = (I + BN - 1) / BN;
+  int32_t* tix = reinterpret_cast<int32_t*>(workspace);
+  {
+    const int64_t n = (int64_t)O * (tiles_n + 1);
+    const int blocks = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+    k_csr_tile_index<<<blocks, 256, 0, st>>>(row_start, row_count, col, O, tiles_n, BN, tix);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  DqtArgs a{scale, zp, tix, col, val, reinterpret_cast<__nv_bfloat16*>(dx), T, I, O, tiles_n};
+  dim3 grid((unsigned)tiles_n, (unsigned)((T + BM - 1) / BM));
+  k_dq_gemm_t<<<grid, NT, SMEM_BYTES, st>>>(tdy, tw, a);
+  return cudaGetLastError();
+}
+
+}  // namespace qftk

@@ -236,6 +236,13 @@ cudaError_t launch_dq_gemm(const void* x, int M, int K, const uint8_t* codes, in
                            const float* scale, const int32_t* zp, const int32_t* row_start,
                            const int32_t* row_count, const int32_t* col, const float* val,
                            void* y, cudaStream_t s);
+// the backward's input gradient dX = dY . W with W dequantized in the operand producer
+// (dqgemm_t.cu); workspace: the per-(row, column tile) CSR index
+size_t dq_gemm_t_workspace_bytes(int O, int I);
+cudaError_t launch_dq_gemm_t(const void* dy, int T, int O, const uint8_t* codes, int I,
+                             const float* scale, const int32_t* zp, const int32_t* row_start,
+                             const int32_t* row_count, const int32_t* col, const float* val,
+                             void* dx, void* workspace, cudaStream_t st);
 // the backward weight gradient with the sink's quantization in the GEMM epilogue (wgrad.cu):
 // codes/scale/zp = quantize_state(dY^T . X [+ dequantize(entry)]); workspace: rows bounds,
 // counters and the error word (its last uint32)

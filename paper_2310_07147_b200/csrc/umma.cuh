@@ -6,6 +6,7 @@
 #pragma once
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_bf16.h>
 #include <cstdint>
 
 #include "qft_device.cuh"
@@ -55,6 +56,59 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
   return r;
+}
+
+// tcgen05.ld 32x32b.x32: lane i of the warp gets 32 consecutive fp32 columns of TMEM lane
+// (warp % 4) * 32 + i (the warp's lane quarter) starting at `addr`; waits for completion
+__device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// The bf16 epilogue of the GEMMs with NACC M=128 accumulators of BN fp32 columns: warp
+// (4 + 4g + q) drains TMEM lanes 32q.. for warp group g of NPW/4 -- the (accumulator,
+// 32-column chunk) units g, g + NPW/4, ... (accumulator a: rows m0 + 128a ..) -- rounds to
+// bf16 (RNE) and stores y[row, n0 + c ..] of the row-major [M, N] output.
+template <int BN, int NACC, int NPW>
+__device__ __forceinline__ void epilogue_bf16(uint32_t tmem_d, int warp, int lane, int m0, int n0,
+                                              int M, int N, __nv_bfloat16* y) {
+  const int wq = (warp - 4) & 3, grp = (warp - 4) >> 2;
+  const uint32_t lane_base = (uint32_t)(32 * wq) << 16;
+  constexpr int CH = BN / 32, GROUPS = NPW / 4;
+#pragma unroll 1
+  for (int u = grp; u < NACC * CH; u += GROUPS) {
+    const int accn = u / CH, c0 = (u % CH) * 32;
+    const int row = m0 + 128 * accn + 32 * wq + lane;
+    uint32_t r[32];
+    tmem_ld32(tmem_d + lane_base + (uint32_t)(accn * BN + c0), r);
+    if (row < M) {
+      __nv_bfloat16* yr = y + (size_t)row * N + n0 + c0;
+      if (n0 + c0 + 32 <= N && (N % 8) == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 o;
+          o.x = pack_bf16(__uint_as_float(r[8 * q]), __uint_as_float(r[8 * q + 1]));
+          o.y = pack_bf16(__uint_as_float(r[8 * q + 2]), __uint_as_float(r[8 * q + 3]));
+          o.z = pack_bf16(__uint_as_float(r[8 * q + 4]), __uint_as_float(r[8 * q + 5]));
+          o.w = pack_bf16(__uint_as_float(r[8 * q + 6]), __uint_as_float(r[8 * q + 7]));
+          reinterpret_cast<uint4*>(yr)[q] = o;
+        }
+      } else {
+        for (int e = 0; e < 32 && n0 + c0 + e < N; ++e)
+          yr[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
+      }
+    }
+  }
 }
 
 // MN-major SWIZZLE_128B descriptor (canonical layout ((8,n),(8,k)) : ((1,LBO),(8,SBO)) in

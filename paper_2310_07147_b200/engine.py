@@ -690,6 +690,31 @@ class QftModelState:
             _p(g.col[cur]), _p(g.val[cur]), _p(y), _stream()))
         return y
 
+    def linear_backward(self, i: int, dy: torch.Tensor,
+                        out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """The backward's input gradient through tensor i: dx = dy . W_i (network.hpp:145
+        backward_core in_grad = matmul(out_grad, w)), dy bf16 [M, rows] -> dx bf16 [M, cols],
+        with W_i dequantized inside the GEMM's operand producer (qftc_dequant_gemm_t: the
+        tensor cores read RNE(reconstruct(W_i)) as an MN-major operand built in shared memory
+        from the u8 codes and the CSR outliers)."""
+        cur = self.cur
+        g = self.groups[self.group_of[i]]
+        r, c = self.shapes[i]
+        if dy.dtype != torch.bfloat16 or dy.dim() != 2 or dy.shape[1] != r or not dy.is_contiguous():
+            raise ValueError(f"linear_backward: dy must be a contiguous bf16 [M, {r}] tensor")
+        dx = out if out is not None else torch.empty((dy.shape[0], c), dtype=torch.bfloat16,
+                                                     device=dy.device)
+        need = int(N.lib.qftc_dequant_gemm_t_workspace_bytes(r, c))
+        ws = getattr(self, "_dqt_ws", None)
+        if ws is None or ws.numel() < need:
+            ws = self._dqt_ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        N.check(N.lib.qftc_dequant_gemm_t(
+            _p(dy), dy.shape[0], r, _p(self._sl(self.w_codes[cur], i)), c,
+            _p(self._rows(self.w_scale, i)), _p(self._rows(self.w_zp, i)),
+            _p(self._rs(self.row_start[cur], i)), _p(self._rows(self.row_count[cur], i)),
+            _p(g.col[cur]), _p(g.val[cur]), _p(dx), _p(ws), _stream()))
+        return dx
+
     def expand_table(self, outs: Sequence[torch.Tensor], rows: Optional[Sequence[int]] = None):
         """ctypes table (qftc_expand_tensor[n]) expanding tensor i's first rows[i] rows into
         outs[i] from the CURRENT state; reusable while `cur` and the buffers are unchanged."""

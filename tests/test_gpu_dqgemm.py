@@ -47,3 +47,39 @@ def test_dequant_gemm_rejects_bad_k(cuda):
     x = torch.zeros(8, 100, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(NotImplementedError):
         st.linear(0, x)
+
+
+@pytest.mark.parametrize("shape,m", [((128, 256), 200), ((384, 1024), 512), ((4096, 4096), 256),
+                                     ((11008, 4096), 130), ((4096, 11008), 64), ((192, 320), 77)])
+def test_dequant_gemm_t_matches_materialised(cuda, shape, m):
+    """The backward weight operand: dx = dy . W (network.hpp:145) with W dequantized as an
+    MN-major operand (qftc_dequant_gemm_t) == the GEMM on the materialised bf16 weights."""
+    torch.manual_seed(shape[1] + m)
+    st = cuda.QftModelState([shape], bit_width=8)
+    st.init_from_weights(lambda i: cuda.synth(shape, 17 + m, 0.02, 0.01), 0.01)
+    c, s, z = st.grad_views(0)
+    q = cuda.quantize_state(cuda.synth(shape, 8, 1e-3, 0.0), 8)
+    c.copy_(q.data); s.copy_(q.params.scale); z.copy_(q.params.zero_point)
+    st.step(lr=2e-4, check=True)  # slotted CSR with drift
+    wb = torch.empty(shape, dtype=torch.bfloat16, device="cuda")
+    st.expand([wb])
+    dy = (torch.randn(m, shape[0], device="cuda") * 0.5).to(torch.bfloat16)
+    dx = st.linear_backward(0, dy)
+    torch.cuda.synchronize()
+    ref = dy.float() @ wb.float()
+    err = (dx.float() - ref).abs()
+    tol = ref.abs() * 2.0 ** -7 + 1e-3 * ref.abs().max()
+    bad = (err > tol).sum().item()
+    assert bad == 0, f"{bad} elements off; max err {err.max().item()}"
+    same = (dx == ref.to(torch.bfloat16)).float().mean().item()
+    assert same > 0.98, f"only {same:.4f} of the bf16 outputs equal the reference's rounding"
+    # every outlier is in the operand: the GEMM on the payload-only weights differs
+    assert st.nnz() > 0
+
+
+def test_dequant_gemm_t_rejects_bad_shapes(cuda):
+    st = cuda.QftModelState([(100, 128)], bit_width=8)
+    st.init_from_weights(lambda i: cuda.synth((100, 128), 1, 0.02, 0.01), 0.01)
+    dy = torch.zeros(8, 100, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(NotImplementedError):
+        st.linear_backward(0, dy)
