@@ -241,6 +241,15 @@ int qftc_lion_step(int rows, int cols, int bit_width, const uint8_t* g_codes,
 
 /* ---------------------------------------------------------------- slotted CSR */
 
+/* Slot capacities for re-planning a slotted CSR after an overflow (the engine's
+ * _replan): per row, want = count_out + (dense codes at 0 or 2^b-1 in `codes` -- the
+ * elements a stable-tier step can turn into outliers), grow = max(count_out - count_in, 0),
+ * caps[r] = want + want/4 + growth_mult*grow + want*level/4 + min(8 << 2 level, 64), rounded
+ * up to a multiple of 4 (16-byte slots).  One pass over the codes, no synchronisation. */
+int qftc_csr_replan_caps(const uint8_t* codes, int rows, int cols, int bit_width,
+                         const int32_t* count_out, const int32_t* count_in, int level,
+                         int growth_mult, int64_t* caps, qftc_stream_t stream);
+
 /* row_start[0..rows] of 16-byte aligned slots with capacity count + count/4 + slack
  * (rounded up to 4 entries), counts taken from `counts` or, if NULL, from a
  * strict `row_ptr`.  Synchronises to return the arena size in *total_host. */

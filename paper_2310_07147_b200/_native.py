@@ -121,6 +121,7 @@ _SIGS = {
     "qftc_lion_step": (_i, [_i, _i, _i] + [_vp] * 21 + [_i64, LionHyperC, C.POINTER(_i64), _vp]),
     "qftc_lion_apply": (_i, [_vp, _vp, _vp, _i64, LionHyperC, _vp]),
     "qftc_synth": (_i, [_vp, _i64, _u64, _d, _d, _vp]),
+    "qftc_csr_replan_caps": (_i, [_vp, _i, _i, _i, _vp, _vp, _i, _i, _vp, _vp]),
     "qftc_csr_plan_slots": (_i, [_vp, _vp, _i, _i, _vp, C.POINTER(_i64), _vp]),
     "qftc_csr_copy_rows": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp]),
     "qftc_csr_compact": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, C.POINTER(_i64),

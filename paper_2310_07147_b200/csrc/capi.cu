@@ -567,6 +567,21 @@ int qftc_reconstruct_slots(const uint8_t* codes, int rows, int cols, const float
 }
 
 // ------------------------------------------------------------------ slotted CSR
+int qftc_csr_replan_caps(const uint8_t* codes, int rows, int cols, int bit_width,
+                         const int32_t* count_out, const int32_t* count_in, int level,
+                         int growth_mult, int64_t* caps, qftc_stream_t stream) {
+  if (int rc = require_shape(rows, cols, "csr_replan_caps")) return rc;
+  if (int rc = require_bit_width(bit_width)) return rc;
+  if (!codes || !count_out || !count_in || !caps)
+    return fail(QFTC_EINVAL, "csr_replan_caps: null pointer");
+  if (level < 0 || growth_mult < 0) return fail(QFTC_EINVAL, "csr_replan_caps: negative level");
+  if (int rc = require_device()) return rc;
+  QFTC_CUDA(launch_replan_caps(codes, rows, cols, bit_width, count_out, count_in, level,
+                               growth_mult, caps, (cudaStream_t)stream),
+            "csr_replan_caps");
+  return QFTC_OK;
+}
+
 int qftc_csr_plan_slots(const int32_t* counts, const int32_t* row_ptr, int rows, int slack,
                         int32_t* row_start, int64_t* total_host, qftc_stream_t stream) {
   if (rows <= 0) return fail(QFTC_EINVAL, "csr_plan_slots: no rows");

@@ -68,6 +68,56 @@ __global__ void k_copy_rows(int rows, const int32_t* src_start, const int32_t* s
   }
 }
 
+// Slot capacities for a re-plan (engine._replan): per row, the used count of the step's
+// output plus its dense codes at 0 / qmax (the only elements a stable-tier step can turn
+// into new outliers: the placement's no-overflow padding), plus growth headroom.  One warp
+// per row, 16 codes per lane load (__vcmpeq4 on 4 words), no temporaries.
+//   want = cnt_out + edge;  grow = max(cnt_out - cnt_in, 0)
+//   cap  = want + want/4 + gmul*grow + want*lvl/4 + min(8 << 2 lvl, 64), rounded up to 4
+__global__ void k_replan_caps(const uint8_t* codes, int rows, int cols, int qmax,
+                              const int32_t* cnt_out, const int32_t* cnt_in, int lvl, int gmul,
+                              int64_t* caps) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t qm4 = 0x01010101u * (uint32_t)qmax;
+  const bool vec = (cols % 16) == 0 && (reinterpret_cast<uintptr_t>(codes) & 15) == 0;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += warps) {
+    const uint8_t* cr = codes + (size_t)r * cols;
+    int edge = 0;
+    if (vec) {
+      const uint4* v = reinterpret_cast<const uint4*>(cr);
+      for (int i = lane; i < cols / 16; i += 32) {
+        const uint4 q = v[i];
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          edge += __popc(__vcmpeq4(w[k], 0u) | __vcmpeq4(w[k], qm4)) >> 3;
+      }
+    } else {
+      for (int i = lane; i < cols; i += 32) edge += (cr[i] == 0 || cr[i] == qmax) ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) edge += __shfl_xor_sync(0xffffffffu, edge, o);
+    if (lane == 0) {
+      const int64_t c = cnt_out[r];
+      const int64_t want = c + edge;
+      const int64_t grow = c > cnt_in[r] ? c - cnt_in[r] : 0;
+      const int64_t slack = (8LL << (2 * lvl)) < 64 ? (8LL << (2 * lvl)) : 64;
+      const int64_t cap = want + want / 4 + gmul * grow + (want * lvl) / 4 + slack;
+      caps[r] = (cap + 3) & ~3LL;
+    }
+  }
+}
+
+cudaError_t launch_replan_caps(const uint8_t* codes, int rows, int cols, int bit_width,
+                               const int32_t* cnt_out, const int32_t* cnt_in, int lvl, int gmul,
+                               int64_t* caps, cudaStream_t st) {
+  const int blocks = std::min(4096, (rows + 7) / 8);
+  k_replan_caps<<<blocks, 256, 0, st>>>(codes, rows, cols, (1 << bit_width) - 1, cnt_out, cnt_in,
+                                        lvl, gmul, caps);
+  return cudaGetLastError();
+}
+
 static cudaError_t exclusive_scan(const int32_t* in, int32_t* out, int n, cudaStream_t st) {
   size_t tmp = 0;
   cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, n, st);

@@ -236,6 +236,10 @@ cudaError_t launch_dq_gemm(const void* x, int M, int K, const uint8_t* codes, in
                            const float* scale, const int32_t* zp, const int32_t* row_start,
                            const int32_t* row_count, const int32_t* col, const float* val,
                            void* y, cudaStream_t s);
+// re-plan slot capacities (csr.cu, k_replan_caps)
+cudaError_t launch_replan_caps(const uint8_t* codes, int rows, int cols, int bit_width,
+                               const int32_t* cnt_out, const int32_t* cnt_in, int lvl, int gmul,
+                               int64_t* caps, cudaStream_t st);
 // the backward's input gradient dX = dY . W with W dequantized in the operand producer
 // (dqgemm_t.cu); workspace: the per-(row, column tile) CSR index
 size_t dq_gemm_t_workspace_bytes(int O, int I);

@@ -37,6 +37,7 @@ from .quantize import _p, _stream, kind_from_name
 
 _GRAD_KINDS = {"u8": N.GRAD_U8, "f32": N.GRAD_F32, "bf16": N.GRAD_BF16}
 SLACK = 8
+GROWTH_STEPS = 16  # a re-planned slot holds this many steps of the row's last growth
 
 
 @dataclass
@@ -196,7 +197,7 @@ class QftModelState:
     def _ensure(self, g: _Group, k: int, need: int, keep: int):
         if g.col[k] is not None and g.col[k].numel() >= need:
             return
-        col, val = self._alloc(int(need * 1.1) + 1024)
+        col, val = self._alloc(int(need * 1.5) + 1024)  # room for a first re-plan
         if keep and g.col[k] is not None:
             col[:keep].copy_(g.col[k][:keep])
             val[:keep].copy_(g.val[k][:keep])
@@ -508,12 +509,11 @@ class QftModelState:
         (_place_strict), the dense elements at code 0 / qmax of the step's output codes:
         only those can become new outliers in a stable-tier step, so the padding keeps the
         no-overflow guarantee of the placement after a replan.  Rows that overflow are
-        drifting (a large lr moves codes every step), so a re-planned slot also holds 8
-        steps of the row's last growth (its count minus the step's input count), and
+        drifting (a large lr moves codes every step), so a re-planned slot also holds
+        GROWTH_STEPS steps of the row's last growth (its count minus the step's input count), and
         every re-plan of the group widens the headroom -- count/4 more per level, the
         slack 8 -> 32 -> 64 entries -- instead of re-planning again the next step.  Batched over the group: one
         row-count pass, one scan, one scatter into the slot starts, one synchronisation."""
-        qmax = (1 << self.bit_width) - 1
         dev = self.device
         if g.layout_idx is None:
             pos, idx, rb = [], [], 0
@@ -527,28 +527,19 @@ class QftModelState:
             contiguous = ps == list(range(ps[0], ps[0] + len(ps)))
             g.layout_idx = (torch.cat(pos).to(dev), torch.cat(idx).to(dev), contiguous)
         rs_pos, scan_idx, contiguous = g.layout_idx
-        if contiguous:   # the group's codes / counts are one [rows, cols] block
-            p0, p1 = self.pos[g.members[0]], self.pos[g.members[-1]] + 1
-            codes = self.w_codes[k][self.off[p0]:self.off[p1]].view(-1, g.cols)
-            want = self.row_count[k][self.roff[p0]:self.roff[p1]].to(torch.int64)
-            grow = (want - self.row_count[1 - k][self.roff[p0]:self.roff[p1]]).clamp_(min=0)
-            step = max(1, (1 << 28) // g.cols)     # bounded temporaries (~256 MB per pass)
-            for r0 in range(0, codes.shape[0], step):
-                c = codes[r0:r0 + step]
-                want[r0:r0 + step] += ((c == 0) | (c == qmax)).sum(dim=1, dtype=torch.int64)
-        else:
-            parts, gparts = [], []
-            for i in g.members:
-                codes = self._sl(self.w_codes[k], i)
-                edge = ((codes == 0) | (codes == qmax)).sum(dim=1, dtype=torch.int64)
-                cnt = self._rows(self.row_count[k], i).to(torch.int64)
-                gparts.append((cnt - self._rows(self.row_count[1 - k], i)).clamp_(min=0))
-                parts.append(cnt + edge)
-            want = torch.cat(parts)
-            grow = torch.cat(gparts)
         lvl = min(g.replans, 3)
-        caps = want + want // 4 + 8 * grow + (want * lvl) // 4 + min(SLACK << (2 * lvl), 64)
-        caps = (caps + 3) & ~3                       # 16-byte aligned slots (TMA)
+        # one pass over the output codes per tensor run (qftc_csr_replan_caps): edge codes,
+        # growth, headroom -> per-row capacities, no temporaries
+        caps = torch.empty(g.rows, dtype=torch.int64, device=dev)
+        runs = ([(g.members[0], g.rows)] if contiguous else
+                [(i, self.shapes[i][0]) for i in g.members])
+        r0 = 0
+        for i, rows in runs:
+            N.check(N.lib.qftc_csr_replan_caps(
+                _p(self._sl(self.w_codes[k], i)), rows, g.cols, self.bit_width,
+                _p(self._rows(self.row_count[k], i)), _p(self._rows(self.row_count[1 - k], i)),
+                lvl, GROWTH_STEPS, _p(caps[r0:r0 + rows]), _stream()))
+            r0 += rows
         cum = torch.zeros(caps.numel() + 1, dtype=torch.int64, device=dev)
         torch.cumsum(caps, 0, out=cum[1:])
         total = int(cum[-1].item())
@@ -556,8 +547,8 @@ class QftModelState:
             raise OverflowError(f"CSR arena of the {g.cols}-column group: {total} entries")
         self.row_start[k].index_copy_(0, rs_pos, cum.index_select(0, scan_idx).to(torch.int32))
         g.replans += 1
-        if g.col[k].numel() < total:
-            g.col[k], g.val[k] = self._alloc(total)
+        if g.col[k].numel() < total:  # grow with headroom: a drifting state re-plans again
+            g.col[k], g.val[k] = self._alloc(total + total // 4)
 
     def _check(self, flip, h):
         out = 1 - flip
