@@ -11,7 +11,9 @@
 // sm_100a, one 512 x 128 output tile per CTA (DQ_BN=128: 4 accumulators; DQ_BN=256 gives
 // 256 x 256 with 2), K in blocks of 64:
 //   warp 0 (lane 0)  TMA: the X tile (512 x 64 bf16, two 256-row boxes, SWIZZLE_128B) of a
-//                    K block into a stage of the X / W-operand ring (2 stages, mbarrier tx)
+//                    K block into a stage of the X ring (2 stages, mbarrier tx); the
+//                    dequantized W operand has its own 4-stage ring, so the producers run
+//                    up to three blocks ahead of the MMAs
 //   warp 3 (lane 0)  TMA: the W code tile (128 x 64 u8) into its own 4-stage ring
 //   warps 4-11       the dequant producers: a thread pair owns W row n0 + j, each thread
 //                    32 columns of a block: its codes of
@@ -60,12 +62,16 @@ constexpr int BK = 64;      // K per block: 128 bytes of bf16 = one SWIZZLE_128B
 #ifndef DQ_CSTAGES
 #define DQ_CSTAGES 4
 #endif
-constexpr int STAGES = DQ_STAGES;    // X / W-operand ring
+#ifndef DQ_WSTAGES
+#define DQ_WSTAGES 4
+#endif
+constexpr int STAGES = DQ_STAGES;    // X ring
+constexpr int WSTAGES = DQ_WSTAGES;  // dequantized W-operand ring (producers run ahead)
 constexpr int CSTAGES = DQ_CSTAGES;  // W-code ring
 constexpr int A_BYTES = BM * BK * 2;  // NACC 128-row blocks of 16 KB
 constexpr int B_BYTES = BN * BK * 2;
 constexpr int C_BYTES = BN * BK;      // codes
-constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + CSTAGES * C_BYTES + 1024;
+constexpr int SMEM_BYTES = STAGES * A_BYTES + WSTAGES * B_BYTES + CSTAGES * C_BYTES + 1024;
 #ifndef DQ_HALVES
 #define DQ_HALVES 2
 #endif
@@ -102,21 +108,24 @@ __global__ void __launch_bounds__(dq::NT, 1)
   // 1024-byte aligned (SWIZZLE_128B atoms); pointer arithmetic on the shared array keeps
   // the address space visible to the compiler (LDS/STS, not generic loads and stores)
   uint8_t* dsm = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
-  __shared__ __align__(8) uint64_t full_a[STAGES], full_b[STAGES], empty_ab[STAGES];
+  __shared__ __align__(8) uint64_t full_a[STAGES], empty_a[STAGES], full_b[WSTAGES], empty_b[WSTAGES];
   __shared__ __align__(8) uint64_t full_c[CSTAGES], empty_c[CSTAGES], acc_full;
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int nkb = a.K / BK;
-  auto a_tile = [&](int s) { return dsm + s * (A_BYTES + B_BYTES); };
-  auto b_tile = [&](int s) { return dsm + s * (A_BYTES + B_BYTES) + A_BYTES; };
-  auto c_tile = [&](int c) { return dsm + STAGES * (A_BYTES + B_BYTES) + c * C_BYTES; };
+  auto a_tile = [&](int s) { return dsm + s * A_BYTES; };
+  auto b_tile = [&](int w) { return dsm + STAGES * A_BYTES + w * B_BYTES; };
+  auto c_tile = [&](int c) { return dsm + STAGES * A_BYTES + WSTAGES * B_BYTES + c * C_BYTES; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_a[s], 1);
-      mbar_init(&full_b[s], NPW);
-      mbar_init(&empty_ab[s], 1);
+      mbar_init(&empty_a[s], 1);
+    }
+    for (int w = 0; w < WSTAGES; ++w) {
+      mbar_init(&full_b[w], NPW);
+      mbar_init(&empty_b[w], 1);
     }
     for (int c = 0; c < CSTAGES; ++c) {
       mbar_init(&full_c[c], 1);
@@ -140,7 +149,7 @@ __global__ void __launch_bounds__(dq::NT, 1)
     if (lane == 0) {  // ---------------- TMA: X tiles
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % STAGES;
-        mbar_wait(&empty_ab[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
+        mbar_wait(&empty_a[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
         mbar_arrive_expect_tx(&full_a[s], (uint32_t)A_BYTES);
 #pragma unroll
         for (int xb = 0; xb < BM / XBOX; ++xb)
@@ -159,12 +168,11 @@ __global__ void __launch_bounds__(dq::NT, 1)
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
       for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (uint32_t)((kb / STAGES) & 1);
-        mbar_wait(&full_a[s], ph);
-        mbar_wait(&full_b[s], ph);
+        const int s = kb % STAGES, w = kb % WSTAGES;
+        mbar_wait(&full_a[s], (uint32_t)((kb / STAGES) & 1));
+        mbar_wait(&full_b[w], (uint32_t)((kb / WSTAGES) & 1));
         tc_after_sync();
-        const uint32_t sa = smem_u32(a_tile(s)), sb = smem_u32(b_tile(s));
+        const uint32_t sa = smem_u32(a_tile(s)), sb = smem_u32(b_tile(w));
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk) {  // every 128-row block shares the W operand
           const uint64_t bd = sw128_desc(sb + 32 * kk);
@@ -173,7 +181,8 @@ __global__ void __launch_bounds__(dq::NT, 1)
           for (int ab = 0; ab < NACC; ++ab)
             mma_bf16(tmem_d + ab * BN, sw128_desc(sa + ab * 128 * 128 + 32 * kk), bd, IDESC, acc);
         }
-        mma_commit(&empty_ab[s]);  // the X / W-operand stage is free once these MMAs read it
+        mma_commit(&empty_a[s]);  // the X and W-operand slots are free once these MMAs read them
+        mma_commit(&empty_b[w]);
       }
       mma_commit(&acc_full);
     }
@@ -216,27 +225,30 @@ __global__ void __launch_bounds__(dq::NT, 1)
     fetch(oc2, ov2);
     fetch(oc3, ov3);
     for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % STAGES, c = kb % CSTAGES;
+      const int w = kb % WSTAGES, c = kb % CSTAGES;
       mbar_wait(&full_c[c], (uint32_t)((kb / CSTAGES) & 1));
 #if DQ_NOPROD  // A/B: the pipeline without the dequantization work (wrong results)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_c[c]);
-      mbar_wait(&empty_ab[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
+      mbar_wait(&empty_b[w], (uint32_t)(((kb / WSTAGES) & 1) ^ 1));
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full_b[s]);
+      if (lane == 0) mbar_arrive(&full_b[w]);
       continue;
 #endif
-      const uint4* cr = reinterpret_cast<const uint4*>(c_tile(c) + j * BK + CPT * hf);
+      // the code tile is TMA-swizzled (SWIZZLE_64B: 16-byte chunk k of the 64-byte row j at
+      // k ^ ((j >> 1) & 3)), so a warp's 32 rows spread over all banks
+      const uint4* cr = reinterpret_cast<const uint4*>(c_tile(c) + j * BK);
       uint4 q4[NQ];
 #pragma unroll
-      for (int c4 = 0; c4 < NQ; ++c4) q4[c4] = live ? cr[c4] : make_uint4(0, 0, 0, 0);
+      for (int c4 = 0; c4 < NQ; ++c4)
+        q4[c4] = live ? cr[(c4 + NQ * hf) ^ ((j >> 1) & 3)] : make_uint4(0, 0, 0, 0);
       // generic-proxy reads of the slot, then the TMA (async proxy) refills it: order them
       fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_c[c]);  // the code slot is consumed
-      // the W-operand slot of stage s is free once the MMAs of its previous use completed
-      mbar_wait(&empty_ab[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
-      uint8_t* bt = b_tile(s) + j * 128;
+      // the W-operand slot w is free once the MMAs of its previous use completed
+      mbar_wait(&empty_b[w], (uint32_t)(((kb / WSTAGES) & 1) ^ 1));
+      uint8_t* bt = b_tile(w) + j * 128;
       // 32 codes -> 4 swizzled 16-byte chunks of bf16: the row's branch (fast magic-number
       // dequant, or the exact form for |z| >= 2^22) is taken once per block
       uint32_t pk[NQ][8];
@@ -299,7 +311,7 @@ __global__ void __launch_bounds__(dq::NT, 1)
       fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor cores
 #endif
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full_b[s]);
+      if (lane == 0) mbar_arrive(&full_b[w]);
     }
     // ---------------- epilogue: TMEM -> bf16 -> HBM
     mbar_wait(&acc_full, 0u);
@@ -338,7 +350,7 @@ cudaError_t launch_dq_gemm(const void* x, int M, int K, const uint8_t* codes, in
     const cuuint32_t box[2] = {BK, BN};
     const cuuint32_t es[2] = {1, 1};
     if (enc(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(codes), dims, strides, box,
-            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }

@@ -17,7 +17,8 @@
 // sm_100a, one 512 x 128 output tile per CTA (four M=128 TMEM accumulators share each
 // dequantized W operand block), K in blocks of 64 W rows:
 //   warp 0 (lane 0)  TMA: the dY tile (512 x 64 bf16, K-major, SWIZZLE_128B) -> X/W ring
-//   warp 3 (lane 0)  TMA: the W code tile (64 rows x 128 columns u8) -> its own 4-stage ring
+//   warp 3 (lane 0)  TMA: the W code tile (64 rows x 128 columns u8, SWIZZLE_128B) -> its
+//                    own 4-stage ring; the W operand has a 4-stage ring of its own
 //   warps 4-11       producers: thread (r, j, h) dequantizes W row k0 + r, columns
 //                    [64j + 32h, +32) of the tile -> 4 swizzled 16-byte chunks of row r of
 //                    the operand's MN chunk j; then its outliers; fence.proxy.async; arrive
@@ -42,12 +43,13 @@ constexpr int BN = 128;          // output columns (W columns) per CTA: UMMA N
 constexpr int NACC = 512 / BN;   // 4 accumulators of M = 128 (all 512 TMEM columns)
 constexpr int BM = 128 * NACC;   // output rows (tokens) per CTA
 constexpr int BK = 64;           // W rows per K block
-constexpr int STAGES = 2;        // dY / W-operand ring
+constexpr int STAGES = 2;        // dY ring
+constexpr int WSTAGES = 4;       // dequantized W-operand ring (producers run ahead)
 constexpr int CSTAGES = 4;       // W-code ring
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = BN * BK * 2;  // BN/64 MN chunks of 64 x 64 bf16 (8 KB each)
 constexpr int C_BYTES = BN * BK;
-constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + CSTAGES * C_BYTES + 1024;
+constexpr int SMEM_BYTES = STAGES * A_BYTES + WSTAGES * B_BYTES + CSTAGES * C_BYTES + 1024;
 constexpr int NPW = 8;                // producer warps
 constexpr int NT = 128 + 32 * NPW;
 constexpr int XBOX = 256;
@@ -100,21 +102,24 @@ __global__ void __launch_bounds__(dqt::NT, 1)
   using namespace dqt;
   extern __shared__ uint8_t dsm_raw[];
   uint8_t* dsm = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
-  __shared__ __align__(8) uint64_t full_a[STAGES], full_b[STAGES], empty_ab[STAGES];
+  __shared__ __align__(8) uint64_t full_a[STAGES], empty_a[STAGES], full_b[WSTAGES], empty_b[WSTAGES];
   __shared__ __align__(8) uint64_t full_c[CSTAGES], empty_c[CSTAGES], acc_full;
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int nkb = a.K / BK;
-  auto a_tile = [&](int s) { return dsm + s * (A_BYTES + B_BYTES); };
-  auto b_tile = [&](int s) { return dsm + s * (A_BYTES + B_BYTES) + A_BYTES; };
-  auto c_tile = [&](int c) { return dsm + STAGES * (A_BYTES + B_BYTES) + c * C_BYTES; };
+  auto a_tile = [&](int s) { return dsm + s * A_BYTES; };
+  auto b_tile = [&](int w) { return dsm + STAGES * A_BYTES + w * B_BYTES; };
+  auto c_tile = [&](int c) { return dsm + STAGES * A_BYTES + WSTAGES * B_BYTES + c * C_BYTES; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_a[s], 1);
-      mbar_init(&full_b[s], NPW);
-      mbar_init(&empty_ab[s], 1);
+      mbar_init(&empty_a[s], 1);
+    }
+    for (int w = 0; w < WSTAGES; ++w) {
+      mbar_init(&full_b[w], NPW);
+      mbar_init(&empty_b[w], 1);
     }
     for (int c = 0; c < CSTAGES; ++c) {
       mbar_init(&full_c[c], 1);
@@ -138,7 +143,7 @@ __global__ void __launch_bounds__(dqt::NT, 1)
     if (lane == 0) {  // ---------------- TMA: dY tiles
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % STAGES;
-        mbar_wait(&empty_ab[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
+        mbar_wait(&empty_a[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
         mbar_arrive_expect_tx(&full_a[s], (uint32_t)A_BYTES);
 #pragma unroll
         for (int xb = 0; xb < BM / XBOX; ++xb)
@@ -157,12 +162,11 @@ __global__ void __launch_bounds__(dqt::NT, 1)
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer
       for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (uint32_t)((kb / STAGES) & 1);
-        mbar_wait(&full_a[s], ph);
-        mbar_wait(&full_b[s], ph);
+        const int s = kb % STAGES, w = kb % WSTAGES;
+        mbar_wait(&full_a[s], (uint32_t)((kb / STAGES) & 1));
+        mbar_wait(&full_b[w], (uint32_t)((kb / WSTAGES) & 1));
         tc_after_sync();
-        const uint32_t sa = smem_u32(a_tile(s)), sb = smem_u32(b_tile(s));
+        const uint32_t sa = smem_u32(a_tile(s)), sb = smem_u32(b_tile(w));
 #pragma unroll
         for (int kk = 0; kk < BK / 16; ++kk) {
           // B MN-major: 16 K rows = two 8-row swizzle atoms (2048 B) per K=16 step
@@ -172,7 +176,8 @@ __global__ void __launch_bounds__(dqt::NT, 1)
           for (int ab = 0; ab < NACC; ++ab)
             mma_bf16(tmem_d + ab * BN, sw128_desc(sa + ab * 128 * 128 + 32 * kk), bd, IDESC, acc);
         }
-        mma_commit(&empty_ab[s]);
+        mma_commit(&empty_a[s]);
+        mma_commit(&empty_b[w]);
       }
       mma_commit(&acc_full);
     }
@@ -196,17 +201,20 @@ __global__ void __launch_bounds__(dqt::NT, 1)
     int eb, ee, eb_nx = 0, ee_nx = 0;
     load_row(0, s_n, z_n, eb, ee);
     for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % STAGES, c = kb % CSTAGES;
+      const int w = kb % WSTAGES, c = kb % CSTAGES;
       if (kb + 1 < nkb) load_row(kb + 1, s_nx, z_nx, eb_nx, ee_nx);
       mbar_wait(&full_c[c], (uint32_t)((kb / CSTAGES) & 1));
-      const uint4* cr = reinterpret_cast<const uint4*>(c_tile(c) + r * BN + 64 * j + 32 * h);
-      const uint4 q0 = cr[0], q1 = cr[1];
+      // the code tile is TMA-swizzled (SWIZZLE_128B: 16-byte chunk k of row r at k ^ (r & 7)),
+      // so the 8 rows a warp reads hit distinct banks
+      const uint4* cr = reinterpret_cast<const uint4*>(c_tile(c) + r * BN);
+      const int k0 = 4 * j + 2 * h;
+      const uint4 q0 = cr[k0 ^ (r & 7)], q1 = cr[(k0 + 1) ^ (r & 7)];
       fence_proxy_async();  // generic reads of the slot before the TMA refills it
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_c[c]);
-      mbar_wait(&empty_ab[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
+      mbar_wait(&empty_b[w], (uint32_t)(((kb / WSTAGES) & 1) ^ 1));
       // row r of MN chunk j: 64 bf16 = 128 bytes, 16-byte chunk k at (k ^ (r & 7)) << 4
-      uint8_t* bt = b_tile(s) + j * B_LBO + r * 128;
+      uint8_t* bt = b_tile(w) + j * B_LBO + r * 128;
       const DequantRow d = make_dequant_row(s_n, z_n);
       const uint32_t w8[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
       uint32_t pk[16];
@@ -249,7 +257,7 @@ __global__ void __launch_bounds__(dqt::NT, 1)
       }
       fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor cores
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full_b[s]);
+      if (lane == 0) mbar_arrive(&full_b[w]);
       s_n = s_nx;
       z_n = z_nx;
       eb = eb_nx;
@@ -295,7 +303,7 @@ cudaError_t launch_dq_gemm_t(const void* dy, int T, int O, const uint8_t* codes,
     const cuuint32_t box[2] = {BN, BK};
     const cuuint32_t es[2] = {1, 1};
     if (enc(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(codes), dims, strides, box,
-            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
