@@ -357,11 +357,14 @@ int qftc_wgrad_quant(const void* dy_bf16, const void* x_bf16, int tokens, int ou
  * y[m,n] = x[m,k] . W^T for a dense-and-sparse weight W [n,k] (codes, per-row params,
  * CSR -- slotted with row_count, or strict with row_count = NULL), x and y bf16 row-major.
  * The tensor cores read bf16 RNE(reconstruct(W)) built in shared memory from the u8
- * codes; W never exists in HBM.  k % 64 == 0; x, codes, y 16-byte aligned. */
+ * codes; W never exists in HBM.  k % 64 == 0; x, codes, y 16-byte aligned.  `workspace`
+ * (qftc_dequant_gemm_workspace_bytes(n, k) bytes, device) receives the per-(row, 32-column)
+ * index of the CSR slots that lets each producer thread load its outliers ahead. */
+int64_t qftc_dequant_gemm_workspace_bytes(int n, int k);
 int qftc_dequant_gemm(const void* x_bf16, int m, int k, const uint8_t* codes, int n,
                       const float* scale, const int32_t* zero_point, const int32_t* row_start,
                       const int32_t* row_count, const int32_t* col_idx, const float* values,
-                      void* y_bf16, qftc_stream_t stream);
+                      void* y_bf16, void* workspace, qftc_stream_t stream);
 
 /* Opt-in QFTC format extensions (checkpoint.cpp:100-140 is the v1
  * layout they extend; the files carry version 0x8001, which the reference rejects):

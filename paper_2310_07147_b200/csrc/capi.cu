@@ -399,19 +399,24 @@ int qftc_expand_plan_destroy(qftc_expand_plan* plan) {
   return QFTC_OK;
 }
 
+int64_t qftc_dequant_gemm_workspace_bytes(int n, int k) {
+  return n > 0 && k > 0 ? (int64_t)dq_gemm_workspace_bytes(n, k) : 0;
+}
+
 int qftc_dequant_gemm(const void* x_bf16, int m, int k, const uint8_t* codes, int n,
                       const float* scale, const int32_t* zero_point, const int32_t* row_start,
                       const int32_t* row_count, const int32_t* col_idx, const float* values,
-                      void* y_bf16, qftc_stream_t stream) {
+                      void* y_bf16, void* workspace, qftc_stream_t stream) {
   if (m <= 0 || n <= 0 || k <= 0) return fail(QFTC_EINVAL, "dequant_gemm: empty shape");
   if (k % 64 != 0) return fail(QFTC_ENOTSUP, "dequant_gemm: K must be a multiple of 64");
-  if (!x_bf16 || !codes || !scale || !zero_point || !row_start || !y_bf16)
+  if (!x_bf16 || !codes || !scale || !zero_point || !row_start || !col_idx || !values ||
+      !y_bf16 || !workspace)
     return fail(QFTC_EINVAL, "dequant_gemm: null pointer");
   if (!al16(x_bf16) || !al16(codes) || !al16(y_bf16))
     return fail(QFTC_EINVAL, "dequant_gemm: x, codes and y must be 16-byte aligned");
   if (int rc = require_device()) return rc;
   QFTC_CUDA(launch_dq_gemm(x_bf16, m, k, codes, n, scale, zero_point, row_start, row_count,
-                           col_idx, values, y_bf16, (cudaStream_t)stream),
+                           col_idx, values, y_bf16, workspace, (cudaStream_t)stream),
             "dequant_gemm kernel");
   return QFTC_OK;
 }

@@ -8,8 +8,8 @@
 // cores read is exactly RNE(reconstruct(W)) -- the bytes qftc_expand(bf16) would write --
 // but it never exists in HBM: W streams as 1 byte per element instead of 2.
 //
-// sm_100a, one 512 x 128 output tile per CTA (DQ_BN=128: 4 accumulators; DQ_BN=256 gives
-// 256 x 256 with 2), K in blocks of 64:
+// sm_100a, K in blocks of 64; two shapes (dq::Shape): a CTA pair (cta_group::2, M > 256)
+// with a 512 x 256 output tile per pair, or one CTA with a 512 x 128 tile.  Per CTA:
 //   warp 0 (lane 0)  TMA: the X tile (512 x 64 bf16, two 256-row boxes, SWIZZLE_128B) of a
 //                    K block into a stage of the X ring (2 stages, mbarrier tx); the
 //                    dequantized W operand has its own 4-stage ring, so the producers run
@@ -47,73 +47,111 @@ using namespace qftd;
 #ifndef DQ_NOFENCE
 #define DQ_NOFENCE 0
 #endif
+#ifndef DQ_PW
+#define DQ_PW 0
+#endif
+#ifndef DQ_NOOUT
+#define DQ_NOOUT 0  // A/B only: outliers not applied (wrong results)
+#endif
+#ifndef DQ_NOX
+#define DQ_NOX 0  // A/B only: no X loads (wrong results)
+#endif
+#ifndef DQ_NOMMA
+#define DQ_NOMMA 0  // A/B only: no MMAs (wrong results)
+#endif
 namespace dq {
 using namespace um;
-#ifndef DQ_BN
-#define DQ_BN 128
-#endif
-constexpr int BN = DQ_BN;          // output columns (W rows) per CTA: UMMA N
-constexpr int NACC = 512 / BN;     // M=128 accumulators: all 512 TMEM columns
-constexpr int BM = 128 * NACC;     // output rows (X rows) per CTA
 constexpr int BK = 64;      // K per block: 128 bytes of bf16 = one SWIZZLE_128B row
-#ifndef DQ_STAGES
-#define DQ_STAGES 2
-#endif
+constexpr int WROWS = 128;  // W rows dequantized per CTA (output columns of a CTA's operand)
 #ifndef DQ_CSTAGES
 #define DQ_CSTAGES 4
 #endif
 #ifndef DQ_WSTAGES
 #define DQ_WSTAGES 4
 #endif
-constexpr int STAGES = DQ_STAGES;    // X ring
 constexpr int WSTAGES = DQ_WSTAGES;  // dequantized W-operand ring (producers run ahead)
 constexpr int CSTAGES = DQ_CSTAGES;  // W-code ring
-constexpr int A_BYTES = BM * BK * 2;  // NACC 128-row blocks of 16 KB
-constexpr int B_BYTES = BN * BK * 2;
-constexpr int C_BYTES = BN * BK;      // codes
-constexpr int SMEM_BYTES = STAGES * A_BYTES + WSTAGES * B_BYTES + CSTAGES * C_BYTES + 1024;
+constexpr int B_BYTES = WROWS * BK * 2;
+constexpr int C_BYTES = WROWS * BK;  // codes
 #ifndef DQ_HALVES
 #define DQ_HALVES 2
 #endif
-constexpr int HALVES = DQ_HALVES;     // producer threads per W row
-constexpr int CPT = BK / HALVES;      // columns of a K block per producer thread
-constexpr int NQ = CPT / 16;          // 16-code vectors per producer thread and block
-constexpr int NPW = BN * HALVES / 32; // producer warps
-constexpr int NT = 128 + BN * HALVES; // TMA (X), MMA, TMEM, TMA (codes) warps + producers
+constexpr int HALVES = DQ_HALVES;        // producer threads per W row
+constexpr int CPT = BK / HALVES;         // columns of a K block per producer thread
+constexpr int NQ = CPT / 16;             // 16-code vectors per producer thread and block
+constexpr int NPW = WROWS * HALVES / 32; // producer warps
+constexpr int NT = 128 + WROWS * HALVES; // TMA (X), MMA, TMEM, TMA (codes) warps + producers
 
-// instruction descriptor: D f32, A/B bf16, both K-major, N = BN, M = 128 (per accumulator)
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(128 >> 4) << 24);
-constexpr int TMEM_COLS = NACC * BN;  // NACC fp32 accumulators of BN columns (512)
-constexpr int XBOX = BM < 256 ? BM : 256;  // TMA box rows (<= 256): BM / XBOX loads per X tile
+// The two tile shapes.  Single CTA: 512 x 128 output tile, four M=128 x N=128 accumulators
+// (cta_group::1), a 2-stage 64 KB X ring.  CTA pair (cta_group::2, cluster of 2): a
+// 512 x 256 output tile per pair -- each CTA holds 256 X rows (two M=256 halves) and
+// dequantizes 128 of the 256 W rows; the leader's M=256 x N=256 MMAs read both CTAs'
+// halves, so each SM's tensor core streams half the operand bytes per flop (the
+// single-CTA shape is shared-memory-bandwidth bound), and a 4-stage 32 KB X ring fits.
+template <bool PAIR>
+struct Shape {
+  static constexpr int BN = PAIR ? 256 : 128;          // UMMA N (output columns per tile)
+  static constexpr int NACC = PAIR ? 2 : 4;            // accumulators (512 TMEM columns)
+  static constexpr int BM = PAIR ? 256 : 512;          // X rows per CTA
+#ifndef DQ_PSTAGES
+#define DQ_PSTAGES 4
+#endif
+  static constexpr int STAGES = PAIR ? DQ_PSTAGES : 2;  // X ring
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int SMEM_BYTES = STAGES * A_BYTES + WSTAGES * B_BYTES + CSTAGES * C_BYTES + 1024;
+  // instruction descriptor: D f32, A/B bf16, both K-major, N = BN, M = 128 or 256 (pair)
+  static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) |
+                                    ((uint32_t)(BN >> 3) << 17) |
+                                    ((uint32_t)((PAIR ? 256 : 128) >> 4) << 24);
+  static constexpr int TMEM_COLS = NACC * BN;  // 512
+  static constexpr int XBOX = 256;             // TMA box rows: BM / XBOX loads per X tile
+};
 
 }  // namespace dq
 
 struct DqArgs {
+  const uint8_t* codes;      // [N, K] u8 W codes
   const float* scale;        // [N]
   const int32_t* zp;         // [N]
   const int32_t* row_start;  // [N] CSR slot starts (arena offsets)
   const int32_t* row_count;  // [N] used entries (null: strict CSR, count = rs[n+1]-rs[n])
   const int32_t* col;        // arena
   const float* val;
+  const int32_t* tix;        // [N][K/32 + 1] per-(row, 32-column) slot index (k_csr_tile_index)
   __nv_bfloat16* y;          // [M, N]
   int M, N, K;
 };
 
-__global__ void __launch_bounds__(dq::NT, 1)
-    k_dq_gemm(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
-              const DqArgs a) {
+template <bool PAIR>
+__device__ __forceinline__ void dq_gemm_body(const CUtensorMap* tm_x, const CUtensorMap* tm_w,
+                                             const DqArgs& a) {
   using namespace dq;
+  using S = Shape<PAIR>;
+  constexpr int STAGES = S::STAGES, A_BYTES = S::A_BYTES, BM = S::BM, BN = S::BN;
+  constexpr int NACC = S::NACC, XBOX = S::XBOX;
   extern __shared__ uint8_t dsm_raw[];
   // 1024-byte aligned (SWIZZLE_128B atoms); pointer arithmetic on the shared array keeps
-  // the address space visible to the compiler (LDS/STS, not generic loads and stores)
+  // the address space visible to the compiler (LDS/STS, not generic loads and stores).
+  // Both CTAs of a pair compute the same offsets (the leader's descriptors address both).
   uint8_t* dsm = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
   __shared__ __align__(8) uint64_t full_a[STAGES], empty_a[STAGES], full_b[WSTAGES], empty_b[WSTAGES];
   __shared__ __align__(8) uint64_t full_c[CSTAGES], empty_c[CSTAGES], acc_full;
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  // pair: blockIdx.x = 2 * (256-column tile) + rank; CTA `rank` holds X rows
+  // m0 = 512 * blockIdx.y + 256 * rank and dequantizes W rows wn0 = n0 + 128 * rank
+  const int n0 = PAIR ? (int)(blockIdx.x >> 1) * BN : (int)blockIdx.x * BN;
+  const int m0 = PAIR ? (int)blockIdx.y * 2 * BM + (int)rank * BM : (int)blockIdx.y * BM;
+  const int wn0 = n0 + (int)rank * WROWS;
   const int nkb = a.K / BK;
+  // pair-path waits: DQ_PW=1 polls without the suspend-time hint (remote arrivals)
+  auto pwait = [&](uint64_t* bar, uint32_t par) {
+    if (PAIR && DQ_PW)
+      mbar_wait_cl(bar, par);
+    else
+      mbar_wait(bar, par);
+  };
   auto a_tile = [&](int s) { return dsm + s * A_BYTES; };
   auto b_tile = [&](int w) { return dsm + STAGES * A_BYTES + w * B_BYTES; };
   auto c_tile = [&](int c) { return dsm + STAGES * A_BYTES + WSTAGES * B_BYTES + c * C_BYTES; };
@@ -124,7 +162,7 @@ __global__ void __launch_bounds__(dq::NT, 1)
       mbar_init(&empty_a[s], 1);
     }
     for (int w = 0; w < WSTAGES; ++w) {
-      mbar_init(&full_b[w], NPW);
+      mbar_init(&full_b[w], PAIR ? 2 * NPW : NPW);  // pair: both CTAs' producers (leader's)
       mbar_init(&empty_b[w], 1);
     }
     for (int c = 0; c < CSTAGES; ++c) {
@@ -134,43 +172,72 @@ __global__ void __launch_bounds__(dq::NT, 1)
     mbar_init(&acc_full, 1);
     mbar_fence_init();
   }
-  if (warp == 2) {  // TMEM: two accumulators of BN fp32 columns x 128 lanes
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&tmem_base)),
-                 "n"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  if (warp == 2) {  // TMEM: the accumulators (pair: the same columns on both SMs)
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&tmem_base)),
+                   "n"(S::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&tmem_base)),
+                   "n"(S::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_before_sync();
-  __syncthreads();
+  if (PAIR)
+    cluster_sync_all();  // barrier inits and the allocation visible to the peer
+  else
+    __syncthreads();
   tc_after_sync();
   const uint32_t tmem_d = tmem_base;
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA: X tiles
+      const uint32_t fa0 = PAIR ? mapa_cl(&full_a[0], 0) : 0u;
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % STAGES;
-        mbar_wait(&empty_a[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
-        mbar_arrive_expect_tx(&full_a[s], (uint32_t)A_BYTES);
+        pwait(&empty_a[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
+        if (DQ_NOX) {
+          if (rank == 0) mbar_arrive(&full_a[s]);
+          continue;
+        }
+        if (PAIR) {
+          // both CTAs' bytes complete on the leader's barrier; the leader expects them all
+          if (rank == 0) mbar_arrive_expect_tx(&full_a[s], (uint32_t)(2 * A_BYTES));
+          const uint32_t bar = fa0 + (uint32_t)(s * sizeof(uint64_t));
 #pragma unroll
-        for (int xb = 0; xb < BM / XBOX; ++xb)
-          tma_load_2d(a_tile(s) + xb * XBOX * 128, &tm_x, kb * BK, m0 + xb * XBOX, &full_a[s]);
+          for (int xb = 0; xb < BM / XBOX; ++xb)
+            tma_load_2d_pair(a_tile(s) + xb * XBOX * 128, tm_x, kb * BK, m0 + xb * XBOX, bar);
+        } else {
+          mbar_arrive_expect_tx(&full_a[s], (uint32_t)A_BYTES);
+#pragma unroll
+          for (int xb = 0; xb < BM / XBOX; ++xb)
+            tma_load_2d(a_tile(s) + xb * XBOX * 128, tm_x, kb * BK, m0 + xb * XBOX, &full_a[s]);
+        }
       }
     }
   } else if (warp == 3) {
     if (lane == 0) {  // ---------------- TMA: W code tiles (their own, deeper ring)
       for (int kb = 0; kb < nkb; ++kb) {
         const int c = kb % CSTAGES;
-        mbar_wait(&empty_c[c], (uint32_t)(((kb / CSTAGES) & 1) ^ 1));
+        pwait(&empty_c[c], (uint32_t)(((kb / CSTAGES) & 1) ^ 1));
         mbar_arrive_expect_tx(&full_c[c], (uint32_t)C_BYTES);
-        tma_load_2d(c_tile(c), &tm_w, kb * BK, n0, &full_c[c]);
+        tma_load_2d(c_tile(c), tm_w, kb * BK, wn0, &full_c[c]);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (the pair's leader)
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % STAGES, w = kb % WSTAGES;
-        mbar_wait(&full_a[s], (uint32_t)((kb / STAGES) & 1));
-        mbar_wait(&full_b[w], (uint32_t)((kb / WSTAGES) & 1));
+        if (PAIR) {
+          mbar_wait_cl(&full_a[s], (uint32_t)((kb / STAGES) & 1));
+          mbar_wait_cl(&full_b[w], (uint32_t)((kb / WSTAGES) & 1));
+        } else {
+          mbar_wait(&full_a[s], (uint32_t)((kb / STAGES) & 1));
+          mbar_wait(&full_b[w], (uint32_t)((kb / WSTAGES) & 1));
+        }
         tc_after_sync();
         const uint32_t sa = smem_u32(a_tile(s)), sb = smem_u32(b_tile(w));
 #pragma unroll
@@ -178,61 +245,99 @@ __global__ void __launch_bounds__(dq::NT, 1)
           const uint64_t bd = sw128_desc(sb + 32 * kk);
           const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
 #pragma unroll
-          for (int ab = 0; ab < NACC; ++ab)
-            mma_bf16(tmem_d + ab * BN, sw128_desc(sa + ab * 128 * 128 + 32 * kk), bd, IDESC, acc);
+          for (int ab = 0; ab < NACC; ++ab) {
+            const uint64_t ad = sw128_desc(sa + ab * 128 * 128 + 32 * kk);
+            if (DQ_NOMMA)
+              ;
+            else if (PAIR)
+              mma_bf16_pair(tmem_d + ab * BN, ad, bd, S::IDESC, acc);
+            else
+              mma_bf16(tmem_d + ab * BN, ad, bd, S::IDESC, acc);
+          }
         }
-        mma_commit(&empty_a[s]);  // the X and W-operand slots are free once these MMAs read them
-        mma_commit(&empty_b[w]);
+        // the X and W-operand slots (of both CTAs) are free once these MMAs read them
+        if (PAIR) {
+          mma_commit_pair(&empty_a[s], 3);
+          mma_commit_pair(&empty_b[w], 3);
+        } else {
+          mma_commit(&empty_a[s]);
+          mma_commit(&empty_b[w]);
+        }
       }
-      mma_commit(&acc_full);
+      if (PAIR)
+        mma_commit_pair(&acc_full, 3);
+      else
+        mma_commit(&acc_full);
     }
   } else if (warp >= 4) {
     // ---------------- dequant producers (then the epilogue)
     const int pt = threadIdx.x - 128;
-    const int j = pt % BN;            // W row n0 + j of the tile ...
-    const int hf = pt / BN;           // ... columns [32 hf, 32 hf + 32) of each block
-    const int n = n0 + j;
+    const int j = pt % WROWS;         // W row wn0 + j of the tile ...
+    const int hf = pt / WROWS;        // ... columns [32 hf, 32 hf + 32) of each block
+    const int n = wn0 + j;
     const bool live = n < a.N;
     float s_n = 0.0f, negc = 0.0f;
     int32_t z_n = 0;
-    int cur = 0, end = 0;
     if (live) {
       s_n = a.scale[n];
       z_n = a.zp[n];
       negc = make_dequant_row(s_n, z_n).negc;
-      cur = a.row_start[n];
-      end = cur + (a.row_count ? min(a.row_count[n], a.row_start[n + 1] - cur)
-                               : a.row_start[n + 1] - cur);
     }
     const bool fast = make_dequant_row(s_n, z_n).fast;
-    // a 4-entry register window over the row's CSR slot (columns ascending): the per-block
-    // test is a register compare, and an entry's load is issued 4 outliers before it is used
-    constexpr int NONE = 0x7fffffff;
-    int oc0 = NONE, oc1 = NONE, oc2 = NONE, oc3 = NONE;
-    float ov0 = 0.0f, ov1 = 0.0f, ov2 = 0.0f, ov3 = 0.0f;
-    int nxt = cur;  // next CSR entry to load into the window
-    auto fetch = [&](int& c, float& v) {
-      if (nxt < end) {
-        c = __ldg(a.col + nxt);
-        v = __ldg(a.val + nxt);
-        ++nxt;
+    const uint32_t fb0 = PAIR ? mapa_cl(&full_b[0], 0) : 0u;
+    // The thread's outliers of block kb are slot entries [tix[2kb + hf], tix[2kb + hf + 1])
+    // of its row (columns ascending, 32-column granularity = exactly its half of the block).
+    // Pipelined without dependent chains: block kb+2's index pair is loaded during block
+    // kb, and block kb+1's first two entries during block kb -- each load is consumed one
+    // block (~1 us) after issue.  More than two entries in a half block (rare at p <= 1%)
+    // are loaded where they are written.
+    const int32_t* tr = a.tix + (size_t)(live ? n : 0) * (size_t)(2 * nkb + 1) + hf;
+    auto tload = [&](int kb, int& s0, int& e0) {
+      if (live && kb < nkb) {
+        s0 = __ldg(tr + 2 * kb);
+        e0 = __ldg(tr + 2 * kb + 1);
       } else {
-        c = NONE;
+        s0 = e0 = 0;
       }
     };
-    fetch(oc0, ov0);
-    fetch(oc1, ov1);
-    fetch(oc2, ov2);
-    fetch(oc3, ov3);
+    int s1, e1, s2, e2;  // index pairs of the next block and the one after
+    tload(0, s1, e1);
+    tload(1, s2, e2);
+    int nS = s1, nN = e1 - s1, nc0 = 0, nc1 = 0;  // the next block's first two entries
+    float nv0 = 0.0f, nv1 = 0.0f;
+    auto eload = [&](int s0, int e0) {
+      nS = s0;
+      nN = e0 - s0;
+      if (nN > 0) {
+        nc0 = __ldg(a.col + s0);
+        nv0 = __ldg(a.val + s0);
+      }
+      if (nN > 1) {
+        nc1 = __ldg(a.col + s0 + 1);
+        nv1 = __ldg(a.val + s0 + 1);
+      }
+    };
+    eload(s1, e1);
     for (int kb = 0; kb < nkb; ++kb) {
       const int w = kb % WSTAGES, c = kb % CSTAGES;
-      mbar_wait(&full_c[c], (uint32_t)((kb / CSTAGES) & 1));
+      // this block's outliers (loaded during the previous block); issue the next block's
+      // entries and the index pair of the block after it
+      const int cS = nS, cN = nN, cc0 = nc0, cc1 = nc1;
+      const float cv0 = nv0, cv1 = nv1;
+      eload(s2, e2);
+      tload(kb + 2, s2, e2);
+      pwait(&full_c[c], (uint32_t)((kb / CSTAGES) & 1));
 #if DQ_NOPROD  // A/B: the pipeline without the dequantization work (wrong results)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_c[c]);
-      mbar_wait(&empty_b[w], (uint32_t)(((kb / WSTAGES) & 1) ^ 1));
+      pwait(&empty_b[w], (uint32_t)(((kb / WSTAGES) & 1) ^ 1));
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full_b[w]);
+      if (lane == 0) {
+        if (PAIR)
+          mbar_arrive_cl(fb0 + (uint32_t)(w * sizeof(uint64_t)));
+        else
+          mbar_arrive(&full_b[w]);
+      }
       continue;
 #endif
       // the code tile is TMA-swizzled (SWIZZLE_64B: 16-byte chunk k of the 64-byte row j at
@@ -247,7 +352,7 @@ __global__ void __launch_bounds__(dq::NT, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_c[c]);  // the code slot is consumed
       // the W-operand slot w is free once the MMAs of its previous use completed
-      mbar_wait(&empty_b[w], (uint32_t)(((kb / WSTAGES) & 1) ^ 1));
+      pwait(&empty_b[w], (uint32_t)(((kb / WSTAGES) & 1) ^ 1));
       uint8_t* bt = b_tile(w) + j * 128;
       // 32 codes -> 4 swizzled 16-byte chunks of bf16: the row's branch (fast magic-number
       // dequant, or the exact form for |z| >= 2^22) is taken once per block
@@ -290,54 +395,91 @@ __global__ void __launch_bounds__(dq::NT, 1)
       }
       // the row's outliers in this K block overwrite their positions with their exact
       // fp32 values (RNE to bf16)
-      const int k0 = kb * BK + CPT * hf;  // this thread's part of the block
-      // (the other half's entries below it are skipped: they belong to the other thread)
-      while (oc0 < k0) {
-        oc0 = oc1; ov0 = ov1;
-        oc1 = oc2; ov1 = ov2;
-        oc2 = oc3; ov2 = ov3;
-        fetch(oc3, ov3);
-      }
-      while (oc0 < k0 + CPT) {
-        const int k = oc0 - kb * BK;
-        const uint32_t h = pack_bf16(ov0, 0.0f) & 0xFFFFu;
+      // the row's outliers in this half block overwrite their positions with their exact
+      // fp32 values (RNE to bf16)
+      auto put = [&](int col, float v) {
+        const int k = col - kb * BK;
+        const uint32_t h = pack_bf16(v, 0.0f) & 0xFFFFu;
         *reinterpret_cast<uint16_t*>(bt + ((((k >> 3) ^ (j & 7)) << 4) | ((k & 7) << 1))) = (uint16_t)h;
-        oc0 = oc1; ov0 = ov1;
-        oc1 = oc2; ov1 = ov2;
-        oc2 = oc3; ov2 = ov3;
-        fetch(oc3, ov3);
+      };
+      if (!DQ_NOOUT && cN > 0) {
+        put(cc0, cv0);
+        if (cN > 1) put(cc1, cv1);
+        for (int e = 2; e < cN; ++e) put(__ldg(a.col + cS + e), __ldg(a.val + cS + e));
       }
 #if !DQ_NOFENCE
       fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor cores
 #endif
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full_b[w]);
+      if (lane == 0) {
+        if (PAIR)  // the leader's MMA reads this CTA's half: arrive on the leader's barrier
+          mbar_arrive_cl(fb0 + (uint32_t)(w * sizeof(uint64_t)));
+        else
+          mbar_arrive(&full_b[w]);
+      }
     }
-    // ---------------- epilogue: TMEM -> bf16 -> HBM
-    mbar_wait(&acc_full, 0u);
+    // ---------------- epilogue: TMEM -> bf16 -> HBM (each CTA its own X rows x all BN)
+    pwait(&acc_full, 0u);
     tc_after_sync();
     epilogue_bf16<BN, NACC, NPW>(tmem_d, warp, lane, m0, n0, a.M, a.N, a.y);
   }
   tc_before_sync();
-  __syncthreads();
-  if (warp == 2)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d),
-                 "n"(TMEM_COLS));
+  if (PAIR) {
+    cluster_sync_all();  // both CTAs done with the pair's TMEM and barriers
+    if (warp == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_d),
+                   "n"(S::TMEM_COLS));
+  } else {
+    __syncthreads();
+    if (warp == 2)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d),
+                   "n"(S::TMEM_COLS));
+  }
+}
+
+__global__ void __launch_bounds__(dq::NT, 1)
+    k_dq_gemm(const __grid_constant__ CUtensorMap tm_x, const __grid_constant__ CUtensorMap tm_w,
+              const DqArgs a) {
+  dq_gemm_body<false>(&tm_x, &tm_w, a);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(dq::NT, 1)
+    k_dq_gemm_pair(const __grid_constant__ CUtensorMap tm_x,
+                   const __grid_constant__ CUtensorMap tm_w, const DqArgs a) {
+  dq_gemm_body<true>(&tm_x, &tm_w, a);
 }
 
 // ------------------------------------------------------------------ host side
+// The pair kernel for M > 256 (its 512-row tile would idle half of a pair below that),
+// the single-CTA one otherwise; QFT_DQ_PAIR=0/1 forces either (A/B).
+static int dq_pair_mode() {
+  static int mode = -2;
+  if (mode == -2) {
+    const char* e = getenv("QFT_DQ_PAIR");
+    mode = e ? atoi(e) : -1;
+  }
+  return mode;
+}
+
+size_t dq_gemm_workspace_bytes(int N, int K) {
+  return (size_t)N * (size_t)(K / 32 + 1) * sizeof(int32_t);
+}
+
 cudaError_t launch_dq_gemm(const void* x, int M, int K, const uint8_t* codes, int N,
                            const float* scale, const int32_t* zp, const int32_t* row_start,
                            const int32_t* row_count, const int32_t* col, const float* val,
-                           void* y, cudaStream_t st) {
+                           void* y, void* workspace, cudaStream_t st) {
   using namespace dq;
   auto enc = um::encode_fn();
   if (!enc) return cudaErrorNotSupported;
+  const int pm = dq_pair_mode();
+  const bool pair = pm >= 0 ? pm != 0 : M > 256;
+  const int XB = 256;
   CUtensorMap tx{}, tw{};
   {
     const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)M};
     const cuuint64_t strides[1] = {(cuuint64_t)K * 2};
-    const cuuint32_t box[2] = {BK, XBOX};
+    const cuuint32_t box[2] = {BK, (cuuint32_t)XB};
     const cuuint32_t es[2] = {1, 1};
     if (enc(&tx, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(x), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -347,23 +489,43 @@ cudaError_t launch_dq_gemm(const void* x, int M, int K, const uint8_t* codes, in
   {
     const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)N};
     const cuuint64_t strides[1] = {(cuuint64_t)K};
-    const cuuint32_t box[2] = {BK, BN};
+    const cuuint32_t box[2] = {BK, WROWS};
     const cuuint32_t es[2] = {1, 1};
     if (enc(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(codes), dims, strides, box,
             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_dq_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         SMEM_BYTES);
+  int32_t* tix = reinterpret_cast<int32_t*>(workspace);
+  {
+    cudaError_t e = launch_csr_tile_index(row_start, row_count, col, N, K / 32, 32, tix, st);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
-  DqArgs a{scale, zp, row_start, row_count, col, val, reinterpret_cast<__nv_bfloat16*>(y), M, N, K};
-  dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((M + BM - 1) / BM));
-  k_dq_gemm<<<grid, NT, SMEM_BYTES, st>>>(tx, tw, a);
+  DqArgs a{codes, scale, zp, row_start, row_count, col, val, tix,
+           reinterpret_cast<__nv_bfloat16*>(y), M, N, K};
+  if (pair) {
+    using S = Shape<true>;
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(k_dq_gemm_pair,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM_BYTES);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    dim3 grid((unsigned)(2 * ((N + S::BN - 1) / S::BN)), (unsigned)((M + 2 * S::BM - 1) / (2 * S::BM)));
+    k_dq_gemm_pair<<<grid, NT, S::SMEM_BYTES, st>>>(tx, tw, a);
+  } else {
+    using S = Shape<false>;
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(k_dq_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           S::SMEM_BYTES);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    dim3 grid((unsigned)((N + S::BN - 1) / S::BN), (unsigned)((M + S::BM - 1) / S::BM));
+    k_dq_gemm<<<grid, NT, S::SMEM_BYTES, st>>>(tx, tw, a);
+  }
   return cudaGetLastError();
 }
 

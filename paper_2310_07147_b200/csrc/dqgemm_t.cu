@@ -275,6 +275,15 @@ __global__ void __launch_bounds__(dqt::NT, 1)
 }
 
 // ------------------------------------------------------------------ host side
+cudaError_t launch_csr_tile_index(const int32_t* row_start, const int32_t* row_count,
+                                  const int32_t* col, int rows, int tiles, int tile_cols,
+                                  int32_t* tix, cudaStream_t st) {
+  const int64_t n = (int64_t)rows * (tiles + 1);
+  const int blocks = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+  k_csr_tile_index<<<blocks, 256, 0, st>>>(row_start, row_count, col, rows, tiles, tile_cols, tix);
+  return cudaGetLastError();
+}
+
 size_t dq_gemm_t_workspace_bytes(int O, int I) {
   return (size_t)O * ((I + dqt::BN - 1) / dqt::BN + 1) * sizeof(int32_t);
 }
@@ -317,10 +326,7 @@ cudaError_t launch_dq_gemm_t(const void* dy, int T, int O, const uint8_t* codes,
   const int tiles_n = (I + BN - 1) / BN;
   int32_t* tix = reinterpret_cast<int32_t*>(workspace);
   {
-    const int64_t n = (int64_t)O * (tiles_n + 1);
-    const int blocks = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
-    k_csr_tile_index<<<blocks, 256, 0, st>>>(row_start, row_count, col, O, tiles_n, BN, tix);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_csr_tile_index(row_start, row_count, col, O, tiles_n, BN, tix, st);
     if (e != cudaSuccess) return e;
   }
   DqtArgs a{scale, zp, tix, col, val, reinterpret_cast<__nv_bfloat16*>(dx), T, I, O, tiles_n};

@@ -230,12 +230,19 @@ cudaError_t crc32_device(const void* const* segs, const int64_t* lens, int n, ui
 // weight expansion (expand.cu): one launch per expand_max_tensors() tensors
 int expand_max_tensors();
 cudaError_t launch_expand(const qftc_expand_tensor* ts, int n, bool bf16, cudaStream_t s);
+// tix[r][t] = the first used slot entry of row r whose column is >= t * tile_cols (t < tiles),
+// tix[r][tiles] = the row's used end (dqgemm_t.cu, k_csr_tile_index)
+cudaError_t launch_csr_tile_index(const int32_t* row_start, const int32_t* row_count,
+                                  const int32_t* col, int rows, int tiles, int tile_cols,
+                                  int32_t* tix, cudaStream_t st);
 // the consumer GEMM with the weight dequantization fused into its operand producer
-// (dqgemm.cu): y[M,N] = x[M,K] . W^T, x / y bf16, W a dense-and-sparse QFT weight
+// (dqgemm.cu): y[M,N] = x[M,K] . W^T, x / y bf16, W a dense-and-sparse QFT weight;
+// workspace: the per-(row, 32-column) CSR index
+size_t dq_gemm_workspace_bytes(int N, int K);
 cudaError_t launch_dq_gemm(const void* x, int M, int K, const uint8_t* codes, int N,
                            const float* scale, const int32_t* zp, const int32_t* row_start,
                            const int32_t* row_count, const int32_t* col, const float* val,
-                           void* y, cudaStream_t s);
+                           void* y, void* workspace, cudaStream_t s);
 // re-plan slot capacities (csr.cu, k_replan_caps)
 cudaError_t launch_replan_caps(const uint8_t* codes, int rows, int cols, int bit_width,
                                const int32_t* cnt_out, const int32_t* cnt_in, int lvl, int gmul,

@@ -674,11 +674,15 @@ class QftModelState:
             raise ValueError(f"linear: x must be a contiguous bf16 [M, {c}] tensor")
         y = out if out is not None else torch.empty((x.shape[0], r), dtype=torch.bfloat16,
                                                     device=x.device)
+        need = int(N.lib.qftc_dequant_gemm_workspace_bytes(r, c))
+        ws = getattr(self, "_dq_ws", None)
+        if ws is None or ws.numel() < need:
+            ws = self._dq_ws = torch.empty(need, dtype=torch.uint8, device=self.device)
         N.check(N.lib.qftc_dequant_gemm(
             _p(x), x.shape[0], c, _p(self._sl(self.w_codes[cur], i)), r,
             _p(self._rows(self.w_scale, i)), _p(self._rows(self.w_zp, i)),
             _p(self._rs(self.row_start[cur], i)), _p(self._rows(self.row_count[cur], i)),
-            _p(g.col[cur]), _p(g.val[cur]), _p(y), _stream()))
+            _p(g.col[cur]), _p(g.val[cur]), _p(y), _p(ws), _stream()))
         return y
 
     def linear_backward(self, i: int, dy: torch.Tensor,

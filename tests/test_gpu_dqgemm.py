@@ -12,8 +12,11 @@ def _ref(x, wb):
     return (x.float() @ wb.float().t())
 
 
+# m <= 256 runs the single-CTA kernel, m > 256 the CTA-pair (cta_group::2) one
 @pytest.mark.parametrize("shape,m", [((256, 512), 200), ((384, 1024), 128), ((128, 4096), 77),
-                                     ((4096, 4096), 256), ((300, 11008), 130), ((11008, 4096), 64)])
+                                     ((4096, 4096), 256), ((300, 11008), 130), ((11008, 4096), 64),
+                                     ((256, 512), 1000), ((384, 1024), 257), ((4096, 4096), 1024),
+                                     ((300, 11008), 600), ((11008, 4096), 513), ((200, 256), 3000)])
 def test_dequant_gemm_matches_materialised(cuda, shape, m):
     torch.manual_seed(shape[0] + m)
     st = cuda.QftModelState([shape], bit_width=8)
