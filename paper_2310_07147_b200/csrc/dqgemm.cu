@@ -285,17 +285,18 @@ __device__ __forceinline__ void dq_gemm_body(const CUtensorMap* tm_x, const CUte
     }
     const bool fast = make_dequant_row(s_n, z_n).fast;
     const uint32_t fb0 = PAIR ? mapa_cl(&full_b[0], 0) : 0u;
-    // The thread's outliers of block kb are slot entries [tix[2kb + hf], tix[2kb + hf + 1])
-    // of its row (columns ascending, 32-column granularity = exactly its half of the block).
+    // The thread's outliers of block kb are slot entries [tix[H kb + hf], tix[H kb + hf + 1])
+    // of its row (H = HALVES; columns ascending, CPT-column granularity = exactly its part
+    // of the block).
     // Pipelined without dependent chains: block kb+2's index pair is loaded during block
     // kb, and block kb+1's first two entries during block kb -- each load is consumed one
     // block (~1 us) after issue.  More than two entries in a half block (rare at p <= 1%)
     // are loaded where they are written.
-    const int32_t* tr = a.tix + (size_t)(live ? n : 0) * (size_t)(2 * nkb + 1) + hf;
+    const int32_t* tr = a.tix + (size_t)(live ? n : 0) * (size_t)(HALVES * nkb + 1) + hf;
     auto tload = [&](int kb, int& s0, int& e0) {
       if (live && kb < nkb) {
-        s0 = __ldg(tr + 2 * kb);
-        e0 = __ldg(tr + 2 * kb + 1);
+        s0 = __ldg(tr + HALVES * kb);
+        e0 = __ldg(tr + HALVES * kb + 1);
       } else {
         s0 = e0 = 0;
       }
@@ -462,7 +463,7 @@ static int dq_pair_mode() {
 }
 
 size_t dq_gemm_workspace_bytes(int N, int K) {
-  return (size_t)N * (size_t)(K / 32 + 1) * sizeof(int32_t);
+  return (size_t)N * (size_t)(K / dq::CPT + 1) * sizeof(int32_t);
 }
 
 cudaError_t launch_dq_gemm(const void* x, int M, int K, const uint8_t* codes, int N,
@@ -498,7 +499,7 @@ cudaError_t launch_dq_gemm(const void* x, int M, int K, const uint8_t* codes, in
   }
   int32_t* tix = reinterpret_cast<int32_t*>(workspace);
   {
-    cudaError_t e = launch_csr_tile_index(row_start, row_count, col, N, K / 32, 32, tix, st);
+    cudaError_t e = launch_csr_tile_index(row_start, row_count, col, N, K / CPT, CPT, tix, st);
     if (e != cudaSuccess) return e;
   }
   DqArgs a{codes, scale, zp, row_start, row_count, col, val, tix,

@@ -71,28 +71,26 @@ struct DqtArgs {
   int tiles_n;
 };
 
-// tix[o][t] = the first entry of row o's slot whose column is >= t * BN (t < tiles_n), and
-// tix[o][tiles_n] = the slot's used end; slot entries are column-ascending.
+// tix[o][t] = the first entry of row o's slot whose column is >= t * tile_cols (t < tiles_n), and
+// tix[o][tiles_n] = the slot's used end; slot entries are column-ascending.  A warp per row,
+// linear in the row's entries: entry i is the answer for the tiles (tile(i-1), tile(i)], the
+// used end for the tiles past the last entry's.
 __global__ void k_csr_tile_index(const int32_t* row_start, const int32_t* row_count,
                                  const int32_t* col, int O, int tiles_n, int tile_cols,
                                  int32_t* tix) {
-  const int64_t n = (int64_t)O * (tiles_n + 1);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int o = (int)(i / (tiles_n + 1)), t = (int)(i % (tiles_n + 1));
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int o = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; o < O; o += warps) {
     const int b = row_start[o];
     const int e = b + (row_count ? min(row_count[o], row_start[o + 1] - b) : row_start[o + 1] - b);
-    int lo = b, hi = e;
-    if (t < tiles_n) {
-      const int c0 = t * tile_cols;
-      while (lo < hi) {  // lower_bound(col[b..e), c0)
-        const int mid = (lo + hi) >> 1;
-        if (col[mid] < c0) lo = mid + 1; else hi = mid;
-      }
-    } else {
-      lo = e;
+    int32_t* out = tix + (size_t)o * (tiles_n + 1);
+    for (int i = b + lane; i < e; i += 32) {
+      const int t = col[i] / tile_cols;
+      const int tp = i > b ? col[i - 1] / tile_cols : -1;
+      for (int u = tp + 1; u <= t; ++u) out[u] = i;
     }
-    tix[i] = lo;
+    const int tl = e > b ? col[e - 1] / tile_cols : -1;
+    for (int u = tl + 1 + lane; u <= tiles_n; u += 32) out[u] = e;
   }
 }
 
@@ -278,8 +276,7 @@ __global__ void __launch_bounds__(dqt::NT, 1)
 cudaError_t launch_csr_tile_index(const int32_t* row_start, const int32_t* row_count,
                                   const int32_t* col, int rows, int tiles, int tile_cols,
                                   int32_t* tix, cudaStream_t st) {
-  const int64_t n = (int64_t)rows * (tiles + 1);
-  const int blocks = (int)((n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096);
+  const int blocks = (rows + 7) / 8 < 4096 ? (rows + 7) / 8 : 4096;  // a warp per row
   k_csr_tile_index<<<blocks, 256, 0, st>>>(row_start, row_count, col, rows, tiles, tile_cols, tix);
   return cudaGetLastError();
 }
