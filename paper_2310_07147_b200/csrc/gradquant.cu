@@ -80,6 +80,51 @@ __device__ __forceinline__ uint32_t gq_quant4(const float* x, const QuantRow& q,
 #endif
 }
 
+#ifndef QFT_GQ_BRANCHFREE
+#define QFT_GQ_BRANCHFREE 1
+#endif
+// The exact quantizer without a fast path or a branch (QFT_GQ_BRANCHFREE), for rows with
+// s in [2^-100, 2^125] and |z| + qmax + 2 < 2^21 (QuantRow.fast && s >= 2^-100):
+//   y = RN(x * RN(1/s)) is within 2^-22 of x/s, so the reference's round_half_away of the
+//   fp64 quotient (quantize.hpp:160-166) is fl or fl + 1, fl = floor(y): it is fl + 1 iff
+//   x/s > h = fl + 1/2, or x/s == h and h > 0 (a tie goes away from zero).  The sign of
+//   h*s - x is exact in one FMA (the product is exact, one rounding keeps the sign; s >=
+//   2^-100 keeps a nonzero difference normal), and RN_d(x/s) == h only when x == h*s
+//   (DESIGN §4).  The code is then clamp(k, -z, qmax - z) + z: the clamp also takes
+//   +-Inf (fl = +-Inf, the FMA is NaN: k = fl) and NaN (fmax/fmin drop it: code 0, the
+//   reference's !(q > 0)) -- no per-value test, no divergent exact path; bf16 gradients
+//   put a quarter of their values near a half-integer, which made the checked fast path
+//   branch and fall back per group of 4.
+__device__ __forceinline__ uint32_t gq_quant4_bf(const float* x, const QuantRow& q) {
+  float t[4];
+#pragma unroll
+  for (int i = 0; i < 4; i += 2) {
+    const float2 xv = make_float2(x[i], x[i + 1]);
+    const float2 y = mul2(xv, f2(q.inv_s));
+    const float2 fl = make_float2(floorf(y.x), floorf(y.y));
+    const float2 h = add2(fl, f2(0.5f));
+    const float2 r = fma2(h, f2(q.s), neg2(xv));
+    float k0 = (r.x < 0.0f || (r.x == 0.0f && h.x > 0.0f)) ? __fadd_rn(fl.x, 1.0f) : fl.x;
+    float k1 = (r.y < 0.0f || (r.y == 0.0f && h.y > 0.0f)) ? __fadd_rn(fl.y, 1.0f) : fl.y;
+    k0 = fminf(fmaxf(k0, q.ylo), q.yhi);
+    k1 = fminf(fmaxf(k1, q.ylo), q.yhi);
+    const float2 m = add2(make_float2(k0, k1), f2(q.magic));  // integers: exact
+    t[i] = m.x;
+    t[i + 1] = m.y;
+  }
+  const uint32_t p01 = __byte_perm(__float_as_uint(t[0]), __float_as_uint(t[1]), 0x0040u);
+  const uint32_t p23 = __byte_perm(__float_as_uint(t[2]), __float_as_uint(t[3]), 0x0040u);
+  return __byte_perm(p01, p23, 0x5410u);
+}
+// the codes of four values of a row whose quantizer is q (bf: the branch-free form applies)
+__device__ __forceinline__ uint32_t gq_codes4(const float* x, const QuantRow& q, bool bf) {
+  if (QFT_GQ_BRANCHFREE && bf) return gq_quant4_bf(x, q);
+  float em = 0.0f;
+  uint32_t c = q.fast ? gq_quant4(x, q, em) : 0u;
+  if (!q.fast || !(em < q.thr)) c = quant4_exact_fast(x, q);
+  return c;
+}
+
 template <bool BF16, int NT, int VPL>
 __global__ void __launch_bounds__(NT + 32) k_grad_quant(const LaunchArgs a, int stage_bytes) {
   using namespace gq;
@@ -132,6 +177,7 @@ __global__ void __launch_bounds__(NT + 32) k_grad_quant(const LaunchArgs a, int 
     q.magic = __fadd_rn(kMagicRound, (float)q.z);
     q.thr = 0.5f - (float)((q.z < 0 ? -(int64_t)q.z : (int64_t)q.z) + qmax + 2) * 0x1.0p-21f;
     q.fast = prm[p][3] != 0.0f;
+    const bool bf = q.fast && q.s >= 0x1.0p-100f;
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
       const int i = t + j * NT;
@@ -140,11 +186,7 @@ __global__ void __launch_bounds__(NT + 32) k_grad_quant(const LaunchArgs a, int 
         unpack<BF16>(vec(st, i), x);
         uint32_t c[EPV / 4];
 #pragma unroll
-        for (int k = 0; k < EPV / 4; ++k) {
-          float em = 0.0f;
-          c[k] = q.fast ? gq_quant4(x + 4 * k, q, em) : 0u;
-          if (!q.fast || !(em < q.thr)) c[k] = quant4_exact_fast(x + 4 * k, q);
-        }
+        for (int k = 0; k < EPV / 4; ++k) c[k] = gq_codes4(x + 4 * k, q, bf);
         if constexpr (BF16)
           __stcs(reinterpret_cast<uint2*>(dst) + i, make_uint2(c[0], c[1]));
         else
@@ -363,6 +405,7 @@ __global__ void __launch_bounds__(NT) k_rs_grad_quant(const LaunchArgs a, const 
     }
     __syncthreads();
     const QuantRow q = make_quant_row(prm[0], __float_as_int(prm[1]), bw);
+    const bool bf = q.fast && q.s >= 0x1.0p-100f;
     uint8_t* dst = const_cast<uint8_t*>(T.g_codes) + (size_t)r * T.cols;
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
@@ -370,11 +413,7 @@ __global__ void __launch_bounds__(NT) k_rs_grad_quant(const LaunchArgs a, const 
       if (i < nv) {
         uint32_t c[2];
 #pragma unroll
-        for (int k = 0; k < 2; ++k) {
-          float em = 0.0f;
-          c[k] = q.fast ? gq_quant4(sum[j] + 4 * k, q, em) : 0u;
-          if (!q.fast || !(em < q.thr)) c[k] = quant4_exact_fast(sum[j] + 4 * k, q);
-        }
+        for (int k = 0; k < 2; ++k) c[k] = gq_codes4(sum[j] + 4 * k, q, bf);
         __stcs(reinterpret_cast<uint2*>(dst) + i, make_uint2(c[0], c[1]));
       }
     }

@@ -17,12 +17,20 @@ def _eq(a, b, what):
     assert n == 0, f"{what}: {n} mismatches, first at {np.argwhere(bad)[:5].tolist()}"
 
 
-def _grad(port, sh, seed, step):
+def _grad(port, sh, seed, step, bw=8):
     g = port.synth(sh, seed, 1e-3, 0.0)
     g[0] = 0.0                       # all-zero gradient row (constant channel params)
     g[1] = 2.5e-4                    # constant row
     g[2] *= 1e-30                    # tiny scale
     g[3, ::7] = 0.05 * (step + 1)    # a few large entries: coarse row scale
+    # exact ties: bounds -c/1024, (qmax-c)/1024 give s = 2^-10, and every other value is a
+    # half-integer multiple of s (bf16-exact) -- round_half_away must go away from zero
+    qmax = (1 << bw) - 1
+    c = (qmax + 1) // 2
+    ties = (np.arange(-c, qmax - c) + 0.5) * 2.0 ** -10
+    g[4] = np.resize(ties, sh[1]).astype(np.float32)
+    g[4, 0], g[4, 1] = -c * 2.0 ** -10, (qmax - c) * 2.0 ** -10
+    g[5, 3::97] = np.nan             # NaN values (not in column 0): code 0
     return g
 
 
@@ -51,7 +59,7 @@ def test_rows_path_raw_gradient_matches_oracle(cuda, port, gkind, cols, bw, lr, 
         assert N.lib.qftc_plan_launches(g.plan) >= 4, "raw gradient did not take the rows path"
     for step in range(4):
         for i, sh in enumerate(shapes):
-            g = _grad(port, sh, 900 + 10 * step + i, step)
+            g = _grad(port, sh, 900 + 10 * step + i, step, bw)
             gt = torch.from_numpy(g)
             if gkind == "bf16":
                 gt = gt.to(torch.bfloat16)
