@@ -231,8 +231,13 @@ class QftModelState:
     def _mirror_layout(self, g: _Group, src: int):
         """Give the other set the same slot layout and an arena of the same size."""
         dst = 1 - src
-        for i in g.members:
-            self._rs(self.row_start[dst], i).copy_(self._rs(self.row_start[src], i))
+        if self._layout(g)[2]:  # contiguous members: one copy of the group's row starts
+            p0 = int(self.rpoff[self.pos[g.members[0]]])
+            p1 = int(self.rpoff[self.pos[g.members[-1]] + 1])
+            self.row_start[dst][p0:p1].copy_(self.row_start[src][p0:p1])
+        else:
+            for i in g.members:
+                self._rs(self.row_start[dst], i).copy_(self._rs(self.row_start[src], i))
         need = g.col[src].numel()
         if g.col[dst] is None or g.col[dst].numel() < need:
             g.col[dst], g.val[dst] = self._alloc(need)
@@ -406,6 +411,7 @@ class QftModelState:
             N.check(N.lib.qftc_plan_create(C.byref(plan), arr, len(g.members), self.bit_width,
                                            self.grad_kind, cols, vals, caps, _stream()))
             g.plan = plan
+            self._layout(g)  # the re-plan bookkeeping, off the checked step's path
         self._plan_order = None
 
     def step_plans(self):
@@ -504,6 +510,34 @@ class QftModelState:
             return
         self._check(*self._last)
 
+    def _layout(self, g: _Group):
+        """(row-start positions of the group's tensors in the flat row_start arrays, their
+        indices in the group's scanned capacities, members contiguous?) -- built once
+        (numpy; 200+ members) and kept on the device."""
+        if g.layout_idx is None:
+            pos, idx, rb = [], [], 0
+            for i in g.members:
+                r = self.shapes[i][0]
+                p0 = int(self.rpoff[self.pos[i]])
+                pos.append(np.arange(p0, p0 + r + 1, dtype=np.int64))
+                idx.append(np.arange(rb, rb + r + 1, dtype=np.int64))
+                rb += r
+            ps = [self.pos[i] for i in g.members]
+            contiguous = ps == list(range(ps[0], ps[0] + len(ps)))
+            g.layout_idx = (torch.from_numpy(np.concatenate(pos)).to(self.device),
+                            torch.from_numpy(np.concatenate(idx)).to(self.device), contiguous)
+            # first use of the re-plan's scan / gather / scatter kernels, on scratch of the
+            # same sizes: their lazy module loads (~30 ms) stay out of the first checked
+            # step that overflows
+            caps = torch.zeros(g.rows, dtype=torch.int64, device=self.device)
+            cum = torch.zeros(g.rows + 1, dtype=torch.int64, device=self.device)
+            torch.cumsum(caps, 0, out=cum[1:])
+            scratch = torch.zeros_like(self.row_start[0])
+            scratch.index_copy_(0, g.layout_idx[0],
+                                cum.index_select(0, g.layout_idx[1]).to(torch.int32))
+            int(cum[-1].item())
+        return g.layout_idx
+
     def _replan(self, g: _Group, k: int):
         """Slots of set k re-sized from its (true) counts plus, as at placement
         (_place_strict), the dense elements at code 0 / qmax of the step's output codes:
@@ -515,18 +549,7 @@ class QftModelState:
         slack 8 -> 32 -> 64 entries -- instead of re-planning again the next step.  Batched over the group: one
         row-count pass, one scan, one scatter into the slot starts, one synchronisation."""
         dev = self.device
-        if g.layout_idx is None:
-            pos, idx, rb = [], [], 0
-            for i in g.members:
-                r = self.shapes[i][0]
-                p0 = int(self.rpoff[self.pos[i]])
-                pos.append(torch.arange(p0, p0 + r + 1, dtype=torch.int64))
-                idx.append(torch.arange(rb, rb + r + 1, dtype=torch.int64))
-                rb += r
-            ps = [self.pos[i] for i in g.members]
-            contiguous = ps == list(range(ps[0], ps[0] + len(ps)))
-            g.layout_idx = (torch.cat(pos).to(dev), torch.cat(idx).to(dev), contiguous)
-        rs_pos, scan_idx, contiguous = g.layout_idx
+        rs_pos, scan_idx, contiguous = self._layout(g)
         lvl = min(g.replans, 3)
         # one pass over the output codes per tensor run (qftc_csr_replan_caps): edge codes,
         # growth, headroom -> per-row capacities, no temporaries
@@ -548,7 +571,7 @@ class QftModelState:
         self.row_start[k].index_copy_(0, rs_pos, cum.index_select(0, scan_idx).to(torch.int32))
         g.replans += 1
         if g.col[k].numel() < total:  # grow with headroom: a drifting state re-plans again
-            g.col[k], g.val[k] = self._alloc(total + total // 4)
+            g.col[k], g.val[k] = self._alloc(total + total // 2)
 
     def _check(self, flip, h):
         out = 1 - flip
