@@ -4,6 +4,7 @@
 # large-lr probes, the launch list of the default bench and ncu --set full captures of the
 # rows kernels, the gradient quantizer, the expansion kernel and the fused GEMM.
 T=$1
+mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/${T}_smi.txt 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1
 python -m pytest tests -m gpu -q > gpurun_out/${T}_pytest.log 2>&1
