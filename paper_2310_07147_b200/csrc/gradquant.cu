@@ -134,6 +134,9 @@ __global__ void __launch_bounds__(NT + 32) k_grad_quant(const LaunchArgs a, int 
   __shared__ float red[2][2][NW];
   __shared__ float prm[2][4];  // per row parity: s, z, RN(1/s), fast
   __shared__ __align__(8) uint64_t bars[GQ_NS];
+  // the tensor of the row each stage holds: written by the issuing thread before the
+  // stage's TMA (read after the stage's barrier), so the workers never walk the table
+  __shared__ int s_ti[GQ_NS];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const bool ctrl = wid == NW;  // the control warp: TMA issue + the row's quantizer
   const int tc = NT;            // its lane 0
@@ -143,14 +146,15 @@ __global__ void __launch_bounds__(NT + 32) k_grad_quant(const LaunchArgs a, int 
   const int G = (int)gridDim.x;
   const int TR = a.total_rows;
   // rows come in increasing order per CTA: the tensor index only moves forward
-  int ti_issue = 0, ti_cur = 0;
+  int ti_issue = 0;
   auto tensor_of = [&](int row, int& ti) -> const DevTensor& {
     while (ti + 1 < a.n_tensors && a.tensors[ti + 1].row_base <= row) ++ti;
     return a.tensors[ti];
   };
-  // thread 0: row `row` into stage st (one bulk copy of the row)
+  // the control thread: row `row` into stage st (one bulk copy of the row)
   auto issue = [&](int row, int st) {
     const DevTensor& T = tensor_of(row, ti_issue);
+    s_ti[st] = ti_issue;
     const uint32_t nb = (uint32_t)T.cols * (BF16 ? 2u : 4u);
     mbar_arrive_expect_tx(&bars[st], nb);
     bulk_g2s(gsm + (size_t)st * stage_bytes,
@@ -161,10 +165,9 @@ __global__ void __launch_bounds__(NT + 32) k_grad_quant(const LaunchArgs a, int 
     return reinterpret_cast<const uint4*>(gsm + (size_t)st * stage_bytes)[i];
   };
   // quantize row `row` (stage st, quantizer of parity p) and store its codes
-  int ti_q = 0;
   auto quantize_store = [&](int row, int st, int p) {
     if (ctrl) return;
-    const DevTensor& T = tensor_of(row, ti_q);
+    const DevTensor& T = a.tensors[s_ti[st]];
     const int nv = T.cols / EPV;
     uint8_t* dst = const_cast<uint8_t*>(T.g_codes) + (size_t)(row - T.row_base) * T.cols;
     QuantRow q;
@@ -209,11 +212,10 @@ __global__ void __launch_bounds__(NT + 32) k_grad_quant(const LaunchArgs a, int 
   int it = 0, par = 0;
   for (;; ++it, par ^= 1) {
     const int st = it % GQ_NS;
-    const DevTensor& T = tensor_of(gr, ti_cur);
     float lo = __int_as_float(0x7f800000), hi = __int_as_float(0xff800000);
     if (!ctrl) {
       mbar_wait(&bars[st], (uint32_t)((it / GQ_NS) & 1));
-      const int nv = T.cols / EPV;
+      const int nv = a.tensors[s_ti[st]].cols / EPV;
       // row gr: min/max partials (vectors past the row end repeat vector 0: same range)
 #pragma unroll
       for (int j = 0; j < VPL; ++j) {
@@ -246,6 +248,7 @@ __global__ void __launch_bounds__(NT + 32) k_grad_quant(const LaunchArgs a, int 
       // column 0: a NaN there is the initial bound and sticks (tensor.hpp:133-148)
       float x0[EPV];
       mbar_wait(&bars[st], (uint32_t)((it / GQ_NS) & 1));  // (complete: the workers saw it)
+      const DevTensor& T = a.tensors[s_ti[st]];
       unpack<BF16>(vec(st, 0), x0);
       if (x0[0] != x0[0]) lo = hi = x0[0];
       float s;
