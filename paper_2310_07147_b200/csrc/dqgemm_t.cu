@@ -10,7 +10,7 @@
 // The forward kernel (dqgemm.cu) reads W K-major (rows of W = output channels = N); here W's
 // rows are the REDUCTION dimension, so the operand is MN-major: a K block is 64 rows of W,
 // each contributing BN contiguous columns -- one 128-byte SWIZZLE_128B row per 64 columns.
-// A W row's CSR outliers inside the CTA's BN columns are located through a per-(row, column
+// A W row's CSR outliers inside a producer's 32 columns are located through a per-(row, 32-column
 // tile) index built by a small pre-pass (k_csr_tile_index: the first slot entry at or past
 // each tile's first column), so a producer scans only the ~1-2 entries of its own window.
 //
@@ -58,12 +58,13 @@ constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
                            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 constexpr int TMEM_COLS = NACC * BN;
 constexpr uint32_t B_LBO = 64 * BK * 2;  // bytes between the operand's 64-column MN chunks
+constexpr int TC = 32;                   // columns per tile of the CSR index (a producer's)
 }  // namespace dqt
 
 struct DqtArgs {
   const float* scale;     // [O]
   const int32_t* zp;      // [O]
-  const int32_t* tix;     // [O, tiles_n + 1] arena positions: first entry of each column tile
+  const int32_t* tix;     // [O, tiles_n + 1] arena positions: first entry of each 32-column tile
   const int32_t* col;     // arena
   const float* val;
   __nv_bfloat16* y;       // [M, N] = dX [T, I]
@@ -183,24 +184,54 @@ __global__ void __launch_bounds__(dqt::NT, 1)
     // ---------------- dequant producers: thread (r, j, h) of the 64 x 2 x 2 units
     const int pt = threadIdx.x - 128;
     const int r = pt >> 2, j = (pt >> 1) & 1, h = pt & 1;
-    const int tn = blockIdx.x;
     const int cbeg = n0 + 64 * j + 32 * h;  // this thread's 32 columns of the W rows
-    // the block's row parameters, loaded one block ahead
-    auto load_row = [&](int kb, float& s, int32_t& z, int& eb, int& ee) {
+    const int tq = cbeg / TC;                // ... = column tile tq of the index
+    // The block's row parameters are loaded one block ahead; the row's slot range of the
+    // thread's 32 columns (the index) two blocks ahead, and its first two entries one block
+    // ahead -- no load is consumed within a block of its issue (a scan that loaded each
+    // entry where it was written stalled every producer on that load)
+    auto load_row = [&](int kb, float& s, int32_t& z) {
       const int o = kb * BK + r;
       s = __ldg(a.scale + o);
       z = __ldg(a.zp + o);
-      const int32_t* t = a.tix + (size_t)o * (a.tiles_n + 1) + tn;
-      eb = __ldg(t);
-      ee = __ldg(t + 1);
+    };
+    auto load_ix = [&](int kb, int& eb, int& ee) {
+      if (kb < nkb && cbeg < a.N) {  // (columns past I: no entries, no index tile)
+        const int32_t* t = a.tix + (size_t)(kb * BK + r) * (a.tiles_n + 1) + tq;
+        eb = __ldg(t);
+        ee = __ldg(t + 1);
+      } else {
+        eb = ee = 0;
+      }
+    };
+    int nS = 0, nN = 0, nc0 = 0, nc1 = 0;  // the next block's range and first two entries
+    float nv0 = 0.0f, nv1 = 0.0f;
+    auto eload = [&](int e0, int e1) {
+      nS = e0;
+      nN = e1 - e0;
+      if (nN > 0) {
+        nc0 = __ldg(a.col + e0);
+        nv0 = __ldg(a.val + e0);
+      }
+      if (nN > 1) {
+        nc1 = __ldg(a.col + e0 + 1);
+        nv1 = __ldg(a.val + e0 + 1);
+      }
     };
     float s_n, s_nx = 0.0f;
     int32_t z_n, z_nx = 0;
-    int eb, ee, eb_nx = 0, ee_nx = 0;
-    load_row(0, s_n, z_n, eb, ee);
+    int ebA, eeA;
+    load_row(0, s_n, z_n);
+    load_ix(0, ebA, eeA);
+    eload(ebA, eeA);
+    load_ix(1, ebA, eeA);
     for (int kb = 0; kb < nkb; ++kb) {
       const int w = kb % WSTAGES, c = kb % CSTAGES;
-      if (kb + 1 < nkb) load_row(kb + 1, s_nx, z_nx, eb_nx, ee_nx);
+      const int cS = nS, cN = nN, cc0 = nc0, cc1 = nc1;
+      const float cv0 = nv0, cv1 = nv1;
+      eload(ebA, eeA);
+      load_ix(kb + 2, ebA, eeA);
+      if (kb + 1 < nkb) load_row(kb + 1, s_nx, z_nx);
       mbar_wait(&full_c[c], (uint32_t)((kb / CSTAGES) & 1));
       // the code tile is TMA-swizzled (SWIZZLE_128B: 16-byte chunk k of row r at k ^ (r & 7)),
       // so the 8 rows a warp reads hit distinct banks
@@ -243,23 +274,22 @@ __global__ void __launch_bounds__(dqt::NT, 1)
             make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
       }
       // the row's outliers in [cbeg, cbeg + 32): exact fp32 values, RNE to bf16
-      for (int e = eb; e < ee; ++e) {
-        const int cc = __ldg(a.col + e);
-        if (cc >= cbeg + 32) break;
-        if (cc >= cbeg) {
-          const int k = cc - n0 - 64 * j;  // 0..63 within the MN chunk row
-          const uint32_t hv = pack_bf16(__ldg(a.val + e), 0.0f) & 0xFFFFu;
-          *reinterpret_cast<uint16_t*>(bt + ((((k >> 3) ^ (r & 7)) << 4) | ((k & 7) << 1))) =
-              (uint16_t)hv;
-        }
+      auto put = [&](int cc, float v) {
+        const int k = cc - n0 - 64 * j;  // 0..63 within the MN chunk row
+        const uint32_t hv = pack_bf16(v, 0.0f) & 0xFFFFu;
+        *reinterpret_cast<uint16_t*>(bt + ((((k >> 3) ^ (r & 7)) << 4) | ((k & 7) << 1))) =
+            (uint16_t)hv;
+      };
+      if (cN > 0) {
+        put(cc0, cv0);
+        if (cN > 1) put(cc1, cv1);
+        for (int e = 2; e < cN; ++e) put(__ldg(a.col + cS + e), __ldg(a.val + cS + e));
       }
       fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor cores
       __syncwarp();
       if (lane == 0) mbar_arrive(&full_b[w]);
       s_n = s_nx;
       z_n = z_nx;
-      eb = eb_nx;
-      ee = ee_nx;
     }
     mbar_wait(&acc_full, 0u);
     tc_after_sync();
@@ -282,7 +312,7 @@ cudaError_t launch_csr_tile_index(const int32_t* row_start, const int32_t* row_c
 }
 
 size_t dq_gemm_t_workspace_bytes(int O, int I) {
-  return (size_t)O * ((I + dqt::BN - 1) / dqt::BN + 1) * sizeof(int32_t);
+  return (size_t)O * ((I + dqt::TC - 1) / dqt::TC + 1) * sizeof(int32_t);
 }
 
 cudaError_t launch_dq_gemm_t(const void* dy, int T, int O, const uint8_t* codes, int I,
@@ -320,13 +350,14 @@ cudaError_t launch_dq_gemm_t(const void* dy, int T, int O, const uint8_t* codes,
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int tiles_n = (I + BN - 1) / BN;
+  const int tiles_n = (I + BN - 1) / BN;  // output column tiles (grid)
+  const int ix_tiles = (I + TC - 1) / TC;  // index tiles: one per producer thread's columns
   int32_t* tix = reinterpret_cast<int32_t*>(workspace);
   {
-    cudaError_t e = launch_csr_tile_index(row_start, row_count, col, O, tiles_n, BN, tix, st);
+    cudaError_t e = launch_csr_tile_index(row_start, row_count, col, O, ix_tiles, TC, tix, st);
     if (e != cudaSuccess) return e;
   }
-  DqtArgs a{scale, zp, tix, col, val, reinterpret_cast<__nv_bfloat16*>(dx), T, I, O, tiles_n};
+  DqtArgs a{scale, zp, tix, col, val, reinterpret_cast<__nv_bfloat16*>(dx), T, I, O, ix_tiles};
   dim3 grid((unsigned)tiles_n, (unsigned)((T + BM - 1) / BM));
   k_dq_gemm_t<<<grid, NT, SMEM_BYTES, st>>>(tdy, tw, a);
   return cudaGetLastError();
