@@ -29,6 +29,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "qft_device.cuh"
 #include "qft_internal.h"
@@ -39,25 +40,33 @@ using namespace qftd;
 
 namespace dqt {
 using namespace um;
-constexpr int BN = 128;          // output columns (W columns) per CTA: UMMA N
-constexpr int NACC = 512 / BN;   // 4 accumulators of M = 128 (all 512 TMEM columns)
-constexpr int BM = 128 * NACC;   // output rows (tokens) per CTA
+constexpr int WC = 128;          // W columns dequantized per CTA (= UMMA N of one CTA)
 constexpr int BK = 64;           // W rows per K block
-constexpr int STAGES = 2;        // dY ring
 constexpr int WSTAGES = 4;       // dequantized W-operand ring (producers run ahead)
 constexpr int CSTAGES = 4;       // W-code ring
-constexpr int A_BYTES = BM * BK * 2;
-constexpr int B_BYTES = BN * BK * 2;  // BN/64 MN chunks of 64 x 64 bf16 (8 KB each)
-constexpr int C_BYTES = BN * BK;
-constexpr int SMEM_BYTES = STAGES * A_BYTES + WSTAGES * B_BYTES + CSTAGES * C_BYTES + 1024;
+constexpr int B_BYTES = WC * BK * 2;  // WC/64 MN chunks of 64 x 64 bf16 (8 KB each)
+constexpr int C_BYTES = WC * BK;
 constexpr int NPW = 8;                // producer warps
 constexpr int NT = 128 + 32 * NPW;
 constexpr int XBOX = 256;
-// D f32, A/B bf16, A K-major, B MN-major (bit 16), N = BN, M = 128
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
-                           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-constexpr int TMEM_COLS = NACC * BN;
 constexpr uint32_t B_LBO = 64 * BK * 2;  // bytes between the operand's 64-column MN chunks
+// single CTA: 512 x 128 output tile, four M=128 x N=128 accumulators, 2-stage dY ring;
+// CTA pair (cta_group::2): 512 x 256 tile per pair, each CTA 256 dY rows (two M=256
+// halves) and 128 of the 256 W columns, 4-stage dY ring (dqgemm.cu has the plumbing notes)
+template <bool PAIR>
+struct ShapeT {
+  static constexpr int BN = PAIR ? 256 : 128;  // UMMA N: output columns per tile
+  static constexpr int NACC = PAIR ? 2 : 4;
+  static constexpr int BM = PAIR ? 256 : 512;  // dY rows per CTA
+  static constexpr int STAGES = PAIR ? 4 : 2;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int SMEM_BYTES = STAGES * A_BYTES + WSTAGES * B_BYTES + CSTAGES * C_BYTES + 1024;
+  // D f32, A/B bf16, A K-major, B MN-major (bit 16), N = BN, M = 128 or 256 (pair)
+  static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
+                                    ((uint32_t)(BN >> 3) << 17) |
+                                    ((uint32_t)((PAIR ? 256 : 128) >> 4) << 24);
+  static constexpr int TMEM_COLS = NACC * BN;  // 512
+};
 constexpr int TC = 32;                   // columns per tile of the CSR index (a producer's)
 }  // namespace dqt
 
@@ -95,17 +104,24 @@ __global__ void k_csr_tile_index(const int32_t* row_start, const int32_t* row_co
   }
 }
 
-__global__ void __launch_bounds__(dqt::NT, 1)
-    k_dq_gemm_t(const __grid_constant__ CUtensorMap tm_dy, const __grid_constant__ CUtensorMap tm_w,
-                const DqtArgs a) {
+template <bool PAIR>
+__device__ __forceinline__ void dq_gemm_t_body(const CUtensorMap* tm_dy, const CUtensorMap* tm_w,
+                                               const DqtArgs& a) {
   using namespace dqt;
+  using S = ShapeT<PAIR>;
+  constexpr int BN = S::BN, NACC = S::NACC, BM = S::BM, STAGES = S::STAGES, A_BYTES = S::A_BYTES;
   extern __shared__ uint8_t dsm_raw[];
   uint8_t* dsm = dsm_raw + ((1024u - (smem_u32(dsm_raw) & 1023u)) & 1023u);
   __shared__ __align__(8) uint64_t full_a[STAGES], empty_a[STAGES], full_b[WSTAGES], empty_b[WSTAGES];
   __shared__ __align__(8) uint64_t full_c[CSTAGES], empty_c[CSTAGES], acc_full;
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  // pair: blockIdx.x = 2 * (256-column tile) + rank; CTA `rank` holds dY rows
+  // m0 = 512 * blockIdx.y + 256 * rank and dequantizes W columns wn0 = n0 + 128 * rank
+  const int n0 = PAIR ? (int)(blockIdx.x >> 1) * BN : (int)blockIdx.x * BN;
+  const int m0 = PAIR ? (int)blockIdx.y * 2 * BM + (int)rank * BM : (int)blockIdx.y * BM;
+  const int wn0 = n0 + (int)rank * WC;
   const int nkb = a.K / BK;
   auto a_tile = [&](int s) { return dsm + s * A_BYTES; };
   auto b_tile = [&](int w) { return dsm + STAGES * A_BYTES + w * B_BYTES; };
@@ -117,7 +133,7 @@ __global__ void __launch_bounds__(dqt::NT, 1)
       mbar_init(&empty_a[s], 1);
     }
     for (int w = 0; w < WSTAGES; ++w) {
-      mbar_init(&full_b[w], NPW);
+      mbar_init(&full_b[w], PAIR ? 2 * NPW : NPW);  // pair: both CTAs' producers (leader's)
       mbar_init(&empty_b[w], 1);
     }
     for (int c = 0; c < CSTAGES; ++c) {
@@ -128,13 +144,23 @@ __global__ void __launch_bounds__(dqt::NT, 1)
     mbar_fence_init();
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&tmem_base)),
-                 "n"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&tmem_base)),
+                   "n"(S::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&tmem_base)),
+                   "n"(S::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_before_sync();
-  __syncthreads();
+  if (PAIR)
+    cluster_sync_all();
+  else
+    __syncthreads();
   tc_after_sync();
   const uint32_t tmem_d = tmem_base;
 
@@ -143,10 +169,18 @@ __global__ void __launch_bounds__(dqt::NT, 1)
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % STAGES;
         mbar_wait(&empty_a[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
-        mbar_arrive_expect_tx(&full_a[s], (uint32_t)A_BYTES);
+        if (PAIR) {  // both CTAs' bytes complete on the leader's barrier
+          if (rank == 0) mbar_arrive_expect_tx(&full_a[s], (uint32_t)(2 * A_BYTES));
+          const uint32_t bar = mapa_cl(&full_a[s], 0);
 #pragma unroll
-        for (int xb = 0; xb < BM / XBOX; ++xb)
-          tma_load_2d(a_tile(s) + xb * XBOX * 128, &tm_dy, kb * BK, m0 + xb * XBOX, &full_a[s]);
+          for (int xb = 0; xb < BM / XBOX; ++xb)
+            tma_load_2d_pair(a_tile(s) + xb * XBOX * 128, tm_dy, kb * BK, m0 + xb * XBOX, bar);
+        } else {
+          mbar_arrive_expect_tx(&full_a[s], (uint32_t)A_BYTES);
+#pragma unroll
+          for (int xb = 0; xb < BM / XBOX; ++xb)
+            tma_load_2d(a_tile(s) + xb * XBOX * 128, tm_dy, kb * BK, m0 + xb * XBOX, &full_a[s]);
+        }
       }
     }
   } else if (warp == 3) {
@@ -155,15 +189,20 @@ __global__ void __launch_bounds__(dqt::NT, 1)
         const int c = kb % CSTAGES;
         mbar_wait(&empty_c[c], (uint32_t)(((kb / CSTAGES) & 1) ^ 1));
         mbar_arrive_expect_tx(&full_c[c], (uint32_t)C_BYTES);
-        tma_load_2d(c_tile(c), &tm_w, n0, kb * BK, &full_c[c]);
+        tma_load_2d(c_tile(c), tm_w, wn0, kb * BK, &full_c[c]);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
+    if (lane == 0 && rank == 0) {  // ---------------- MMA issuer (the pair's leader)
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % STAGES, w = kb % WSTAGES;
-        mbar_wait(&full_a[s], (uint32_t)((kb / STAGES) & 1));
-        mbar_wait(&full_b[w], (uint32_t)((kb / WSTAGES) & 1));
+        if (PAIR) {
+          mbar_wait_cl(&full_a[s], (uint32_t)((kb / STAGES) & 1));
+          mbar_wait_cl(&full_b[w], (uint32_t)((kb / WSTAGES) & 1));
+        } else {
+          mbar_wait(&full_a[s], (uint32_t)((kb / STAGES) & 1));
+          mbar_wait(&full_b[w], (uint32_t)((kb / WSTAGES) & 1));
+        }
         tc_after_sync();
         const uint32_t sa = smem_u32(a_tile(s)), sb = smem_u32(b_tile(w));
 #pragma unroll
@@ -172,19 +211,33 @@ __global__ void __launch_bounds__(dqt::NT, 1)
           const uint64_t bd = sw128_desc_mn(sb + 2048 * kk, B_LBO, 1024u);
           const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
 #pragma unroll
-          for (int ab = 0; ab < NACC; ++ab)
-            mma_bf16(tmem_d + ab * BN, sw128_desc(sa + ab * 128 * 128 + 32 * kk), bd, IDESC, acc);
+          for (int ab = 0; ab < NACC; ++ab) {
+            const uint64_t ad = sw128_desc(sa + ab * 128 * 128 + 32 * kk);
+            if (PAIR)
+              mma_bf16_pair(tmem_d + ab * BN, ad, bd, S::IDESC, acc);
+            else
+              mma_bf16(tmem_d + ab * BN, ad, bd, S::IDESC, acc);
+          }
         }
-        mma_commit(&empty_a[s]);
-        mma_commit(&empty_b[w]);
+        if (PAIR) {
+          mma_commit_pair(&empty_a[s], 3);
+          mma_commit_pair(&empty_b[w], 3);
+        } else {
+          mma_commit(&empty_a[s]);
+          mma_commit(&empty_b[w]);
+        }
       }
-      mma_commit(&acc_full);
+      if (PAIR)
+        mma_commit_pair(&acc_full, 3);
+      else
+        mma_commit(&acc_full);
     }
   } else if (warp >= 4) {
     // ---------------- dequant producers: thread (r, j, h) of the 64 x 2 x 2 units
     const int pt = threadIdx.x - 128;
     const int r = pt >> 2, j = (pt >> 1) & 1, h = pt & 1;
-    const int cbeg = n0 + 64 * j + 32 * h;  // this thread's 32 columns of the W rows
+    const int cbeg = wn0 + 64 * j + 32 * h;  // this thread's 32 columns of the W rows
+    const uint32_t fb0 = PAIR ? mapa_cl(&full_b[0], 0) : 0u;
     const int tq = cbeg / TC;                // ... = column tile tq of the index
     // The block's row parameters are loaded one block ahead; the row's slot range of the
     // thread's 32 columns (the index) two blocks ahead, and its first two entries one block
@@ -235,7 +288,7 @@ __global__ void __launch_bounds__(dqt::NT, 1)
       mbar_wait(&full_c[c], (uint32_t)((kb / CSTAGES) & 1));
       // the code tile is TMA-swizzled (SWIZZLE_128B: 16-byte chunk k of row r at k ^ (r & 7)),
       // so the 8 rows a warp reads hit distinct banks
-      const uint4* cr = reinterpret_cast<const uint4*>(c_tile(c) + r * BN);
+      const uint4* cr = reinterpret_cast<const uint4*>(c_tile(c) + r * WC);
       const int k0 = 4 * j + 2 * h;
       const uint4 q0 = cr[k0 ^ (r & 7)], q1 = cr[(k0 + 1) ^ (r & 7)];
       fence_proxy_async();  // generic reads of the slot before the TMA refills it
@@ -275,7 +328,7 @@ __global__ void __launch_bounds__(dqt::NT, 1)
       }
       // the row's outliers in [cbeg, cbeg + 32): exact fp32 values, RNE to bf16
       auto put = [&](int cc, float v) {
-        const int k = cc - n0 - 64 * j;  // 0..63 within the MN chunk row
+        const int k = cc - wn0 - 64 * j;  // 0..63 within the MN chunk row
         const uint32_t hv = pack_bf16(v, 0.0f) & 0xFFFFu;
         *reinterpret_cast<uint16_t*>(bt + ((((k >> 3) ^ (r & 7)) << 4) | ((k & 7) << 1))) =
             (uint16_t)hv;
@@ -287,7 +340,12 @@ __global__ void __launch_bounds__(dqt::NT, 1)
       }
       fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor cores
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full_b[w]);
+      if (lane == 0) {
+        if (PAIR)  // the leader's MMA reads this CTA's half: arrive on the leader's barrier
+          mbar_arrive_cl(fb0 + (uint32_t)(w * sizeof(uint64_t)));
+        else
+          mbar_arrive(&full_b[w]);
+      }
       s_n = s_nx;
       z_n = z_nx;
     }
@@ -296,10 +354,29 @@ __global__ void __launch_bounds__(dqt::NT, 1)
     epilogue_bf16<BN, NACC, NPW>(tmem_d, warp, lane, m0, n0, a.M, a.N, a.y);
   }
   tc_before_sync();
-  __syncthreads();
-  if (warp == 2)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d),
-                 "n"(TMEM_COLS));
+  if (PAIR) {
+    cluster_sync_all();
+    if (warp == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_d),
+                   "n"(S::TMEM_COLS));
+  } else {
+    __syncthreads();
+    if (warp == 2)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d),
+                   "n"(S::TMEM_COLS));
+  }
+}
+
+__global__ void __launch_bounds__(dqt::NT, 1)
+    k_dq_gemm_t(const __grid_constant__ CUtensorMap tm_dy, const __grid_constant__ CUtensorMap tm_w,
+                const DqtArgs a) {
+  dq_gemm_t_body<false>(&tm_dy, &tm_w, a);
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(dqt::NT, 1)
+    k_dq_gemm_t_pair(const __grid_constant__ CUtensorMap tm_dy,
+                     const __grid_constant__ CUtensorMap tm_w, const DqtArgs a) {
+  dq_gemm_t_body<true>(&tm_dy, &tm_w, a);
 }
 
 // ------------------------------------------------------------------ host side
@@ -336,21 +413,13 @@ cudaError_t launch_dq_gemm_t(const void* dy, int T, int O, const uint8_t* codes,
   {
     const cuuint64_t dims[2] = {(cuuint64_t)I, (cuuint64_t)O};
     const cuuint64_t strides[1] = {(cuuint64_t)I};
-    const cuuint32_t box[2] = {BN, BK};
+    const cuuint32_t box[2] = {WC, BK};
     const cuuint32_t es[2] = {1, 1};
     if (enc(&tw, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(codes), dims, strides, box,
             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_dq_gemm_t, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  const int tiles_n = (I + BN - 1) / BN;  // output column tiles (grid)
   const int ix_tiles = (I + TC - 1) / TC;  // index tiles: one per producer thread's columns
   int32_t* tix = reinterpret_cast<int32_t*>(workspace);
   {
@@ -358,8 +427,32 @@ cudaError_t launch_dq_gemm_t(const void* dy, int T, int O, const uint8_t* codes,
     if (e != cudaSuccess) return e;
   }
   DqtArgs a{scale, zp, tix, col, val, reinterpret_cast<__nv_bfloat16*>(dx), T, I, O, ix_tiles};
-  dim3 grid((unsigned)tiles_n, (unsigned)((T + BM - 1) / BM));
-  k_dq_gemm_t<<<grid, NT, SMEM_BYTES, st>>>(tdy, tw, a);
+  // the CTA pair for T > 256 (as the forward GEMM; QFT_DQ_PAIR=0/1 forces either)
+  const char* pe = getenv("QFT_DQ_PAIR");
+  const bool pair = pe ? atoi(pe) != 0 : T > 256;
+  if (pair) {
+    using S = ShapeT<true>;
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(k_dq_gemm_t_pair,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM_BYTES);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    dim3 grid((unsigned)(2 * ((I + S::BN - 1) / S::BN)), (unsigned)((T + 2 * S::BM - 1) / (2 * S::BM)));
+    k_dq_gemm_t_pair<<<grid, NT, S::SMEM_BYTES, st>>>(tdy, tw, a);
+  } else {
+    using S = ShapeT<false>;
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(k_dq_gemm_t, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           S::SMEM_BYTES);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    dim3 grid((unsigned)((I + S::BN - 1) / S::BN), (unsigned)((T + S::BM - 1) / S::BM));
+    k_dq_gemm_t<<<grid, NT, S::SMEM_BYTES, st>>>(tdy, tw, a);
+  }
   return cudaGetLastError();
 }
 

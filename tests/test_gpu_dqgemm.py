@@ -52,8 +52,11 @@ def test_dequant_gemm_rejects_bad_k(cuda):
         st.linear(0, x)
 
 
+# tokens <= 256: the single-CTA kernel; > 256: the CTA pair
 @pytest.mark.parametrize("shape,m", [((128, 256), 200), ((384, 1024), 512), ((4096, 4096), 256),
-                                     ((11008, 4096), 130), ((4096, 11008), 64), ((192, 320), 77)])
+                                     ((11008, 4096), 130), ((4096, 11008), 64), ((192, 320), 77),
+                                     ((4096, 4096), 1024), ((11008, 4096), 600),
+                                     ((4096, 11008), 513), ((192, 320), 300), ((128, 256), 1000)])
 def test_dequant_gemm_t_matches_materialised(cuda, shape, m):
     """The backward weight operand: dx = dy . W (network.hpp:145) with W dequantized as an
     MN-major operand (qftc_dequant_gemm_t) == the GEMM on the materialised bf16 weights."""
