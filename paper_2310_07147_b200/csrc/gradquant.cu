@@ -85,30 +85,35 @@ __device__ __forceinline__ uint32_t gq_quant4(const float* x, const QuantRow& q,
 #endif
 // The exact quantizer without a fast path or a branch (QFT_GQ_BRANCHFREE), for rows with
 // s in [2^-100, 2^125] and |z| + qmax + 2 < 2^21 (QuantRow.fast && s >= 2^-100):
-//   y = RN(x * RN(1/s)) is within 2^-22 of x/s, so the reference's round_half_away of the
-//   fp64 quotient (quantize.hpp:160-166) is fl or fl + 1, fl = floor(y): it is fl + 1 iff
-//   x/s > h = fl + 1/2, or x/s == h and h > 0 (a tie goes away from zero).  The sign of
-//   h*s - x is exact in one FMA (the product is exact, one rounding keeps the sign; s >=
-//   2^-100 keeps a nonzero difference normal), and RN_d(x/s) == h only when x == h*s
-//   (DESIGN §4).  The code is then clamp(k, -z, qmax - z) + z: the clamp also takes
-//   +-Inf (fl = +-Inf, the FMA is NaN: k = fl) and NaN (fmax/fmin drop it: code 0, the
+//   the reference's round_half_away of the fp64 quotient (quantize.hpp:160-166) is
+//   sign(x) * floor(a/s + 1/2), a = |x|.  y = RN(a * RN(1/s)) is within 2^-22 of a/s, so
+//   with fl = floor(y) the magnitude is fl or fl + 1: fl + 1 iff a >= h*s, h = fl + 1/2 (a
+//   tie goes up in magnitude, away from zero).  The sign of h*s - a is exact in one FMA
+//   (the product is exact, one rounding keeps the sign; s >= 2^-100 keeps a nonzero
+//   difference normal), and RN_d(x/s) lands on a half-integer only when x is exactly
+//   one.  The code is then clamp(k, -z, qmax - z) + z: the clamp also takes
+//   +-Inf (fl = Inf, the FMA is NaN: k = +-Inf) and NaN (fmax/fmin drop it: code 0, the
 //   reference's !(q > 0)) -- no per-value test, no divergent exact path; bf16 gradients
 //   put a quarter of their values near a half-integer, which made the checked fast path
 //   branch and fall back per group of 4.
 __device__ __forceinline__ uint32_t gq_quant4_bf(const float* x, const QuantRow& q) {
   float t[4];
+  // (on magnitudes: one compare per value instead of the three of the signed tie rule;
+  // the sign goes back on with one LOP3, NaN stays NaN and clamps to code 0)
 #pragma unroll
   for (int i = 0; i < 4; i += 2) {
-    const float2 xv = make_float2(x[i], x[i + 1]);
-    const float2 y = mul2(xv, f2(q.inv_s));
+    const float2 av = make_float2(fabsf(x[i]), fabsf(x[i + 1]));
+    const float2 y = mul2(av, f2(q.inv_s));
     const float2 fl = make_float2(floorf(y.x), floorf(y.y));
     const float2 h = add2(fl, f2(0.5f));
-    const float2 r = fma2(h, f2(q.s), neg2(xv));
-    float k0 = (r.x < 0.0f || (r.x == 0.0f && h.x > 0.0f)) ? __fadd_rn(fl.x, 1.0f) : fl.x;
-    float k1 = (r.y < 0.0f || (r.y == 0.0f && h.y > 0.0f)) ? __fadd_rn(fl.y, 1.0f) : fl.y;
+    const float2 r = fma2(h, f2(q.s), neg2(av));
+    float k0 = r.x <= 0.0f ? __fadd_rn(fl.x, 1.0f) : fl.x;
+    float k1 = r.y <= 0.0f ? __fadd_rn(fl.y, 1.0f) : fl.y;
+    k0 = __uint_as_float(__float_as_uint(k0) | (__float_as_uint(x[i]) & 0x80000000u));
+    k1 = __uint_as_float(__float_as_uint(k1) | (__float_as_uint(x[i + 1]) & 0x80000000u));
     k0 = fminf(fmaxf(k0, q.ylo), q.yhi);
     k1 = fminf(fmaxf(k1, q.ylo), q.yhi);
-    const float2 m = add2(make_float2(k0, k1), f2(q.magic));  // integers: exact
+    const float2 m = add2(make_float2(k0, k1), f2(q.magic));
     t[i] = m.x;
     t[i + 1] = m.y;
   }
@@ -137,6 +142,12 @@ __global__ void __launch_bounds__(NT + 32) k_grad_quant(const LaunchArgs a, int 
   // the tensor of the row each stage holds: written by the issuing thread before the
   // stage's TMA (read after the stage's barrier), so the workers never walk the table
   __shared__ int s_ti[GQ_NS];
+  // the tensors' first rows (the issuing thread's walk reads them per row): in shared
+  // memory when the table is small, so the control warp's serial section per row has no
+  // global load
+  constexpr int RBMAX = 512;
+  __shared__ int s_rb[RBMAX];
+  const bool rb_smem = a.n_tensors <= RBMAX;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const bool ctrl = wid == NW;  // the control warp: TMA issue + the row's quantizer
   const int tc = NT;            // its lane 0
@@ -148,7 +159,10 @@ __global__ void __launch_bounds__(NT + 32) k_grad_quant(const LaunchArgs a, int 
   // rows come in increasing order per CTA: the tensor index only moves forward
   int ti_issue = 0;
   auto tensor_of = [&](int row, int& ti) -> const DevTensor& {
-    while (ti + 1 < a.n_tensors && a.tensors[ti + 1].row_base <= row) ++ti;
+    if (rb_smem)
+      while (ti + 1 < a.n_tensors && s_rb[ti + 1] <= row) ++ti;
+    else
+      while (ti + 1 < a.n_tensors && a.tensors[ti + 1].row_base <= row) ++ti;
     return a.tensors[ti];
   };
   // the control thread: row `row` into stage st (one bulk copy of the row)
@@ -204,6 +218,8 @@ __global__ void __launch_bounds__(NT + 32) k_grad_quant(const LaunchArgs a, int 
     for (int i = 0; i < GQ_NS; ++i) mbar_init(&bars[i], 1);
     mbar_fence_init();
   }
+  if (rb_smem)
+    for (int i = t; i < a.n_tensors; i += NT + 32) s_rb[i] = a.tensors[i].row_base;
   __syncthreads();
   if (t == tc) {  // this CTA's first two rows in flight
     for (int k = 0; k < GQ_NS - 2; ++k)
