@@ -50,6 +50,9 @@ using namespace qftd;
 #ifndef DQ_PW
 #define DQ_PW 0
 #endif
+#ifndef DQ_PUNROLL
+#define DQ_PUNROLL 2  // producer loop unrolled by 2 (measured +4%; 4: no better)
+#endif
 #ifndef DQ_NOOUT
 #define DQ_NOOUT 0  // A/B only: outliers not applied (wrong results)
 #endif
@@ -61,6 +64,7 @@ using namespace qftd;
 #endif
 namespace dq {
 using namespace um;
+constexpr int kProdUnroll = DQ_PUNROLL;
 constexpr int BK = 64;      // K per block: 128 bytes of bf16 = one SWIZZLE_128B row
 constexpr int WROWS = 128;  // W rows dequantized per CTA (output columns of a CTA's operand)
 #ifndef DQ_CSTAGES
@@ -319,6 +323,7 @@ __device__ __forceinline__ void dq_gemm_body(const CUtensorMap* tm_x, const CUte
       }
     };
     eload(s1, e1);
+#pragma unroll kProdUnroll
     for (int kb = 0; kb < nkb; ++kb) {
       const int w = kb % WSTAGES, c = kb % CSTAGES;
       // this block's outliers (loaded during the previous block); issue the next block's

@@ -38,8 +38,12 @@
 namespace qftk {
 using namespace qftd;
 
+#ifndef DQT_PUNROLL
+#define DQT_PUNROLL 2  // producer loop unroll (A/B)
+#endif
 namespace dqt {
 using namespace um;
+constexpr int kProdUnrollT = DQT_PUNROLL;
 constexpr int WC = 128;          // W columns dequantized per CTA (= UMMA N of one CTA)
 constexpr int BK = 64;           // W rows per K block
 constexpr int WSTAGES = 4;       // dequantized W-operand ring (producers run ahead)
@@ -278,6 +282,7 @@ __device__ __forceinline__ void dq_gemm_t_body(const CUtensorMap* tm_dy, const C
     load_ix(0, ebA, eeA);
     eload(ebA, eeA);
     load_ix(1, ebA, eeA);
+#pragma unroll kProdUnrollT
     for (int kb = 0; kb < nkb; ++kb) {
       const int w = kb % WSTAGES, c = kb % CSTAGES;
       const int cS = nS, cN = nN, cc0 = nc0, cc1 = nc1;
