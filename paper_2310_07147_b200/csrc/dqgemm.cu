@@ -53,6 +53,9 @@ using namespace qftd;
 #ifndef DQ_PUNROLL
 #define DQ_PUNROLL 2  // producer loop unrolled by 2 (measured +4%; 4: no better)
 #endif
+#ifndef DQ_NOEPI
+#define DQ_NOEPI 0  // A/B only: no epilogue (no output)
+#endif
 #ifndef DQ_NOOUT
 #define DQ_NOOUT 0  // A/B only: outliers not applied (wrong results)
 #endif
@@ -427,7 +430,7 @@ __device__ __forceinline__ void dq_gemm_body(const CUtensorMap* tm_x, const CUte
     // ---------------- epilogue: TMEM -> bf16 -> HBM (each CTA its own X rows x all BN)
     pwait(&acc_full, 0u);
     tc_after_sync();
-    epilogue_bf16<BN, NACC, NPW>(tmem_d, warp, lane, m0, n0, a.M, a.N, a.y);
+    if (!DQ_NOEPI) epilogue_bf16<BN, NACC, NPW>(tmem_d, warp, lane, m0, n0, a.M, a.N, a.y);
   }
   tc_before_sync();
   if (PAIR) {

@@ -52,6 +52,9 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                    smem_u32(bar))
                : "memory");
 }
+#ifndef UMMA_EPI_V8
+#define UMMA_EPI_V8 1
+#endif
 #ifndef DQ_CLREL
 #define DQ_CLREL 0
 #endif
@@ -149,6 +152,34 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, uint32_t* r) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// tcgen05.ld 32x32b.x32 without the wait (the registers are undefined until tmem_wait32)
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t addr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(addr));
+}
+// wait for the thread's outstanding tcgen05.ld; `r` as in-out operands, so no use of the
+// loaded registers moves above the wait
+__device__ __forceinline__ void tmem_wait32(uint32_t* r) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]),
+                 "+r"(r[6]), "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]),
+                 "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]),
+                 "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]),
+                 "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]),
+                 "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
+
 // The bf16 epilogue of the GEMMs with NACC M=128 accumulators of BN fp32 columns: warp
 // (4 + 4g + q) drains TMEM lanes 32q.. for warp group g of NPW/4 -- the (accumulator,
 // 32-column chunk) units g, g + NPW/4, ... (accumulator a: rows m0 + 128a ..) -- rounds to
@@ -158,16 +189,42 @@ __device__ __forceinline__ void epilogue_bf16(uint32_t tmem_d, int warp, int lan
                                               int M, int N, __nv_bfloat16* y) {
   const int wq = (warp - 4) & 3, grp = (warp - 4) >> 2;
   const uint32_t lane_base = (uint32_t)(32 * wq) << 16;
-  constexpr int CH = BN / 32, GROUPS = NPW / 4;
-#pragma unroll 1
-  for (int u = grp; u < NACC * CH; u += GROUPS) {
+  constexpr int CH = BN / 32, GROUPS = NPW / 4, NU = NACC * CH / GROUPS;
+  static_assert(NACC * CH % GROUPS == 0, "epilogue units per warp");
+  // the warp's units k = 0..NU-1 (unit u = grp + k * GROUPS: accumulator u / CH, columns
+  // (u % CH) * 32 ..), double-buffered: unit k+1's TMEM load is in flight while unit k
+  // is converted and stored
+  auto taddr = [&](int k) {
+    const int u = grp + k * GROUPS;
+    return tmem_d + lane_base + (uint32_t)((u / CH) * BN + (u % CH) * 32);
+  };
+  uint32_t rb[2][32];
+  tmem_ld32_issue(taddr(0), rb[0]);
+  tmem_wait32(rb[0]);
+#pragma unroll
+  for (int k = 0; k < NU; ++k) {
+    if (k + 1 < NU) tmem_ld32_issue(taddr(k + 1), rb[(k + 1) & 1]);
+    uint32_t* r = rb[k & 1];
+    const int u = grp + k * GROUPS;
     const int accn = u / CH, c0 = (u % CH) * 32;
     const int row = m0 + 128 * accn + 32 * wq + lane;
-    uint32_t r[32];
-    tmem_ld32(tmem_d + lane_base + (uint32_t)(accn * BN + c0), r);
     if (row < M) {
       __nv_bfloat16* yr = y + (size_t)row * N + n0 + c0;
-      if (n0 + c0 + 32 <= N && (N % 8) == 0) {
+      if (UMMA_EPI_V8 && n0 + c0 + 32 <= N && (N % 16) == 0) {
+        // two 32-byte stores (STG.256): every store fills whole L2 sectors of its row
+        // (16-byte stores left each sector half-written per instruction: ncu-measured
+        // the epilogue at ~1.6 TB/s, 15% of a 4096^3 GEMM)
+        uint32_t o[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          o[q] = pack_bf16(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(yr + 16 * h),
+                       "r"(o[8 * h]), "r"(o[8 * h + 1]), "r"(o[8 * h + 2]), "r"(o[8 * h + 3]),
+                       "r"(o[8 * h + 4]), "r"(o[8 * h + 5]), "r"(o[8 * h + 6]), "r"(o[8 * h + 7])
+                       : "memory");
+      } else if (n0 + c0 + 32 <= N && (N % 8) == 0) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           uint4 o;
@@ -178,10 +235,12 @@ __device__ __forceinline__ void epilogue_bf16(uint32_t tmem_d, int warp, int lan
           reinterpret_cast<uint4*>(yr)[q] = o;
         }
       } else {
-        for (int e = 0; e < 32 && n0 + c0 + e < N; ++e)
-          yr[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
+#pragma unroll
+        for (int e = 0; e < 32; ++e)  // (static indices: r stays in registers)
+          if (n0 + c0 + e < N) yr[e] = __float2bfloat16_rn(__uint_as_float(r[e]));
       }
     }
+    if (k + 1 < NU) tmem_wait32(rb[(k + 1) & 1]);
   }
 }
 
