@@ -1103,6 +1103,9 @@ static cudaError_t rows_resolve(const LaunchArgs& a, KLaunch* out, int cps) {
   return rows_resolve_t<512, 1, 2>(a, nt, smem, out, cps);
 }
 
+#ifndef QFT_GEN_MINB_M
+#define QFT_GEN_MINB_M QFT_ROWS_MINB_M  // GEN tier, 11008 columns (A/B: 1 = no spills)
+#endif
 #ifndef QFT_GEN_MINB_S
 #define QFT_GEN_MINB_S 4  // GEN tier, rows of <= 4096 columns: 4 CTAs/SM (128 registers)
 #endif
@@ -1119,7 +1122,7 @@ static cudaError_t rows_resolve_gen(const LaunchArgs& a, KLaunch* out, int cps) 
   if (nt == 128 && geom_ok(4096, 3) && b8)
     return rows_resolve_t<128, QFT_GEN_MINB_S, 3, 2, 4096, 8, true>(a, nt, smem, out, cps);
   if (geom_ok(11008, 2) && b8)
-    return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 11008, 8, true>(a, nt, smem, out, cps);
+    return rows_resolve_t<384, QFT_GEN_MINB_M, 2, 1, 11008, 8, true>(a, nt, smem, out, cps);
   if (nt <= 128) return rows_resolve_t<128, QFT_GEN_MINB_S, 3, 0, 0, 0, true>(a, nt, smem, out, cps);
   if (nt <= 384 && c / 16 >= nt)
     return rows_resolve_t<384, QFT_ROWS_MINB_M, 2, 1, 0, 0, true>(a, nt, smem, out, cps);
