@@ -2,6 +2,7 @@
 producer (qftc_dequant_gemm, tcgen05 + TMA).  y = x . W^T must equal the same GEMM on the
 materialised bf16 weights (qftc_expand bf16 = RNE(reconstruct(W)), quantize.hpp:331-338)
 up to fp32 accumulation order: within one bf16 rounding of the fp32 reference."""
+import numpy as np
 import pytest
 import torch
 
@@ -89,3 +90,45 @@ def test_dequant_gemm_t_rejects_bad_shapes(cuda):
     dy = torch.zeros(8, 100, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(NotImplementedError):
         st.linear_backward(0, dy)
+
+
+@pytest.mark.parametrize("shape,m", [((4096, 4096), 200), ((4096, 4096), 600),
+                                     ((256, 1024), 1000), ((320, 512), 77)])
+def test_dequant_gemms_strict_csr_via_c_abi(cuda, port, shape, m):
+    """Both GEMM entry points through the raw C-ABI with a STRICT CSR (row_count = NULL:
+    row r's entries are row_ptr[r] .. row_ptr[r+1]) straight from the oracle's
+    decompose_weight (quantize.hpp:301-314), single CTA and CTA pair: equal to the GEMMs on
+    RNE(reconstruct(W)) (the oracle's fp32 reconstruction rounded to bf16)."""
+    import ctypes as C
+    N = cuda._native
+    r, c = shape
+    w = port.synth(shape, 4000 + m, 0.02, 0.005)
+    d = port.decompose_weight(w, 0.01, 8)
+    wb = torch.from_numpy(port.reconstruct(d)).cuda().to(torch.bfloat16)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    codes, sc, zp = dev(d.codes), dev(d.scale), dev(d.zero_point)
+    rp, col, val = dev(d.row_ptr.astype(np.int32)), dev(d.col_idx.astype(np.int32)), dev(d.values)
+    vp = lambda t: C.c_void_p(t.data_ptr())
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    # forward: y = x . W^T
+    x = (torch.randn(m, c, device="cuda") * 0.5).to(torch.bfloat16)
+    y = torch.empty((m, r), dtype=torch.bfloat16, device="cuda")
+    ws = torch.empty(int(N.lib.qftc_dequant_gemm_workspace_bytes(r, c)), dtype=torch.uint8, device="cuda")
+    N.check(N.lib.qftc_dequant_gemm(vp(x), m, c, vp(codes), r, vp(sc), vp(zp), vp(rp), None,
+                                    vp(col), vp(val), vp(y), vp(ws), s))
+    # backward: dx = dy . W
+    dy = (torch.randn(m, r, device="cuda") * 0.5).to(torch.bfloat16)
+    dx = torch.empty((m, c), dtype=torch.bfloat16, device="cuda")
+    wst = torch.empty(int(N.lib.qftc_dequant_gemm_t_workspace_bytes(r, c)), dtype=torch.uint8,
+                      device="cuda")
+    N.check(N.lib.qftc_dequant_gemm_t(vp(dy), m, r, vp(codes), c, vp(sc), vp(zp), vp(rp), None,
+                                      vp(col), vp(val), vp(dx), vp(wst), s))
+    torch.cuda.synchronize()
+    for got, ref, what in ((y, x.float() @ wb.float().t(), "forward"),
+                           (dx, dy.float() @ wb.float(), "dx")):
+        err = (got.float() - ref).abs()
+        tol = ref.abs() * 2.0 ** -7 + 1e-3 * ref.abs().max()
+        assert int((err > tol).sum()) == 0, f"{what}: max err {err.max().item()}"
+        same = (got == ref.to(torch.bfloat16)).float().mean().item()
+        assert same > 0.98, f"{what}: only {same:.4f} equal the reference's rounding"
+    assert d.row_ptr[-1] > 0
