@@ -53,6 +53,9 @@ using namespace qftd;
 #ifndef DQ_PUNROLL
 #define DQ_PUNROLL 2  // producer loop unrolled by 2 (measured +4%; 4: no better)
 #endif
+#ifndef DQ_ONEFENCE
+#define DQ_ONEFENCE 1  // one proxy fence per block (measured +0.5-1%)
+#endif
 #ifndef DQ_NOEPI
 #define DQ_NOEPI 0  // A/B only: no epilogue (no output)
 #endif
@@ -357,9 +360,13 @@ __device__ __forceinline__ void dq_gemm_body(const CUtensorMap* tm_x, const CUte
       for (int c4 = 0; c4 < NQ; ++c4)
         q4[c4] = live ? cr[(c4 + NQ * hf) ^ ((j >> 1) & 3)] : make_uint4(0, 0, 0, 0);
       // generic-proxy reads of the slot, then the TMA (async proxy) refills it: order them
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_c[c]);  // the code slot is consumed
+      // (DQ_ONEFENCE: the slot is released after the block's operand writes, behind the
+      // one fence that also publishes them)
+      if (!DQ_ONEFENCE) {
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_c[c]);  // the code slot is consumed
+      }
       // the W-operand slot w is free once the MMAs of its previous use completed
       pwait(&empty_b[w], (uint32_t)(((kb / WSTAGES) & 1) ^ 1));
       uint8_t* bt = b_tile(w) + j * 128;
@@ -421,6 +428,7 @@ __device__ __forceinline__ void dq_gemm_body(const CUtensorMap* tm_x, const CUte
 #endif
       __syncwarp();
       if (lane == 0) {
+        if (DQ_ONEFENCE) mbar_arrive(&empty_c[c]);  // the code slot is consumed
         if (PAIR)  // the leader's MMA reads this CTA's half: arrive on the leader's barrier
           mbar_arrive_cl(fb0 + (uint32_t)(w * sizeof(uint64_t)));
         else
