@@ -10,24 +10,24 @@
 //
 // sm_100a, K in blocks of 64; two shapes (dq::Shape): a CTA pair (cta_group::2, M > 256)
 // with a 512 x 256 output tile per pair, or one CTA with a 512 x 128 tile.  Per CTA:
-//   warp 0 (lane 0)  TMA: the X tile (512 x 64 bf16, two 256-row boxes, SWIZZLE_128B) of a
-//                    K block into a stage of the X ring (2 stages, mbarrier tx); the
-//                    dequantized W operand has its own 4-stage ring, so the producers run
-//                    up to three blocks ahead of the MMAs
-//   warp 3 (lane 0)  TMA: the W code tile (128 x 64 u8) into its own 4-stage ring
-//   warps 4-11       the dequant producers: a thread pair owns W row n0 + j, each thread
-//                    32 columns of a block: its codes of
-//                    the stage -> s*(q-z) (fp32, one rounding, quantize.hpp:209) -> its
-//                    CSR outliers in [k0, k0+64) overwrite their positions -> bf16 (RNE)
-//                    -> the K-major SWIZZLE_128B layout tcgen05 reads; fence.proxy.async;
-//                    one arrive per warp.  Each keeps a cursor into its row's CSR slot
-//                    (columns ascending), so the outliers cost O(nnz) per row in total.
-//   warp 1 (lane 0)  tcgen05.mma.cta_group::1.kind::f16, M=128, N=128, K=16 x 4 per block
-//                    for each of the four 128-row blocks of X (all read the same
-//                    dequantized W operand: each dequantized element feeds 4 x 128 rows of
-//                    MMA), into four TMEM accumulators (fp32); tcgen05.commit frees the stage
-//   warps 4-11       the epilogue after the last block: tcgen05.ld 32x32b -> bf16 -> HBM
-//   warp 2           TMEM allocation (512 columns: the accumulators) and release
+//   warp 0 (lane 0)  TMA: the CTA's X rows of a K block (SWIZZLE_128B, 256-row boxes) into
+//                    the X ring (pair: 4 stages of 256 rows, both CTAs' bytes completing
+//                    on the leader's barrier; single: 2 stages of 512 rows)
+//   warp 3 (lane 0)  TMA: the CTA's 128 x 64 W code tile into its own 4-stage ring
+//   warps 4-11       the dequant producers: a thread pair owns one of the CTA's 128 W rows,
+//                    each thread 32 columns of a block: codes -> s*(q-z) (fp32, one
+//                    rounding, quantize.hpp:209) -> its CSR outliers of the block (from the
+//                    per-(row, 32-column) slot index, loaded a block ahead) overwrite their
+//                    positions -> bf16 (RNE) -> the K-major SWIZZLE_128B operand ring (4
+//                    stages); one fence.proxy.async, then the code slot and the operand
+//                    slot are released / published (pair: on the leader's barrier)
+//   warp 1 (lane 0)  the MMA issuer (pair: the leader only): tcgen05.mma kind::f16 --
+//                    pair M=256 x N=256 (cta_group::2, each SM supplies its A and B halves)
+//                    into two TMEM accumulators, single M=128 x N=128 into four; all read
+//                    the same dequantized W operand; tcgen05.commit (multicast to both
+//                    CTAs of a pair) frees the slots and finally signals the accumulators
+//   warps 4-11       the epilogue: tcgen05.ld 32x32b (double-buffered) -> bf16 -> HBM
+//   warp 2           TMEM allocation (512 columns) and release
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>

@@ -14,15 +14,16 @@
 // tile) index built by a small pre-pass (k_csr_tile_index: the first slot entry at or past
 // each tile's first column), so a producer scans only the ~1-2 entries of its own window.
 //
-// sm_100a, one 512 x 128 output tile per CTA (four M=128 TMEM accumulators share each
-// dequantized W operand block), K in blocks of 64 W rows:
+// sm_100a, K in blocks of 64 W rows; a CTA pair (cta_group::2, more than 256 tokens: a
+// 512 x 256 tile per pair, each CTA 256 dY rows and 128 of the W columns, two M=256
+// accumulators) or one CTA (512 x 128, four M=128 accumulators), per CTA:
 //   warp 0 (lane 0)  TMA: the dY tile (512 x 64 bf16, K-major, SWIZZLE_128B) -> X/W ring
 //   warp 3 (lane 0)  TMA: the W code tile (64 rows x 128 columns u8, SWIZZLE_128B) -> its
 //                    own 4-stage ring; the W operand has a 4-stage ring of its own
 //   warps 4-11       producers: thread (r, j, h) dequantizes W row k0 + r, columns
 //                    [64j + 32h, +32) of the tile -> 4 swizzled 16-byte chunks of row r of
 //                    the operand's MN chunk j; then its outliers; fence.proxy.async; arrive
-//   warp 1 (lane 0)  tcgen05.mma kind::f16, A K-major, B MN-major, M=128 x4, N=128, K=16 x4
+//   warp 1 (lane 0)  tcgen05.mma kind::f16, A K-major, B MN-major (pair: the leader only)
 //   warps 4-11       the bf16 epilogue (umma.cuh)
 #include <cuda.h>
 #include <cudaTypedefs.h>
