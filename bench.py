@@ -922,10 +922,17 @@ def run_gemm(args):
             torch.cuda.synchronize()
             return e0.elapsed_time(e1) / n
 
-        fused = timeit(lambda: st.linear(0, x, out=y))
+        # the CSR slot index is a function of the weight: built once per weight version
+        # (csr_index, timed on its own) and reused by the micro-batches' GEMMs; the per-call
+        # form (index rebuilt inside every call) is reported beside it
+        idx = st.csr_index(0)
+        index_ms = timeit(lambda: st.csr_index(0))
+        fused = timeit(lambda: st.linear(0, x, out=y, index=idx))
+        fused_rebuild = timeit(lambda: st.linear(0, x, out=y))
         dy = (torch.randn(tokens, r, device="cuda") * 0.5).to(torch.bfloat16)
         dx = torch.empty((tokens, c), dtype=torch.bfloat16, device="cuda")
-        fused_t = timeit(lambda: st.linear_backward(0, dy, out=dx))
+        fused_t = timeit(lambda: st.linear_backward(0, dy, out=dx, index=idx))
+        fused_t_rebuild = timeit(lambda: st.linear_backward(0, dy, out=dx))
         mat = timeit(lambda: (plan.run(), torch.matmul(x, wb.t(), out=y)))
         plan.run()
         cublas = timeit(lambda: torch.matmul(x, wb.t(), out=y))
@@ -934,6 +941,9 @@ def run_gemm(args):
         flops = 2.0 * tokens * r * c
         out.append({"proj": name, "M": tokens, "N": r, "K": c,
                     "fused_ms": fused, "fused_tflops": flops / fused / 1e9,
+                    "csr_index_ms": index_ms,
+                    "fused_with_index_rebuild_ms": fused_rebuild,
+                    "backward_dx_fused_with_index_rebuild_ms": fused_t_rebuild,
                     "fused_frac_of_bf16_peak": flops / fused / 1e9 / peak_tf,
                     "expand_plus_cublas_ms": mat, "cublas_only_ms": cublas,
                     "cublas_tflops": flops / cublas / 1e9,
@@ -1002,6 +1012,9 @@ def run_wgrad(args):
         flops = 2.0 * tokens * r * c
         out.append({"proj": name, "out": r, "in": c, "tokens": tokens,
                     "fused_ms": fused, "fused_tflops": flops / fused / 1e9,
+                    "csr_index_ms": index_ms,
+                    "fused_with_index_rebuild_ms": fused_rebuild,
+                    "backward_dx_fused_with_index_rebuild_ms": fused_t_rebuild,
                     "fused_frac_of_bf16_peak": flops / fused / 1e9 / peak_tf,
                     "fused_accumulate_ms": fused_acc,
                     "cublas_f32_plus_quantize_state_ms": mat,

@@ -327,6 +327,22 @@ int qftc_expand(const qftc_expand_tensor* tensors, int n_tensors, int bf16,
  * per-column-tile CSR index rebuilt by the call).  out % 64 == 0, in % 64 == 0; dy, codes, dx
  * 16-byte aligned. */
 int64_t qftc_dequant_gemm_t_workspace_bytes(int out_features, int in_features);
+/* The per-(row, 32-column) CSR slot index both GEMMs build into their workspace, built once
+ * (qftc_dequant_gemm_workspace_bytes(rows, cols) == qftc_dequant_gemm_t_workspace_bytes(
+ * rows, cols) bytes) and reused by the _prebuilt forms while the weight's CSR is unchanged
+ * -- e.g. across the micro-batches between two optimizer steps. */
+int qftc_dequant_gemm_index(const int32_t* row_start, const int32_t* row_count,
+                            const int32_t* col_idx, int rows, int cols, void* index,
+                            qftc_stream_t stream);
+int qftc_dequant_gemm_prebuilt(const void* x_bf16, int m, int k, const uint8_t* codes, int n,
+                               const float* scale, const int32_t* zero_point,
+                               const int32_t* col_idx, const float* values, const void* index,
+                               void* y_bf16, qftc_stream_t stream);
+int qftc_dequant_gemm_t_prebuilt(const void* dy_bf16, int tokens, int out_features,
+                                 const uint8_t* codes, int in_features, const float* scale,
+                                 const int32_t* zero_point, const int32_t* col_idx,
+                                 const float* values, const void* index, void* dx_bf16,
+                                 qftc_stream_t stream);
 int qftc_dequant_gemm_t(const void* dy_bf16, int tokens, int out_features, const uint8_t* codes,
                         int in_features, const float* scale, const int32_t* zero_point,
                         const int32_t* row_start, const int32_t* row_count,

@@ -96,6 +96,9 @@ _SIGS = {
     "qftc_momentum_to_blocks": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "qftc_momentum_from_blocks": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "qftc_dequant_gemm_workspace_bytes": (_i64, [_i, _i]),
+    "qftc_dequant_gemm_index": (_i, [_vp, _vp, _vp, _i, _i, _vp, _vp]),
+    "qftc_dequant_gemm_prebuilt": (_i, [_vp, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "qftc_dequant_gemm_t_prebuilt": (_i, [_vp, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "qftc_dequant_gemm": (_i, [_vp, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "qftc_wgrad_workspace_bytes": (_i64, [_i]),
     "qftc_dequant_gemm_t_workspace_bytes": (_i64, [_i, _i]),

@@ -449,6 +449,57 @@ int qftc_dequant_gemm_t(const void* dy_bf16, int tokens, int out_features, const
   return QFTC_OK;
 }
 
+int qftc_dequant_gemm_index(const int32_t* row_start, const int32_t* row_count,
+                            const int32_t* col_idx, int rows, int cols, void* index,
+                            qftc_stream_t stream) {
+  if (rows <= 0 || cols <= 0 || cols % 64 != 0)
+    return fail(QFTC_EINVAL, "dequant_gemm_index: bad shape (cols must be a multiple of 64)");
+  if (!row_start || !col_idx || !index) return fail(QFTC_EINVAL, "dequant_gemm_index: null pointer");
+  if (int rc = require_device()) return rc;
+  QFTC_CUDA(launch_csr_tile_index(row_start, row_count, col_idx, rows, cols / 32, 32,
+                                  reinterpret_cast<int32_t*>(index), (cudaStream_t)stream),
+            "dequant_gemm_index kernel");
+  return QFTC_OK;
+}
+
+int qftc_dequant_gemm_prebuilt(const void* x_bf16, int m, int k, const uint8_t* codes, int n,
+                               const float* scale, const int32_t* zero_point,
+                               const int32_t* col_idx, const float* values, const void* index,
+                               void* y_bf16, qftc_stream_t stream) {
+  if (m <= 0 || n <= 0 || k <= 0) return fail(QFTC_EINVAL, "dequant_gemm: empty shape");
+  if (k % 64 != 0) return fail(QFTC_ENOTSUP, "dequant_gemm: K must be a multiple of 64");
+  if (!x_bf16 || !codes || !scale || !zero_point || !col_idx || !values || !index || !y_bf16)
+    return fail(QFTC_EINVAL, "dequant_gemm: null pointer");
+  if (!al16(x_bf16) || !al16(codes) || !al16(y_bf16))
+    return fail(QFTC_EINVAL, "dequant_gemm: x, codes and y must be 16-byte aligned");
+  if (int rc = require_device()) return rc;
+  QFTC_CUDA(launch_dq_gemm(x_bf16, m, k, codes, n, scale, zero_point, nullptr, nullptr, col_idx,
+                           values, y_bf16, const_cast<void*>(index), (cudaStream_t)stream, false),
+            "dequant_gemm kernel");
+  return QFTC_OK;
+}
+
+int qftc_dequant_gemm_t_prebuilt(const void* dy_bf16, int tokens, int out_features,
+                                 const uint8_t* codes, int in_features, const float* scale,
+                                 const int32_t* zero_point, const int32_t* col_idx,
+                                 const float* values, const void* index, void* dx_bf16,
+                                 qftc_stream_t stream) {
+  if (tokens <= 0 || out_features <= 0 || in_features <= 0)
+    return fail(QFTC_EINVAL, "dequant_gemm_t: empty shape");
+  if (out_features % 64 != 0 || in_features % 64 != 0)
+    return fail(QFTC_ENOTSUP, "dequant_gemm_t: out_features and in_features must be multiples of 64");
+  if (!dy_bf16 || !codes || !scale || !zero_point || !col_idx || !values || !index || !dx_bf16)
+    return fail(QFTC_EINVAL, "dequant_gemm_t: null pointer");
+  if (!al16(dy_bf16) || !al16(codes) || !al16(dx_bf16))
+    return fail(QFTC_EINVAL, "dequant_gemm_t: dy, codes and dx must be 16-byte aligned");
+  if (int rc = require_device()) return rc;
+  QFTC_CUDA(launch_dq_gemm_t(dy_bf16, tokens, out_features, codes, in_features, scale, zero_point,
+                             nullptr, nullptr, col_idx, values, dx_bf16, const_cast<void*>(index),
+                             (cudaStream_t)stream, false),
+            "dequant_gemm_t kernel");
+  return QFTC_OK;
+}
+
 int64_t qftc_wgrad_workspace_bytes(int out_features) {
   return out_features > 0 ? (int64_t)wgrad_workspace_bytes(out_features) : 0;
 }

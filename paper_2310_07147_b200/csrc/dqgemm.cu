@@ -485,7 +485,7 @@ size_t dq_gemm_workspace_bytes(int N, int K) {
 cudaError_t launch_dq_gemm(const void* x, int M, int K, const uint8_t* codes, int N,
                            const float* scale, const int32_t* zp, const int32_t* row_start,
                            const int32_t* row_count, const int32_t* col, const float* val,
-                           void* y, void* workspace, cudaStream_t st) {
+                           void* y, void* workspace, cudaStream_t st, bool build_index) {
   using namespace dq;
   auto enc = um::encode_fn();
   if (!enc) return cudaErrorNotSupported;
@@ -514,7 +514,7 @@ cudaError_t launch_dq_gemm(const void* x, int M, int K, const uint8_t* codes, in
       return cudaErrorInvalidValue;
   }
   int32_t* tix = reinterpret_cast<int32_t*>(workspace);
-  {
+  if (build_index) {  // (else: the caller's workspace already holds this CSR's index)
     cudaError_t e = launch_csr_tile_index(row_start, row_count, col, N, K / CPT, CPT, tix, st);
     if (e != cudaSuccess) return e;
   }

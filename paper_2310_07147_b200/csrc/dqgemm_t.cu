@@ -401,7 +401,7 @@ size_t dq_gemm_t_workspace_bytes(int O, int I) {
 cudaError_t launch_dq_gemm_t(const void* dy, int T, int O, const uint8_t* codes, int I,
                              const float* scale, const int32_t* zp, const int32_t* row_start,
                              const int32_t* row_count, const int32_t* col, const float* val,
-                             void* dx, void* workspace, cudaStream_t st) {
+                             void* dx, void* workspace, cudaStream_t st, bool build_index) {
   using namespace dqt;
   auto enc = um::encode_fn();
   if (!enc) return cudaErrorNotSupported;
@@ -428,7 +428,7 @@ cudaError_t launch_dq_gemm_t(const void* dy, int T, int O, const uint8_t* codes,
   }
   const int ix_tiles = (I + TC - 1) / TC;  // index tiles: one per producer thread's columns
   int32_t* tix = reinterpret_cast<int32_t*>(workspace);
-  {
+  if (build_index) {  // (else: the caller's workspace already holds this CSR's index)
     cudaError_t e = launch_csr_tile_index(row_start, row_count, col, O, ix_tiles, TC, tix, st);
     if (e != cudaSuccess) return e;
   }

@@ -242,7 +242,7 @@ size_t dq_gemm_workspace_bytes(int N, int K);
 cudaError_t launch_dq_gemm(const void* x, int M, int K, const uint8_t* codes, int N,
                            const float* scale, const int32_t* zp, const int32_t* row_start,
                            const int32_t* row_count, const int32_t* col, const float* val,
-                           void* y, void* workspace, cudaStream_t s);
+                           void* y, void* workspace, cudaStream_t s, bool build_index = true);
 // re-plan slot capacities (csr.cu, k_replan_caps)
 cudaError_t launch_replan_caps(const uint8_t* codes, int rows, int cols, int bit_width,
                                const int32_t* cnt_out, const int32_t* cnt_in, int lvl, int gmul,
@@ -253,7 +253,7 @@ size_t dq_gemm_t_workspace_bytes(int O, int I);
 cudaError_t launch_dq_gemm_t(const void* dy, int T, int O, const uint8_t* codes, int I,
                              const float* scale, const int32_t* zp, const int32_t* row_start,
                              const int32_t* row_count, const int32_t* col, const float* val,
-                             void* dx, void* workspace, cudaStream_t st);
+                             void* dx, void* workspace, cudaStream_t st, bool build_index = true);
 // the backward weight gradient with the sink's quantization in the GEMM epilogue (wgrad.cu):
 // codes/scale/zp = quantize_state(dY^T . X [+ dequantize(entry)]); workspace: rows bounds,
 // counters and the error word (its last uint32)

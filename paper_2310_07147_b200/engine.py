@@ -685,7 +685,22 @@ class QftModelState:
             0 if out.dtype == torch.float32 else 1, _stream()))
         return out
 
-    def linear(self, i: int, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    def csr_index(self, i: int) -> torch.Tensor:
+        """Tensor i's per-(row, 32-column) CSR slot index (qftc_dequant_gemm_index) for the
+        CURRENT state: pass it as ``index=`` to linear / linear_backward while the weights
+        are unchanged (the micro-batches between two steps) and the GEMMs skip its rebuild."""
+        cur = self.cur
+        g = self.groups[self.group_of[i]]
+        r, c = self.shapes[i]
+        idx = torch.empty(int(N.lib.qftc_dequant_gemm_workspace_bytes(r, c)), dtype=torch.uint8,
+                          device=self.device)
+        N.check(N.lib.qftc_dequant_gemm_index(
+            _p(self._rs(self.row_start[cur], i)), _p(self._rows(self.row_count[cur], i)),
+            _p(g.col[cur]), r, c, _p(idx), _stream()))
+        return idx
+
+    def linear(self, i: int, x: torch.Tensor, out: Optional[torch.Tensor] = None,
+               index: Optional[torch.Tensor] = None) -> torch.Tensor:
         """The forward consumer of tensor i: y = x . W_i^T (network.hpp:113-129), x bf16
         [M, cols] -> y bf16 [M, rows], with W_i dequantized inside the GEMM's operand producer
         (qftc_dequant_gemm: tcgen05 tensor cores read RNE(reconstruct(W_i)) built in shared
@@ -697,6 +712,12 @@ class QftModelState:
             raise ValueError(f"linear: x must be a contiguous bf16 [M, {c}] tensor")
         y = out if out is not None else torch.empty((x.shape[0], r), dtype=torch.bfloat16,
                                                     device=x.device)
+        if index is not None:  # csr_index(i) of the current state
+            N.check(N.lib.qftc_dequant_gemm_prebuilt(
+                _p(x), x.shape[0], c, _p(self._sl(self.w_codes[cur], i)), r,
+                _p(self._rows(self.w_scale, i)), _p(self._rows(self.w_zp, i)),
+                _p(g.col[cur]), _p(g.val[cur]), _p(index), _p(y), _stream()))
+            return y
         need = int(N.lib.qftc_dequant_gemm_workspace_bytes(r, c))
         ws = getattr(self, "_dq_ws", None)
         if ws is None or ws.numel() < need:
@@ -708,8 +729,8 @@ class QftModelState:
             _p(g.col[cur]), _p(g.val[cur]), _p(y), _p(ws), _stream()))
         return y
 
-    def linear_backward(self, i: int, dy: torch.Tensor,
-                        out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    def linear_backward(self, i: int, dy: torch.Tensor, out: Optional[torch.Tensor] = None,
+                        index: Optional[torch.Tensor] = None) -> torch.Tensor:
         """The backward's input gradient through tensor i: dx = dy . W_i (network.hpp:145
         backward_core in_grad = matmul(out_grad, w)), dy bf16 [M, rows] -> dx bf16 [M, cols],
         with W_i dequantized inside the GEMM's operand producer (qftc_dequant_gemm_t: the
@@ -722,6 +743,12 @@ class QftModelState:
             raise ValueError(f"linear_backward: dy must be a contiguous bf16 [M, {r}] tensor")
         dx = out if out is not None else torch.empty((dy.shape[0], c), dtype=torch.bfloat16,
                                                      device=dy.device)
+        if index is not None:  # csr_index(i) of the current state
+            N.check(N.lib.qftc_dequant_gemm_t_prebuilt(
+                _p(dy), dy.shape[0], r, _p(self._sl(self.w_codes[cur], i)), c,
+                _p(self._rows(self.w_scale, i)), _p(self._rows(self.w_zp, i)),
+                _p(g.col[cur]), _p(g.val[cur]), _p(index), _p(dx), _stream()))
+            return dx
         need = int(N.lib.qftc_dequant_gemm_t_workspace_bytes(r, c))
         ws = getattr(self, "_dqt_ws", None)
         if ws is None or ws.numel() < need:

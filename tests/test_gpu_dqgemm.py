@@ -132,3 +132,27 @@ def test_dequant_gemms_strict_csr_via_c_abi(cuda, port, shape, m):
         same = (got == ref.to(torch.bfloat16)).float().mean().item()
         assert same > 0.98, f"{what}: only {same:.4f} equal the reference's rounding"
     assert d.row_ptr[-1] > 0
+
+
+@pytest.mark.parametrize("shape,m", [((4096, 4096), 600), ((384, 1024), 128), ((11008, 4096), 513)])
+def test_dequant_gemms_prebuilt_index_equal(cuda, shape, m):
+    """The _prebuilt forms with csr_index(i) (built once per weight version) give the same
+    bytes as the calls that rebuild the index, forward and dx; the forward and dx index
+    workspaces have the same size (one index serves both)."""
+    N = cuda._native
+    r, c = shape
+    assert (int(N.lib.qftc_dequant_gemm_workspace_bytes(r, c)) ==
+            int(N.lib.qftc_dequant_gemm_t_workspace_bytes(r, c)))
+    st = cuda.QftModelState([shape], bit_width=8)
+    st.init_from_weights(lambda i: cuda.synth(shape, 5 + m, 0.02, 0.01), 0.01)
+    cc, s, z = st.grad_views(0)
+    q = cuda.quantize_state(cuda.synth(shape, 9, 1e-3, 0.0), 8)
+    cc.copy_(q.data); s.copy_(q.params.scale); z.copy_(q.params.zero_point)
+    st.step(lr=2e-4, check=True)  # slotted CSR with drift
+    x = (torch.randn(m, c, device="cuda") * 0.5).to(torch.bfloat16)
+    dy = (torch.randn(m, r, device="cuda") * 0.5).to(torch.bfloat16)
+    idx = st.csr_index(0)
+    y0, y1 = st.linear(0, x), st.linear(0, x, index=idx)
+    d0, d1 = st.linear_backward(0, dy), st.linear_backward(0, dy, index=idx)
+    torch.cuda.synchronize()
+    assert torch.equal(y0, y1) and torch.equal(d0, d1)
