@@ -297,9 +297,8 @@ __device__ __forceinline__ void dq_gemm_t_body(const CUtensorMap* tm_dy, const C
       const uint4* cr = reinterpret_cast<const uint4*>(c_tile(c) + r * WC);
       const int k0 = 4 * j + 2 * h;
       const uint4 q0 = cr[k0 ^ (r & 7)], q1 = cr[(k0 + 1) ^ (r & 7)];
-      fence_proxy_async();  // generic reads of the slot before the TMA refills it
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_c[c]);
+      // (the code slot is released after the block's operand writes, behind the one fence
+      // that also publishes them: one proxy fence per block)
       mbar_wait(&empty_b[w], (uint32_t)(((kb / WSTAGES) & 1) ^ 1));
       // row r of MN chunk j: 64 bf16 = 128 bytes, 16-byte chunk k at (k ^ (r & 7)) << 4
       uint8_t* bt = b_tile(w) + j * B_LBO + r * 128;
@@ -344,9 +343,10 @@ __device__ __forceinline__ void dq_gemm_t_body(const CUtensorMap* tm_dy, const C
         if (cN > 1) put(cc1, cv1);
         for (int e = 2; e < cN; ++e) put(__ldg(a.col + cS + e), __ldg(a.val + cS + e));
       }
-      fence_proxy_async();  // generic-proxy smem writes -> visible to the tensor cores
+      fence_proxy_async();  // smem reads and writes of the block -> ordered with the async proxy
       __syncwarp();
       if (lane == 0) {
+        mbar_arrive(&empty_c[c]);  // the code slot is consumed
         if (PAIR)  // the leader's MMA reads this CTA's half: arrive on the leader's barrier
           mbar_arrive_cl(fb0 + (uint32_t)(w * sizeof(uint64_t)));
         else
