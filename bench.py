@@ -1012,9 +1012,6 @@ def run_wgrad(args):
         flops = 2.0 * tokens * r * c
         out.append({"proj": name, "out": r, "in": c, "tokens": tokens,
                     "fused_ms": fused, "fused_tflops": flops / fused / 1e9,
-                    "csr_index_ms": index_ms,
-                    "fused_with_index_rebuild_ms": fused_rebuild,
-                    "backward_dx_fused_with_index_rebuild_ms": fused_t_rebuild,
                     "fused_frac_of_bf16_peak": flops / fused / 1e9 / peak_tf,
                     "fused_accumulate_ms": fused_acc,
                     "cublas_f32_plus_quantize_state_ms": mat,
