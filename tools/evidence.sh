@@ -14,6 +14,7 @@ python bench.py --zero1 --no-e2e --no-cpu --no-side > gpurun_out/${T}_zero1.json
 python bench.py --mode sweep --steps 5 > gpurun_out/${T}_sweep.json 2>&1
 python bench.py --mode 13b --steps 5 > gpurun_out/${T}_13b.json 2>&1
 python bench.py --mode gemm > gpurun_out/${T}_gemm.json 2>&1
+python bench.py --mode wgrad > gpurun_out/${T}_wgrad.json 2>&1
 python tools/bf16_probe.py --steps 5 > gpurun_out/${T}_bf16.json 2>&1
 python tools/lr_probe.py --steps 5 > gpurun_out/${T}_lr.json 2>&1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"k_step_prep|rows_kernel|step_kernel" --csv --log-file gpurun_out/${T}_launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-side > /dev/null 2>&1
