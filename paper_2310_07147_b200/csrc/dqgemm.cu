@@ -47,26 +47,11 @@ using namespace qftd;
 #ifndef DQ_NOFENCE
 #define DQ_NOFENCE 0
 #endif
-#ifndef DQ_PW
-#define DQ_PW 0
-#endif
 #ifndef DQ_PUNROLL
 #define DQ_PUNROLL 2  // producer loop unrolled by 2 (measured +4%; 4: no better)
 #endif
 #ifndef DQ_ONEFENCE
 #define DQ_ONEFENCE 1  // one proxy fence per block (measured +0.5-1%)
-#endif
-#ifndef DQ_NOEPI
-#define DQ_NOEPI 0  // A/B only: no epilogue (no output)
-#endif
-#ifndef DQ_NOOUT
-#define DQ_NOOUT 0  // A/B only: outliers not applied (wrong results)
-#endif
-#ifndef DQ_NOX
-#define DQ_NOX 0  // A/B only: no X loads (wrong results)
-#endif
-#ifndef DQ_NOMMA
-#define DQ_NOMMA 0  // A/B only: no MMAs (wrong results)
 #endif
 namespace dq {
 using namespace um;
@@ -155,13 +140,6 @@ __device__ __forceinline__ void dq_gemm_body(const CUtensorMap* tm_x, const CUte
   const int m0 = PAIR ? (int)blockIdx.y * 2 * BM + (int)rank * BM : (int)blockIdx.y * BM;
   const int wn0 = n0 + (int)rank * WROWS;
   const int nkb = a.K / BK;
-  // pair-path waits: DQ_PW=1 polls without the suspend-time hint (remote arrivals)
-  auto pwait = [&](uint64_t* bar, uint32_t par) {
-    if (PAIR && DQ_PW)
-      mbar_wait_cl(bar, par);
-    else
-      mbar_wait(bar, par);
-  };
   auto a_tile = [&](int s) { return dsm + s * A_BYTES; };
   auto b_tile = [&](int w) { return dsm + STAGES * A_BYTES + w * B_BYTES; };
   auto c_tile = [&](int c) { return dsm + STAGES * A_BYTES + WSTAGES * B_BYTES + c * C_BYTES; };
@@ -208,11 +186,7 @@ __device__ __forceinline__ void dq_gemm_body(const CUtensorMap* tm_x, const CUte
       const uint32_t fa0 = PAIR ? mapa_cl(&full_a[0], 0) : 0u;
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % STAGES;
-        pwait(&empty_a[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
-        if (DQ_NOX) {
-          if (rank == 0) mbar_arrive(&full_a[s]);
-          continue;
-        }
+        mbar_wait(&empty_a[s], (uint32_t)(((kb / STAGES) & 1) ^ 1));
         if (PAIR) {
           // both CTAs' bytes complete on the leader's barrier; the leader expects them all
           if (rank == 0) mbar_arrive_expect_tx(&full_a[s], (uint32_t)(2 * A_BYTES));
@@ -232,7 +206,7 @@ __device__ __forceinline__ void dq_gemm_body(const CUtensorMap* tm_x, const CUte
     if (lane == 0) {  // ---------------- TMA: W code tiles (their own, deeper ring)
       for (int kb = 0; kb < nkb; ++kb) {
         const int c = kb % CSTAGES;
-        pwait(&empty_c[c], (uint32_t)(((kb / CSTAGES) & 1) ^ 1));
+        mbar_wait(&empty_c[c], (uint32_t)(((kb / CSTAGES) & 1) ^ 1));
         mbar_arrive_expect_tx(&full_c[c], (uint32_t)C_BYTES);
         tma_load_2d(c_tile(c), tm_w, kb * BK, wn0, &full_c[c]);
       }
@@ -257,9 +231,7 @@ __device__ __forceinline__ void dq_gemm_body(const CUtensorMap* tm_x, const CUte
 #pragma unroll
           for (int ab = 0; ab < NACC; ++ab) {
             const uint64_t ad = sw128_desc(sa + ab * 128 * 128 + 32 * kk);
-            if (DQ_NOMMA)
-              ;
-            else if (PAIR)
+            if (PAIR)
               mma_bf16_pair(tmem_d + ab * BN, ad, bd, S::IDESC, acc);
             else
               mma_bf16(tmem_d + ab * BN, ad, bd, S::IDESC, acc);
@@ -338,11 +310,11 @@ __device__ __forceinline__ void dq_gemm_body(const CUtensorMap* tm_x, const CUte
       const float cv0 = nv0, cv1 = nv1;
       eload(s2, e2);
       tload(kb + 2, s2, e2);
-      pwait(&full_c[c], (uint32_t)((kb / CSTAGES) & 1));
+      mbar_wait(&full_c[c], (uint32_t)((kb / CSTAGES) & 1));
 #if DQ_NOPROD  // A/B: the pipeline without the dequantization work (wrong results)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_c[c]);
-      pwait(&empty_b[w], (uint32_t)(((kb / WSTAGES) & 1) ^ 1));
+      mbar_wait(&empty_b[w], (uint32_t)(((kb / WSTAGES) & 1) ^ 1));
       __syncwarp();
       if (lane == 0) {
         if (PAIR)
@@ -368,7 +340,7 @@ __device__ __forceinline__ void dq_gemm_body(const CUtensorMap* tm_x, const CUte
         if (lane == 0) mbar_arrive(&empty_c[c]);  // the code slot is consumed
       }
       // the W-operand slot w is free once the MMAs of its previous use completed
-      pwait(&empty_b[w], (uint32_t)(((kb / WSTAGES) & 1) ^ 1));
+      mbar_wait(&empty_b[w], (uint32_t)(((kb / WSTAGES) & 1) ^ 1));
       uint8_t* bt = b_tile(w) + j * 128;
       // 32 codes -> 4 swizzled 16-byte chunks of bf16: the row's branch (fast magic-number
       // dequant, or the exact form for |z| >= 2^22) is taken once per block
@@ -418,7 +390,7 @@ __device__ __forceinline__ void dq_gemm_body(const CUtensorMap* tm_x, const CUte
         const uint32_t h = pack_bf16(v, 0.0f) & 0xFFFFu;
         *reinterpret_cast<uint16_t*>(bt + ((((k >> 3) ^ (j & 7)) << 4) | ((k & 7) << 1))) = (uint16_t)h;
       };
-      if (!DQ_NOOUT && cN > 0) {
+      if (cN > 0) {
         put(cc0, cv0);
         if (cN > 1) put(cc1, cv1);
         for (int e = 2; e < cN; ++e) put(__ldg(a.col + cS + e), __ldg(a.val + cS + e));
@@ -436,9 +408,9 @@ __device__ __forceinline__ void dq_gemm_body(const CUtensorMap* tm_x, const CUte
       }
     }
     // ---------------- epilogue: TMEM -> bf16 -> HBM (each CTA its own X rows x all BN)
-    pwait(&acc_full, 0u);
+    mbar_wait(&acc_full, 0u);
     tc_after_sync();
-    if (!DQ_NOEPI) epilogue_bf16<BN, NACC, NPW>(tmem_d, warp, lane, m0, n0, a.M, a.N, a.y);
+    epilogue_bf16<BN, NACC, NPW>(tmem_d, warp, lane, m0, n0, a.M, a.N, a.y);
   }
   tc_before_sync();
   if (PAIR) {

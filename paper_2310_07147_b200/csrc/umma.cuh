@@ -55,9 +55,6 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 #ifndef UMMA_EPI_V8
 #define UMMA_EPI_V8 1
 #endif
-#ifndef DQ_CLREL
-#define DQ_CLREL 0
-#endif
 // ---- CTA-pair (cta_group::2) plumbing: the MMA of a 2-SM pair is issued by the leader
 // (cluster rank 0) and reads A and B halves from both CTAs' shared memory at the same
 // offsets; barriers the leader waits on receive the peer's TMA bytes and arrivals through
@@ -78,12 +75,9 @@ __device__ __forceinline__ void cluster_sync_all() {
                    : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_cl(uint32_t cl_addr) {
-#if DQ_CLREL
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr)
-               : "memory");
-#else  // default semantics (release.cta), the form CUTLASS's 2-SM pipelines use
+  // default semantics (release.cta), the form CUTLASS's 2-SM pipelines use; .release.cluster
+  // compiles to MEMBAR.ALL.GPU + ERRBAR per arrive and cost the pair kernel ~40%
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
-#endif
 }
 __device__ __forceinline__ bool mbar_try_wait_cl(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
