@@ -113,3 +113,19 @@ def test_no_contracted_packed_fma_in_sass():
                 bad.append(line.strip())
         sign_regs.discard(dst) if op != "FFMA2" else None
     assert not bad, f"contracted packed FMA: {bad[:4]}"
+
+
+def test_gemm_entry_points_validate_before_the_device():
+    """The GEMM entry points reject bad shapes / null pointers before touching the device
+    (no GPU needed), and the forward and dx index workspaces have the same size."""
+    from paper_2310_07147_b200 import _native as N
+    p = C.c_void_p(16)  # a dummy (16-byte aligned) pointer: never dereferenced here
+    assert N.lib.qftc_dequant_gemm_index(p, None, p, 8, 100, p, None) == N.QFTC_EINVAL
+    assert N.lib.qftc_dequant_gemm_index(None, None, p, 8, 128, p, None) == N.QFTC_EINVAL
+    assert N.lib.qftc_dequant_gemm_prebuilt(p, 4, 100, p, 8, p, p, p, p, p, p, None) == N.QFTC_ENOTSUP
+    assert N.lib.qftc_dequant_gemm_prebuilt(p, 4, 128, p, 8, p, p, p, p, None, p, None) == N.QFTC_EINVAL
+    assert N.lib.qftc_dequant_gemm_t_prebuilt(p, 4, 96, p, 128, p, p, p, p, p, p, None) == N.QFTC_ENOTSUP
+    assert N.lib.qftc_dequant_gemm(p, 4, 128, p, 8, p, p, p, None, p, p, p, None, None) == N.QFTC_EINVAL
+    for r, c in ((4096, 4096), (11008, 4096), (4096, 11008), (192, 320)):
+        assert (N.lib.qftc_dequant_gemm_workspace_bytes(r, c) ==
+                N.lib.qftc_dequant_gemm_t_workspace_bytes(r, c) == r * (c // 32 + 1) * 4)
